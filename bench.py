@@ -1,0 +1,440 @@
+#!/usr/bin/env python3
+"""BLCO MTTKRP benchmark (BASELINE.json metric) -- one JSON line on rank 0.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config nell2|cfg1|amazon|enron|delicious]
+
+A step = one all-mode MTTKRP (modes 0..N-1, fixed factors) over the whole
+synthetic tensor, inputs resident in HBM.  `value` = algorithmic bytes of the
+step (B_elem = nnz * (8 + 8 + N*R*8) per mode) / device time,
+whole job, max over ranks.  With torchrun (N > 1) the element spans are
+partitioned contiguously across ranks (no data-path collective inside the
+kernel) and each mode's partial M is summed with an NCCL all-reduce inside the
+timed region: strong scaling on a fixed tensor.
+
+`--impl reference` times the reference's own CPU implementation
+(oracle/_ref/libblco_ref.so = the unmodified proj/src compiled here) on a
+bounded ALTO-contiguous sample of the same tensor, on rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    # name: (dims, nnz, rank, description)
+    "cfg1": ([1000, 1000, 1000], 1_000_000, 16, "synthetic 1000^3, 1M nnz, R=16 (BASELINE configs[0])"),
+    "nell2": ([12092, 9184, 28818], 76_879_419, 32,
+              "synthetic NELL-2-shaped 12092x9184x28818, 76,879,419 nnz, R=32, all-mode (BASELINE configs[1])"),
+    "amazon": ([4821207, 1774269, 1805187], 1_741_809_018, 32,
+               "synthetic Amazon-shaped 4821207x1774269x1805187, 1.74B nnz, R=32 (BASELINE configs[2])"),
+    "enron": ([6066, 5699, 244268, 1176], 54_202_099, 16, "synthetic uniform Enron-shaped 4-mode, R=16"),
+    "delicious": ([532924, 17262471, 2480308, 1443], 140_126_181, 16,
+                  "synthetic uniform Delicious-shaped 4-mode, R=16"),
+}
+TENSOR_SEED, FACTOR_SEED = 42, 7
+
+
+def bytes_per_elem(order: int, rank: int, s: int = 8) -> int:
+    return 8 + s + order * rank * s
+
+
+# ------------------------------------------------------------------ clocks
+
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "100",
+                 "-i", str(self.device)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.15)
+            self.proc.terminate()
+            out, _ = self.proc.communicate(timeout=10)
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], None, set()
+        for ln in getattr(self, "lines", []):
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for name, flag in zip(self.NAMES, parts[4:8]):
+                if flag.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------- distributed
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# --------------------------------------------------------- CPU reference
+
+
+def reference_sample_run(dims, nnz, rank, steps, warmup, target_step_s=4.0, threads=None):
+    """Times the reference's blco::mttkrp (all modes) on the host.
+
+    The sample is the `S` elements of smallest ALTO index of the synthetic
+    tensor -- a contiguous prefix of the BLCO element order, i.e. exactly the
+    first S elements (first spans) the GPU processes -- built by the
+    reference's own build_blco from the COO subset.  S is calibrated so one
+    step takes ~target_step_s.  Returns (GB/s, dict).
+    """
+    sys.path.insert(0, str(ROOT / "oracle"))
+    from pyoracle import Oracle, RefLib, cfg_array
+
+    oracle, ref = Oracle(), RefLib()
+    threads = threads or os.cpu_count() or 1
+    order = len(dims)
+    t0 = time.perf_counter()
+    # Generate the tensor lazily in ALTO-prefix order: full COO then select.
+    gen_n = nnz
+    if int(np.prod(np.array(dims, dtype=object))) >= 2**64 or make_wide(dims):
+        raise RuntimeError("reference sample: layouts wider than 64 bits not supported here")
+    idx, vals = oracle.synth_uniform(dims, gen_n, TENSOR_SEED)
+    alto = oracle.alto_lo(dims, idx)
+    order_idx = None
+    factors = oracle.factors_random(dims, rank, FACTOR_SEED)
+    cfg = cfg_array(num_threads=threads)
+    setup_s = time.perf_counter() - t0
+
+    def sample(S):
+        nonlocal order_idx
+        S = min(S, gen_n)
+        sel = np.argpartition(alto, S - 1)[:S] if S < gen_n else np.arange(gen_n)
+        return ref.build(dims, idx[:, sel], vals[sel], 64), S
+
+    def one_step(t):
+        s = time.perf_counter()
+        for mode in range(order):
+            t.mttkrp(factors, mode, cfg)
+        return time.perf_counter() - s
+
+    # calibrate
+    S = min(gen_n, 1 << 17)
+    t, S = sample(S)
+    dt = one_step(t)
+    while dt < target_step_s / 4 and S < gen_n:
+        S = min(gen_n, int(S * max(2.0, min(16.0, target_step_s / max(dt, 1e-3)))))
+        t, S = sample(S)
+        dt = one_step(t)
+    for _ in range(warmup):
+        one_step(t)
+    times = [one_step(t) for _ in range(steps)]
+    bpe = bytes_per_elem(order, rank)
+    step_s = sum(times) / len(times)
+    gbps = S * order * bpe / step_s / 1e9
+    return gbps, {"sample_nnz": S, "step_s": step_s, "threads": threads, "setup_s": setup_s,
+                  "sample": f"first {S} elements in ALTO order of the {nnz}-nnz tensor "
+                            f"(reference build_blco on that COO subset), all {order} modes, R={rank}"}
+
+
+def make_wide(dims) -> bool:
+    return sum(int(d - 1).bit_length() for d in dims) > 64
+
+
+# ------------------------------------------------------------------ our arm
+
+
+def run_ours(args, world, rank_id, local):
+    import torch
+
+    import paper_2201_12523_b200 as b
+
+    dims, nnz, R, desc = CONFIGS[args.config]
+    if args.rank:
+        R = args.rank
+    N = len(dims)
+    dev = local
+    torch.cuda.set_device(dev)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+    stream = torch.cuda.current_stream()
+    sptr = stream.cuda_stream
+
+    # --- build the BLCO tensor on the device (timed separately)
+    bst = b.BuildStats()
+    t0 = time.perf_counter()
+    full = b.DeviceTensor.synthetic(dims, nnz, TENSOR_SEED, device=dev, stats=bst)
+    build_s = time.perf_counter() - t0
+    if world > 1:
+        ranges = b.partition(full.block_nnz(), 1024, world)
+        lo, hi = ranges[rank_id]
+        dt = full.slice(lo, hi, dev)
+        del full
+    else:
+        dt = full
+    local_nnz = dt.nnz
+
+    fac = [torch.empty((d, R), dtype=torch.float64, device=f"cuda:{dev}") for d in dims]
+    b.factors_random_device(dims, R, FACTOR_SEED, [a.data_ptr() for a in fac], sptr)
+    outs = [torch.empty((d, R), dtype=torch.float64, device=f"cuda:{dev}") for d in dims]
+    fptr = [a.data_ptr() for a in fac]
+    strategy = b.Strategy[args.strategy]
+    cfg = b.ExecConfig(num_compute_units=torch.cuda.get_device_properties(dev).multi_processor_count)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{dev}")
+
+    def step(ev=None):
+        for o in outs:
+            o.zero_()
+        for m in range(N):
+            if ev is not None:
+                ev[m][0].record(stream)
+            dt.mttkrp_device(fptr, R, m, outs[m].data_ptr(), strategy, cfg, accumulate=True, stream=sptr)
+            if ev is not None:
+                ev[m][1].record(stream)
+            if world > 1:
+                import torch.distributed as dist
+                dist.all_reduce(outs[m])
+
+    stats = b.MttkrpStats()
+    dt.mttkrp_device(fptr, R, 0, outs[0].data_ptr(), strategy, cfg, stream=sptr, stats=stats)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(N)] for _ in range(args.steps)]
+    sev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = b.kernel_launch_count()
+    with ClockSampler(dev) as clk:
+        for k in range(args.steps):
+            flush.zero_()  # L2 flush between steps (outside the step events)
+            sev[k][0].record(stream)
+            step(evs[k])
+            sev[k][1].record(stream)
+        torch.cuda.synchronize()
+    launches = b.kernel_launch_count() - launches0
+    if world > 1:
+        dist.barrier()
+    step_ms = [sev[k][0].elapsed_time(sev[k][1]) for k in range(args.steps)]
+    mode_ms = [[evs[k][m][0].elapsed_time(evs[k][m][1]) for k in range(args.steps)] for m in range(N)]
+    ms = sum(step_ms) / len(step_ms)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    bpe = bytes_per_elem(N, R)
+    total_bytes = nnz * N * bpe
+    value = total_bytes / (ms * 1e-3) / 1e9
+    kern_ms = sum(statistics.mean(x) for x in mode_ms)
+    achieved = local_nnz * N * bpe / (kern_ms * 1e-3) / 1e9
+    peaks = {}
+    try:
+        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except (OSError, ValueError):
+        pass
+    peak = peaks.get("hbm_gbs") or 6650.0
+    traffic = None
+    prof = ROOT / "profiles" / f"ncu_{args.config}.json"
+    if prof.exists():
+        try:
+            traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch_all_modes")
+        except ValueError:
+            traffic = None
+
+    result = {
+        "metric": "MTTKRP all-mode throughput (algorithmic B_elem bytes / time)",
+        "value": round(value, 2),
+        "unit": "GB/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms, 4),
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded Feistel-permuted unique coordinates, uniform [0,1) values; "
+                "FactorMatrices::random factors)",
+        "config": {"workload": desc, "dims": dims, "nnz": nnz, "rank": R, "modes": N,
+                   "tensor_seed": TENSOR_SEED, "factor_seed": FACTOR_SEED, "strategy": args.strategy,
+                   "l2": "flushed between steps (512 MiB write, outside the timed events)",
+                   "parallelism": f"span partition x{world}" + (" + NCCL all-reduce of M per mode" if world > 1 else ""),
+                   "bytes_per_elem_per_mode": bpe},
+        "per_mode_ms": [round(statistics.mean(x), 4) for x in mode_ms],
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "kernel": "k_mttkrp_register (one launch per mode)",
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks.get("hbm_gbs") else "fallback"},
+        "clocks": clk.summary(),
+        "gpu_launches": launches,
+        "build": {"seconds": round(build_s, 4), "device_stage_s": {k: round(getattr(bst, k), 4) for k in
+                                                                   ("sort_seconds", "block_seconds", "reencode_seconds",
+                                                                    "batch_seconds")},
+                  "nnz_per_s": round(nnz / build_s, 1)},
+        "segments_mode0": stats.segments,
+    }
+    if not args.no_e2e:
+        result["e2e"] = e2e_run(b, torch, dt if world == 1 else dt, dims, R, N, nnz if world == 1 else local_nnz,
+                                args, dev, world)
+    if rank_id == 0 and world == 1 and not args.no_cpu_baseline and args.config in ("cfg1", "nell2"):
+        try:
+            gbps, info = reference_sample_run(dims, nnz, R, steps=2, warmup=1)
+            result["cpu_baseline"] = {"value": round(gbps, 4), "unit": "GB/s", "cores": info["threads"],
+                                      "kind": "reference", "sample": info["sample"],
+                                      "step_s": round(info["step_s"], 3)}
+        except Exception as e:  # noqa: BLE001
+            result["cpu_baseline"] = {"value": None, "unit": "GB/s", "cores": None, "kind": "reference",
+                                      "sample": f"failed: {e}"}
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank_id == 0:
+        print(json.dumps(result), flush=True)
+
+
+def e2e_run(b, torch, dt, dims, R, N, nnz, args, dev, world):
+    """Same metric through the public host API: every step uploads the BLCO
+    payload from pinned host memory (blco_tensor_upload), runs blco_mttkrp per
+    mode with host factors (H2D) and reads M back (D2H)."""
+    host = dt.to_host()
+    idx = b.api.pinned_empty(host.idx.size, np.uint64)
+    vals = b.api.pinned_empty(host.vals.size, np.float64)
+    idx[:] = host.idx
+    vals[:] = host.vals
+    ht = b.BlcoTensor(host.layout, host.max_nnz_per_block, host.keys, host.offsets, idx, vals)
+    f = b.FactorMatrices.random(dims, R, FACTOR_SEED)
+    cfg = b.ExecConfig(num_compute_units=torch.cuda.get_device_properties(dev).multi_processor_count)
+    strategy = b.Strategy[args.strategy]
+
+    def step():
+        d = b.DeviceTensor.upload(ht, dev)
+        for m in range(N):
+            b.mttkrp(d, f, m, cfg, strategy)
+        d.free()
+
+    for _ in range(max(1, min(args.warmup, 2))):
+        step()
+    torch.cuda.synchronize()
+    n = max(1, min(args.steps, 5))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    w0 = time.perf_counter()
+    e0.record()
+    for _ in range(n):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    wall_ms = (time.perf_counter() - w0) * 1e3 / n
+    ms = e0.elapsed_time(e1) / n
+    bpe = bytes_per_elem(N, R)
+    h2d = nnz * 16 + N * sum(d * R * 8 for d in dims)
+    d2h = sum(d * R * 8 for d in dims)
+    return {"value": round(nnz * N * bpe / (ms * 1e-3) / 1e9, 2), "unit": "GB/s", "ms_per_step": round(ms, 3),
+            "wall_ms_per_step": round(wall_ms, 3), "steps": n,
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "path": "blco_tensor_upload (pinned host payload) + blco_mttkrp x modes (host factors in, host M out)"}
+
+
+# ------------------------------------------------------------ reference arm
+
+
+def run_reference(args, world, rank_id):
+    if rank_id != 0:
+        return
+    dims, nnz, R, desc = CONFIGS[args.config]
+    if args.rank:
+        R = args.rank
+    N = len(dims)
+    try:
+        gbps, info = reference_sample_run(dims, nnz, R, steps=args.steps, warmup=args.warmup,
+                                          target_step_s=args.ref_step_s)
+    except Exception as e:  # noqa: BLE001
+        print(json.dumps({"impl": "reference", "unavailable": f"{type(e).__name__}: {e}"}), flush=True)
+        return
+    result = {
+        "impl": "reference",
+        "metric": "MTTKRP all-mode throughput (algorithmic B_elem bytes / time)",
+        "value": round(gbps, 4),
+        "unit": "GB/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(info["step_s"] * 1e3, 3),
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (same generator and seeds as the ours arm)",
+        "config": {"workload": desc, "dims": dims, "nnz": nnz, "rank": R, "modes": N,
+                   "bytes_per_elem_per_mode": bytes_per_elem(N, R)},
+        "cpu_baseline": {"value": round(gbps, 4), "unit": "GB/s", "cores": info["threads"], "kind": "reference",
+                         "sample": info["sample"]},
+        "e2e": {"value": round(gbps, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "path": "unmodified reference blco::build_blco + blco::mttkrp (proj/src, compiled into "
+                "oracle/_ref/libblco_ref.so), ExecConfig{num_threads = all host threads}",
+    }
+    print(json.dumps(result), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="nell2")
+    ap.add_argument("--rank", type=int, default=0)
+    ap.add_argument("--strategy", choices=["Auto", "Register", "Hierarchical"], default="Auto")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-step-s", type=float, default=4.0)
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    world, rank_id, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, world, rank_id)
+    else:
+        run_ours(args, world, rank_id, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,3 @@
+// Forwarding header: the reference's blco/types.hpp, served by the B200 build.
+#pragma once
+#include "blco/b200.hpp"

@@ -1,0 +1,294 @@
+/*
+ * blco_b200.h -- C ABI of libblco_b200.so, the B200-native BLCO MTTKRP path.
+ *
+ * The reference (proj/, a CPU C++20 library) has no C ABI: its boundary is the
+ * link-level C++ API in the proj/include/blco headers.  This header is the plain-C
+ * layer underneath our re-declaration of that C++ API (include/blco/,
+ * implemented in paper_2201_12523_b200/csrc/cxx_api.cpp); every entry point
+ * names the reference declaration it replaces.  Plain pointers and sizes only.
+ *
+ * Conventions
+ *   - Every function returning int returns a blco_status; on failure
+ *     blco_last_error() holds a thread-local message whose prefix matches the
+ *     reference exception text (e.g. "blco: duplicate coordinate tuple").
+ *   - Modes are 0-based (proj/include/blco/mttkrp.hpp:107-109).
+ *   - Sparse coordinates are passed mode-major: idx[m * nnz + e].
+ *   - Dense matrices are row-major doubles (proj/include/blco/types.hpp:12-28).
+ *   - Device-side limits: dims[m] < 2^32 and order <= 8 for tensors that are
+ *     built or multiplied on the GPU (a mode of 2^32 rows would need a factor
+ *     matrix of >= 32 GiB per rank column); layouts stripped_bits <= 64.
+ */
+#ifndef BLCO_B200_H
+#define BLCO_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BLCO_MAX_ORDER 32     /* host-side layouts */
+#define BLCO_MAX_DEV_ORDER 8  /* device kernels */
+#define BLCO_MAX_BITS 128
+
+typedef enum blco_status {
+  BLCO_OK = 0,
+  BLCO_ERROR = 1,   /* blco::Error */
+  BLCO_EFORMAT = 2, /* blco::FormatError (proj/include/blco/common.hpp:31-34) */
+  BLCO_EIO = 3,     /* blco::IoError */
+  BLCO_EVERIFY = 4, /* blco::VerifyError */
+  BLCO_ECUDA = 5,
+  BLCO_ENCCL = 6
+} blco_status;
+
+typedef enum blco_strategy {
+  BLCO_STRATEGY_AUTO = 0, /* proj/include/blco/mttkrp.hpp:9 (enum class Strategy) */
+  BLCO_STRATEGY_REGISTER = 1,
+  BLCO_STRATEGY_HIERARCHICAL = 2
+} blco_strategy;
+
+const char* blco_last_error(void);
+int blco_abi_version(void);
+
+/* ---------------------------------------------------------------- layout
+ * Replaces blco::BitLayout / make_layout (proj/include/blco/layout.hpp:19-55,
+ * proj/src/layout.cpp:15-69).  key_slices are implied: stripped position p
+ * (p >= total - stripped) carries bit imap_bit[p] of mode imap_mode[p]. */
+typedef struct blco_layout {
+  int32_t order;
+  int32_t total_bits;
+  int32_t target_bits;
+  int32_t stripped_bits;
+  uint64_t dims[BLCO_MAX_ORDER];
+  int32_t mode_bits[BLCO_MAX_ORDER];
+  int32_t rem_bits[BLCO_MAX_ORDER];
+  int32_t field_shift[BLCO_MAX_ORDER];
+  uint64_t field_mask[BLCO_MAX_ORDER];
+  uint8_t imap_mode[BLCO_MAX_BITS]; /* interleaved position -> mode */
+  uint8_t imap_bit[BLCO_MAX_BITS];  /* interleaved position -> bit within mode */
+} blco_layout;
+
+/* make_layout (layout.hpp:55) */
+int blco_make_layout(const uint64_t* dims, int order, int target_bits, blco_layout* out);
+/* linearize (layout.hpp:58): 128-bit ALTO index as (hi, lo) */
+int blco_linearize(const blco_layout* l, const uint64_t* coords, uint64_t* alto_hi,
+                   uint64_t* alto_lo);
+/* split_block_key (layout.hpp:66) */
+int blco_split_block_key(const blco_layout* l, uint64_t alto_hi, uint64_t alto_lo,
+                         uint64_t* key, uint64_t* reencoded);
+/* encode_coords (layout.hpp:70) */
+int blco_encode_coords(const blco_layout* l, const uint64_t* coords, uint64_t* key,
+                       uint64_t* reencoded);
+/* delinearize (layout.hpp:73-74) */
+int blco_delinearize(const blco_layout* l, uint64_t reencoded, uint64_t key, uint64_t* coords);
+/* interleaved_remainder (layout.hpp:78) */
+int blco_interleaved_remainder(const blco_layout* l, uint64_t reencoded, uint64_t* hi,
+                               uint64_t* lo);
+/* BitLayout::key_upper / block_base (layout.hpp:42-50) */
+uint64_t blco_key_upper(const blco_layout* l, int mode, uint64_t key);
+
+/* compute_batch_table (proj/include/blco/blco_format.hpp:64-65): writes
+ * (block, offset, count) triples into spans (NULL = count only). */
+uint64_t blco_batch_table(const uint64_t* block_nnz, uint64_t nblocks, uint64_t quota,
+                          uint64_t* spans);
+
+/* -------------------------------------------------------------- config
+ * Replaces blco::ExecConfig (proj/include/blco/exec.hpp:15-30); same fields in
+ * the same order.  On the GPU, workgroup_size/tile_size/coarsening are hints
+ * (DESIGN.md), num_compute_units feeds choose_strategy exactly as in
+ * proj/src/mttkrp.cpp:17-21, num_factor_copies is honoured by the
+ * hierarchical kernel, stash_slots is a lower bound on the shared-memory
+ * stash, deterministic/num_threads have no device meaning. */
+typedef struct blco_exec_config {
+  int32_t workgroup_size;
+  int32_t tile_size;
+  int32_t coarsening;
+  int32_t num_compute_units;
+  int32_t num_factor_copies;
+  int32_t stash_slots;
+  int32_t deterministic;
+  int32_t num_threads;
+} blco_exec_config;
+
+void blco_exec_config_default(blco_exec_config* cfg);
+/* ExecConfig::validate (proj/src/exec.cpp:11-20) */
+int blco_exec_config_validate(const blco_exec_config* cfg);
+/* choose_strategy (proj/src/mttkrp.cpp:17-21) */
+int blco_choose_strategy(uint64_t target_mode_length, const blco_exec_config* cfg);
+
+/* MttkrpStats (proj/include/blco/mttkrp.hpp:18-25).  On the GPU a segment is
+ * one run of equal target rows inside a 32-element warp tile;
+ * commit_events counts per-lane RED.ADD.F64 commit lanes (segments x
+ * committing lanes), scalar_adds counts committed scalars. */
+typedef struct blco_mttkrp_stats {
+  int32_t strategy;
+  uint64_t workgroups;
+  uint64_t segments;
+  uint64_t stash_flushes;
+  uint64_t commit_events;
+  uint64_t scalar_adds;
+  float kernel_ms; /* device time of the MTTKRP kernel(s), CUDA events */
+} blco_mttkrp_stats;
+
+/* BuildStats (proj/include/blco/blco_format.hpp:49-54), device stage times */
+typedef struct blco_build_stats {
+  double sort_seconds;
+  double block_seconds;
+  double reencode_seconds;
+  double batch_seconds;
+} blco_build_stats;
+
+/* ------------------------------------------------------- device tensor
+ * A BLCO tensor resident in HBM: block-concatenated re-encoded indices (u64)
+ * and values (f64) in ALTO order, per-block keys / offsets / decoded base
+ * coordinates, and the CTA tile table the kernels consume. */
+typedef struct blco_tensor blco_tensor;
+
+/* build_blco (blco_format.hpp:59-61) on the device from a host COO.
+ * Bit-exact with the reference: same blocks, keys, order, indices, values. */
+int blco_build(const uint64_t* dims, int order, uint64_t nnz, const uint64_t* idx,
+               const double* vals, int target_bits, uint64_t max_nnz_per_block, int device,
+               blco_tensor** out, blco_build_stats* stats);
+
+/* Same, from a seeded synthetic uniform COO generated on the device
+ * (identical to blco_synth_uniform_host). */
+int blco_build_synthetic(const uint64_t* dims, int order, uint64_t nnz, uint64_t seed,
+                         int target_bits, uint64_t max_nnz_per_block, int device,
+                         blco_tensor** out, blco_build_stats* stats);
+
+/* Upload host-resident blocks (a reference BlcoTensor's payload). */
+int blco_tensor_upload(const blco_layout* layout, uint64_t max_nnz_per_block, uint64_t nblocks,
+                       const uint64_t* keys, const uint64_t* block_nnz,
+                       const uint64_t* const* idx, const double* const* vals, int device,
+                       blco_tensor** out);
+
+/* A new device tensor holding elements [elem_begin, elem_end) of t (block
+ * boundaries and keys kept); the multi-GPU partition unit. */
+int blco_tensor_slice(const blco_tensor* t, uint64_t elem_begin, uint64_t elem_end, int device,
+                      blco_tensor** out);
+
+int blco_tensor_info(const blco_tensor* t, blco_layout* layout, uint64_t* nblocks,
+                     uint64_t* nnz, uint64_t* max_nnz_per_block);
+int blco_tensor_blocks(const blco_tensor* t, uint64_t* keys, uint64_t* block_nnz);
+int blco_tensor_download(const blco_tensor* t, uint64_t* idx, double* vals);
+/* Device pointers (idx, vals) of the resident payload. */
+int blco_tensor_device_ptrs(const blco_tensor* t, const uint64_t** idx, const double** vals);
+void blco_tensor_free(blco_tensor* t);
+
+/* -------------------------------------------------------------- MTTKRP
+ * mttkrp (proj/include/blco/mttkrp.hpp:110-112): host factors in, host M out
+ * (dims[mode] x rank, overwritten). */
+int blco_mttkrp(const blco_tensor* t, const double* const* factors, uint64_t rank, int mode,
+                int strategy, const blco_exec_config* cfg, double* out,
+                blco_mttkrp_stats* stats);
+
+/* Device-resident variant: factors[m] and out are device pointers, work is
+ * enqueued on `stream` (cudaStream_t; NULL = legacy default stream) and not
+ * synchronised.  out is zeroed first unless accumulate != 0. */
+int blco_mttkrp_device(const blco_tensor* t, const double* const* d_factors, uint64_t rank,
+                       int mode, int strategy, const blco_exec_config* cfg, double* d_out,
+                       int accumulate, void* stream, blco_mttkrp_stats* stats);
+
+/* merge_copies (mttkrp.hpp:103): out = sum_c copies[c], copy 0 first. */
+int blco_merge_copies(const double* const* copies, uint64_t ncopies, uint64_t elems,
+                      double* out);
+
+/* ----------------------------------------------------------- streaming
+ * DeviceBudget / BlockSource / StreamReport / stream_mttkrp
+ * (proj/include/blco/streaming.hpp:12-94).  Blocks arrive through a pull
+ * callback called from the calling thread in order (BlockSource::next). */
+typedef struct blco_block_view {
+  uint64_t key;
+  uint64_t nnz;
+  const uint64_t* idx;
+  const double* vals;
+} blco_block_view;
+
+/* returns 1 = block produced, 0 = end of stream, < 0 = error (message via
+ * blco_set_error from the callback, status = -return) */
+typedef int (*blco_block_source_fn)(void* ctx, blco_block_view* out);
+
+typedef struct blco_device_budget {
+  uint64_t capacity_bytes;
+  int32_t num_queues;
+  uint64_t reservation_bytes;
+  double injected_transfer_latency_s;
+} blco_device_budget;
+
+typedef struct blco_stream_event {
+  int32_t kind; /* 0 = transfer, 1 = compute */
+  int32_t queue;
+  uint64_t block;
+  double begin_s, end_s;
+} blco_stream_event;
+
+typedef struct blco_stream_report {
+  uint64_t blocks;
+  uint64_t bytes_streamed;
+  double total_seconds;
+  double transfer_busy_seconds;
+  double compute_busy_seconds;
+  double overall_gbps;
+  double compute_gbps;
+  uint64_t peak_resident_bytes;
+  /* caller-provided arrays (may be NULL); filled up to the capacities */
+  int32_t* block_queue;
+  uint64_t block_queue_capacity;
+  blco_stream_event* timeline;
+  uint64_t timeline_capacity;
+  uint64_t timeline_count;
+} blco_stream_report;
+
+int blco_stream_mttkrp(const blco_layout* layout, uint64_t max_nnz_per_block,
+                       blco_block_source_fn next, void* ctx, const double* const* factors,
+                       uint64_t rank, int mode, const blco_device_budget* budget,
+                       const blco_exec_config* cfg, int strategy, int device, double* out,
+                       blco_stream_report* report);
+
+void blco_set_error(int status, const char* msg);
+
+/* Pinned host memory for stream sources (true async H2D); pageable source
+ * memory is accepted but each of its transfers completes before next(). */
+void* blco_host_alloc_pinned(uint64_t bytes);
+void blco_host_free_pinned(void* p);
+int blco_host_register(void* p, uint64_t bytes);
+int blco_host_unregister(void* p);
+
+/* -------------------------------------------------------------- CP-ALS
+ * cp_als / fit (proj/include/blco/cpals.hpp:38-43).  MTTKRP, Gram, normal
+ * solve and normalisation run on the device; factors_out[m] (host) receives
+ * dims[m] x rank, fit_out[max_iters] the fit history. */
+int blco_cp_als(const blco_tensor* t, uint64_t rank, int max_iters, double tol, uint64_t seed,
+                int strategy, const blco_exec_config* cfg, double* const* factors_out,
+                double* lambda_out, double* fit_out, int* iters_out);
+int blco_fit(const blco_tensor* t, const double* const* factors, const double* lambda,
+             uint64_t rank, const blco_exec_config* cfg, double* fit_out);
+
+/* ----------------------------------------------------------- factories
+ * FactorMatrices::random (proj/src/types.cpp:118-130), SplitMix64; host and
+ * device (d_out[m] device pointers) produce identical bits. */
+int blco_factors_random(const uint64_t* dims, int order, uint64_t rank, uint64_t seed,
+                        double* const* out);
+int blco_factors_random_device(const uint64_t* dims, int order, uint64_t rank, uint64_t seed,
+                               double* const* d_out, void* stream);
+/* Host restatement of the device synthetic generator (small sizes). */
+int blco_synth_uniform_host(int order, const uint64_t* dims, uint64_t nnz, uint64_t seed,
+                            uint64_t* idx, double* vals);
+
+/* ---------------------------------------------------------- multi-GPU
+ * Contiguous, nnz-balanced partition of the batch-table spans (quota
+ * elements each, never straddling blocks) into nparts ranges; part p gets
+ * global elements [begin[p], end[p]). */
+int blco_partition(const uint64_t* block_nnz, uint64_t nblocks, uint64_t quota, int nparts,
+                   uint64_t* begin, uint64_t* end);
+
+/* --------------------------------------------------------- diagnostics */
+int blco_device_count(void);
+/* Number of kernels this library launched since load (tests/bench audit). */
+uint64_t blco_kernel_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

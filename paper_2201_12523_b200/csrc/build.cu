@@ -1,0 +1,598 @@
+// build.cu -- BLCO construction on the device (K1 encode, K2 radix sort,
+// K3 segment/chunk/gather) plus device-tensor management.
+//
+// Reference: build_blco, proj/src/blco_format.cpp:62-134.  The reference
+// linearizes every non-zero to a <=128-bit ALTO index (layout.cpp:71-82),
+// stable-sorts by it (:80-83), groups runs of equal block key rejecting
+// duplicate tuples (:86-106), chunks every run into <= max_nnz_per_block
+// pieces restarting at the run start (:107-110), stores the re-encoded
+// index of each element (:115-126) and builds the batch table (:129-131).
+//
+// Device design:
+//   K1 k_encode   : one thread per element; ALTO (lo, hi) via a constant-memory
+//                   interleave map, re-encoded index via shift/mask.
+//   K2 sort       : CUB onesweep LSD radix sort of the 64-bit low ALTO word
+//                   carrying a 32-bit element id, then (total_bits > 64 only) a
+//                   stable sort of the high word -- LSD stability makes the
+//                   pair sort equal to a 128-bit sort.  Keys are unique unless
+//                   the input has duplicates, so any correct sort reproduces
+//                   std::stable_sort's order.
+//   K3 k_runs     : adjacent compare on the sorted ALTO words -> duplicate
+//                   flag + key-run starts (compacted with CUB select); the
+//                   host chunks the (few) runs; k_gather places idx/values.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_select.cuh>
+#include <thrust/iterator/counting_iterator.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+
+#include "internal.hpp"
+#include "synth.hpp"
+
+namespace b200 {
+
+namespace synth {
+Feistel make_feistel(const uint64_t* dims, int order, uint64_t nnz, uint64_t seed) {
+  unsigned __int128 cells = 1;
+  for (int m = 0; m < order; ++m) cells *= dims[m];
+  if (cells > static_cast<unsigned __int128>(UINT64_MAX))
+    throw_format("synth: cell count exceeds 2^64-1");
+  Feistel f{};
+  f.cells = static_cast<uint64_t>(cells);
+  if (nnz > f.cells) throw_format("synth: more non-zeros than cells");
+  int kb = bits_for_extent(f.cells);
+  if (kb & 1) ++kb;
+  if (kb < 2) kb = 2;
+  f.half = kb / 2;
+  f.mask = (uint64_t{1} << f.half) - 1;
+  for (int r = 0; r < 4; ++r) f.key[r] = mix64(seed + static_cast<uint64_t>(r + 1) * kGolden);
+  return f;
+}
+}  // namespace synth
+
+namespace {
+
+struct EncodeParams {
+  int order;
+  int total_bits;
+  int kept_bits;  // total - stripped
+  uint32_t dims[BLCO_MAX_DEV_ORDER];
+  uint32_t shift[BLCO_MAX_DEV_ORDER];
+  uint64_t mask[BLCO_MAX_DEV_ORDER];
+  uint8_t imap_mode[BLCO_MAX_BITS];
+  uint8_t imap_bit[BLCO_MAX_BITS];
+};
+
+EncodeParams encode_params(const blco_layout& l) {
+  EncodeParams p{};
+  p.order = l.order;
+  p.total_bits = l.total_bits;
+  p.kept_bits = l.total_bits - l.stripped_bits;
+  for (int m = 0; m < l.order; ++m) {
+    p.dims[m] = static_cast<uint32_t>(l.dims[m]);
+    p.shift[m] = static_cast<uint32_t>(l.field_shift[m]);
+    p.mask[m] = l.field_mask[m];
+  }
+  std::memcpy(p.imap_mode, l.imap_mode, sizeof p.imap_mode);
+  std::memcpy(p.imap_bit, l.imap_bit, sizeof p.imap_bit);
+  return p;
+}
+
+constexpr int kThreads = 256;
+
+inline unsigned grid_for(uint64_t n, int per_thread = 1) {
+  uint64_t g = (n + static_cast<uint64_t>(kThreads) * per_thread - 1) /
+               (static_cast<uint64_t>(kThreads) * per_thread);
+  return static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(g, 1u << 30)));
+}
+
+// Host COO (u64, validated here) -> u32 device coordinates.
+__global__ void k_narrow_coords(const uint64_t* __restrict__ in, uint32_t* __restrict__ out,
+                                uint64_t n, uint64_t dim, unsigned* __restrict__ bad) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t c = in[i];
+    if (c >= dim) atomicOr(bad, 1u);
+    out[i] = static_cast<uint32_t>(c);
+  }
+}
+
+__global__ void k_synth(synth::Feistel f, uint64_t seed, int order, uint64_t nnz,
+                        const uint64_t* __restrict__ dims, uint32_t* __restrict__ coords,
+                        double* __restrict__ vals) {
+  for (uint64_t e = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; e < nnz;
+       e += uint64_t(gridDim.x) * blockDim.x) {
+    uint64_t x = f.permute(e);
+    for (int m = 0; m < order; ++m) {
+      const uint64_t d = dims[m];
+      coords[m * nnz + e] = static_cast<uint32_t>(x % d);
+      x /= d;
+    }
+    vals[e] = synth::element_value(seed, e);
+  }
+}
+
+// K1: ALTO words + re-encoded index; perm = element id.
+__global__ void k_encode(EncodeParams p, uint64_t nnz, const uint32_t* __restrict__ coords,
+                         uint64_t* __restrict__ alto_lo, uint64_t* __restrict__ alto_hi,
+                         uint64_t* __restrict__ reenc, uint32_t* __restrict__ perm) {
+  for (uint64_t e = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; e < nnz;
+       e += uint64_t(gridDim.x) * blockDim.x) {
+    uint32_t c[BLCO_MAX_DEV_ORDER];
+    uint64_t r = 0;
+    for (int m = 0; m < p.order; ++m) {
+      c[m] = coords[m * nnz + e];
+      r |= (static_cast<uint64_t>(c[m]) & p.mask[m]) << p.shift[m];
+    }
+    uint64_t lo = 0, hi = 0;
+    const int n_lo = p.total_bits < 64 ? p.total_bits : 64;
+    for (int q = 0; q < n_lo; ++q) lo |= static_cast<uint64_t>((c[p.imap_mode[q]] >> p.imap_bit[q]) & 1u) << q;
+    for (int q = 64; q < p.total_bits; ++q)
+      hi |= static_cast<uint64_t>((c[p.imap_mode[q]] >> p.imap_bit[q]) & 1u) << (q - 64);
+    alto_lo[e] = lo;
+    if (alto_hi) alto_hi[e] = hi;
+    reenc[e] = r;
+    perm[e] = static_cast<uint32_t>(e);
+  }
+}
+
+template <class T>
+__global__ void k_gather(const T* __restrict__ src, const uint32_t* __restrict__ perm,
+                         T* __restrict__ dst, uint64_t n) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    dst[i] = src[perm[i]];
+}
+
+// K3: sorted ALTO (lo[], hi[] in sorted order) -> run-start flags + dup flag.
+__global__ void k_runs(const uint64_t* __restrict__ lo, const uint64_t* __restrict__ hi,
+                       uint64_t n, int kept_bits, int stripped, uint8_t* __restrict__ flag,
+                       unsigned* __restrict__ dup) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    if (i == 0) {
+      flag[0] = 1;
+      continue;
+    }
+    const uint64_t l0 = lo[i - 1], l1 = lo[i];
+    const uint64_t h0 = hi ? hi[i - 1] : 0, h1 = hi ? hi[i] : 0;
+    if (l0 == l1 && h0 == h1) atomicOr(dup, 1u);
+    uint8_t f = 0;
+    if (stripped > 0) {
+      const unsigned __int128 a0 = (static_cast<unsigned __int128>(h0) << 64) | l0;
+      const unsigned __int128 a1 = (static_cast<unsigned __int128>(h1) << 64) | l1;
+      f = static_cast<uint64_t>(a0 >> kept_bits) != static_cast<uint64_t>(a1 >> kept_bits);
+    }
+    flag[i] = f;
+  }
+}
+
+__global__ void k_run_keys(const uint64_t* __restrict__ starts, uint64_t nruns,
+                           const uint64_t* __restrict__ lo, const uint64_t* __restrict__ hi,
+                           int kept_bits, uint64_t* __restrict__ keys) {
+  const uint64_t r = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (r >= nruns) return;
+  const uint64_t i = starts[r];
+  const unsigned __int128 a = (static_cast<unsigned __int128>(hi ? hi[i] : 0) << 64) | lo[i];
+  keys[r] = static_cast<uint64_t>(a >> kept_bits);
+}
+
+__global__ void k_block_base(const uint64_t* __restrict__ keys, uint64_t nblocks, int order,
+                             int kept, int total, const uint8_t* __restrict__ imap_mode,
+                             const uint8_t* __restrict__ imap_bit, const int32_t* __restrict__ rem,
+                             uint32_t* __restrict__ base) {
+  const uint64_t b = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (b >= nblocks) return;
+  uint64_t up[BLCO_MAX_DEV_ORDER] = {};
+  const uint64_t key = keys[b];
+  for (int p = kept; p < total; ++p) {
+    const int m = imap_mode[p];
+    up[m] |= ((key >> (p - kept)) & 1u) << (imap_bit[p] - rem[m]);
+  }
+  for (int m = 0; m < order; ++m) base[b * order + m] = static_cast<uint32_t>(up[m] << rem[m]);
+}
+
+__global__ void k_fill_factors(double* __restrict__ out, uint64_t n, uint64_t first,
+                               uint64_t seed) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    out[i] = synth::factor_value(seed, first + i);
+}
+
+double secs(std::chrono::steady_clock::time_point t0) {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+// Core pipeline: device u32 coords (mode-major) + values -> tensor payload.
+// Consumes (frees) coords/vals.
+void build_from_device_coo(blco_tensor& t, DevBuf<uint32_t>& coords, DevBuf<double>& vals,
+                           uint64_t nnz, blco_build_stats* stats) {
+  const blco_layout& l = t.layout;
+  if (nnz >= (uint64_t{1} << 32))
+    throw_format("b200: device build handles < 2^32 elements per call (got " +
+                 std::to_string(nnz) + ")");
+  t.nnz = nnz;
+  cudaStream_t s = 0;
+  auto t0 = std::chrono::steady_clock::now();
+  if (nnz == 0) {
+    t.keys.clear();
+    t.offsets.assign(1, 0);
+    finalize_tensor(t);
+    if (stats) *stats = blco_build_stats{};
+    return;
+  }
+  const bool wide = l.total_bits > 64;
+  DevBuf<uint64_t> lo(nnz), hi(wide ? nnz : 0), reenc(nnz);
+  DevBuf<uint32_t> perm(nnz);
+  const EncodeParams ep = encode_params(l);
+  k_encode<<<grid_for(nnz, 4), kThreads, 0, s>>>(ep, nnz, coords.ptr, lo.ptr, hi.ptr, reenc.ptr,
+                                                  perm.ptr);
+  count_launch();
+  check_launch("k_encode");
+  coords.reset();
+
+  // K2: LSD radix sort (low word, then high word), payload = element id.
+  DevBuf<uint64_t> keys_out(nnz);
+  DevBuf<uint32_t> perm_out(nnz);
+  size_t tmp_bytes = 0;
+  const int lo_bits = std::max(1, std::min(64, l.total_bits));
+  B200_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, lo.ptr, keys_out.ptr, perm.ptr,
+                                            perm_out.ptr, nnz, 0, lo_bits, s));
+  DevBuf<unsigned char> tmp(tmp_bytes);
+  B200_CUDA(cub::DeviceRadixSort::SortPairs(tmp.ptr, tmp_bytes, lo.ptr, keys_out.ptr, perm.ptr,
+                                            perm_out.ptr, nnz, 0, lo_bits, s));
+  count_launch();
+  // sorted_lo = keys_out, order = perm_out
+  DevBuf<uint64_t> sorted_hi;
+  if (wide) {
+    DevBuf<uint64_t> hi_g(nnz);
+    k_gather<uint64_t><<<grid_for(nnz, 4), kThreads, 0, s>>>(hi.ptr, perm_out.ptr, hi_g.ptr, nnz);
+    count_launch();
+    check_launch("k_gather(hi)");
+    sorted_hi.alloc(nnz);
+    const int hi_bits = l.total_bits - 64;
+    size_t tb2 = 0;
+    B200_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb2, hi_g.ptr, sorted_hi.ptr, perm_out.ptr,
+                                              perm.ptr, nnz, 0, hi_bits, s));
+    if (tb2 > tmp.n) tmp.alloc(tb2);
+    B200_CUDA(cub::DeviceRadixSort::SortPairs(tmp.ptr, tb2, hi_g.ptr, sorted_hi.ptr, perm_out.ptr,
+                                              perm.ptr, nnz, 0, hi_bits, s));
+    count_launch();
+    // final order in perm; re-gather the low word in that order
+    k_gather<uint64_t><<<grid_for(nnz, 4), kThreads, 0, s>>>(lo.ptr, perm.ptr, keys_out.ptr, nnz);
+    count_launch();
+    check_launch("k_gather(lo)");
+    std::swap(perm.ptr, perm_out.ptr);  // perm_out := final order
+  }
+  hi.reset();
+  B200_CUDA(cudaStreamSynchronize(s));
+  if (stats) stats->sort_seconds = secs(t0);
+
+  // K3: key runs, duplicate check.
+  t0 = std::chrono::steady_clock::now();
+  DevBuf<uint8_t> flags(nnz);
+  DevBuf<unsigned> dflag(1);
+  B200_CUDA(cudaMemsetAsync(dflag.ptr, 0, sizeof(unsigned), s));
+  k_runs<<<grid_for(nnz, 4), kThreads, 0, s>>>(keys_out.ptr, wide ? sorted_hi.ptr : nullptr, nnz,
+                                                l.total_bits - l.stripped_bits, l.stripped_bits,
+                                                flags.ptr, dflag.ptr);
+  count_launch();
+  check_launch("k_runs");
+  unsigned dup = 0;
+  B200_CUDA(cudaMemcpyAsync(&dup, dflag.ptr, sizeof dup, cudaMemcpyDeviceToHost, s));
+  B200_CUDA(cudaStreamSynchronize(s));
+  if (dup) throw_format("blco: duplicate coordinate tuple in input");
+
+  DevBuf<uint64_t> run_starts(nnz);
+  DevBuf<uint64_t> nsel(1);
+  size_t sb = 0;
+  thrust::counting_iterator<uint64_t> iota(0);
+  B200_CUDA(cub::DeviceSelect::Flagged(nullptr, sb, iota, flags.ptr, run_starts.ptr, nsel.ptr, nnz, s));
+  if (sb > tmp.n) tmp.alloc(sb);
+  B200_CUDA(cub::DeviceSelect::Flagged(tmp.ptr, sb, iota, flags.ptr, run_starts.ptr, nsel.ptr, nnz, s));
+  count_launch();
+  uint64_t nruns = 0;
+  B200_CUDA(cudaMemcpyAsync(&nruns, nsel.ptr, sizeof nruns, cudaMemcpyDeviceToHost, s));
+  B200_CUDA(cudaStreamSynchronize(s));
+  std::vector<uint64_t> starts(nruns);
+  B200_CUDA(cudaMemcpy(starts.data(), run_starts.ptr, nruns * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  // block key of each run, read off the sorted ALTO words at the run start
+  std::vector<uint64_t> run_keys(nruns, 0);
+  if (l.stripped_bits > 0 && nruns) {
+    DevBuf<uint64_t> dkeys(nruns);
+    k_run_keys<<<grid_for(nruns), kThreads, 0, s>>>(run_starts.ptr, nruns, keys_out.ptr,
+                                                     wide ? sorted_hi.ptr : nullptr,
+                                                     l.total_bits - l.stripped_bits, dkeys.ptr);
+    count_launch();
+    check_launch("k_run_keys");
+    B200_CUDA(cudaMemcpy(run_keys.data(), dkeys.ptr, nruns * 8, cudaMemcpyDeviceToHost));
+  }
+  t.keys.clear();
+  t.offsets.clear();
+  for (uint64_t r = 0; r < nruns; ++r) {
+    const uint64_t b = starts[r], e = r + 1 < nruns ? starts[r + 1] : nnz;
+    for (uint64_t c = b; c < e; c += t.max_nnz_per_block) {
+      t.keys.push_back(run_keys[r]);
+      t.offsets.push_back(c);
+    }
+  }
+  t.offsets.push_back(nnz);
+  if (stats) stats->block_seconds = secs(t0);
+
+  // Re-encoded indices and values in ALTO order.
+  t0 = std::chrono::steady_clock::now();
+  flags.reset();
+  keys_out.reset();
+  sorted_hi.reset();
+  t.idx.alloc(nnz);
+  t.vals.alloc(nnz);
+  k_gather<uint64_t><<<grid_for(nnz, 4), kThreads, 0, s>>>(reenc.ptr, perm_out.ptr, t.idx.ptr, nnz);
+  k_gather<double><<<grid_for(nnz, 4), kThreads, 0, s>>>(vals.ptr, perm_out.ptr, t.vals.ptr, nnz);
+  count_launch(2);
+  check_launch("k_gather(payload)");
+  B200_CUDA(cudaStreamSynchronize(s));
+  if (stats) stats->reencode_seconds = secs(t0);
+
+  t0 = std::chrono::steady_clock::now();
+  finalize_tensor(t);
+  if (stats) stats->batch_seconds = secs(t0);
+}
+
+blco_tensor* new_tensor(const uint64_t* dims, int order, int target_bits, uint64_t max_nnz,
+                        int device) {
+  if (max_nnz < 1) throw_format("blco: max_nnz_per_block must be >= 1");
+  auto* t = new blco_tensor;
+  t->layout = make_layout(dims, order, target_bits);
+  t->device = device;
+  t->max_nnz_per_block = max_nnz;
+  try {
+    check_device_layout(t->layout);
+  } catch (...) {
+    delete t;
+    throw;
+  }
+  return t;
+}
+
+}  // namespace
+
+void finalize_tensor(blco_tensor& t) {
+  const blco_layout& l = t.layout;
+  const uint64_t nb = t.nblocks();
+  t.block_base.alloc(std::max<uint64_t>(1, nb * l.order));
+  if (nb) {
+    DevBuf<uint64_t> dkeys(nb);
+    DevBuf<uint8_t> dmode(BLCO_MAX_BITS), dbit(BLCO_MAX_BITS);
+    DevBuf<int32_t> drem(BLCO_MAX_ORDER);
+    B200_CUDA(cudaMemcpy(dkeys.ptr, t.keys.data(), nb * 8, cudaMemcpyHostToDevice));
+    B200_CUDA(cudaMemcpy(dmode.ptr, l.imap_mode, BLCO_MAX_BITS, cudaMemcpyHostToDevice));
+    B200_CUDA(cudaMemcpy(dbit.ptr, l.imap_bit, BLCO_MAX_BITS, cudaMemcpyHostToDevice));
+    B200_CUDA(cudaMemcpy(drem.ptr, l.rem_bits, sizeof(int32_t) * BLCO_MAX_ORDER, cudaMemcpyHostToDevice));
+    k_block_base<<<static_cast<unsigned>((nb + 127) / 128), 128>>>(
+        dkeys.ptr, nb, l.order, l.total_bits - l.stripped_bits, l.total_bits, dmode.ptr, dbit.ptr,
+        drem.ptr, t.block_base.ptr);
+    count_launch();
+    check_launch("k_block_base");
+    B200_CUDA(cudaDeviceSynchronize());
+  }
+  std::lock_guard<std::mutex> g(t.mu);
+  t.tiles.clear();
+}
+
+const TileDesc* tile_table(const blco_tensor& t, uint32_t tile_elems, uint64_t* ntiles) {
+  std::lock_guard<std::mutex> g(t.mu);
+  auto it = t.tiles.find(tile_elems);
+  if (it == t.tiles.end()) {
+    std::vector<TileDesc> h;
+    for (uint64_t b = 0; b < t.nblocks(); ++b)
+      for (uint64_t off = t.offsets[b]; off < t.offsets[b + 1]; off += tile_elems)
+        h.push_back(TileDesc{off, static_cast<uint32_t>(std::min<uint64_t>(tile_elems, t.offsets[b + 1] - off)),
+                             static_cast<uint32_t>(b)});
+    DevBuf<TileDesc> d(h.size());
+    if (!h.empty())
+      B200_CUDA(cudaMemcpy(d.ptr, h.data(), h.size() * sizeof(TileDesc), cudaMemcpyHostToDevice));
+    it = t.tiles.emplace(tile_elems, std::move(d)).first;
+  }
+  *ntiles = it->second.n;
+  return it->second.ptr;
+}
+
+}  // namespace b200
+
+using namespace b200;
+
+extern "C" {
+
+int blco_build(const uint64_t* dims, int order, uint64_t nnz, const uint64_t* idx,
+               const double* vals, int target_bits, uint64_t max_nnz, int device,
+               blco_tensor** out, blco_build_stats* stats) {
+  *out = nullptr;
+  return guarded([&] {
+    DeviceGuard dg(device);
+    blco_tensor* t = new_tensor(dims, order, target_bits, max_nnz, device);
+    try {
+      DevBuf<uint32_t> coords(static_cast<size_t>(nnz) * order);
+      DevBuf<double> dv(nnz);
+      DevBuf<unsigned> bad(1);
+      B200_CUDA(cudaMemset(bad.ptr, 0, sizeof(unsigned)));
+      if (nnz) {
+        // stage one mode at a time through a u64 buffer
+        DevBuf<uint64_t> stage(nnz);
+        for (int m = 0; m < order; ++m) {
+          B200_CUDA(cudaMemcpy(stage.ptr, idx + static_cast<uint64_t>(m) * nnz, nnz * 8,
+                               cudaMemcpyHostToDevice));
+          k_narrow_coords<<<grid_for(nnz, 4), kThreads>>>(stage.ptr, coords.ptr + static_cast<uint64_t>(m) * nnz,
+                                                          nnz, dims[m], bad.ptr);
+          count_launch();
+          check_launch("k_narrow_coords");
+        }
+        B200_CUDA(cudaMemcpy(dv.ptr, vals, nnz * 8, cudaMemcpyHostToDevice));
+      }
+      unsigned b = 0;
+      B200_CUDA(cudaMemcpy(&b, bad.ptr, sizeof b, cudaMemcpyDeviceToHost));
+      if (b) throw_format("coo: coordinate out of range");
+      build_from_device_coo(*t, coords, dv, nnz, stats);
+    } catch (...) {
+      delete t;
+      throw;
+    }
+    *out = t;
+  });
+}
+
+int blco_build_synthetic(const uint64_t* dims, int order, uint64_t nnz, uint64_t seed,
+                         int target_bits, uint64_t max_nnz, int device, blco_tensor** out,
+                         blco_build_stats* stats) {
+  *out = nullptr;
+  return guarded([&] {
+    DeviceGuard dg(device);
+    blco_tensor* t = new_tensor(dims, order, target_bits, max_nnz, device);
+    try {
+      const synth::Feistel f = synth::make_feistel(dims, order, nnz, seed);
+      DevBuf<uint32_t> coords(static_cast<size_t>(nnz) * order);
+      DevBuf<double> dv(nnz);
+      DevBuf<uint64_t> ddims(order);
+      B200_CUDA(cudaMemcpy(ddims.ptr, dims, order * 8, cudaMemcpyHostToDevice));
+      if (nnz) {
+        k_synth<<<grid_for(nnz, 2), kThreads>>>(f, seed, order, nnz, ddims.ptr, coords.ptr, dv.ptr);
+        count_launch();
+        check_launch("k_synth");
+      }
+      build_from_device_coo(*t, coords, dv, nnz, stats);
+    } catch (...) {
+      delete t;
+      throw;
+    }
+    *out = t;
+  });
+}
+
+int blco_tensor_upload(const blco_layout* layout, uint64_t max_nnz, uint64_t nblocks,
+                       const uint64_t* keys, const uint64_t* block_nnz, const uint64_t* const* idx,
+                       const double* const* vals, int device, blco_tensor** out) {
+  *out = nullptr;
+  return guarded([&] {
+    DeviceGuard dg(device);
+    blco_tensor* t = new_tensor(layout->dims, layout->order, layout->target_bits,
+                                std::max<uint64_t>(1, max_nnz), device);
+    try {
+      uint64_t total = 0;
+      for (uint64_t b = 0; b < nblocks; ++b) {
+        t->keys.push_back(keys[b]);
+        t->offsets.push_back(total);
+        total += block_nnz[b];
+      }
+      t->offsets.push_back(total);
+      t->nnz = total;
+      t->idx.alloc(total);
+      t->vals.alloc(total);
+      for (uint64_t b = 0; b < nblocks; ++b) {
+        if (!block_nnz[b]) continue;
+        B200_CUDA(cudaMemcpy(t->idx.ptr + t->offsets[b], idx[b], block_nnz[b] * 8, cudaMemcpyHostToDevice));
+        B200_CUDA(cudaMemcpy(t->vals.ptr + t->offsets[b], vals[b], block_nnz[b] * 8, cudaMemcpyHostToDevice));
+      }
+      finalize_tensor(*t);
+    } catch (...) {
+      delete t;
+      throw;
+    }
+    *out = t;
+  });
+}
+
+int blco_tensor_slice(const blco_tensor* src, uint64_t begin, uint64_t end, int device,
+                      blco_tensor** out) {
+  *out = nullptr;
+  return guarded([&] {
+    if (begin > end || end > src->nnz) throw_format("slice: element range out of bounds");
+    DeviceGuard dg(device);
+    blco_tensor* t = new_tensor(src->layout.dims, src->layout.order, src->layout.target_bits,
+                                src->max_nnz_per_block, device);
+    try {
+      for (uint64_t b = 0; b < src->nblocks(); ++b) {
+        const uint64_t lo = std::max(begin, src->offsets[b]), hi = std::min(end, src->offsets[b + 1]);
+        if (lo >= hi) continue;
+        t->keys.push_back(src->keys[b]);
+        t->offsets.push_back(lo - begin);
+      }
+      t->offsets.push_back(end - begin);
+      t->nnz = end - begin;
+      t->idx.alloc(t->nnz);
+      t->vals.alloc(t->nnz);
+      if (t->nnz) {
+        B200_CUDA(cudaMemcpyPeer(t->idx.ptr, device, src->idx.ptr + begin, src->device, t->nnz * 8));
+        B200_CUDA(cudaMemcpyPeer(t->vals.ptr, device, src->vals.ptr + begin, src->device, t->nnz * 8));
+      }
+      finalize_tensor(*t);
+    } catch (...) {
+      delete t;
+      throw;
+    }
+    *out = t;
+  });
+}
+
+int blco_tensor_info(const blco_tensor* t, blco_layout* layout, uint64_t* nblocks, uint64_t* nnz,
+                     uint64_t* max_nnz) {
+  return guarded([&] {
+    if (layout) *layout = t->layout;
+    if (nblocks) *nblocks = t->nblocks();
+    if (nnz) *nnz = t->nnz;
+    if (max_nnz) *max_nnz = t->max_nnz_per_block;
+  });
+}
+
+int blco_tensor_blocks(const blco_tensor* t, uint64_t* keys, uint64_t* block_nnz) {
+  return guarded([&] {
+    for (uint64_t b = 0; b < t->nblocks(); ++b) {
+      if (keys) keys[b] = t->keys[b];
+      if (block_nnz) block_nnz[b] = t->offsets[b + 1] - t->offsets[b];
+    }
+  });
+}
+
+int blco_tensor_download(const blco_tensor* t, uint64_t* idx, double* vals) {
+  return guarded([&] {
+    DeviceGuard dg(t->device);
+    if (!t->nnz) return;
+    if (idx) B200_CUDA(cudaMemcpy(idx, t->idx.ptr, t->nnz * 8, cudaMemcpyDeviceToHost));
+    if (vals) B200_CUDA(cudaMemcpy(vals, t->vals.ptr, t->nnz * 8, cudaMemcpyDeviceToHost));
+  });
+}
+
+int blco_tensor_device_ptrs(const blco_tensor* t, const uint64_t** idx, const double** vals) {
+  return guarded([&] {
+    *idx = t->idx.ptr;
+    *vals = t->vals.ptr;
+  });
+}
+
+void blco_tensor_free(blco_tensor* t) {
+  if (!t) return;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(t->device);
+  delete t;
+  cudaSetDevice(prev);
+}
+
+int blco_factors_random_device(const uint64_t* dims, int order, uint64_t rank, uint64_t seed,
+                               double* const* d_out, void* stream) {
+  return guarded([&] {
+    if (rank < 1) throw_format("factors: rank must be >= 1");
+    uint64_t first = 0;
+    for (int m = 0; m < order; ++m) {
+      const uint64_t n = dims[m] * rank;
+      if (n) {
+        k_fill_factors<<<grid_for(n, 4), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(d_out[m], n, first, seed);
+        count_launch();
+        check_launch("k_fill_factors");
+      }
+      first += n;
+    }
+  });
+}
+
+}  // extern "C"

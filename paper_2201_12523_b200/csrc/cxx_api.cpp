@@ -1,0 +1,579 @@
+// cxx_api.cpp -- the reference's C++ API (include/blco/b200.hpp) implemented
+// over the C ABI (include/blco_b200.h).  Host-side data stays in the
+// reference's std::vector containers; every compute call goes to the device.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <numeric>
+#include <thread>
+
+#include <cuda_runtime.h>
+
+#include "blco/b200.hpp"
+#include "blco_b200.h"
+
+namespace blco {
+
+namespace {
+
+[[noreturn]] void rethrow(int status) {
+  const std::string msg = blco_last_error();
+  switch (status) {
+    case BLCO_EFORMAT: throw FormatError(msg);
+    case BLCO_EIO: throw IoError(msg);
+    case BLCO_EVERIFY: throw VerifyError(msg);
+    default: throw Error(msg);
+  }
+}
+
+inline void ck(int status) {
+  if (status != BLCO_OK) rethrow(status);
+}
+
+int current_device() {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess) throw Error("cuda: no device available");
+  return d;
+}
+
+blco_layout to_c(const BitLayout& l) {
+  blco_layout c;
+  ck(blco_make_layout(l.dims.data(), l.order(), l.target_bits, &c));
+  return c;
+}
+
+BitLayout from_c(const blco_layout& c) {
+  BitLayout l;
+  l.dims.assign(c.dims, c.dims + c.order);
+  l.mode_bits.assign(c.mode_bits, c.mode_bits + c.order);
+  l.total_bits = c.total_bits;
+  l.target_bits = c.target_bits;
+  l.stripped_bits = c.stripped_bits;
+  l.rem_bits.assign(c.rem_bits, c.rem_bits + c.order);
+  l.field_shift.assign(c.field_shift, c.field_shift + c.order);
+  l.field_mask.assign(c.field_mask, c.field_mask + c.order);
+  l.mode_positions.assign(c.order, {});
+  for (int m = 0; m < c.order; ++m) l.mode_positions[m].resize(c.mode_bits[m]);
+  l.key_slices.assign(c.order, {});
+  const int kept = c.total_bits - c.stripped_bits;
+  for (int p = 0; p < c.total_bits; ++p) {
+    const int m = c.imap_mode[p], k = c.imap_bit[p];
+    l.interleave_map.emplace_back(m, k);
+    l.mode_positions[m][k] = p;
+    if (p >= kept) l.key_slices[m].emplace_back(p - kept, k - c.rem_bits[m]);
+  }
+  return l;
+}
+
+blco_exec_config to_c(const ExecConfig& e) {
+  return blco_exec_config{e.workgroup_size,    e.tile_size,        e.coarsening,
+                          e.num_compute_units, e.num_factor_copies, e.stash_slots,
+                          e.deterministic ? 1 : 0, e.num_threads};
+}
+
+std::vector<const double*> factor_ptrs(const FactorMatrices& f) {
+  std::vector<const double*> p;
+  for (const auto& a : f.factors) p.push_back(a.data.data());
+  return p;
+}
+
+// ---- device cache for host BlcoTensors
+struct Fingerprint {
+  const void* first = nullptr;
+  const void* last = nullptr;
+  std::uint64_t nnz = 0, nblocks = 0;
+  int device = -1;
+  bool operator==(const Fingerprint&) const = default;
+};
+
+struct CacheEntry {
+  Fingerprint fp;
+  blco_tensor* dev = nullptr;
+};
+
+std::mutex g_cache_mu;
+std::map<const BlcoTensor*, CacheEntry> g_cache;
+
+Fingerprint fingerprint(const BlcoTensor& t, int device) {
+  Fingerprint f;
+  f.nnz = t.total_nnz;
+  f.nblocks = t.blocks.size();
+  f.device = device;
+  if (!t.blocks.empty()) {
+    f.first = t.blocks.front().linear_indices.data();
+    f.last = t.blocks.back().values.data();
+  }
+  return f;
+}
+
+const blco_tensor* device_tensor(const BlcoTensor& t) {
+  const int dev = current_device();
+  const Fingerprint fp = fingerprint(t, dev);
+  std::lock_guard<std::mutex> g(g_cache_mu);
+  auto it = g_cache.find(&t);
+  if (it != g_cache.end() && it->second.fp == fp) return it->second.dev;
+  if (it != g_cache.end()) {
+    blco_tensor_free(it->second.dev);
+    g_cache.erase(it);
+  }
+  const blco_layout l = to_c(t.layout);
+  std::vector<std::uint64_t> keys, nnz;
+  std::vector<const std::uint64_t*> idx;
+  std::vector<const double*> vals;
+  for (const auto& b : t.blocks) {
+    if (b.linear_indices.size() != b.values.size())
+      throw FormatError("blco: block index/value arrays have mismatched lengths");
+    keys.push_back(b.key);
+    nnz.push_back(b.nnz());
+    idx.push_back(b.linear_indices.data());
+    vals.push_back(b.values.data());
+  }
+  blco_tensor* d = nullptr;
+  ck(blco_tensor_upload(&l, t.max_nnz_per_block, keys.size(), keys.data(), nnz.data(), idx.data(),
+                        vals.data(), dev, &d));
+  g_cache[&t] = CacheEntry{fp, d};
+  return d;
+}
+
+}  // namespace
+
+void release_device_cache(const BlcoTensor* t) {
+  std::lock_guard<std::mutex> g(g_cache_mu);
+  for (auto it = g_cache.begin(); it != g_cache.end();) {
+    if (!t || it->first == t) {
+      blco_tensor_free(it->second.dev);
+      it = g_cache.erase(it);
+    } else {
+      ++it;
+    }
+  }
+}
+
+// ------------------------------------------------------------------- types
+bool DenseMatrix::all_finite() const {
+  return std::all_of(data.begin(), data.end(), [](double v) { return std::isfinite(v); });
+}
+
+void SparseTensorCoo::validate(bool check_duplicates) const {
+  if (static_cast<std::size_t>(order()) != indices.size())
+    throw FormatError("coo: index array count does not match order");
+  for (int m = 0; m < order(); ++m) {
+    if (dims[m] < 1) throw FormatError("coo: mode length must be >= 1");
+    if (indices[m].size() != values.size())
+      throw FormatError("coo: index/value arrays have mismatched lengths");
+    if (std::any_of(indices[m].begin(), indices[m].end(), [&](index_t i) { return i >= dims[m]; }))
+      throw FormatError("coo: coordinate out of range");
+  }
+  if (!check_duplicates || nnz() < 2) return;
+  std::vector<std::size_t> p(nnz());
+  std::iota(p.begin(), p.end(), 0);
+  auto lex = [&](std::size_t a, std::size_t b) {
+    for (int m = 0; m < order(); ++m)
+      if (indices[m][a] != indices[m][b]) return indices[m][a] < indices[m][b];
+    return false;
+  };
+  std::sort(p.begin(), p.end(), lex);
+  for (std::size_t e = 1; e < p.size(); ++e)
+    if (!lex(p[e - 1], p[e])) throw FormatError("coo: duplicate coordinate tuple");
+}
+
+SparseTensorCoo SparseTensorCoo::from_arrays(std::vector<index_t> dims,
+                                             std::vector<std::vector<index_t>> indices,
+                                             std::vector<double> values) {
+  const int n = static_cast<int>(indices.size());
+  if (n == 0) throw FormatError("coo: at least one mode required");
+  for (const auto& v : indices)
+    if (v.size() != values.size()) throw FormatError("coo: index/value arrays have mismatched lengths");
+  if (dims.empty()) {
+    dims.assign(n, 1);
+    for (int m = 0; m < n; ++m)
+      for (index_t i : indices[m]) dims[m] = std::max(dims[m], i + 1);
+  }
+  // lexicographic stable order, equal tuples summed in input order
+  std::vector<std::size_t> p(values.size());
+  std::iota(p.begin(), p.end(), 0);
+  auto lex = [&](std::size_t a, std::size_t b) {
+    for (int m = 0; m < n; ++m)
+      if (indices[m][a] != indices[m][b]) return indices[m][a] < indices[m][b];
+    return false;
+  };
+  std::stable_sort(p.begin(), p.end(), lex);
+  SparseTensorCoo out;
+  out.dims = std::move(dims);
+  out.indices.assign(n, {});
+  for (std::size_t e = 0; e < p.size();) {
+    std::size_t f = e + 1;
+    double sum = values[p[e]];
+    while (f < p.size() && !lex(p[e], p[f]) && !lex(p[f], p[e])) sum += values[p[f++]];
+    for (int m = 0; m < n; ++m) out.indices[m].push_back(indices[m][p[e]]);
+    out.values.push_back(sum);
+    e = f;
+  }
+  out.validate();
+  return out;
+}
+
+double SparseTensorCoo::norm_squared() const {
+  double s = 0.0;
+  for (double v : values) s += v * v;
+  return s;
+}
+
+void FactorMatrices::validate(std::span<const index_t> dims) const {
+  if (factors.size() != dims.size()) throw FormatError("factors: mode count does not match tensor order");
+  for (std::size_t m = 0; m < factors.size(); ++m) {
+    const DenseMatrix& a = factors[m];
+    if (a.rows != dims[m] || a.cols != rank)
+      throw FormatError("factors: mode " + std::to_string(m + 1) + " has shape " +
+                        std::to_string(a.rows) + "x" + std::to_string(a.cols) + ", expected " +
+                        std::to_string(dims[m]) + "x" + std::to_string(rank));
+    if (a.data.size() != a.rows * a.cols) throw FormatError("factors: malformed matrix storage");
+  }
+}
+
+FactorMatrices FactorMatrices::random(std::span<const index_t> dims, std::size_t rank,
+                                      std::uint64_t seed) {
+  if (rank < 1) throw FormatError("factors: rank must be >= 1");
+  FactorMatrices f;
+  f.rank = rank;
+  std::vector<double*> p;
+  for (index_t d : dims) f.factors.emplace_back(d, rank);
+  for (auto& a : f.factors) p.push_back(a.data.data());
+  ck(blco_factors_random(dims.data(), static_cast<int>(dims.size()), rank, seed, p.data()));
+  return f;
+}
+
+FactorMatrices FactorMatrices::ones(std::span<const index_t> dims, std::size_t rank) {
+  FactorMatrices f;
+  f.rank = rank;
+  for (index_t d : dims) {
+    DenseMatrix a(d, rank);
+    std::fill(a.data.begin(), a.data.end(), 1.0);
+    f.factors.push_back(std::move(a));
+  }
+  return f;
+}
+
+// ------------------------------------------------------------------ layout
+std::vector<index_t> BitLayout::block_base(index_t packed_key) const {
+  std::vector<index_t> base(dims.size());
+  for (int m = 0; m < order(); ++m) base[m] = key_upper(m, packed_key) << rem_bits[m];
+  return base;
+}
+
+BitLayout make_layout(std::span<const index_t> dims, int target_bits) {
+  blco_layout c;
+  ck(blco_make_layout(dims.data(), static_cast<int>(dims.size()), target_bits, &c));
+  return from_c(c);
+}
+
+alto_t linearize(const BitLayout& layout, std::span<const index_t> coords) {
+  if (coords.size() != layout.dims.size())
+    throw FormatError("linearize: coordinate count does not match order");
+  const blco_layout c = to_c(layout);
+  std::uint64_t hi = 0, lo = 0;
+  ck(blco_linearize(&c, coords.data(), &hi, &lo));
+  return (static_cast<alto_t>(hi) << 64) | lo;
+}
+
+SplitIndex split_block_key(const BitLayout& layout, alto_t alto) {
+  const blco_layout c = to_c(layout);
+  SplitIndex s;
+  ck(blco_split_block_key(&c, static_cast<std::uint64_t>(alto >> 64), static_cast<std::uint64_t>(alto),
+                          &s.block_key, &s.reencoded));
+  return s;
+}
+
+SplitIndex encode_coords(const BitLayout& layout, std::span<const index_t> coords) {
+  const blco_layout c = to_c(layout);
+  SplitIndex s;
+  ck(blco_encode_coords(&c, coords.data(), &s.block_key, &s.reencoded));
+  return s;
+}
+
+void delinearize(const BitLayout& layout, index_t reencoded, index_t block_key,
+                 std::span<index_t> coords_out) {
+  const blco_layout c = to_c(layout);
+  ck(blco_delinearize(&c, reencoded, block_key, coords_out.data()));
+}
+
+alto_t interleaved_remainder(const BitLayout& layout, index_t reencoded) {
+  const blco_layout c = to_c(layout);
+  std::uint64_t hi = 0, lo = 0;
+  ck(blco_interleaved_remainder(&c, reencoded, &hi, &lo));
+  return (static_cast<alto_t>(hi) << 64) | lo;
+}
+
+// ------------------------------------------------------------------- build
+bool BlcoTensor::structurally_equal(const BlcoTensor& o) const {
+  if (layout.dims != o.layout.dims || layout.target_bits != o.layout.target_bits ||
+      max_nnz_per_block != o.max_nnz_per_block || total_nnz != o.total_nnz ||
+      blocks.size() != o.blocks.size())
+    return false;
+  for (std::size_t b = 0; b < blocks.size(); ++b) {
+    const BlcoBlock &x = blocks[b], &y = o.blocks[b];
+    if (x.key != y.key || x.linear_indices != y.linear_indices || x.values != y.values) return false;
+  }
+  return true;
+}
+
+std::vector<BatchSpan> compute_batch_table(const BlcoTensor& t, std::uint64_t quota) {
+  if (quota < 1) throw FormatError("blco: elements_per_workgroup must be >= 1");
+  std::vector<std::uint64_t> nnz;
+  for (const auto& b : t.blocks) nnz.push_back(b.nnz());
+  const std::uint64_t n = blco_batch_table(nnz.data(), nnz.size(), quota, nullptr);
+  std::vector<std::uint64_t> raw(3 * n);
+  blco_batch_table(nnz.data(), nnz.size(), quota, raw.data());
+  std::vector<BatchSpan> spans(n);
+  for (std::uint64_t i = 0; i < n; ++i) spans[i] = BatchSpan{raw[3 * i], raw[3 * i + 1], raw[3 * i + 2]};
+  return spans;
+}
+
+BlcoTensor build_blco(const SparseTensorCoo& coo, int target_bits, std::uint64_t max_nnz,
+                      BuildStats* stats) {
+  coo.validate();
+  if (max_nnz < 1) throw FormatError("blco: max_nnz_per_block must be >= 1");
+  const std::size_t nnz = coo.nnz();
+  std::vector<std::uint64_t> flat(static_cast<std::size_t>(coo.order()) * nnz);
+  for (int m = 0; m < coo.order(); ++m)
+    std::copy(coo.indices[m].begin(), coo.indices[m].end(), flat.begin() + m * nnz);
+  blco_tensor* d = nullptr;
+  blco_build_stats bs{};
+  ck(blco_build(coo.dims.data(), coo.order(), nnz, flat.data(), coo.values.data(), target_bits,
+                max_nnz, current_device(), &d, &bs));
+  std::unique_ptr<blco_tensor, void (*)(blco_tensor*)> guard(d, blco_tensor_free);
+  blco_layout c;
+  std::uint64_t nb = 0, total = 0, mx = 0;
+  ck(blco_tensor_info(d, &c, &nb, &total, &mx));
+  std::vector<std::uint64_t> keys(nb), bn(nb), idx(total);
+  std::vector<double> vals(total);
+  ck(blco_tensor_blocks(d, keys.data(), bn.data()));
+  ck(blco_tensor_download(d, idx.data(), vals.data()));
+  BlcoTensor t;
+  t.layout = from_c(c);
+  t.max_nnz_per_block = max_nnz;
+  t.total_nnz = total;
+  std::uint64_t off = 0;
+  for (std::uint64_t b = 0; b < nb; ++b) {
+    BlcoBlock blk;
+    blk.key = keys[b];
+    blk.linear_indices.assign(idx.begin() + off, idx.begin() + off + bn[b]);
+    blk.values.assign(vals.begin() + off, vals.begin() + off + bn[b]);
+    off += bn[b];
+    t.blocks.push_back(std::move(blk));
+  }
+  t.batch_quota = kDefaultBatchQuota;
+  t.batch_table = compute_batch_table(t, t.batch_quota);
+  if (stats) *stats = BuildStats{bs.sort_seconds, bs.block_seconds, bs.reencode_seconds, bs.batch_seconds};
+  return t;
+}
+
+SparseTensorCoo delinearize_all(const BlcoTensor& t) {
+  SparseTensorCoo coo;
+  coo.dims = t.dims();
+  coo.indices.assign(t.order(), {});
+  std::vector<index_t> c(t.order());
+  for (const auto& b : t.blocks)
+    for (std::size_t e = 0; e < b.nnz(); ++e) {
+      delinearize(t.layout, b.linear_indices[e], b.key, c);
+      for (int m = 0; m < t.order(); ++m) coo.indices[m].push_back(c[m]);
+      coo.values.push_back(b.values[e]);
+    }
+  return coo;
+}
+
+// ------------------------------------------------------------------ config
+void ExecConfig::validate() const {
+  const blco_exec_config c = to_c(*this);
+  ck(blco_exec_config_validate(&c));
+}
+
+int ExecConfig::host_threads() const {
+  if (num_threads > 0) return num_threads;
+  const unsigned hw = std::thread::hardware_concurrency();
+  return hw ? static_cast<int>(hw) : 1;
+}
+
+const char* strategy_name(Strategy s) {
+  switch (s) {
+    case Strategy::Auto: return "auto";
+    case Strategy::Register: return "register";
+    case Strategy::Hierarchical: return "hierarchical";
+  }
+  return "?";
+}
+
+Strategy choose_strategy(index_t len, const ExecConfig& config) {
+  const blco_exec_config c = to_c(config);
+  return blco_choose_strategy(len, &c) == BLCO_STRATEGY_HIERARCHICAL ? Strategy::Hierarchical
+                                                                     : Strategy::Register;
+}
+
+// ------------------------------------------------------------------ mttkrp
+DenseMatrix merge_copies(std::span<const DenseMatrix> copies) {
+  if (copies.empty()) throw FormatError("merge_copies: no copies");
+  std::vector<const double*> p;
+  for (const auto& c : copies) {
+    if (!c.same_shape(copies[0])) throw FormatError("merge_copies: shape mismatch");
+    p.push_back(c.data.data());
+  }
+  DenseMatrix m(copies[0].rows, copies[0].cols);
+  ck(blco_merge_copies(p.data(), p.size(), m.data.size(), m.data.data()));
+  return m;
+}
+
+DenseMatrix mttkrp(const BlcoTensor& t, const FactorMatrices& f, int mode, const ExecConfig& config,
+                   Strategy strategy, MttkrpStats* stats) {
+  config.validate();
+  f.validate(t.dims());
+  if (mode < 0 || mode >= t.order())
+    throw FormatError("mttkrp: mode " + std::to_string(mode + 1) + " out of range for order " +
+                      std::to_string(t.order()));
+  const blco_tensor* d = device_tensor(t);
+  const auto ptrs = factor_ptrs(f);
+  const blco_exec_config c = to_c(config);
+  DenseMatrix m(t.dims()[mode], f.rank);
+  blco_mttkrp_stats s{};
+  ck(blco_mttkrp(d, ptrs.data(), f.rank, mode, static_cast<int>(strategy), &c, m.data.data(),
+                 stats ? &s : nullptr));
+  if (stats) {
+    stats->strategy = s.strategy == BLCO_STRATEGY_HIERARCHICAL ? Strategy::Hierarchical : Strategy::Register;
+    stats->workgroups = s.workgroups;
+    stats->segments = s.segments;
+    stats->stash_flushes = s.stash_flushes;
+    stats->commit_events = s.commit_events;
+    stats->scalar_adds = s.scalar_adds;
+  }
+  return m;
+}
+
+// --------------------------------------------------------------- streaming
+bool MemoryBlockSource::next(BlcoBlock& out) {
+  if (cursor_ >= t_->blocks.size()) return false;
+  out = t_->blocks[cursor_++];
+  return true;
+}
+
+const BlcoBlock* MemoryBlockSource::next_view() {
+  if (cursor_ >= t_->blocks.size()) return nullptr;
+  return &t_->blocks[cursor_++];
+}
+
+ThroughputSummary throughput_report(const StreamReport& r) { return {r.overall_gbps, r.compute_gbps}; }
+
+namespace {
+struct SourceCtx {
+  BlockSource* src;
+  MemoryBlockSource* mem;
+  BlcoBlock scratch;
+  std::exception_ptr error;
+};
+
+int pull(void* ctx, blco_block_view* out) {
+  auto* c = static_cast<SourceCtx*>(ctx);
+  try {
+    const BlcoBlock* b = nullptr;
+    if (c->mem) {
+      b = c->mem->next_view();
+    } else if (c->src->next(c->scratch)) {
+      b = &c->scratch;
+    }
+    if (!b) return 0;
+    if (b->linear_indices.size() != b->values.size()) throw FormatError("stream: malformed block");
+    *out = blco_block_view{b->key, b->nnz(), b->linear_indices.data(), b->values.data()};
+    return 1;
+  } catch (...) {
+    c->error = std::current_exception();
+    blco_set_error(BLCO_ERROR, "stream: block source failed");
+    return -BLCO_ERROR;
+  }
+}
+}  // namespace
+
+DenseMatrix stream_mttkrp(BlockSource& source, const FactorMatrices& f, int mode,
+                          const DeviceBudget& budget, const ExecConfig& config, Strategy strategy,
+                          StreamReport* report) {
+  config.validate();
+  const BitLayout& layout = source.layout();
+  f.validate(layout.dims);
+  if (mode < 0 || mode >= layout.order()) throw FormatError("stream: mode out of range");
+  const blco_layout l = to_c(layout);
+  const blco_exec_config c = to_c(config);
+  const blco_device_budget b{budget.capacity_bytes, budget.num_queues, budget.reservation_bytes,
+                             budget.injected_transfer_latency_s};
+  SourceCtx ctx{&source, dynamic_cast<MemoryBlockSource*>(&source), {}, nullptr};
+  const auto ptrs = factor_ptrs(f);
+  DenseMatrix m(layout.dims[mode], f.rank);
+  const std::uint64_t nb = source.block_count();
+  std::vector<int32_t> bq(nb);
+  std::vector<blco_stream_event> tl(2 * nb);
+  blco_stream_report r{};
+  r.block_queue = bq.data();
+  r.block_queue_capacity = nb;
+  r.timeline = tl.data();
+  r.timeline_capacity = tl.size();
+  const int status = blco_stream_mttkrp(&l, source.max_nnz_per_block(), pull, &ctx, ptrs.data(),
+                                        f.rank, mode, &b, &c, static_cast<int>(strategy),
+                                        current_device(), m.data.data(), &r);
+  if (ctx.error) std::rethrow_exception(ctx.error);
+  ck(status);
+  if (report) {
+    report->blocks = r.blocks;
+    report->bytes_streamed = r.bytes_streamed;
+    report->total_seconds = r.total_seconds;
+    report->transfer_busy_seconds = r.transfer_busy_seconds;
+    report->compute_busy_seconds = r.compute_busy_seconds;
+    report->overall_gbps = r.overall_gbps;
+    report->compute_gbps = r.compute_gbps;
+    report->peak_resident_bytes = r.peak_resident_bytes;
+    report->block_queue.assign(bq.begin(), bq.begin() + std::min<std::uint64_t>(nb, r.blocks));
+    report->timeline.clear();
+    for (std::uint64_t i = 0; i < std::min<std::uint64_t>(r.timeline_count, tl.size()); ++i)
+      report->timeline.push_back(StreamEvent{tl[i].kind == 0 ? StreamEvent::Kind::Transfer
+                                                              : StreamEvent::Kind::Compute,
+                                             tl[i].queue, tl[i].block, tl[i].begin_s, tl[i].end_s});
+  }
+  return m;
+}
+
+// ------------------------------------------------------------------- cp-als
+CpModel cp_als(const BlcoTensor& t, const CpAlsOptions& opts, const ExecConfig& config) {
+  if (opts.rank < 1) throw FormatError("cp_als: rank must be >= 1");
+  if (opts.max_iters < 0) throw FormatError("cp_als: max_iters must be >= 0");
+  config.validate();
+  const blco_tensor* d = device_tensor(t);
+  const blco_exec_config c = to_c(config);
+  CpModel model;
+  model.seed = opts.seed;
+  model.factors.rank = opts.rank;
+  std::vector<double*> out;
+  for (index_t dim : t.dims()) model.factors.factors.emplace_back(dim, opts.rank);
+  for (auto& a : model.factors.factors) out.push_back(a.data.data());
+  model.lambda.assign(opts.rank, 1.0);
+  std::vector<double> fits(std::max(1, opts.max_iters));
+  int iters = 0;
+  const int status = blco_cp_als(d, opts.rank, opts.max_iters, opts.tol, opts.seed,
+                                 static_cast<int>(opts.strategy), &c, out.data(),
+                                 model.lambda.data(), fits.data(), &iters);
+  model.fit_history.assign(fits.begin(), fits.begin() + iters);
+  if (status == BLCO_ERROR && std::string(blco_last_error()).rfind("cp_als: non-finite", 0) == 0)
+    throw CpAlsError(blco_last_error(), model.fit_history);
+  ck(status);
+  return model;
+}
+
+double fit(const BlcoTensor& t, const CpModel& model, const ExecConfig& config) {
+  model.factors.validate(t.dims());
+  if (model.lambda.size() != model.factors.rank)
+    throw FormatError("fit: lambda length does not match rank");
+  const blco_tensor* d = device_tensor(t);
+  const blco_exec_config c = to_c(config);
+  const auto ptrs = factor_ptrs(model.factors);
+  double f = 0;
+  ck(blco_fit(d, ptrs.data(), model.lambda.data(), model.factors.rank, &c, &f));
+  return f;
+}
+
+}  // namespace blco

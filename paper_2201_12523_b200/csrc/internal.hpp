@@ -1,0 +1,167 @@
+// internal.hpp -- shared internals of libblco_b200 (not installed).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <map>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "blco_b200.h"
+
+namespace b200 {
+
+// ------------------------------------------------------------------ errors
+// Internal code throws Status; the C ABI converts to (code, message).
+struct Status : std::runtime_error {
+  int code;
+  Status(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void throw_format(const std::string& m) { throw Status(BLCO_EFORMAT, m); }
+[[noreturn]] inline void throw_error(const std::string& m) { throw Status(BLCO_ERROR, m); }
+
+void cuda_check(cudaError_t e, const char* what, const char* file, int line);
+#define B200_CUDA(expr) ::b200::cuda_check((expr), #expr, __FILE__, __LINE__)
+
+void set_error(int code, const std::string& msg);
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return BLCO_OK;
+  } catch (const Status& s) {
+    set_error(s.code, s.what());
+    return s.code;
+  } catch (const std::exception& e) {
+    set_error(BLCO_ERROR, e.what());
+    return BLCO_ERROR;
+  }
+}
+
+extern std::atomic<uint64_t> g_launches;
+inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+void check_launch(const char* what);
+
+// ----------------------------------------------------------------- layout
+int bits_for_extent(uint64_t extent);
+blco_layout make_layout(const uint64_t* dims, int order, int target_bits);
+uint64_t key_upper(const blco_layout& l, int mode, uint64_t key);
+
+// --------------------------------------------------------- device buffers
+template <class T>
+struct DevBuf {
+  T* ptr = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  explicit DevBuf(size_t count) { alloc(count); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : ptr(o.ptr), n(o.n) { o.ptr = nullptr, o.n = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      reset();
+      ptr = o.ptr, n = o.n;
+      o.ptr = nullptr, o.n = 0;
+    }
+    return *this;
+  }
+  ~DevBuf() { reset(); }
+  void alloc(size_t count) {
+    reset();
+    if (count) B200_CUDA(cudaMalloc(&ptr, count * sizeof(T)));
+    n = count;
+  }
+  void reset() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr, n = 0;
+  }
+  size_t bytes() const { return n * sizeof(T); }
+};
+
+// Scoped device selection (restores the caller's device).
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    B200_CUDA(cudaGetDevice(&prev));
+    if (dev != prev) B200_CUDA(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    int cur;
+    if (cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// CTA work unit of the MTTKRP kernels: contiguous elements of one block.
+struct TileDesc {
+  uint64_t start;  // global element offset
+  uint32_t count;  // <= tile elements
+  uint32_t block;  // block ordinal
+};
+static_assert(sizeof(TileDesc) == 16, "TileDesc must stay 16 bytes");
+
+}  // namespace b200
+
+// ------------------------------------------------------- the opaque tensor
+struct blco_tensor {
+  blco_layout layout{};
+  int device = 0;
+  uint64_t nnz = 0;
+  uint64_t max_nnz_per_block = 0;
+  std::vector<uint64_t> keys;     // per block
+  std::vector<uint64_t> offsets;  // nblocks + 1 element offsets
+  b200::DevBuf<uint64_t> idx;     // re-encoded indices, ALTO order
+  b200::DevBuf<double> vals;
+  b200::DevBuf<uint32_t> block_base;  // [nblocks * order] decoded base coords
+  // tile tables keyed by tile size, built lazily
+  mutable std::mutex mu;
+  mutable std::map<uint32_t, b200::DevBuf<b200::TileDesc>> tiles;
+
+  uint64_t nblocks() const { return keys.size(); }
+};
+
+namespace b200 {
+// What one MTTKRP launch reads: the payload, its tile table and block bases.
+struct KernelView {
+  const blco_layout* layout;
+  const TileDesc* tiles;
+  uint64_t ntiles;
+  uint64_t elem_end;
+  const uint64_t* idx;
+  const double* vals;
+  const uint32_t* block_base;
+};
+
+struct MttkrpLaunch {
+  KernelView view;
+  const double* const* factors;  // device pointers, one per mode
+  uint64_t rank;
+  int mode;
+  int strategy;  // resolved (not AUTO) when enqueued
+  blco_exec_config cfg;
+  double* out;  // device, dims[mode] x rank
+  int accumulate;
+  cudaStream_t stream;
+  double* hier_copies = nullptr;           // persistent copies (caller merges)
+  unsigned long long* counters = nullptr;  // stats counters or null
+  uint64_t workgroups = 0;                 // out
+  int stash_slots = 0;                     // out
+};
+
+KernelView view_of(const blco_tensor& t);
+void mttkrp_enqueue(MttkrpLaunch& a);
+void merge_copies_enqueue(const double* copies, uint64_t elems, int ncopies, double* out,
+                          int accumulate, cudaStream_t s);
+uint32_t mttkrp_tile_elems();
+
+// Builds per-block base coordinates on the device and finalises a tensor
+// whose idx/vals/keys/offsets are populated.
+void finalize_tensor(blco_tensor& t);
+const TileDesc* tile_table(const blco_tensor& t, uint32_t tile_elems, uint64_t* ntiles);
+void check_device_layout(const blco_layout& l);
+}  // namespace b200

@@ -1,0 +1,314 @@
+// stream.cu -- out-of-memory BLCO MTTKRP: blocks stream from host memory
+// through per-queue device reservations on Q CUDA streams (K6).
+//
+// Reference: stream_mttkrp, proj/src/streaming.cpp:103-309.  Same budget
+// arithmetic (:117-136), same round-robin queue assignment (:265), same
+// rejection of a block larger than its queue reservation before it is
+// transferred (:257-264), same report fields (:292-307).  What is real here
+// and simulated there: capacity_bytes caps actual cudaMalloc'd bytes, a
+// "transfer" is a cudaMemcpyAsync H2D into the queue's reservation and a
+// "compute" is the MTTKRP kernel on the same stream, so block b+1's copy
+// (queue (b+1) % Q) overlaps block b's kernel (queue b % Q).  Timeline
+// intervals come from CUDA events.
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <thread>
+
+#include "internal.hpp"
+
+namespace b200 {
+namespace {
+
+__global__ void k_one_block_base(uint64_t key, int order, int kept, int total,
+                                 const uint8_t* __restrict__ imap_mode,
+                                 const uint8_t* __restrict__ imap_bit,
+                                 const int32_t* __restrict__ rem, uint32_t* __restrict__ base) {
+  if (threadIdx.x != 0) return;
+  uint64_t up[BLCO_MAX_DEV_ORDER] = {};
+  for (int p = kept; p < total; ++p) {
+    const int m = imap_mode[p];
+    up[m] |= ((key >> (p - kept)) & 1u) << (imap_bit[p] - rem[m]);
+  }
+  for (int m = 0; m < order; ++m) base[m] = static_cast<uint32_t>(up[m] << rem[m]);
+}
+
+void CUDART_CB host_sleep(void* arg) {
+  const double s = *static_cast<double*>(arg);
+  std::this_thread::sleep_for(std::chrono::duration<double>(s));
+}
+
+struct Queue {
+  cudaStream_t stream = nullptr;
+  DevBuf<uint64_t> idx;
+  DevBuf<double> vals;
+  DevBuf<uint32_t> base;
+  DevBuf<TileDesc> tiles;
+  uint64_t capacity = 0;  // elements
+};
+
+struct Interval {
+  int kind, queue;
+  uint64_t block;
+  cudaEvent_t b, e;
+};
+
+double union_seconds(std::vector<std::pair<double, double>> iv) {
+  std::sort(iv.begin(), iv.end());
+  double total = 0, hi = -1;
+  for (auto [b, e] : iv) {
+    if (b > hi) {
+      total += e - b;
+      hi = e;
+    } else if (e > hi) {
+      total += e - hi;
+      hi = e;
+    }
+  }
+  return total;
+}
+
+bool is_pinned(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+}  // namespace
+}  // namespace b200
+
+using namespace b200;
+
+extern "C" int blco_stream_mttkrp(const blco_layout* layout, uint64_t max_nnz_per_block,
+                                  blco_block_source_fn next, void* ctx,
+                                  const double* const* factors, uint64_t rank, int mode,
+                                  const blco_device_budget* budget, const blco_exec_config* cfg,
+                                  int strategy, int device, double* out,
+                                  blco_stream_report* report) {
+  return guarded([&] {
+    blco_exec_config c;
+    if (cfg) c = *cfg; else blco_exec_config_default(&c);
+    if (blco_exec_config_validate(&c) != BLCO_OK) throw_format(blco_last_error());
+    const blco_layout& l = *layout;
+    check_device_layout(l);
+    if (rank < 1) throw_format("factors: rank must be >= 1");
+    if (mode < 0 || mode >= l.order) throw_format("stream: mode out of range");
+    if (budget->num_queues < 1) throw_format("stream: num_queues must be >= 1");
+    if (strategy == BLCO_STRATEGY_AUTO) strategy = blco_choose_strategy(l.dims[mode], &c);
+    const bool hier = strategy == BLCO_STRATEGY_HIERARCHICAL;
+    const uint64_t out_rows = l.dims[mode];
+    const uint64_t out_elems = out_rows * rank;
+    const int C = std::max(1, c.num_factor_copies);
+
+    // Resident set: factors + output (+ copies), streaming.cpp:117-124.
+    uint64_t pinned = 0;
+    for (int m = 0; m < l.order; ++m) pinned += l.dims[m] * rank * sizeof(double);
+    pinned += out_elems * sizeof(double) * (hier ? C : 1);
+    if (pinned > budget->capacity_bytes)
+      throw_format("stream: factor matrices and output (" + std::to_string(pinned) +
+                   " bytes) exceed device capacity " + std::to_string(budget->capacity_bytes));
+    const int Q = budget->num_queues;
+    uint64_t reservation = budget->reservation_bytes;
+    if (reservation == 0) reservation = (budget->capacity_bytes - pinned) / Q;
+    if (reservation < sizeof(uint64_t) + sizeof(double))
+      throw_format("stream: budget leaves no room for a per-queue reservation");
+    if (pinned + static_cast<uint64_t>(Q) * reservation > budget->capacity_bytes)
+      throw_format("stream: reservations exceed device capacity");
+    const uint64_t max_staged = reservation / (sizeof(uint64_t) + sizeof(double));
+    const uint64_t resident = pinned + static_cast<uint64_t>(Q) * reservation;
+
+    DeviceGuard dg(device);
+    // factors + output
+    std::vector<DevBuf<double>> df(l.order);
+    std::vector<const double*> fptr(l.order);
+    for (int m = 0; m < l.order; ++m) {
+      df[m].alloc(l.dims[m] * rank);
+      if (df[m].n) B200_CUDA(cudaMemcpy(df[m].ptr, factors[m], df[m].bytes(), cudaMemcpyHostToDevice));
+      fptr[m] = df[m].ptr;
+    }
+    DevBuf<double> dout(out_elems), copies(hier ? out_elems * C : 0);
+    if (dout.n) B200_CUDA(cudaMemset(dout.ptr, 0, dout.bytes()));
+    if (copies.n) B200_CUDA(cudaMemset(copies.ptr, 0, copies.bytes()));
+    DevBuf<uint8_t> dmode(BLCO_MAX_BITS), dbit(BLCO_MAX_BITS);
+    DevBuf<int32_t> drem(BLCO_MAX_ORDER);
+    B200_CUDA(cudaMemcpy(dmode.ptr, l.imap_mode, BLCO_MAX_BITS, cudaMemcpyHostToDevice));
+    B200_CUDA(cudaMemcpy(dbit.ptr, l.imap_bit, BLCO_MAX_BITS, cudaMemcpyHostToDevice));
+    B200_CUDA(cudaMemcpy(drem.ptr, l.rem_bits, sizeof(int32_t) * BLCO_MAX_ORDER, cudaMemcpyHostToDevice));
+
+    // Reservations are allocated lazily at the size of the largest block seen
+    // (bounded by the reservation), so capacity is a real cap.
+    const uint32_t tile = mttkrp_tile_elems();
+    std::vector<Queue> qs(Q);
+    for (auto& q : qs) B200_CUDA(cudaStreamCreateWithFlags(&q.stream, cudaStreamNonBlocking));
+    cudaEvent_t start, stop;
+    B200_CUDA(cudaEventCreate(&start));
+    B200_CUDA(cudaEventCreate(&stop));
+    B200_CUDA(cudaDeviceSynchronize());
+    B200_CUDA(cudaEventRecord(start, qs[0].stream));
+    for (int q = 1; q < Q; ++q) B200_CUDA(cudaStreamWaitEvent(qs[q].stream, start, 0));
+
+    std::vector<Interval> timeline;
+    std::vector<int32_t> block_queue;
+    std::vector<double> sleep_arg(1, budget->injected_transfer_latency_s);
+    uint64_t ordinal = 0, bytes = 0;
+    std::string err;
+    int err_code = BLCO_OK;
+    try {
+      for (;;) {
+        blco_block_view bv{};
+        const int r = next(ctx, &bv);
+        if (r < 0) throw Status(-r, blco_last_error());
+        if (r == 0) break;
+        const uint64_t bbytes = bv.nnz * (sizeof(uint64_t) + sizeof(double));
+        if (bbytes > reservation)
+          throw_format("stream: block " + std::to_string(ordinal) + " (" + std::to_string(bbytes) +
+                       " bytes) exceeds queue reservation " + std::to_string(reservation));
+        if (bv.nnz > max_nnz_per_block && max_nnz_per_block)
+          throw_format("blco: block exceeds max_nnz_per_block");
+        const int qi = static_cast<int>(ordinal % Q);
+        Queue& q = qs[qi];
+        block_queue.push_back(qi);
+        if (bv.nnz > q.capacity) {
+          // grow this queue's reservation (waits for its stream first)
+          B200_CUDA(cudaStreamSynchronize(q.stream));
+          const uint64_t cap = std::min<uint64_t>(max_staged, std::max<uint64_t>(bv.nnz, 1));
+          q.idx.alloc(cap);
+          q.vals.alloc(cap);
+          q.base.alloc(BLCO_MAX_DEV_ORDER);
+          std::vector<TileDesc> h;
+          for (uint64_t off = 0; off < cap; off += tile)
+            h.push_back(TileDesc{off, static_cast<uint32_t>(std::min<uint64_t>(tile, cap - off)), 0u});
+          q.tiles.alloc(h.size());
+          B200_CUDA(cudaMemcpy(q.tiles.ptr, h.data(), h.size() * sizeof(TileDesc), cudaMemcpyHostToDevice));
+          q.capacity = cap;
+        }
+        Interval tr{0, qi, ordinal, nullptr, nullptr}, cp{1, qi, ordinal, nullptr, nullptr};
+        B200_CUDA(cudaEventCreate(&tr.b));
+        B200_CUDA(cudaEventCreate(&tr.e));
+        B200_CUDA(cudaEventCreate(&cp.b));
+        B200_CUDA(cudaEventCreate(&cp.e));
+        timeline.push_back(tr);
+        timeline.push_back(cp);
+        B200_CUDA(cudaEventRecord(tr.b, q.stream));
+        if (bv.nnz) {
+          B200_CUDA(cudaMemcpyAsync(q.idx.ptr, bv.idx, bv.nnz * 8, cudaMemcpyHostToDevice, q.stream));
+          B200_CUDA(cudaMemcpyAsync(q.vals.ptr, bv.vals, bv.nnz * 8, cudaMemcpyHostToDevice, q.stream));
+        }
+        k_one_block_base<<<1, 32, 0, q.stream>>>(bv.key, l.order, l.total_bits - l.stripped_bits,
+                                                 l.total_bits, dmode.ptr, dbit.ptr, drem.ptr, q.base.ptr);
+        count_launch();
+        check_launch("k_one_block_base");
+        if (budget->injected_transfer_latency_s > 0)
+          B200_CUDA(cudaLaunchHostFunc(q.stream, host_sleep, sleep_arg.data()));
+        B200_CUDA(cudaEventRecord(tr.e, q.stream));
+        // pageable source memory may be reused by the source after next()
+        if (bv.nnz && (!is_pinned(bv.idx) || !is_pinned(bv.vals)))
+          B200_CUDA(cudaEventSynchronize(tr.e));
+
+        B200_CUDA(cudaEventRecord(cp.b, q.stream));
+        MttkrpLaunch a{};
+        a.view.layout = &l;
+        a.view.tiles = q.tiles.ptr;
+        a.view.ntiles = (bv.nnz + tile - 1) / tile;
+        a.view.elem_end = bv.nnz;
+        a.view.idx = q.idx.ptr;
+        a.view.vals = q.vals.ptr;
+        a.view.block_base = q.base.ptr;
+        a.factors = fptr.data();
+        a.rank = rank;
+        a.mode = mode;
+        a.strategy = strategy;
+        a.cfg = c;
+        a.out = dout.ptr;
+        a.accumulate = 1;
+        a.stream = q.stream;
+        a.hier_copies = hier ? copies.ptr : nullptr;
+        mttkrp_enqueue(a);
+        B200_CUDA(cudaEventRecord(cp.e, q.stream));
+        bytes += bbytes;
+        ++ordinal;
+      }
+    } catch (const Status& s) {
+      err = s.what();
+      err_code = s.code;
+    }
+    for (auto& q : qs) B200_CUDA(cudaStreamSynchronize(q.stream));
+    if (err_code != BLCO_OK) {
+      for (auto& iv : timeline) cudaEventDestroy(iv.b), cudaEventDestroy(iv.e);
+      for (auto& q : qs) cudaStreamDestroy(q.stream);
+      throw Status(err_code, err);
+    }
+    for (int q = 1; q < Q; ++q) {
+      cudaEvent_t done;
+      B200_CUDA(cudaEventCreate(&done));
+      B200_CUDA(cudaEventRecord(done, qs[q].stream));
+      B200_CUDA(cudaStreamWaitEvent(qs[0].stream, done, 0));
+      cudaEventDestroy(done);
+    }
+    if (hier) merge_copies_enqueue(copies.ptr, out_elems, C, dout.ptr, 1, qs[0].stream);
+    B200_CUDA(cudaEventRecord(stop, qs[0].stream));
+    B200_CUDA(cudaStreamSynchronize(qs[0].stream));
+    if (out_elems) B200_CUDA(cudaMemcpy(out, dout.ptr, dout.bytes(), cudaMemcpyDeviceToHost));
+
+    if (report) {
+      float total_ms = 0;
+      B200_CUDA(cudaEventElapsedTime(&total_ms, start, stop));
+      std::vector<std::pair<double, double>> tr_iv, cp_iv;
+      std::vector<blco_stream_event> evs;
+      for (auto& iv : timeline) {
+        float b = 0, e = 0;
+        B200_CUDA(cudaEventElapsedTime(&b, start, iv.b));
+        B200_CUDA(cudaEventElapsedTime(&e, start, iv.e));
+        (iv.kind == 0 ? tr_iv : cp_iv).emplace_back(b * 1e-3, e * 1e-3);
+        evs.push_back(blco_stream_event{iv.kind, iv.queue, iv.block, b * 1e-3, e * 1e-3});
+      }
+      std::sort(evs.begin(), evs.end(), [](const blco_stream_event& x, const blco_stream_event& y) {
+        return x.begin_s < y.begin_s;
+      });
+      report->blocks = ordinal;
+      report->bytes_streamed = bytes;
+      report->total_seconds = total_ms * 1e-3;
+      report->transfer_busy_seconds = union_seconds(tr_iv);
+      report->compute_busy_seconds = union_seconds(cp_iv);
+      const double gb = static_cast<double>(bytes) / 1e9;
+      report->overall_gbps = report->total_seconds > 0 ? gb / report->total_seconds : 0;
+      report->compute_gbps = report->compute_busy_seconds > 0 ? gb / report->compute_busy_seconds : 0;
+      report->peak_resident_bytes = resident;
+      if (report->block_queue)
+        for (uint64_t i = 0; i < std::min<uint64_t>(report->block_queue_capacity, block_queue.size()); ++i)
+          report->block_queue[i] = block_queue[i];
+      report->timeline_count = evs.size();
+      if (report->timeline)
+        for (uint64_t i = 0; i < std::min<uint64_t>(report->timeline_capacity, evs.size()); ++i)
+          report->timeline[i] = evs[i];
+    }
+    for (auto& iv : timeline) cudaEventDestroy(iv.b), cudaEventDestroy(iv.e);
+    cudaEventDestroy(start);
+    cudaEventDestroy(stop);
+    for (auto& q : qs) cudaStreamDestroy(q.stream);
+  });
+}
+
+extern "C" void* blco_host_alloc_pinned(uint64_t bytes) {
+  void* p = nullptr;
+  if (cudaHostAlloc(&p, bytes ? bytes : 1, cudaHostAllocPortable) != cudaSuccess) {
+    set_error(BLCO_ECUDA, "cuda: cudaHostAlloc failed");
+    return nullptr;
+  }
+  return p;
+}
+
+extern "C" void blco_host_free_pinned(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
+extern "C" int blco_host_register(void* p, uint64_t bytes) {
+  return guarded([&] { B200_CUDA(cudaHostRegister(p, bytes, cudaHostRegisterPortable)); });
+}
+
+extern "C" int blco_host_unregister(void* p) {
+  return guarded([&] { B200_CUDA(cudaHostUnregister(p)); });
+}

@@ -1,0 +1,160 @@
+"""MTTKRP on the device vs the oracle (relative Frobenius <= 1e-12 in fp64,
+the reference's own bar, proj/tests/test_mttkrp.cpp:267-290)."""
+import numpy as np
+import pytest
+
+from conftest import rel_frobenius
+
+pytestmark = pytest.mark.gpu
+
+GI = np.array([[0, 0, 0, 1, 1, 2, 2, 3, 3, 3, 3, 3],
+               [0, 0, 2, 0, 0, 0, 3, 1, 1, 2, 2, 3],
+               [0, 1, 2, 1, 2, 1, 3, 0, 1, 2, 3, 3]], np.uint64)
+GV = np.arange(1, 13, dtype=np.float64)
+TOL = 1e-12
+
+
+def test_all_ones_rows(gpu):  # test_mttkrp.cpp:33-47
+    t = gpu.build_blco(gpu.SparseTensorCoo([4, 4, 4], GI, GV), 5, 6)
+    f = gpu.FactorMatrices.ones([4, 4, 4], 2)
+    m1 = gpu.mttkrp(t, f, 0, strategy=gpu.Strategy.Register)
+    assert np.allclose(m1[:, 0], [6, 9, 13, 50], rtol=1e-13) and np.allclose(m1[:, 1], [6, 9, 13, 50])
+    m3 = gpu.mttkrp(t, f, 2, strategy=gpu.Strategy.Hierarchical)
+    assert np.allclose(m3[:, 0], [9, 21, 18, 30], rtol=1e-13)
+
+
+def test_golden_grid_both_strategies(gpu, golden):
+    """Every golden build x rank x mode x strategy x factor copies."""
+    z, meta = golden
+    for j, ent in enumerate(meta["mttkrps"]):
+        b = ent["build"]
+        bm = meta["builds"][b]
+        dims = bm["dims"]
+        t = gpu.BlcoTensor(gpu.make_layout(dims, bm["target"]), bm["max_nnz"], z[f"b{b}_keys"],
+                           z[f"b{b}_offsets"], z[f"b{b}_idx"], z[f"b{b}_vals"])
+        f = gpu.FactorMatrices(ent["rank"], [z[f"m{j}_f{m}"] for m in range(len(dims))])
+        for mode in range(len(dims)):
+            want = z[f"m{j}_coo{mode}"]
+            for strat in (gpu.Strategy.Register, gpu.Strategy.Hierarchical):
+                for copies in (1, 3):
+                    cfg = gpu.ExecConfig(num_factor_copies=copies, stash_slots=4)
+                    got = gpu.mttkrp(t, f, mode, cfg, strat)
+                    assert rel_frobenius(got, want) <= TOL, (j, mode, strat, copies)
+
+
+@pytest.mark.parametrize("order", [1, 2, 3, 4, 5, 6, 7, 8])
+@pytest.mark.parametrize("rank", [1, 3, 8, 16, 32, 33, 64, 100])
+def test_orders_and_ranks(gpu, oracle, order, rank):
+    rng = np.random.default_rng(order * 131 + rank)
+    dims = [int(x) for x in rng.integers(2, 60, size=order)]
+    cells = int(np.prod(dims))
+    nnz = min(cells, 3000)
+    coo = gpu.synth_uniform_host(dims, nnz, order + rank)
+    f = gpu.FactorMatrices(rank, [rng.uniform(-1, 1, (d, rank)) for d in dims])
+    t = gpu.build_blco(coo, 64)
+    for mode in range(order):
+        want = oracle.mttkrp_coo(dims, coo.indices, coo.values, f.factors, mode)
+        for strat in (gpu.Strategy.Register, gpu.Strategy.Hierarchical):
+            got = gpu.mttkrp(t, f, mode, strategy=strat)
+            assert rel_frobenius(got, want) <= TOL, (mode, strat)
+
+
+@pytest.mark.parametrize("target,cap", [(64, 1 << 27), (12, 64), (9, 1000), (20, 1)])
+def test_multiblock_layouts(gpu, oracle, target, cap):
+    dims = [700, 90, 1300]
+    coo = gpu.synth_uniform_host(dims, 40_000, 17)
+    f = gpu.FactorMatrices.random(dims, 16, 7)
+    t = gpu.build_blco(coo, target, cap)
+    for mode in range(3):
+        want = oracle.mttkrp_coo(dims, coo.indices, coo.values, f.factors, mode)
+        for strat in (gpu.Strategy.Register, gpu.Strategy.Hierarchical):
+            assert rel_frobenius(gpu.mttkrp(t, f, mode, strategy=strat), want) <= TOL
+
+
+def test_config1_full_size(gpu, oracle):
+    """BASELINE config 1: 1000^3, 1M nnz, R=16, every mode, against the oracle."""
+    dims = [1000, 1000, 1000]
+    dt = gpu.DeviceTensor.synthetic(dims, 1_000_000, 42)
+    idx, vals = oracle.synth_uniform(dims, 1_000_000, 42)
+    f = gpu.FactorMatrices.random(dims, 16, 7)
+    for mode in range(3):
+        want = oracle.mttkrp_coo(dims, idx, vals, f.factors, mode)
+        st = gpu.MttkrpStats()
+        got = gpu.mttkrp(dt, f, mode, stats=st)
+        assert rel_frobenius(got, want) <= TOL
+        assert st.strategy == gpu.Strategy.Register and 0 < st.segments <= 1_000_000
+
+
+def test_high_conflict_short_mode(gpu, oracle):
+    """Many elements per row (short target mode): hierarchical stash path."""
+    dims = [24, 3000, 50]
+    coo = gpu.synth_uniform_host(dims, 200_000, 8)
+    f = gpu.FactorMatrices.random(dims, 16, 3)
+    t = gpu.build_blco(coo)
+    want = oracle.mttkrp_coo(dims, coo.indices, coo.values, f.factors, 0)
+    for cfg in (gpu.ExecConfig(), gpu.ExecConfig(num_factor_copies=4), gpu.ExecConfig(num_compute_units=148)):
+        st = gpu.MttkrpStats()
+        got = gpu.mttkrp(t, f, 0, cfg, stats=st)  # Auto -> Hierarchical (24 < CUs)
+        assert st.strategy == gpu.Strategy.Hierarchical
+        assert rel_frobenius(got, want) <= TOL
+    reg = gpu.mttkrp(t, f, 0, strategy=gpu.Strategy.Register)
+    assert rel_frobenius(reg, want) <= TOL
+
+
+def test_stats_register_commits(gpu):  # test_mttkrp.cpp:152-188 (GPU meaning)
+    coo = gpu.SparseTensorCoo([4, 8], np.array([[1, 1, 2], [0, 4, 1]], np.uint64), [1.0, 2.0, 3.0])
+    t = gpu.build_blco(coo)
+    f = gpu.FactorMatrices.ones([4, 8], 4)
+    st = gpu.MttkrpStats()
+    m = gpu.mttkrp(t, f, 0, strategy=gpu.Strategy.Register, stats=st)
+    assert st.segments == 2 and st.scalar_adds == 8
+    assert m[1, 0] == 3.0 and m[2, 0] == 3.0
+
+
+def test_validation(gpu):  # test_mttkrp.cpp:319-326
+    t = gpu.build_blco(gpu.SparseTensorCoo([4, 4, 4], GI, GV))
+    f = gpu.FactorMatrices.ones([4, 4, 4], 2)
+    with pytest.raises(gpu.FormatError):
+        gpu.mttkrp(t, f, 5)
+    bad = gpu.FactorMatrices(2, [f.factors[0], np.zeros((3, 2)), f.factors[2]])
+    with pytest.raises(gpu.FormatError):
+        gpu.mttkrp(t, bad, 0)
+
+
+def test_device_pointer_entry(gpu, oracle):
+    """blco_mttkrp_device on torch-owned buffers, on torch's current stream."""
+    import torch
+    dims = [300, 200, 100]
+    dt = gpu.DeviceTensor.synthetic(dims, 50_000, 1)
+    fs = [torch.empty((d, 32), dtype=torch.float64, device="cuda") for d in dims]
+    gpu.factors_random_device(dims, 32, 7, [a.data_ptr() for a in fs],
+                              torch.cuda.current_stream().cuda_stream)
+    out = torch.empty((dims[1], 32), dtype=torch.float64, device="cuda")
+    dt.mttkrp_device([a.data_ptr() for a in fs], 32, 1, out.data_ptr(),
+                     stream=torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    idx, vals = oracle.synth_uniform(dims, 50_000, 1)
+    hf = oracle.factors_random(dims, 32, 7)
+    for a, b in zip(fs, hf):
+        assert np.array_equal(a.cpu().numpy(), b)
+    want = oracle.mttkrp_coo(dims, idx, vals, hf, 1)
+    assert rel_frobenius(out.cpu().numpy(), want) <= TOL
+    # accumulate=True adds onto the existing output
+    dt.mttkrp_device([a.data_ptr() for a in fs], 32, 1, out.data_ptr(), accumulate=True,
+                     stream=torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert rel_frobenius(out.cpu().numpy(), 2 * want) <= TOL
+
+
+def test_slices_sum_to_whole(gpu, oracle):
+    """Multi-GPU partition unit: span-aligned slices' partial outputs sum to M."""
+    dims = [500, 400, 300]
+    dt = gpu.DeviceTensor.synthetic(dims, 200_000, 4, 20, 30_000)
+    f = gpu.FactorMatrices.random(dims, 16, 2)
+    idx, vals = oracle.synth_uniform(dims, 200_000, 4)
+    for parts in (2, 3, 8):
+        ranges = gpu.partition(dt.block_nnz(), 512, parts)
+        for mode in range(3):
+            acc = sum(gpu.mttkrp(dt.slice(b, e), f, mode) for b, e in ranges)
+            want = oracle.mttkrp_coo(dims, idx, vals, f.factors, mode)
+            assert rel_frobenius(acc, want) <= TOL

@@ -1,0 +1,109 @@
+"""Out-of-memory streaming (proj/tests/test_streaming.cpp) and CP-ALS
+(proj/src/cpals.cpp) on the device."""
+import numpy as np
+import pytest
+
+from conftest import rel_frobenius
+
+pytestmark = pytest.mark.gpu
+
+
+def factor_bytes(f, out_rows):  # test_streaming.cpp:12-16
+    return out_rows * f.rank * 8 + sum(a.size * 8 for a in f.factors)
+
+
+def small_tensor(gpu, dims, nnz, seed, target, cap):
+    coo = gpu.synth_uniform_host(dims, nnz, seed)
+    return coo, gpu.build_blco(coo, target, cap)
+
+
+def test_streamed_equals_in_memory(gpu):  # test_streaming.cpp:21-52
+    coo, t = small_tensor(gpu, [50, 40, 60], 600, 83, 8, 64)
+    assert t.keys.size >= 4
+    f = gpu.FactorMatrices.random([50, 40, 60], 4, 1)
+    want = gpu.mttkrp(t, f, 0, strategy=gpu.Strategy.Register)
+    for queues in (1, 2, 4):
+        b = gpu.DeviceBudget(num_queues=queues, reservation_bytes=t.max_nnz_per_block * 16)
+        b.capacity_bytes = factor_bytes(f, 50) + queues * b.reservation_bytes
+        rep = gpu.StreamReport()
+        got = gpu.stream_mttkrp(t, f, 0, b, strategy=gpu.Strategy.Register, report=rep)
+        assert rel_frobenius(got, want) <= 1e-12
+        assert rep.blocks == t.keys.size and rep.peak_resident_bytes <= b.capacity_bytes
+        assert rep.block_queue == [i % queues for i in range(t.keys.size)]
+        assert rep.bytes_streamed == t.total_nnz * 16
+
+
+def test_streaming_matches_reference_stream(gpu, golden):
+    z, meta = golden
+    for j, ent in enumerate(meta["streams"]):
+        bm = meta["builds"][ent["build"]]
+        b = ent["build"]
+        dims = bm["dims"]
+        t = gpu.BlcoTensor(gpu.make_layout(dims, bm["target"]), bm["max_nnz"], z[f"b{b}_keys"],
+                           z[f"b{b}_offsets"], z[f"b{b}_idx"], z[f"b{b}_vals"])
+        f = gpu.FactorMatrices(ent["rank"], [z[f"s{j}_f{m}"] for m in range(len(dims))])
+        res = bm["max_nnz"] * 16
+        budget = gpu.DeviceBudget(factor_bytes(f, dims[0]) + 2 * res, 2, res)
+        for strat in (gpu.Strategy.Register, gpu.Strategy.Hierarchical):
+            got = gpu.stream_mttkrp(t, f, 0, budget, gpu.ExecConfig(num_factor_copies=2), strat)
+            assert rel_frobenius(got, z[f"s{j}_out"]) <= 1e-12
+
+
+def test_overlap_with_injected_latency(gpu):  # test_streaming.cpp:105-139
+    coo, t = small_tensor(gpu, [6, 4000], 3000, 101, 9, 512)
+    f = gpu.FactorMatrices.random([6, 4000], 8, 2)
+    b = gpu.DeviceBudget(num_queues=2, reservation_bytes=t.max_nnz_per_block * 16,
+                         injected_transfer_latency_s=0.02)
+    b.capacity_bytes = factor_bytes(f, 6) + 2 * b.reservation_bytes
+    rep = gpu.StreamReport()
+    gpu.stream_mttkrp(t, f, 0, b, report=rep)
+    tr = [e for e in rep.timeline if e.kind == "transfer"]
+    cp = [e for e in rep.timeline if e.kind == "compute"]
+    assert any(x.begin_s < y.end_s and y.begin_s < x.end_s and x.block != y.block for x in tr for y in cp)
+    assert rep.transfer_busy_seconds > 0 and rep.compute_busy_seconds > 0
+    assert rep.overall_gbps < rep.compute_gbps  # transfer-dominated (test_streaming.cpp:164-170)
+
+
+def test_budget_errors(gpu):  # test_streaming.cpp:173-199
+    coo, t = small_tensor(gpu, [30, 30], 100, 107, 6, 32)
+    f = gpu.FactorMatrices.random([30, 30], 4, 1)
+    with pytest.raises(gpu.FormatError, match="exceed device capacity"):
+        gpu.stream_mttkrp(t, f, 0, gpu.DeviceBudget(capacity_bytes=64))
+    b = gpu.DeviceBudget(num_queues=2, reservation_bytes=8)
+    b.capacity_bytes = factor_bytes(f, 30) + 16
+    with pytest.raises(gpu.FormatError, match="reservation"):
+        gpu.stream_mttkrp(t, f, 0, b)
+
+
+def test_oversized_budget(gpu):  # test_streaming.cpp:201-217
+    coo, t = small_tensor(gpu, [25, 25, 25], 250, 109, 64, 1 << 27)
+    f = gpu.FactorMatrices.random([25, 25, 25], 4, 3)
+    want = gpu.mttkrp(t, f, 0)
+    got = gpu.stream_mttkrp(t, f, 0, gpu.DeviceBudget(capacity_bytes=1 << 34, num_queues=4))
+    assert rel_frobenius(got, want) <= 1e-12
+
+
+def test_cp_als_matches_reference(gpu, golden):
+    """fit history within 1e-10 absolute, factors within 1e-8 relative."""
+    z, meta = golden
+    for j, ent in enumerate(meta["cpals"]):
+        dims = ent["dims"]
+        t = gpu.build_blco(gpu.SparseTensorCoo(dims, z[f"c{j}_in_idx"], z[f"c{j}_in_vals"]))
+        model = gpu.cp_als(t, gpu.CpAlsOptions(rank=ent["rank"], max_iters=ent["iters"], tol=ent["tol"],
+                                               seed=ent["seed"]))
+        want = z[f"c{j}_fit"]
+        assert len(model.fit_history) == want.size
+        assert np.max(np.abs(np.array(model.fit_history) - want)) <= 1e-10
+        for m in range(len(dims)):
+            assert rel_frobenius(model.factors.factors[m], z[f"c{j}_f{m}"]) <= 1e-8
+        assert np.allclose(model.lambda_, z[f"c{j}_lambda"], rtol=1e-9)
+        assert abs(gpu.fit(t, model) - model.final_fit()) <= 1e-10
+
+
+def test_cp_als_zero_iters_and_errors(gpu):
+    coo, t = small_tensor(gpu, [5, 6, 7], 50, 1, 64, 1 << 27)
+    m = gpu.cp_als(t, gpu.CpAlsOptions(rank=3, max_iters=0, seed=9))
+    ref = gpu.FactorMatrices.random([5, 6, 7], 3, 9)
+    assert all(np.array_equal(a, b) for a, b in zip(m.factors.factors, ref.factors))
+    with pytest.raises(gpu.FormatError):
+        gpu.cp_als(t, gpu.CpAlsOptions(rank=0))
