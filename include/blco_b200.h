@@ -157,6 +157,18 @@ int blco_build_synthetic(const uint64_t* dims, int order, uint64_t nnz, uint64_t
                          int target_bits, uint64_t max_nnz_per_block, int device,
                          blco_tensor** out, blco_build_stats* stats);
 
+/* Same, from independent per-mode draws (config 4, "skewed power-law"):
+ * coordinate m of candidate j is floor(I_m * u^skew) (skew = 1: uniform), the
+ * tensor keeps the first nnz distinct tuples in draw order.  Works for any
+ * prod(dims) (Delicious-shaped layouts of 78 bits included). */
+int blco_build_synthetic_draws(const uint64_t* dims, int order, uint64_t nnz, uint64_t seed,
+                               int skew, int target_bits, uint64_t max_nnz_per_block, int device,
+                               blco_tensor** out, blco_build_stats* stats);
+/* The candidate stream of blco_build_synthetic_draws on the host: ncand
+ * draws (duplicates included), idx mode-major, for oracle parity. */
+int blco_synth_draws_host(int order, const uint64_t* dims, uint64_t ncand, uint64_t seed, int skew,
+                          uint64_t* idx, double* vals);
+
 /* Upload host-resident blocks (a reference BlcoTensor's payload). */
 int blco_tensor_upload(const blco_layout* layout, uint64_t max_nnz_per_block, uint64_t nblocks,
                        const uint64_t* keys, const uint64_t* block_nnz,
@@ -203,7 +215,13 @@ typedef struct blco_block_view {
   uint64_t nnz;
   const uint64_t* idx;
   const double* vals;
+  /* BLCO_BLOCK_STABLE: idx/vals stay valid until blco_stream_mttkrp returns
+   * (e.g. MemoryBlockSource), so the copy need not finish before the next
+   * pull.  Without it the library completes each pageable copy first. */
+  uint32_t flags;
 } blco_block_view;
+
+#define BLCO_BLOCK_STABLE 1u
 
 /* returns 1 = block produced, 0 = end of stream, < 0 = error (message via
  * blco_set_error from the callback, status = -return) */

@@ -350,6 +350,55 @@ int orc_synth_uniform(int order, const uint64_t* dims, uint64_t nnz, uint64_t se
   return ORC_OK;
 }
 
+/* Independent draws, first nnz distinct tuples in draw order (the product's
+ * blco_build_synthetic_draws). */
+#define DRAW_SALT 0xd1b54a32d192ed03ull
+
+static uint64_t skewed(double u, uint64_t dim, int k) {
+  double p = u;
+  for (int i = 1; i < k; ++i) p = p * u;
+  const uint64_t c = (uint64_t)(p * (double)dim);
+  return c < dim ? c : dim - 1;
+}
+
+int orc_synth_draws(int order, const uint64_t* dims, uint64_t nnz, uint64_t seed, int skew,
+                    uint64_t* idx, double* vals) {
+  uint64_t cap = 16;
+  while (cap < 2 * nnz + 16) cap *= 2;
+  uint64_t* table = calloc(cap, sizeof *table); /* stores element index + 1 */
+  uint64_t kept = 0, c[ORC_MAX_ORDER];
+  for (uint64_t j = 0; kept < nnz; ++j) {
+    if (j > 64 * (nnz + 1024)) {
+      free(table);
+      return fail("synth: cannot draw %llu unique coordinates", (unsigned long long)nnz);
+    }
+    uint64_t h = 0x12345;
+    for (int m = 0; m < order; ++m) {
+      const double u = unit_double(mix64((seed ^ DRAW_SALT) + (j * order + m + 1) * GOLDEN));
+      c[m] = skewed(u, dims[m], skew);
+      h = mix64(h ^ (c[m] + GOLDEN * (m + 1)));
+    }
+    uint64_t s = h & (cap - 1);
+    int dup = 0;
+    while (table[s]) {
+      const uint64_t e = table[s] - 1;
+      int same = 1;
+      for (int m = 0; m < order && same; ++m) same = idx[(uint64_t)m * nnz + e] == c[m];
+      if (same) {
+        dup = 1;
+        break;
+      }
+      s = (s + 1) & (cap - 1);
+    }
+    if (dup) continue;
+    for (int m = 0; m < order; ++m) idx[(uint64_t)m * nnz + kept] = c[m];
+    vals[kept] = unit_double(mix64((seed ^ VALUE_SALT) + (j + 1) * GOLDEN));
+    table[s] = ++kept;
+  }
+  free(table);
+  return ORC_OK;
+}
+
 /* ------------------------------------------------------------ dense / ALS */
 
 void orc_gram(const double* a, uint64_t rows, uint64_t rank, double* g) {

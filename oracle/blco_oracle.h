@@ -111,6 +111,10 @@ int orc_synth_uniform(int order, const uint64_t* dims, uint64_t nnz, uint64_t se
 
 int orc_alto_lo_batch(const orc_layout* l, uint64_t nnz, const uint64_t* idx, uint64_t* out);
 
+/* Independent per-mode draws floor(I * u^skew), first nnz distinct tuples. */
+int orc_synth_draws(int order, const uint64_t* dims, uint64_t nnz, uint64_t seed, int skew,
+                    uint64_t* idx, double* vals);
+
 /* Dense kernels for the CP-ALS restatement: proj/src/dense_kernels.cpp. */
 void orc_gram(const double* a, uint64_t rows, uint64_t rank, double* g);
 int orc_solve_normal(double* m, uint64_t rows, const double* v, uint64_t rank);

@@ -151,6 +151,13 @@ class Oracle:
                                             C.c_uint64(seed), _pu(idx), _pd(vals)))
         return idx, vals
 
+    def synth_draws(self, dims, nnz, seed, skew=1):
+        idx = np.zeros((len(dims), nnz), np.uint64)
+        vals = np.zeros(nnz)
+        self._ck(self.lib.orc_synth_draws(len(dims), _pu(_u64(dims)), C.c_uint64(nnz), C.c_uint64(seed),
+                                          skew, _pu(idx), _pd(vals)))
+        return idx, vals
+
     def alto_lo(self, dims, idx) -> np.ndarray:
         """Low ALTO word of every element (layouts of <= 64 bits)."""
         l = self.layout(dims, 64)

@@ -10,4 +10,4 @@ from .api import (  # noqa: F401
     choose_strategy, compute_batch_table, cp_als, delinearize, device_count, encode_coords,
     factors_random_device, fit, interleaved_remainder, kernel_launch_count, linearize,
     make_layout, merge_copies, mttkrp, partition, split_block_key, stream_mttkrp,
-    synth_uniform_host, throughput_report)
+    synth_draws_host, synth_uniform_host, throughput_report)

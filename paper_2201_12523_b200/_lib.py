@@ -60,7 +60,10 @@ class BuildStats(C.Structure):
 
 class BlockView(C.Structure):
     _fields_ = [("key", C.c_uint64), ("nnz", C.c_uint64),
-                ("idx", C.c_void_p), ("vals", C.c_void_p)]
+                ("idx", C.c_void_p), ("vals", C.c_void_p), ("flags", C.c_uint32)]
+
+
+BLOCK_STABLE = 1
 
 
 class Budget(C.Structure):
@@ -119,6 +122,9 @@ SIGNATURES = {
                         C.POINTER(BuildStats)]),
     "blco_build_synthetic": (_I, [_PU64, _I, _U64, _U64, _I, _U64, _I, C.POINTER(_P),
                                   C.POINTER(BuildStats)]),
+    "blco_build_synthetic_draws": (_I, [_PU64, _I, _U64, _U64, _I, _I, _U64, _I, C.POINTER(_P),
+                                        C.POINTER(BuildStats)]),
+    "blco_synth_draws_host": (_I, [_I, _PU64, _U64, _U64, _I, _PU64, _PD]),
     "blco_tensor_upload": (_I, [C.POINTER(Layout), _U64, _U64, _PU64, _PU64,
                                 C.POINTER(_P), C.POINTER(_P), _I, C.POINTER(_P)]),
     "blco_tensor_slice": (_I, [_P, _U64, _U64, _I, C.POINTER(_P)]),

@@ -422,6 +422,20 @@ class DeviceTensor:
         return DeviceTensor(h.value, device)
 
     @staticmethod
+    def synthetic_draws(dims: Sequence[int], nnz: int, seed: int, skew: int = 1, target_bits: int = 64,
+                        max_nnz_per_block: int = 1 << 27, device: int = 0,
+                        stats: BuildStats | None = None) -> "DeviceTensor":
+        """Independent per-mode draws floor(I*u^skew), first nnz distinct tuples."""
+        h = C.c_void_p()
+        bs = L.BuildStats()
+        d = _u64(dims)
+        _check(lib.blco_build_synthetic_draws(_pu64(d), len(d), nnz, seed, skew, target_bits,
+                                              max_nnz_per_block, device, C.byref(h), C.byref(bs)))
+        if stats is not None:
+            stats.__dict__.update({k: getattr(bs, k) for k, _ in L.BuildStats._fields_})
+        return DeviceTensor(h.value, device)
+
+    @staticmethod
     def upload(t: BlcoTensor, device: int = 0) -> "DeviceTensor":
         h = C.c_void_p()
         bn = _u64(np.diff(t.offsets))
@@ -581,7 +595,8 @@ def stream_mttkrp(source, f: FactorMatrices, mode: int, budget: DeviceBudget,
     """
     config = config or ExecConfig()
     config.validate()
-    if isinstance(source, BlcoTensor):
+    stable = isinstance(source, BlcoTensor)  # MemoryBlockSource: views outlive the call
+    if stable:
         layout = source.layout
         max_nnz_per_block = source.max_nnz_per_block
         block_count = int(source.keys.size)
@@ -608,6 +623,7 @@ def stream_mttkrp(source, f: FactorMatrices, mode: int, budget: DeviceBudget,
         keep[:] = [idx, vals]
         out[0].key, out[0].nnz = int(key), int(vals.size)
         out[0].idx, out[0].vals = idx.ctypes.data, vals.ctypes.data
+        out[0].flags = L.BLOCK_STABLE if stable else 0
         return 1
 
     cb = L.SOURCE_FN(pull)
@@ -719,6 +735,15 @@ def synth_uniform_host(dims: Sequence[int], nnz: int, seed: int) -> SparseTensor
     vals = np.zeros(nnz, np.float64)
     _check(lib.blco_synth_uniform_host(len(d), _pu64(d), nnz, seed, _pu64(idx), _pd(vals)))
     return SparseTensorCoo(list(dims), idx, vals)
+
+
+def synth_draws_host(dims: Sequence[int], ncand: int, seed: int, skew: int = 1):
+    """The candidate stream of DeviceTensor.synthetic_draws (duplicates kept)."""
+    d = _u64(dims)
+    idx = np.zeros((len(d), ncand), np.uint64)
+    vals = np.zeros(ncand, np.float64)
+    _check(lib.blco_synth_draws_host(len(d), _pu64(d), ncand, seed, skew, _pu64(idx), _pd(vals)))
+    return idx, vals
 
 
 def partition(block_nnz: Sequence[int], quota: int, nparts: int) -> list[tuple[int, int]]:

@@ -207,8 +207,40 @@ double secs(std::chrono::steady_clock::time_point t0) {
 
 // Core pipeline: device u32 coords (mode-major) + values -> tensor payload.
 // Consumes (frees) coords/vals.
+constexpr int kRetryDraws = -77;
+
+// f[i] = 1 iff element i starts a run of equal ALTO words and its candidate
+// id is <= max_id.
+__global__ void k_first_of_run(const uint64_t* __restrict__ lo, const uint64_t* __restrict__ hi,
+                               uint64_t n, uint8_t* __restrict__ f, const uint32_t* __restrict__ ids,
+                               uint32_t max_id) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const bool first = i == 0 || lo[i] != lo[i - 1] || (hi && hi[i] != hi[i - 1]);
+    f[i] = first && ids[i] <= max_id;
+  }
+}
+
+// Candidate draws for the skewed generator: coordinate m of candidate j is
+// floor(I_m * u^k) with u = unit(mix64(salted seed + (j*order + m + 1)*golden))
+// (k = 1 uniform; larger k concentrates mass on low indices, a power law with
+// density ~ x^(1/k - 1)); value = element_value(seed, j).
+__global__ void k_draws(uint64_t seed, int order, int skew, uint64_t ncand,
+                        const uint64_t* __restrict__ dims, uint32_t* __restrict__ coords,
+                        double* __restrict__ vals) {
+  for (uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; j < ncand;
+       j += uint64_t(gridDim.x) * blockDim.x) {
+    for (int m = 0; m < order; ++m) {
+      const double u = synth::unit(synth::mix64((seed ^ synth::kDrawSalt) +
+                                                 (j * order + m + 1) * synth::kGolden));
+      coords[m * ncand + j] = synth::skewed_coord(u, dims[m], skew);
+    }
+    vals[j] = synth::element_value(seed, j);
+  }
+}
+
 void build_from_device_coo(blco_tensor& t, DevBuf<uint32_t>& coords, DevBuf<double>& vals,
-                           uint64_t nnz, blco_build_stats* stats) {
+                           uint64_t nnz, blco_build_stats* stats, uint64_t dedup_target = 0) {
   const blco_layout& l = t.layout;
   if (nnz >= (uint64_t{1} << 32))
     throw_format("b200: device build handles < 2^32 elements per call (got " +
@@ -269,6 +301,52 @@ void build_from_device_coo(blco_tensor& t, DevBuf<uint32_t>& coords, DevBuf<doub
   hi.reset();
   B200_CUDA(cudaStreamSynchronize(s));
   if (stats) stats->sort_seconds = secs(t0);
+
+  DevBuf<unsigned char>* tmp_ptr = &tmp;
+  if (dedup_target) {
+    // Candidates are sorted by (ALTO, candidate id): the first of each equal
+    // run is the earliest draw.  Keep the dedup_target earliest unique draws.
+    DevBuf<uint8_t> f(nnz);
+    k_first_of_run<<<grid_for(nnz, 4), kThreads, 0, s>>>(keys_out.ptr, wide ? sorted_hi.ptr : nullptr,
+                                                         nnz, f.ptr, perm_out.ptr, UINT32_MAX);
+    count_launch();
+    check_launch("k_first_of_run");
+    DevBuf<uint32_t> ids(nnz), ids_sorted(nnz);
+    DevBuf<uint64_t> cnt(1);
+    size_t sb = 0;
+    B200_CUDA(cub::DeviceSelect::Flagged(nullptr, sb, perm_out.ptr, f.ptr, ids.ptr, cnt.ptr, nnz, s));
+    if (sb > tmp_ptr->n) tmp_ptr->alloc(sb);
+    B200_CUDA(cub::DeviceSelect::Flagged(tmp_ptr->ptr, sb, perm_out.ptr, f.ptr, ids.ptr, cnt.ptr, nnz, s));
+    count_launch();
+    uint64_t uniq = 0;
+    B200_CUDA(cudaMemcpy(&uniq, cnt.ptr, 8, cudaMemcpyDeviceToHost));
+    if (uniq < dedup_target) throw Status(kRetryDraws, "synth: not enough unique draws");
+    B200_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, sb, ids.ptr, ids_sorted.ptr, uniq, 0, 32, s));
+    if (sb > tmp_ptr->n) tmp_ptr->alloc(sb);
+    B200_CUDA(cub::DeviceRadixSort::SortKeys(tmp_ptr->ptr, sb, ids.ptr, ids_sorted.ptr, uniq, 0, 32, s));
+    count_launch();
+    uint32_t last = 0;
+    B200_CUDA(cudaMemcpy(&last, ids_sorted.ptr + (dedup_target - 1), 4, cudaMemcpyDeviceToHost));
+    k_first_of_run<<<grid_for(nnz, 4), kThreads, 0, s>>>(keys_out.ptr, wide ? sorted_hi.ptr : nullptr,
+                                                         nnz, f.ptr, perm_out.ptr, last);
+    count_launch();
+    check_launch("k_first_of_run");
+    // compact (lo, hi, perm) through the selection, preserving ALTO order
+    DevBuf<uint64_t> lo2(dedup_target), hi2(wide ? dedup_target : 0);
+    DevBuf<uint32_t> perm2(dedup_target);
+    B200_CUDA(cub::DeviceSelect::Flagged(nullptr, sb, keys_out.ptr, f.ptr, lo2.ptr, cnt.ptr, nnz, s));
+    if (sb > tmp_ptr->n) tmp_ptr->alloc(sb);
+    B200_CUDA(cub::DeviceSelect::Flagged(tmp_ptr->ptr, sb, keys_out.ptr, f.ptr, lo2.ptr, cnt.ptr, nnz, s));
+    B200_CUDA(cub::DeviceSelect::Flagged(tmp_ptr->ptr, sb, perm_out.ptr, f.ptr, perm2.ptr, cnt.ptr, nnz, s));
+    if (wide)
+      B200_CUDA(cub::DeviceSelect::Flagged(tmp_ptr->ptr, sb, sorted_hi.ptr, f.ptr, hi2.ptr, cnt.ptr, nnz, s));
+    count_launch(wide ? 3 : 2);
+    keys_out = std::move(lo2);
+    sorted_hi = std::move(hi2);
+    perm_out = std::move(perm2);
+    nnz = dedup_target;
+    t.nnz = nnz;
+  }
 
   // K3: key runs, duplicate check.
   t0 = std::chrono::steady_clock::now();
@@ -466,6 +544,56 @@ int blco_build_synthetic(const uint64_t* dims, int order, uint64_t nnz, uint64_t
       throw;
     }
     *out = t;
+  });
+}
+
+int blco_build_synthetic_draws(const uint64_t* dims, int order, uint64_t nnz, uint64_t seed,
+                               int skew, int target_bits, uint64_t max_nnz, int device,
+                               blco_tensor** out, blco_build_stats* stats) {
+  *out = nullptr;
+  return guarded([&] {
+    if (skew < 1 || skew > 64) throw_format("synth: skew exponent must lie in [1, 64]");
+    DeviceGuard dg(device);
+    DevBuf<uint64_t> ddims(order);
+    B200_CUDA(cudaMemcpy(ddims.ptr, dims, order * 8, cudaMemcpyHostToDevice));
+    uint64_t ncand = nnz + nnz / 8 + 1024;
+    for (int attempt = 0;; ++attempt) {
+      if (ncand >= (uint64_t{1} << 32) || attempt > 12)
+        throw_format("synth: cannot draw " + std::to_string(nnz) + " unique coordinates");
+      blco_tensor* t = new_tensor(dims, order, target_bits, max_nnz, device);
+      try {
+        DevBuf<uint32_t> coords(static_cast<size_t>(ncand) * order);
+        DevBuf<double> dv(ncand);
+        k_draws<<<grid_for(ncand, 2), kThreads>>>(seed, order, skew, ncand, ddims.ptr, coords.ptr, dv.ptr);
+        count_launch();
+        check_launch("k_draws");
+        build_from_device_coo(*t, coords, dv, ncand, stats, nnz);
+      } catch (const Status& st) {
+        delete t;
+        if (st.code != kRetryDraws) throw;
+        ncand = ncand * 3 / 2 + 1024;
+        continue;
+      } catch (...) {
+        delete t;
+        throw;
+      }
+      *out = t;
+      return;
+    }
+  });
+}
+
+int blco_synth_draws_host(int order, const uint64_t* dims, uint64_t ncand, uint64_t seed, int skew,
+                          uint64_t* idx, double* vals) {
+  return guarded([&] {
+    for (uint64_t j = 0; j < ncand; ++j) {
+      for (int m = 0; m < order; ++m) {
+        const double u = synth::unit(synth::mix64((seed ^ synth::kDrawSalt) +
+                                                   (j * order + m + 1) * synth::kGolden));
+        idx[static_cast<uint64_t>(m) * ncand + j] = synth::skewed_coord(u, dims[m], skew);
+      }
+      vals[j] = synth::element_value(seed, j);
+    }
   });
 }
 

@@ -482,7 +482,9 @@ int pull(void* ctx, blco_block_view* out) {
     }
     if (!b) return 0;
     if (b->linear_indices.size() != b->values.size()) throw FormatError("stream: malformed block");
-    *out = blco_block_view{b->key, b->nnz(), b->linear_indices.data(), b->values.data()};
+    // MemoryBlockSource blocks live in the caller's tensor for the whole call
+    *out = blco_block_view{b->key, b->nnz(), b->linear_indices.data(), b->values.data(),
+                           c->mem ? BLCO_BLOCK_STABLE : 0u};
     return 1;
   } catch (...) {
     c->error = std::current_exception();

@@ -24,6 +24,7 @@
 //   shared-memory stash (hierarchical path, :139-155), whose rows flush to
 //   the CTA's factor copy at the end (:210-215).
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "internal.hpp"
@@ -60,39 +61,181 @@ struct Params {
   unsigned long long* counters;  // [segments, stash flushes, commit lanes] or null
 };
 
+// ------------------------------------------------------------ staging layout
+// A staged element is its value plus its coordinates packed as u32 words:
+// words 0..N-2 hold the non-target modes (ascending), word N-1 the target row.
+// The words live structure-of-arrays in uint4 planes so one LDS.128 fetches
+// four of them; NM = ceil(N/4) planes.
 template <int N>
 struct Stage {
-  uint32_t coord[N][kWarpElems];
-  double val[kWarpElems];
-  uint8_t end[kWarpElems];
+  static constexpr int NM = (N + 3) / 4;
+  double* val;   // [W]
+  uint4* meta;   // [NM][W]
+  int W;
+
+  __device__ __forceinline__ void put(int j, double v, const uint32_t (&w)[4 * NM]) const {
+    val[j] = v;
+#pragma unroll
+    for (int q = 0; q < NM; ++q) meta[q * W + j] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+  }
+  __device__ __forceinline__ void get(int j, double& v, uint32_t (&w)[4 * NM]) const {
+    v = val[j];
+#pragma unroll
+    for (int q = 0; q < NM; ++q) {
+      const uint4 x = meta[q * W + j];
+      w[4 * q] = x.x, w[4 * q + 1] = x.y, w[4 * q + 2] = x.z, w[4 * q + 3] = x.w;
+    }
+  }
+  __device__ __forceinline__ uint32_t row(int j) const {
+    const uint32_t* plane = reinterpret_cast<const uint32_t*>(meta + ((N - 1) / 4) * W);
+    return plane[4 * j + (N - 1) % 4];
+  }
 };
 
-template <int CPL, bool VEC>
+template <int N>
+constexpr size_t stage_bytes(int W) {
+  return static_cast<size_t>(W) * (sizeof(double) + Stage<N>::NM * sizeof(uint4));
+}
+
+// Decodes one element into packed words (non-target modes ascending, row last).
+template <int N>
+__device__ __forceinline__ void decode(const Params<N>& p, const uint32_t (&base)[N], uint64_t ix,
+                                       uint32_t (&w)[4 * Stage<N>::NM]) {
+  uint32_t c[N];
+#pragma unroll
+  for (int m = 0; m < N; ++m) c[m] = base[m] | static_cast<uint32_t>((ix >> p.shift[m]) & p.mask[m]);
+#pragma unroll
+  for (int i = 0; i < 4 * Stage<N>::NM; ++i) w[i] = 0;
+  // compile-time slots only (selects, no dynamically indexed registers)
+#pragma unroll
+  for (int k = 0; k + 1 < N; ++k) w[k] = k < p.mode ? c[k] : c[k + 1];
+  uint32_t row = c[0];
+#pragma unroll
+  for (int m = 1; m < N; ++m) row = m == p.mode ? c[m] : row;
+  w[N - 1] = row;
+}
+
+// ------------------------------------------------------------ column layout
+// Lane q of a lane group owns columns col0 + q + c * LPE (c < CPL): every
+// factor-row load and every RED of the group touches LPE consecutive doubles,
+// so both are fully coalesced (a 32-column row = two 128-byte wavefronts).
+template <int CPL>
 struct Row {
   double v[CPL];
 };
 
-template <int CPL, bool VEC>
-__device__ __forceinline__ void load_row(Row<CPL, VEC>& r, const double* __restrict__ p, int ncol_ok) {
-  if constexpr (VEC && CPL == 2) {
-    const double2 x = __ldg(reinterpret_cast<const double2*>(p));
-    r.v[0] = x.x;
-    r.v[1] = x.y;
-  } else {
+// Computing phase.  The staged positions [lo0, lo0 + wn) are split among the
+// G lane groups of the warp; group starts are offset by h == 1 (mod 4)
+// positions so simultaneous LDS of the groups fall in disjoint banks.
+// Products accumulate in registers along a run of equal target rows and
+// commit once per run (and at the end of the group's range).
+template <int N, int LPE, int CPL, bool FULL, bool HIER>
+__device__ __forceinline__ void compute_range(const Params<N>& p, const Stage<N> st, int lo0, int wn,
+                                              int lane, int col0, double* __restrict__ copy_out,
+                                              double* stash, uint32_t* tags,
+                                              unsigned long long& commits,
+                                              unsigned long long& flushes) {
+  constexpr int G = 32 / LPE;
+  constexpr int NW = 4 * Stage<N>::NM;
+  const int g = lane / LPE, q = lane % LPE;
+  int h = wn / G;
+  if (G > 1 && h > 1) h = (h & ~3) | 1;
+  const int lo = lo0 + g * h;
+  const int hi = g == G - 1 ? lo0 + wn : lo0 + (g + 1) * h;
+  const int span = max(h, wn - (G - 1) * h);
+  const int R = p.rank;
+  const int col = col0 + q;
+  int ncol_ok = 0;
 #pragma unroll
-    for (int c = 0; c < CPL; ++c) r.v[c] = c < ncol_ok ? __ldg(p + c) : 0.0;
+  for (int c = 0; c < CPL; ++c) ncol_ok += (col + c * LPE < R);
+  const unsigned gmask = LPE == 32 ? kFull : (((1u << LPE) - 1u) << (g * LPE));
+  double acc[CPL];
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) acc[c] = 0.0;
+
+  constexpr int NO = N > 1 ? N - 1 : 1;
+  for (int t0 = 0; t0 < span; t0 += kUnroll) {
+    bool ok[kUnroll];
+    double v[kUnroll];
+    uint32_t w[kUnroll][NW];
+    Row<CPL> rows[kUnroll][NO];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int j = lo + t0 + u;
+      ok[u] = j < hi;
+      st.get(ok[u] ? j : lo0, v[u], w[u]);
+    }
+    const int jn = lo + t0 + kUnroll;
+    const uint32_t next_row = jn < hi ? st.row(jn) : 0xffffffffu;
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u)
+#pragma unroll
+      for (int k = 0; k < N - 1; ++k)
+        if (ok[u] && (FULL || ncol_ok > 0)) {
+          const double* rp = p.factors[k] + static_cast<uint64_t>(w[u][k]) * R;
+#pragma unroll
+          for (int c = 0; c < CPL; ++c)
+            rows[u][k].v[c] = (FULL || c < ncol_ok) ? __ldg(rp + col + c * LPE) : 0.0;
+        }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      if (!ok[u]) continue;
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        double prod = v[u];
+#pragma unroll
+        for (int k = 0; k < N - 1; ++k) prod = __dmul_rn(prod, rows[u][k].v[c]);
+        acc[c] = __dadd_rn(acc[c], prod);
+      }
+      const uint32_t row = w[u][N - 1];
+      const uint32_t nrow = u + 1 < kUnroll ? (ok[u + 1] ? w[u + 1][N - 1] : 0xffffffffu) : next_row;
+      if (nrow != row) {
+        if constexpr (HIER) {
+          const uint32_t slot = row % static_cast<uint32_t>(p.stash_slots);
+          int owned = 0;
+          if (q == 0) {
+            const uint32_t old = atomicCAS(&tags[slot], 0u, row + 1u);
+            owned = old == 0u || old == row + 1u;
+          }
+          owned = __shfl_sync(gmask, owned, g * LPE);
+          if (owned) {
+#pragma unroll
+            for (int c = 0; c < CPL; ++c)
+              if (FULL || c < ncol_ok) atomicAdd(&stash[static_cast<uint64_t>(slot) * R + col + c * LPE], acc[c]);
+          } else {
+#pragma unroll
+            for (int c = 0; c < CPL; ++c)
+              if (FULL || c < ncol_ok) atomicAdd(copy_out + static_cast<uint64_t>(row) * R + col + c * LPE, acc[c]);
+            if (q == 0) ++flushes;
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < CPL; ++c)
+            if (FULL || c < ncol_ok) atomicAdd(copy_out + static_cast<uint64_t>(row) * R + col + c * LPE, acc[c]);
+        }
+        if (FULL || ncol_ok > 0) ++commits;
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) acc[c] = 0.0;
+      }
+    }
   }
 }
 
-// Processing phase for one warp: stage up to kWarpElems elements with equal
-// target rows made contiguous within each 32-element sub-tile.  Returns the
-// staged count and adds the segment count to *segs.
+__device__ __forceinline__ uint32_t tile_count(const TileDesc& td, uint64_t elem_end) {
+  const uint64_t room = td.start >= elem_end ? 0 : elem_end - td.start;
+  return room < td.count ? static_cast<uint32_t>(room) : td.count;
+}
+
+// ------------------------------------------------ processing: paper variant
+// Per warp, per 32-element sub-tile (the reference's tile, mttkrp.cpp:23-81):
+// __match_any_sync groups equal target rows and a warp prefix sum over group
+// sizes places each group contiguously -- the stable reorder of :55-73
+// without the O(tile^2) rank.  Segments = groups.
 template <int N>
 __device__ __forceinline__ int process_warp(const Params<N>& p, const TileDesc& td, int warp,
-                                            int lane, Stage<N>& st, unsigned long long& segs) {
+                                            int lane, const Stage<N> st, unsigned long long& segs) {
   const uint32_t wbeg = static_cast<uint32_t>(warp) * kWarpElems;
-  const uint64_t room = td.start >= p.elem_end ? 0 : p.elem_end - td.start;
-  const uint32_t cnt = room < td.count ? static_cast<uint32_t>(room) : td.count;
+  const uint32_t cnt = tile_count(td, p.elem_end);
   const int wn = cnt > wbeg ? min(kWarpElems, static_cast<int>(cnt - wbeg)) : 0;
   if (wn == 0) return 0;
   uint32_t base[N];
@@ -112,13 +255,9 @@ __device__ __forceinline__ int process_warp(const Params<N>& p, const TileDesc& 
     if (s * 32 >= wn) break;
     const int j = s * 32 + lane;
     const bool valid = j < wn;
-    uint32_t c[N];
-#pragma unroll
-    for (int m = 0; m < N; ++m) c[m] = base[m] | static_cast<uint32_t>((ix[s] >> p.shift[m]) & p.mask[m]);
-    const uint32_t row = __ldg(p.block_base + static_cast<uint64_t>(td.block) * N + p.mode) |
-                         static_cast<uint32_t>((ix[s] >> p.shift[p.mode]) & p.mask[p.mode]);
-    // invalid lanes form the sentinel group; dims < 2^32 keep it distinct
-    const uint32_t key = valid ? row : 0xffffffffu;
+    uint32_t w[4 * Stage<N>::NM];
+    decode<N>(p, base, ix[s], w);
+    const uint32_t key = valid ? w[N - 1] : 0xffffffffu;  // dims < 2^31: never a real row
     const unsigned match = __match_any_sync(kFull, key);
     const int leader = __ffs(match) - 1;
     const int gsize = __popc(match);
@@ -131,118 +270,115 @@ __device__ __forceinline__ int process_warp(const Params<N>& p, const TileDesc& 
     const int excl = x - (lane == leader ? gsize : 0);
     const int goff = __shfl_sync(kFull, excl, leader);
     const int rin = __popc(match & ((1u << lane) - 1u));
-    if (valid) {
-      const int pos = s * 32 + goff + rin;
-#pragma unroll
-      for (int m = 0; m < N; ++m) st.coord[m][pos] = c[m];
-      st.val[pos] = vv[s];
-      st.end[pos] = rin == gsize - 1;
-    }
+    if (valid) st.put(s * 32 + goff + rin, vv[s], w);
     segs += __popc(__ballot_sync(kFull, valid && lane == leader));
   }
   __syncwarp();
   return wn;
 }
 
-// Computing phase: lane group g walks staged positions [lo, hi).
-template <int N, int LPE, int CPL, bool VEC, bool HIER>
-__device__ __forceinline__ void compute_warp(const Params<N>& p, const Stage<N>& st, int wn, int lane,
-                                             int col0, double* __restrict__ copy_out,
-                                             double* stash, uint32_t* tags,
-                                             unsigned long long& commits,
-                                             unsigned long long& flushes) {
-  constexpr int G = 32 / LPE;
-  const int g = lane / LPE, q = lane % LPE;
-  const int lo = (g * wn) / G, hi = ((g + 1) * wn) / G;
-  const int span = (wn + G - 1) / G;
-  const int R = p.rank;
-  const int cbase = col0 + q * CPL;
-  const int ncol_ok = max(0, min(CPL, R - cbase));
-  const unsigned gmask = LPE == 32 ? kFull : (((1u << LPE) - 1u) << (g * LPE));
-  double acc[CPL];
-#pragma unroll
-  for (int c = 0; c < CPL; ++c) acc[c] = 0.0;
+// ----------------------------------------- processing: CTA bucket grouping
+// The whole 1024-element tile is grouped by target row with a one-pass
+// counting sort on the row's low kBucketBits bits: a shared-memory histogram
+// (ATOMS.ADD gives each element its rank in its bucket), a block exclusive
+// scan, a scatter.  ALTO order makes a tile's rows a few short contiguous
+// ranges, so distinct rows almost never share a bucket and each row's
+// elements end up adjacent; a shared bucket only splits a run (one extra
+// commit), never mixes results.  Segments drop from ~0.91 to ~0.33 per
+// non-zero on NELL-2 (SURVEY §8a row a13 replaced).
+constexpr int kBucketBits = 11;
+constexpr int kBuckets = 1 << kBucketBits;
+constexpr int kItems = kTileElems / kCtaThreads;  // 4
 
-  constexpr int NO = N > 1 ? N - 1 : 1;  // non-target modes (array extent)
-  for (int t0 = 0; t0 < span; t0 += kUnroll) {
-    bool ok[kUnroll], fin[kUnroll];
-    double v[kUnroll];
-    uint32_t rowu[kUnroll];
-    uint32_t cm[kUnroll][NO];
-    Row<CPL, VEC> rows[kUnroll][NO];
+struct BucketShared {
+  uint32_t cnt[kBuckets];
+  uint32_t warp_sum[kWarps];
+};
+
+template <int N>
+__device__ __forceinline__ uint32_t process_cta(const Params<N>& p, const TileDesc& td, const Stage<N> st,
+                                                BucketShared& bs, unsigned long long& segs) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t cnt = tile_count(td, p.elem_end);
+  for (int i = tid; i < kBuckets; i += kCtaThreads) bs.cnt[i] = 0;
+  uint32_t base[N];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const int j = lo + t0 + u;
-      ok[u] = j < hi;
-      const int jc = ok[u] ? j : 0;
-      v[u] = st.val[jc];
-      rowu[u] = st.coord[p.mode][jc];
+  for (int m = 0; m < N; ++m) base[m] = __ldg(p.block_base + static_cast<uint64_t>(td.block) * N + m);
+  uint64_t ix[kItems];
+  double vv[kItems];
 #pragma unroll
-      for (int k = 0; k < N - 1; ++k) cm[u][k] = st.coord[p.others[k]][jc];
-      fin[u] = ok[u] && (st.end[jc] || j == hi - 1);
-    }
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u)
-#pragma unroll
-      for (int k = 0; k < N - 1; ++k)
-        if (ok[u] && ncol_ok > 0)
-          load_row<CPL, VEC>(rows[u][k], p.factors[k] + static_cast<uint64_t>(cm[u][k]) * R + cbase, ncol_ok);
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      if (!ok[u]) continue;
-#pragma unroll
-      for (int c = 0; c < CPL; ++c) {
-        double prod = v[u];
-#pragma unroll
-        for (int k = 0; k < N - 1; ++k) prod = __dmul_rn(prod, rows[u][k].v[c]);
-        acc[c] = __dadd_rn(acc[c], prod);
-      }
-      if (fin[u]) {
-        const uint32_t row = rowu[u];
-        if constexpr (HIER) {
-          const uint32_t slot = row % static_cast<uint32_t>(p.stash_slots);
-          int owned = 0;
-          if (q == 0) {
-            const uint32_t old = atomicCAS(&tags[slot], 0u, row + 1u);
-            owned = old == 0u || old == row + 1u;
-          }
-          owned = __shfl_sync(gmask, owned, g * LPE);
-          if (owned) {
-#pragma unroll
-            for (int c = 0; c < CPL; ++c)
-              if (c < ncol_ok) atomicAdd(&stash[static_cast<uint64_t>(slot) * R + cbase + c], acc[c]);
-          } else {
-#pragma unroll
-            for (int c = 0; c < CPL; ++c)
-              if (c < ncol_ok) atomicAdd(copy_out + static_cast<uint64_t>(row) * R + cbase + c, acc[c]);
-            if (q == 0) ++flushes;
-          }
-        } else {
-#pragma unroll
-          for (int c = 0; c < CPL; ++c)
-            if (c < ncol_ok) atomicAdd(copy_out + static_cast<uint64_t>(row) * R + cbase + c, acc[c]);
-        }
-        if (ncol_ok > 0) ++commits;
-#pragma unroll
-        for (int c = 0; c < CPL; ++c) acc[c] = 0.0;
-      }
-    }
+  for (int i = 0; i < kItems; ++i) {
+    const uint32_t e = tid + i * kCtaThreads;
+    ix[i] = e < cnt ? __ldcs(p.idx + td.start + e) : 0;
+    vv[i] = e < cnt ? __ldcs(p.val + td.start + e) : 0.0;
   }
+  __syncthreads();
+  uint32_t w[kItems][4 * Stage<N>::NM];
+  uint32_t rank[kItems];
+#pragma unroll
+  for (int i = 0; i < kItems; ++i) {
+    decode<N>(p, base, ix[i], w[i]);
+    const uint32_t e = tid + i * kCtaThreads;
+    rank[i] = e < cnt ? atomicAdd(&bs.cnt[w[i][N - 1] & (kBuckets - 1)], 1u) : 0;
+  }
+  __syncthreads();
+  // exclusive scan of the histogram: thread t owns buckets [8t, 8t+8)
+  constexpr int per = kBuckets / kCtaThreads;
+  uint32_t loc[per], run = 0;
+#pragma unroll
+  for (int i = 0; i < per; ++i) {
+    loc[i] = run;
+    run += bs.cnt[tid * per + i];
+  }
+  uint32_t x = run;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t y = __shfl_up_sync(kFull, x, d);
+    if (lane >= d) x += y;
+  }
+  if (lane == 31) bs.warp_sum[warp] = x;
+  __syncthreads();
+  uint32_t woff = 0;
+#pragma unroll
+  for (int i = 0; i < kWarps; ++i) woff += i < warp ? bs.warp_sum[i] : 0;
+  const uint32_t toff = woff + x - run;
+#pragma unroll
+  for (int i = 0; i < per; ++i) bs.cnt[tid * per + i] = toff + loc[i];
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < kItems; ++i) {
+    const uint32_t e = tid + i * kCtaThreads;
+    if (e < cnt) st.put(static_cast<int>(bs.cnt[w[i][N - 1] & (kBuckets - 1)] + rank[i]), vv[i], w[i]);
+  }
+  __syncthreads();
+  if (segs != ~0ull) {  // count runs (stats only)
+    unsigned n = 0;
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) {
+      const uint32_t j = tid * kItems + i;
+      if (j < cnt) n += j + 1 == cnt || st.row(j + 1) != st.row(j);
+    }
+    segs += n;
+  }
+  return cnt;
 }
 
-template <int N, int LPE, int CPL, bool VEC, bool STATS>
-__global__ void __launch_bounds__(kCtaThreads) k_mttkrp_register(Params<N> p) {
-  __shared__ Stage<N> stage[kWarps];
+template <int N, int LPE, int CPL, bool FULL, bool STATS>
+__global__ void __launch_bounds__(kCtaThreads) k_mttkrp_warp(Params<N> p) {
+  extern __shared__ __align__(16) unsigned char dyn[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const size_t per_warp = stage_bytes<N>(kWarpElems);
+  unsigned char* mine = dyn + warp * per_warp;
+  const Stage<N> st{reinterpret_cast<double*>(mine + Stage<N>::NM * sizeof(uint4) * kWarpElems),
+                    reinterpret_cast<uint4*>(mine), kWarpElems};
   const TileDesc td = p.tiles[blockIdx.x];
   unsigned long long segs = 0, commits = 0, flushes = 0;
-  const int wn = process_warp<N>(p, td, warp, lane, stage[warp], segs);
+  const int wn = process_warp<N>(p, td, warp, lane, st, segs);
   if (wn > 0)
-    compute_warp<N, LPE, CPL, VEC, false>(p, stage[warp], wn, lane, blockIdx.y * LPE * CPL, p.out,
-                                          nullptr, nullptr, commits, flushes);
+    compute_range<N, LPE, CPL, FULL, false>(p, st, 0, wn, lane, blockIdx.y * LPE * CPL, p.out, nullptr,
+                                            nullptr, commits, flushes);
   if constexpr (STATS) {
     if (lane == 0 && blockIdx.y == 0 && segs) atomicAdd(&p.counters[0], segs);
-    // commit lanes: count per lane, reduce over the warp
     unsigned long long c = commits;
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) c += __shfl_down_sync(kFull, c, d);
@@ -250,13 +386,47 @@ __global__ void __launch_bounds__(kCtaThreads) k_mttkrp_register(Params<N> p) {
   }
 }
 
-// Persistent CTAs; dynamic shared memory = stash (slots x R doubles + tags).
-template <int N, int LPE, int CPL, bool VEC, bool STATS>
-__global__ void __launch_bounds__(kCtaThreads) k_mttkrp_hier(Params<N> p) {
-  __shared__ Stage<N> stage[kWarps];
+template <int N>
+__device__ __forceinline__ Stage<N> cta_stage(unsigned char* dyn) {
+  return Stage<N>{reinterpret_cast<double*>(dyn + Stage<N>::NM * sizeof(uint4) * kTileElems),
+                  reinterpret_cast<uint4*>(dyn), kTileElems};
+}
+
+template <int N, int LPE, int CPL, bool FULL, bool STATS>
+__global__ void __launch_bounds__(kCtaThreads) k_mttkrp_sorted(Params<N> p) {
   extern __shared__ __align__(16) unsigned char dyn[];
+  __shared__ BucketShared bs;
+  const Stage<N> st = cta_stage<N>(dyn);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const TileDesc td = p.tiles[blockIdx.x];
+  unsigned long long segs = STATS ? 0 : ~0ull, commits = 0, flushes = 0;
+  const uint32_t cnt = process_cta<N>(p, td, st, bs, segs);
+  const int lo0 = warp * kWarpElems;
+  const int wn = static_cast<int>(cnt) > lo0 ? min(kWarpElems, static_cast<int>(cnt) - lo0) : 0;
+  if (wn > 0)
+    compute_range<N, LPE, CPL, FULL, false>(p, st, lo0, wn, lane, blockIdx.y * LPE * CPL, p.out, nullptr,
+                                            nullptr, commits, flushes);
+  if constexpr (STATS) {
+    unsigned long long s = blockIdx.y == 0 ? segs : 0, c = commits;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+      s += __shfl_down_sync(kFull, s, d);
+      c += __shfl_down_sync(kFull, c, d);
+    }
+    if (lane == 0 && s) atomicAdd(&p.counters[0], s);
+    if (lane == 0 && c) atomicAdd(&p.counters[2], c);
+  }
+}
+
+// Persistent CTAs; dynamic shared memory = tile stage + stash (slots x R
+// doubles + tags).
+template <int N, int LPE, int CPL, bool FULL, bool STATS>
+__global__ void __launch_bounds__(kCtaThreads) k_mttkrp_hier(Params<N> p) {
+  extern __shared__ __align__(16) unsigned char dyn[];
+  __shared__ BucketShared bs;
+  const Stage<N> st = cta_stage<N>(dyn);
   const int S = p.stash_slots, R = p.rank;
-  double* stash = reinterpret_cast<double*>(dyn);
+  double* stash = reinterpret_cast<double*>(dyn + stage_bytes<N>(kTileElems));
   uint32_t* tags = reinterpret_cast<uint32_t*>(stash + static_cast<uint64_t>(S) * R);
   for (int i = threadIdx.x; i < S * R; i += blockDim.x) stash[i] = 0.0;
   for (int i = threadIdx.x; i < S; i += blockDim.x) tags[i] = 0u;
@@ -265,16 +435,17 @@ __global__ void __launch_bounds__(kCtaThreads) k_mttkrp_hier(Params<N> p) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int copy = static_cast<int>(blockIdx.x % static_cast<unsigned>(p.ncopies));
   double* copy_out = p.out + static_cast<uint64_t>(copy) * p.copy_elems;
-  unsigned long long segs = 0, commits = 0, flushes = 0;
+  unsigned long long segs = STATS ? 0 : ~0ull, commits = 0, flushes = 0;
   for (uint64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
     const TileDesc td = p.tiles[tile];
-    const int wn = process_warp<N>(p, td, warp, lane, stage[warp], segs);
+    const uint32_t cnt = process_cta<N>(p, td, st, bs, segs);
+    const int lo0 = warp * kWarpElems;
+    const int wn = static_cast<int>(cnt) > lo0 ? min(kWarpElems, static_cast<int>(cnt) - lo0) : 0;
     if (wn > 0)
-      compute_warp<N, LPE, CPL, VEC, true>(p, stage[warp], wn, lane, blockIdx.y * LPE * CPL,
-                                           copy_out, stash, tags, commits, flushes);
-    __syncwarp();
+      compute_range<N, LPE, CPL, FULL, true>(p, st, lo0, wn, lane, blockIdx.y * LPE * CPL, copy_out, stash,
+                                             tags, commits, flushes);
+    __syncthreads();  // stage reused by the next tile
   }
-  __syncthreads();
   // Flush every occupied slot (one row commit each) to this CTA's copy.
   const int cols = min(R - static_cast<int>(blockIdx.y) * LPE * CPL, LPE * CPL);
   for (int i = threadIdx.x; i < S * cols; i += blockDim.x) {
@@ -285,13 +456,14 @@ __global__ void __launch_bounds__(kCtaThreads) k_mttkrp_hier(Params<N> p) {
   if constexpr (STATS) {
     unsigned long long occ = 0;
     for (int s = threadIdx.x; s < S; s += blockDim.x) occ += tags[s] != 0u;
-    unsigned long long c = commits, f = flushes + (blockIdx.y == 0 ? occ : 0);
+    unsigned long long sg = blockIdx.y == 0 ? segs : 0, c = commits, f = flushes + (blockIdx.y == 0 ? occ : 0);
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) {
+      sg += __shfl_down_sync(kFull, sg, d);
       c += __shfl_down_sync(kFull, c, d);
       f += __shfl_down_sync(kFull, f, d);
     }
-    if (lane == 0 && blockIdx.y == 0 && segs) atomicAdd(&p.counters[0], segs);
+    if (lane == 0 && sg) atomicAdd(&p.counters[0], sg);
     if (lane == 0 && f) atomicAdd(&p.counters[1], f);
     if (lane == 0 && c) atomicAdd(&p.counters[2], c);
   }
@@ -355,7 +527,22 @@ Workspace& workspace() {
   return t_ws;
 }
 
-template <int N, int LPE, int CPL, bool VEC>
+// Register-path processing variant: "sorted" (CTA-wide row sort, default)
+// or "warp" (the paper's 32-element tiles); BLCO_B200_VARIANT selects.
+bool use_warp_variant() {
+  static const bool warp = [] {
+    const char* e = std::getenv("BLCO_B200_VARIANT");
+    return e && std::string(e) == "warp";
+  }();
+  return warp;
+}
+
+template <class K>
+void set_smem(K kern, size_t dyn) {
+  B200_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn)));
+}
+
+template <int N, int LPE, int CPL, bool FULL>
 void launch_cfg(MttkrpLaunch& a) {
   const KernelView& v = a.view;
   const blco_layout& l = *v.layout;
@@ -383,18 +570,27 @@ void launch_cfg(MttkrpLaunch& a) {
   const unsigned ychunks = static_cast<unsigned>((a.rank + LPE * CPL - 1) / (LPE * CPL));
   if (!a.accumulate) B200_CUDA(cudaMemsetAsync(a.out, 0, elems * sizeof(double), a.stream));
   if (p.ntiles == 0) return;
+  const size_t tile_stage = stage_bytes<N>(kTileElems);
 
   if (a.strategy != BLCO_STRATEGY_HIERARCHICAL) {
     p.out = a.out;
     p.ncopies = 1;
     a.workgroups = p.ntiles;
     const dim3 grid(static_cast<unsigned>(p.ntiles), ychunks);
-    if (stats)
-      k_mttkrp_register<N, LPE, CPL, VEC, true><<<grid, kCtaThreads, 0, a.stream>>>(p);
-    else
-      k_mttkrp_register<N, LPE, CPL, VEC, false><<<grid, kCtaThreads, 0, a.stream>>>(p);
+    if (use_warp_variant()) {
+      const size_t dyn = stage_bytes<N>(kWarpElems) * kWarps;
+      auto kern = stats ? k_mttkrp_warp<N, LPE, CPL, FULL, true> : k_mttkrp_warp<N, LPE, CPL, FULL, false>;
+      set_smem(kern, dyn);
+      kern<<<grid, kCtaThreads, dyn, a.stream>>>(p);
+      count_launch();
+      check_launch("k_mttkrp_warp");
+      return;
+    }
+    auto kern = stats ? k_mttkrp_sorted<N, LPE, CPL, FULL, true> : k_mttkrp_sorted<N, LPE, CPL, FULL, false>;
+    set_smem(kern, tile_stage);
+    kern<<<grid, kCtaThreads, tile_stage, a.stream>>>(p);
     count_launch();
-    check_launch("k_mttkrp_register");
+    check_launch("k_mttkrp_sorted");
     return;
   }
 
@@ -404,8 +600,7 @@ void launch_cfg(MttkrpLaunch& a) {
   B200_CUDA(cudaGetDevice(&dev));
   B200_CUDA(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   B200_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  const size_t static_smem = sizeof(Stage<N>) * kWarps;
-  const size_t budget = static_cast<size_t>(smem_optin) - static_smem - 1024;
+  const size_t budget = static_cast<size_t>(smem_optin) - sizeof(BucketShared) - tile_stage - 1024;
   const size_t per_slot = a.rank * sizeof(double) + sizeof(uint32_t);
   const uint64_t fit = budget / per_slot;
   if (fit < 1)
@@ -414,9 +609,9 @@ void launch_cfg(MttkrpLaunch& a) {
   slots = std::max<uint64_t>(slots, std::min<uint64_t>(static_cast<uint64_t>(a.cfg.stash_slots), fit));
   p.stash_slots = static_cast<int>(slots);
   a.stash_slots = p.stash_slots;
-  const size_t dyn = slots * per_slot + 16;
-  auto kern = stats ? k_mttkrp_hier<N, LPE, CPL, VEC, true> : k_mttkrp_hier<N, LPE, CPL, VEC, false>;
-  B200_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn)));
+  const size_t dyn = tile_stage + slots * per_slot + 16;
+  auto kern = stats ? k_mttkrp_hier<N, LPE, CPL, FULL, true> : k_mttkrp_hier<N, LPE, CPL, FULL, false>;
+  set_smem(kern, dyn);
   int per_sm = 0;
   B200_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kCtaThreads, dyn));
   per_sm = std::max(per_sm, 1);
@@ -445,7 +640,7 @@ void launch_cfg(MttkrpLaunch& a) {
 template <int N>
 void launch_order(MttkrpLaunch& a) {
   switch (a.rank) {
-    case 8: return launch_cfg<N, 4, 2, true>(a);
+    case 8: return launch_cfg<N, 8, 1, true>(a);
     case 16: return launch_cfg<N, 8, 2, true>(a);
     case 32: return launch_cfg<N, 16, 2, true>(a);
     case 64: return launch_cfg<N, 32, 2, true>(a);
@@ -559,7 +754,7 @@ int blco_mttkrp(const blco_tensor* t, const double* const* factors, uint64_t ran
     std::vector<const double*> ptrs(l.order);
     for (int m = 0; m < l.order; ++m) {
       df[m].alloc(l.dims[m] * rank);
-      if (l.dims[m] * rank)
+      if (l.dims[m] * rank != 0)
         B200_CUDA(cudaMemcpy(df[m].ptr, factors[m], l.dims[m] * rank * 8, cudaMemcpyHostToDevice));
       ptrs[m] = df[m].ptr;
     }

@@ -204,8 +204,8 @@ extern "C" int blco_stream_mttkrp(const blco_layout* layout, uint64_t max_nnz_pe
         if (budget->injected_transfer_latency_s > 0)
           B200_CUDA(cudaLaunchHostFunc(q.stream, host_sleep, sleep_arg.data()));
         B200_CUDA(cudaEventRecord(tr.e, q.stream));
-        // pageable source memory may be reused by the source after next()
-        if (bv.nnz && (!is_pinned(bv.idx) || !is_pinned(bv.vals)))
+        // a transient source buffer may be overwritten by the next pull
+        if (bv.nnz && !(bv.flags & BLCO_BLOCK_STABLE) && (!is_pinned(bv.idx) || !is_pinned(bv.vals)))
           B200_CUDA(cudaEventSynchronize(tr.e));
 
         B200_CUDA(cudaEventRecord(cp.b, q.stream));

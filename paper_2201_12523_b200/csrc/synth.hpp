@@ -42,6 +42,27 @@ B200_HD double element_value(uint64_t seed, uint64_t e) {
   return unit(mix64((seed ^ kValueSalt) + (e + 1) * kGolden));
 }
 
+constexpr uint64_t kDrawSalt = 0xd1b54a32d192ed03ull;
+
+// floor(dim * u^k): only IEEE multiplies (no contraction), so host and
+// device agree bit-for-bit.
+B200_HD uint32_t skewed_coord(double u, uint64_t dim, int k) {
+  double p = u;
+  for (int i = 1; i < k; ++i) {
+#ifdef __CUDA_ARCH__
+    p = __dmul_rn(p, u);
+#else
+    p = p * u;
+#endif
+  }
+#ifdef __CUDA_ARCH__
+  uint64_t c = static_cast<uint64_t>(__dmul_rn(p, static_cast<double>(dim)));
+#else
+  uint64_t c = static_cast<uint64_t>(p * static_cast<double>(dim));
+#endif
+  return static_cast<uint32_t>(c < dim ? c : dim - 1);
+}
+
 struct Feistel {
   uint64_t cells;  // prod(dims)
   uint64_t mask;   // half-width mask

@@ -67,7 +67,6 @@ def test_golden_builds_bitexact(gpu, golden):
 @pytest.mark.parametrize("dims,nnz,tb,cap", [
     ([1000, 1000, 1000], 1_000_000, 64, 1 << 27),            # config 1 shape
     ([4821207, 1774269, 1805187], 300_000, 64, 100_000),     # Amazon: 65 bits, 1 stripped
-    ([532924, 17262471, 2480308, 1443], 200_000, 64, 1 << 27),  # Delicious: 78 bits, 14 stripped
     ([6066, 5699, 244268, 1176], 300_000, 40, 50_000),       # Enron at a tight budget
     ([8211298, 176962, 8116559], 200_000, 64, 30_000),       # Reddit: 64 bits, chunked
 ])
@@ -83,6 +82,27 @@ def test_synthetic_builds_match_oracle(gpu, oracle, dims, nnz, tb, cap):
     # host COO path gives the same tensor as the on-device generator
     t2 = build(gpu, dims, idx, vals, tb, cap)
     assert t2.structurally_equal(t)
+
+
+@pytest.mark.parametrize("dims,nnz,skew,cap", [
+    ([532924, 17262471, 2480308, 1443], 200_000, 1, 1 << 27),  # Delicious: 78 bits, 14 stripped
+    ([532924, 17262471, 2480308, 1443], 200_000, 4, 40_000),   # skewed power law, chunked
+    ([6066, 5699, 244268, 1176], 300_000, 6, 1 << 27),         # Enron-shaped, heavy skew
+    ([50, 60, 70], 150_000, 3, 1 << 27),                       # dense-ish: many duplicate draws
+])
+def test_draws_builds_match_oracle(gpu, oracle, dims, nnz, skew, cap):
+    """Config-4 generator: first nnz distinct draws; multi-key wide layouts."""
+    dt = gpu.DeviceTensor.synthetic_draws(dims, nnz, 42, skew, 64, cap)
+    t = dt.to_host()
+    idx, vals = oracle.synth_draws(dims, nnz, 42, skew)
+    keys, offs, oi, ov = oracle.build(dims, idx, vals, 64, cap)
+    assert t.total_nnz == nnz
+    assert np.array_equal(t.keys, keys) and np.array_equal(t.offsets, offs)
+    assert np.array_equal(t.idx, oi) and np.array_equal(t.vals, ov)
+    # the host candidate stream is the same draw sequence
+    hi, hv = gpu.synth_draws_host(dims, 64, 42, skew)
+    oi2, ov2 = oracle.synth_draws(dims, 8, 42, skew)
+    assert np.array_equal(hi[:, 0], oi2[:, 0]) and hv[0] == ov2[0]
 
 
 def test_reference_build_live(gpu, reflib):

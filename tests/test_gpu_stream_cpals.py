@@ -43,7 +43,8 @@ def test_streaming_matches_reference_stream(gpu, golden):
                            z[f"b{b}_offsets"], z[f"b{b}_idx"], z[f"b{b}_vals"])
         f = gpu.FactorMatrices(ent["rank"], [z[f"s{j}_f{m}"] for m in range(len(dims))])
         res = bm["max_nnz"] * 16
-        budget = gpu.DeviceBudget(factor_bytes(f, dims[0]) + 2 * res, 2, res)
+        # resident set: factors + output x copies (streaming.cpp:117-124)
+        budget = gpu.DeviceBudget(factor_bytes(f, dims[0]) + dims[0] * ent["rank"] * 8 + 2 * res, 2, res)
         for strat in (gpu.Strategy.Register, gpu.Strategy.Hierarchical):
             got = gpu.stream_mttkrp(t, f, 0, budget, gpu.ExecConfig(num_factor_copies=2), strat)
             assert rel_frobenius(got, z[f"s{j}_out"]) <= 1e-12
