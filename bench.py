@@ -197,7 +197,10 @@ def run_ours(args, world, rank_id, local):
     # --- build the BLCO tensor on the device (timed separately)
     bst = b.BuildStats()
     t0 = time.perf_counter()
-    full = b.DeviceTensor.synthetic(dims, nnz, TENSOR_SEED, device=dev, stats=bst)
+    if int(np.prod(np.array(dims, dtype=object))) < 2**64:
+        full = b.DeviceTensor.synthetic(dims, nnz, TENSOR_SEED, device=dev, stats=bst)
+    else:  # cell space beyond 2^64: independent uniform draws (skew 1), first nnz distinct
+        full = b.DeviceTensor.synthetic_draws(dims, nnz, TENSOR_SEED, 1, device=dev, stats=bst)
     build_s = time.perf_counter() - t0
     if world > 1:
         ranges = b.partition(full.block_nnz(), 1024, world)
@@ -275,7 +278,8 @@ def run_ours(args, world, rank_id, local):
     prof = ROOT / "profiles" / f"ncu_{args.config}.json"
     if prof.exists():
         try:
-            traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch_all_modes")
+            per_launch = json.loads(prof.read_text()).get("dram_bytes_per_launch_all_modes") or []
+            traffic = round(sum(per_launch) / len(per_launch)) if per_launch else None
         except ValueError:
             traffic = None
 
@@ -376,6 +380,84 @@ def e2e_run(b, torch, dt, dims, R, N, nnz, args, dev, world):
 # ------------------------------------------------------------ reference arm
 
 
+ALS_CONFIGS = {
+    # BASELINE configs[3]: 4-mode Delicious-shaped tensor with skewed power-law
+    # indices (floor(I * u^skew), first nnz distinct draws), R=16, 10 iterations
+    "delicious_als": ([532924, 17262471, 2480308, 1443], 140_126_181, 16, 4,
+                      "synthetic Delicious-shaped 532924x17262471x2480308x1443, 140,126,181 nnz, "
+                      "power-law draws floor(I*u^4), R=16, CP-ALS 10 iterations (BASELINE configs[3])"),
+    "enron_als": ([6066, 5699, 244268, 1176], 54_202_099, 16, 4,
+                  "synthetic Enron-shaped 6066x5699x244268x1176, 54,202,099 nnz, power-law draws floor(I*u^4), "
+                  "R=16, CP-ALS 10 iterations"),
+}
+
+
+def run_cpals(args):
+    """CP-ALS (proj/src/cpals.cpp:66-111) with every step on the device."""
+    import torch
+
+    import paper_2201_12523_b200 as b
+
+    dims, nnz, R, skew, desc = ALS_CONFIGS[args.config]
+    N = len(dims)
+    torch.cuda.set_device(0)
+    bst = b.BuildStats()
+    t0 = time.perf_counter()
+    dt = b.DeviceTensor.synthetic_draws(dims, nnz, TENSOR_SEED, skew, 64, 1 << 27, 0, bst)
+    build_s = time.perf_counter() - t0
+    cfg = b.ExecConfig(num_compute_units=torch.cuda.get_device_properties(0).multi_processor_count)
+    iters = 10
+    b.cp_als(dt, b.CpAlsOptions(rank=R, max_iters=2, tol=-1e300, seed=FACTOR_SEED), cfg)  # warm-up
+    torch.cuda.synchronize()
+    launches0 = b.kernel_launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(0) as clk:
+        e0.record()
+        model = b.cp_als(dt, b.CpAlsOptions(rank=R, max_iters=iters, tol=-1e300, seed=FACTOR_SEED), cfg)
+        e1.record()
+        torch.cuda.synchronize()
+    ms_iter = e0.elapsed_time(e1) / iters
+    # MTTKRP alone on the final factors: per-mode kernel time (roofline)
+    fac = [torch.from_numpy(a).cuda() for a in model.factors.factors]
+    outs = [torch.empty((d, R), dtype=torch.float64, device="cuda") for d in dims]
+    sptr = torch.cuda.current_stream().cuda_stream
+    for _ in range(3):
+        for m in range(N):
+            dt.mttkrp_device([a.data_ptr() for a in fac], R, m, outs[m].data_ptr(), config=cfg, stream=sptr)
+    mode_ms = []
+    for m in range(N):
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record()
+        for _ in range(5):
+            dt.mttkrp_device([a.data_ptr() for a in fac], R, m, outs[m].data_ptr(), config=cfg, stream=sptr)
+        a1.record()
+        torch.cuda.synchronize()
+        mode_ms.append(a0.elapsed_time(a1) / 5)
+    bpe = bytes_per_elem(N, R)
+    mttkrp_gbps = nnz * N * bpe / (sum(mode_ms) * 1e-3) / 1e9
+    peaks = {}
+    try:
+        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except (OSError, ValueError):
+        pass
+    peak = peaks.get("hbm_gbs") or 6650.0
+    print(json.dumps({
+        "metric": "CP-ALS time per iteration (N MTTKRPs + device Gram/solve/normalise + fit)",
+        "value": round(ms_iter, 3), "unit": "ms", "n_gpus": 1, "steps": iters, "warmup": 2,
+        "ms_per_step": round(ms_iter, 3), "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic power-law draws (seeded)",
+        "config": {"workload": desc, "dims": dims, "nnz": nnz, "rank": R, "skew": skew,
+                   "iterations": iters, "tol": "-inf (exactly 10 iterations, cpals.cpp:107)"},
+        "fit_history": model.fit_history,
+        "mttkrp_per_mode_ms": [round(x, 4) for x in mode_ms],
+        "roofline": {"bound": "hbm", "achieved": round(mttkrp_gbps, 2), "peak": peak, "unit": "GB/s",
+                     "frac": round(mttkrp_gbps / peak, 4), "traffic": None,
+                     "kernel": "k_mttkrp_sorted (one launch per mode)"},
+        "clocks": clk.summary(), "gpu_launches": b.kernel_launch_count() - launches0,
+        "build": {"seconds": round(build_s, 3), "nnz_per_s": round(nnz / build_s, 1)},
+    }), flush=True)
+
+
 def run_reference(args, world, rank_id):
     if rank_id != 0:
         return
@@ -420,7 +502,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", choices=sorted(CONFIGS), default="nell2")
+    ap.add_argument("--config", choices=sorted(CONFIGS) + sorted(ALS_CONFIGS), default="nell2")
     ap.add_argument("--rank", type=int, default=0)
     ap.add_argument("--strategy", choices=["Auto", "Register", "Hierarchical"], default="Auto")
     ap.add_argument("--no-e2e", action="store_true")
@@ -430,6 +512,13 @@ def main():
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
     world, rank_id, local = dist_env()
+    if args.config in ALS_CONFIGS:
+        if args.impl == "reference":
+            print(json.dumps({"impl": "reference", "unavailable": "CP-ALS reference timing not sampled "
+                              "(140M-nnz reference build needs ~10 GB and hours of CPU)"}), flush=True)
+        elif rank_id == 0:
+            run_cpals(args)
+        return
     if args.impl == "reference":
         run_reference(args, world, rank_id)
     else:
