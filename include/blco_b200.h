@@ -169,6 +169,16 @@ int blco_build_synthetic_draws(const uint64_t* dims, int order, uint64_t nnz, ui
 int blco_synth_draws_host(int order, const uint64_t* dims, uint64_t ncand, uint64_t seed, int skew,
                           uint64_t* idx, double* vals);
 
+/* Out-of-core generator (config 5): chunk `chunk` of `nchunks` equal ALTO
+ * ranges of a layout with no stripped bits.  ncand uniform ALTO candidates in
+ * the range; those decoding inside dims, deduplicated, are written in ALTO
+ * order to host_idx (re-encoded) / host_vals (capacity >= ncand); *count gets
+ * their number.  Concatenating chunks 0..nchunks-1 yields the BLCO element
+ * order of one uniform random tensor (a single key run). */
+int blco_synth_alto_chunk(const uint64_t* dims, int order, uint64_t chunk, uint64_t nchunks,
+                          uint64_t ncand, uint64_t seed, int device, uint64_t* host_idx,
+                          double* host_vals, uint64_t* count);
+
 /* Upload host-resident blocks (a reference BlcoTensor's payload). */
 int blco_tensor_upload(const blco_layout* layout, uint64_t max_nnz_per_block, uint64_t nblocks,
                        const uint64_t* keys, const uint64_t* block_nnz,

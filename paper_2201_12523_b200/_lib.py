@@ -10,7 +10,7 @@ import ctypes as C
 import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "lib" / "libblco_b200.so"
+LIB_PATH = Path(os.environ.get("BLCO_B200_LIB") or Path(__file__).resolve().parent / "lib" / "libblco_b200.so")
 
 MAX_ORDER = 32
 MAX_DEV_ORDER = 8
@@ -125,6 +125,7 @@ SIGNATURES = {
     "blco_build_synthetic_draws": (_I, [_PU64, _I, _U64, _U64, _I, _I, _U64, _I, C.POINTER(_P),
                                         C.POINTER(BuildStats)]),
     "blco_synth_draws_host": (_I, [_I, _PU64, _U64, _U64, _I, _PU64, _PD]),
+    "blco_synth_alto_chunk": (_I, [_PU64, _I, _U64, _U64, _U64, _U64, _I, _PU64, _PD, _PU64]),
     "blco_tensor_upload": (_I, [C.POINTER(Layout), _U64, _U64, _PU64, _PU64,
                                 C.POINTER(_P), C.POINTER(_P), _I, C.POINTER(_P)]),
     "blco_tensor_slice": (_I, [_P, _U64, _U64, _I, C.POINTER(_P)]),

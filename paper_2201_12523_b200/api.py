@@ -746,6 +746,17 @@ def synth_draws_host(dims: Sequence[int], ncand: int, seed: int, skew: int = 1):
     return idx, vals
 
 
+def synth_alto_chunk(dims: Sequence[int], chunk: int, nchunks: int, ncand: int, seed: int,
+                     idx_out: np.ndarray, vals_out: np.ndarray, device: int = 0) -> int:
+    """Chunk of an out-of-core uniform tensor, in BLCO order, into host arrays
+    (ideally pinned, see pinned_empty).  Returns the element count."""
+    n = C.c_uint64()
+    _check(lib.blco_synth_alto_chunk(_pu64(_u64(dims)), len(dims), chunk, nchunks, ncand, seed, device,
+                                     idx_out.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                     vals_out.ctypes.data_as(C.POINTER(C.c_double)), C.byref(n)))
+    return n.value
+
+
 def partition(block_nnz: Sequence[int], quota: int, nparts: int) -> list[tuple[int, int]]:
     """Contiguous nnz-balanced span ranges, one per GPU."""
     bn = _u64(block_nnz)

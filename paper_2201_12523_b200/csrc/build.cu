@@ -239,6 +239,47 @@ __global__ void k_draws(uint64_t seed, int order, int skew, uint64_t ncand,
   }
 }
 
+// ALTO-chunked generator (config 5): candidate j of a chunk is a uniform ALTO
+// value in [lo, lo + width); it is a cell of the tensor iff every decoded
+// coordinate lies inside dims.
+constexpr uint64_t kAltoSalt = 0x8cb92ba72f3d8dd7ull;
+
+__device__ __forceinline__ void alto_decode(const EncodeParams& p, uint64_t a, uint32_t (&c)[BLCO_MAX_DEV_ORDER]) {
+  for (int m = 0; m < BLCO_MAX_DEV_ORDER; ++m) c[m] = 0;
+  for (int q = 0; q < p.total_bits; ++q) c[p.imap_mode[q]] |= static_cast<uint32_t>((a >> q) & 1u) << p.imap_bit[q];
+}
+
+__global__ void k_alto_cand(EncodeParams p, uint64_t seed, uint64_t id0, uint64_t lo, uint64_t width,
+                            uint64_t ncand, uint64_t* __restrict__ alto, uint32_t* __restrict__ ids,
+                            uint8_t* __restrict__ flag) {
+  for (uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; j < ncand;
+       j += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t r = synth::mix64((seed ^ kAltoSalt) + (id0 + j + 1) * synth::kGolden);
+    const uint64_t a = lo + (width ? r % width : r);
+    bool ok = p.total_bits >= 64 || (a >> p.total_bits) == 0;
+    uint32_t c[BLCO_MAX_DEV_ORDER];
+    alto_decode(p, a, c);
+    for (int m = 0; m < p.order; ++m) ok = ok && c[m] < p.dims[m];
+    alto[j] = a;
+    ids[j] = static_cast<uint32_t>(j);
+    flag[j] = ok;
+  }
+}
+
+__global__ void k_alto_finish(EncodeParams p, uint64_t seed, uint64_t id0, uint64_t n,
+                              const uint64_t* __restrict__ alto, const uint32_t* __restrict__ ids,
+                              uint64_t* __restrict__ out_idx, double* __restrict__ out_val) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    uint32_t c[BLCO_MAX_DEV_ORDER];
+    alto_decode(p, alto[i], c);
+    uint64_t r = 0;
+    for (int m = 0; m < p.order; ++m) r |= (static_cast<uint64_t>(c[m]) & p.mask[m]) << p.shift[m];
+    out_idx[i] = r;
+    out_val[i] = synth::element_value(seed, id0 + ids[i]);
+  }
+}
+
 void build_from_device_coo(blco_tensor& t, DevBuf<uint32_t>& coords, DevBuf<double>& vals,
                            uint64_t nnz, blco_build_stats* stats, uint64_t dedup_target = 0) {
   const blco_layout& l = t.layout;
@@ -580,6 +621,72 @@ int blco_build_synthetic_draws(const uint64_t* dims, int order, uint64_t nnz, ui
       *out = t;
       return;
     }
+  });
+}
+
+int blco_synth_alto_chunk(const uint64_t* dims, int order, uint64_t chunk, uint64_t nchunks,
+                          uint64_t ncand, uint64_t seed, int device, uint64_t* host_idx,
+                          double* host_vals, uint64_t* count) {
+  return guarded([&] {
+    const blco_layout l = make_layout(dims, order, 64);
+    check_device_layout(l);
+    if (l.stripped_bits != 0 || l.total_bits < 1)
+      throw_format("synth: ALTO-chunked generation needs a layout with no stripped bits");
+    if (nchunks < 1 || chunk >= nchunks) throw_format("synth: chunk out of range");
+    if (ncand >= (uint64_t{1} << 32)) throw_format("synth: too many candidates per chunk");
+    const unsigned __int128 space = static_cast<unsigned __int128>(1) << l.total_bits;
+    const uint64_t width = static_cast<uint64_t>((space + nchunks - 1) / nchunks);
+    const uint64_t lo = static_cast<uint64_t>(space * chunk / nchunks);
+    DeviceGuard dg(device);
+    cudaStream_t s = 0;
+    DevBuf<uint64_t> alto(ncand), alto_s(ncand), out_idx(ncand), nsel(1);
+    DevBuf<uint32_t> ids(ncand), ids_s(ncand), ids_sel(ncand);
+    DevBuf<uint8_t> flag(ncand);
+    DevBuf<double> out_val(ncand);
+    const EncodeParams ep = encode_params(l);
+    // 1. candidates uniform in the chunk's ALTO range, valid iff every
+    //    decoded coordinate lies inside dims
+    k_alto_cand<<<grid_for(ncand, 2), kThreads, 0, s>>>(ep, seed, chunk * ncand, lo, width, ncand, alto.ptr,
+                                                        ids.ptr, flag.ptr);
+    count_launch();
+    check_launch("k_alto_cand");
+    size_t sb = 0;
+    B200_CUDA(cub::DeviceSelect::Flagged(nullptr, sb, alto.ptr, flag.ptr, alto_s.ptr, nsel.ptr, ncand, s));
+    DevBuf<unsigned char> tmp(sb);
+    B200_CUDA(cub::DeviceSelect::Flagged(tmp.ptr, sb, alto.ptr, flag.ptr, alto_s.ptr, nsel.ptr, ncand, s));
+    B200_CUDA(cub::DeviceSelect::Flagged(tmp.ptr, sb, ids.ptr, flag.ptr, ids_s.ptr, nsel.ptr, ncand, s));
+    count_launch(2);
+    uint64_t nv = 0;
+    B200_CUDA(cudaMemcpy(&nv, nsel.ptr, 8, cudaMemcpyDeviceToHost));
+    // 2. ALTO order (stable: equal keys keep candidate order)
+    size_t tb = 0;
+    B200_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, alto_s.ptr, alto.ptr, ids_s.ptr, ids.ptr, nv, 0,
+                                              l.total_bits, s));
+    if (tb > tmp.n) tmp.alloc(tb);
+    B200_CUDA(cub::DeviceRadixSort::SortPairs(tmp.ptr, tb, alto_s.ptr, alto.ptr, ids_s.ptr, ids.ptr, nv, 0,
+                                              l.total_bits, s));
+    count_launch();
+    // 3. duplicates: keep the first (earliest) candidate of each equal run
+    k_first_of_run<<<grid_for(nv, 4), kThreads, 0, s>>>(alto.ptr, nullptr, nv, flag.ptr, ids.ptr, UINT32_MAX);
+    count_launch();
+    check_launch("k_first_of_run");
+    B200_CUDA(cub::DeviceSelect::Flagged(nullptr, sb, alto.ptr, flag.ptr, alto_s.ptr, nsel.ptr, nv, s));
+    if (sb > tmp.n) tmp.alloc(sb);
+    B200_CUDA(cub::DeviceSelect::Flagged(tmp.ptr, sb, alto.ptr, flag.ptr, alto_s.ptr, nsel.ptr, nv, s));
+    B200_CUDA(cub::DeviceSelect::Flagged(tmp.ptr, sb, ids.ptr, flag.ptr, ids_sel.ptr, nsel.ptr, nv, s));
+    count_launch(2);
+    uint64_t n = 0;
+    B200_CUDA(cudaMemcpy(&n, nsel.ptr, 8, cudaMemcpyDeviceToHost));
+    alto = std::move(alto_s);
+    if (n) {
+      k_alto_finish<<<grid_for(n, 2), kThreads, 0, s>>>(ep, seed, chunk * ncand, n, alto.ptr, ids_sel.ptr,
+                                                         out_idx.ptr, out_val.ptr);
+      count_launch();
+      check_launch("k_alto_finish");
+      B200_CUDA(cudaMemcpy(host_idx, out_idx.ptr, n * 8, cudaMemcpyDeviceToHost));
+      B200_CUDA(cudaMemcpy(host_vals, out_val.ptr, n * 8, cudaMemcpyDeviceToHost));
+    }
+    *count = n;
   });
 }
 

@@ -93,36 +93,6 @@ struct Stage {
 };
 
 template <int N>
-__device__ __forceinline__ void decode(const Params<N>& p, const uint32_t (&base)[N], uint64_t ix,
-                                       uint32_t (&w)[4 * Stage<N>::NM]);
-
-// CTA-path staging: the element's raw 16-byte stream record {re-encoded
-// index, value} in grouped order; coordinates are re-derived with shift/mask
-// when the element is consumed (ALU is cheaper than shared-memory wavefronts,
-// and one LDS.128 per element serves any order N).
-template <int N>
-struct RecStage {
-  static constexpr int NM = Stage<N>::NM;
-  ulonglong2* rec;  // [W]
-  const Params<N>* p;
-  uint32_t base[N];
-  uint32_t rbase;
-
-  __device__ __forceinline__ void put(int j, uint64_t ix, double v) const {
-    rec[j] = make_ulonglong2(ix, static_cast<unsigned long long>(__double_as_longlong(v)));
-  }
-  __device__ __forceinline__ void get(int j, double& v, uint32_t (&w)[4 * NM]) const {
-    const ulonglong2 r = rec[j];
-    v = __longlong_as_double(static_cast<long long>(r.y));
-    decode<N>(*p, base, r.x, w);
-  }
-  __device__ __forceinline__ uint32_t row(int j) const {
-    const uint64_t ix = reinterpret_cast<const uint64_t*>(rec)[2 * j];
-    return rbase | static_cast<uint32_t>((ix >> p->shift[p->mode]) & p->mask[p->mode]);
-  }
-};
-
-template <int N>
 constexpr size_t stage_bytes(int W) {
   return static_cast<size_t>(W) * (sizeof(double) + Stage<N>::NM * sizeof(uint4));
 }
@@ -159,8 +129,8 @@ struct Row {
 // positions so simultaneous LDS of the groups fall in disjoint banks.
 // Products accumulate in registers along a run of equal target rows and
 // commit once per run (and at the end of the group's range).
-template <int N, int LPE, int CPL, bool FULL, bool HIER, class ST>
-__device__ __forceinline__ void compute_range(const Params<N>& p, const ST& st, int lo0, int wn,
+template <int N, int LPE, int CPL, bool FULL, bool HIER>
+__device__ __forceinline__ void compute_range(const Params<N>& p, const Stage<N> st, int lo0, int wn,
                                               int lane, int col0, double* __restrict__ copy_out,
                                               double* stash, uint32_t* tags,
                                               unsigned long long& commits,
@@ -319,10 +289,6 @@ __device__ __forceinline__ int process_warp(const Params<N>& p, const TileDesc& 
 constexpr int kBucketBits = 11;
 constexpr int kBuckets = 1 << kBucketBits;
 constexpr int kItems = kTileElems / kCtaThreads;  // 4
-#ifndef B200_SORTED_MIN_BLOCKS
-#define B200_SORTED_MIN_BLOCKS 3
-#endif
-constexpr int kSortedMinBlocks = B200_SORTED_MIN_BLOCKS;
 
 struct BucketShared {
   uint32_t cnt[kBuckets];
@@ -330,14 +296,14 @@ struct BucketShared {
 };
 
 template <int N>
-__device__ __forceinline__ uint32_t process_cta(const Params<N>& p, const TileDesc& td, RecStage<N>& st,
+__device__ __forceinline__ uint32_t process_cta(const Params<N>& p, const TileDesc& td, const Stage<N> st,
                                                 BucketShared& bs, unsigned long long& segs) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t cnt = tile_count(td, p.elem_end);
   for (int i = tid; i < kBuckets; i += kCtaThreads) bs.cnt[i] = 0;
+  uint32_t base[N];
 #pragma unroll
-  for (int m = 0; m < N; ++m) st.base[m] = __ldg(p.block_base + static_cast<uint64_t>(td.block) * N + m);
-  st.rbase = __ldg(p.block_base + static_cast<uint64_t>(td.block) * N + p.mode);
+  for (int m = 0; m < N; ++m) base[m] = __ldg(p.block_base + static_cast<uint64_t>(td.block) * N + m);
   uint64_t ix[kItems];
   double vv[kItems];
 #pragma unroll
@@ -347,12 +313,13 @@ __device__ __forceinline__ uint32_t process_cta(const Params<N>& p, const TileDe
     vv[i] = e < cnt ? __ldcs(p.val + td.start + e) : 0.0;
   }
   __syncthreads();
-  uint32_t bucket[kItems], rank[kItems];
+  uint32_t w[kItems][4 * Stage<N>::NM];
+  uint32_t rank[kItems];
 #pragma unroll
   for (int i = 0; i < kItems; ++i) {
+    decode<N>(p, base, ix[i], w[i]);
     const uint32_t e = tid + i * kCtaThreads;
-    bucket[i] = (st.rbase | static_cast<uint32_t>((ix[i] >> p.shift[p.mode]) & p.mask[p.mode])) & (kBuckets - 1);
-    rank[i] = e < cnt ? atomicAdd(&bs.cnt[bucket[i]], 1u) : 0;
+    rank[i] = e < cnt ? atomicAdd(&bs.cnt[w[i][N - 1] & (kBuckets - 1)], 1u) : 0;
   }
   __syncthreads();
   // exclusive scan of the histogram: thread t owns buckets [8t, 8t+8)
@@ -381,7 +348,7 @@ __device__ __forceinline__ uint32_t process_cta(const Params<N>& p, const TileDe
 #pragma unroll
   for (int i = 0; i < kItems; ++i) {
     const uint32_t e = tid + i * kCtaThreads;
-    if (e < cnt) st.put(static_cast<int>(bs.cnt[bucket[i]] + rank[i]), ix[i], vv[i]);
+    if (e < cnt) st.put(static_cast<int>(bs.cnt[w[i][N - 1] & (kBuckets - 1)] + rank[i]), vv[i], w[i]);
   }
   __syncthreads();
   if (segs != ~0ull) {  // count runs (stats only)
@@ -420,20 +387,16 @@ __global__ void __launch_bounds__(kCtaThreads) k_mttkrp_warp(Params<N> p) {
 }
 
 template <int N>
-__device__ __forceinline__ RecStage<N> cta_stage(unsigned char* dyn, const Params<N>& p) {
-  RecStage<N> st;
-  st.rec = reinterpret_cast<ulonglong2*>(dyn);
-  st.p = &p;
-  return st;
+__device__ __forceinline__ Stage<N> cta_stage(unsigned char* dyn) {
+  return Stage<N>{reinterpret_cast<double*>(dyn + Stage<N>::NM * sizeof(uint4) * kTileElems),
+                  reinterpret_cast<uint4*>(dyn), kTileElems};
 }
 
-constexpr size_t kRecStageBytes = sizeof(ulonglong2) * kTileElems;
-
 template <int N, int LPE, int CPL, bool FULL, bool STATS>
-__global__ void __launch_bounds__(kCtaThreads, kSortedMinBlocks) k_mttkrp_sorted(Params<N> p) {
+__global__ void __launch_bounds__(kCtaThreads) k_mttkrp_sorted(Params<N> p) {
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ BucketShared bs;
-  RecStage<N> st = cta_stage<N>(dyn, p);
+  const Stage<N> st = cta_stage<N>(dyn);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const TileDesc td = p.tiles[blockIdx.x];
   unsigned long long segs = STATS ? 0 : ~0ull, commits = 0, flushes = 0;
@@ -461,9 +424,9 @@ template <int N, int LPE, int CPL, bool FULL, bool STATS>
 __global__ void __launch_bounds__(kCtaThreads) k_mttkrp_hier(Params<N> p) {
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ BucketShared bs;
-  RecStage<N> st = cta_stage<N>(dyn, p);
+  const Stage<N> st = cta_stage<N>(dyn);
   const int S = p.stash_slots, R = p.rank;
-  double* stash = reinterpret_cast<double*>(dyn + kRecStageBytes);
+  double* stash = reinterpret_cast<double*>(dyn + stage_bytes<N>(kTileElems));
   uint32_t* tags = reinterpret_cast<uint32_t*>(stash + static_cast<uint64_t>(S) * R);
   for (int i = threadIdx.x; i < S * R; i += blockDim.x) stash[i] = 0.0;
   for (int i = threadIdx.x; i < S; i += blockDim.x) tags[i] = 0u;
@@ -607,7 +570,7 @@ void launch_cfg(MttkrpLaunch& a) {
   const unsigned ychunks = static_cast<unsigned>((a.rank + LPE * CPL - 1) / (LPE * CPL));
   if (!a.accumulate) B200_CUDA(cudaMemsetAsync(a.out, 0, elems * sizeof(double), a.stream));
   if (p.ntiles == 0) return;
-  const size_t tile_stage = kRecStageBytes;
+  const size_t tile_stage = stage_bytes<N>(kTileElems);
 
   if (a.strategy != BLCO_STRATEGY_HIERARCHICAL) {
     p.out = a.out;

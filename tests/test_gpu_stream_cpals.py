@@ -84,6 +84,39 @@ def test_oversized_budget(gpu):  # test_streaming.cpp:201-217
     assert rel_frobenius(got, want) <= 1e-12
 
 
+def test_alto_chunk_generator_is_blco_order(gpu, oracle):
+    """Config-5 generator: concatenated chunks are the BLCO element order of
+    the tensor they describe (same bytes as building that COO), and streaming
+    them equals the in-memory MTTKRP."""
+    dims, nchunks, ncand = [300, 200, 250], 5, 4000
+    idx = np.zeros(nchunks * ncand, np.uint64)
+    vals = np.zeros(nchunks * ncand)
+    off = 0
+    for c in range(nchunks):
+        off += gpu.api.synth_alto_chunk(dims, c, nchunks, ncand, 42, idx[off:], vals[off:])
+    idx, vals = idx[:off], vals[:off]
+    # valid fraction = prod(dims) / 2^total_bits = 15e6 / 2^25 = 0.447
+    assert 0.40 * nchunks * ncand < off < 0.50 * nchunks * ncand
+    layout = gpu.make_layout(dims, 64)
+    coords = np.array([gpu.delinearize(layout, int(i), 0) for i in idx], np.uint64).T
+    assert all((coords[m] < dims[m]).all() for m in range(3))
+    t = gpu.build_blco(gpu.SparseTensorCoo(dims, coords, vals), 64, 3000)
+    assert np.array_equal(t.idx, idx) and np.array_equal(t.vals, vals)
+    f = gpu.FactorMatrices.random(dims, 32, 3)
+    blocks = [(0, idx[o:o + 3000], vals[o:o + 3000]) for o in range(0, off, 3000)]
+    budget = gpu.DeviceBudget(capacity_bytes=1 << 30, num_queues=3, reservation_bytes=3000 * 16)
+    for mode in range(3):
+        want = oracle.mttkrp_coo(dims, coords, vals, f.factors, mode)
+        got = gpu.stream_mttkrp(iter(blocks), f, mode, budget, layout=layout, max_nnz_per_block=3000,
+                                block_count=len(blocks))
+        assert rel_frobenius(got, want) <= 1e-12
+    # determinism
+    idx2 = np.zeros(ncand, np.uint64)
+    vals2 = np.zeros(ncand)
+    n2 = gpu.api.synth_alto_chunk(dims, 0, nchunks, ncand, 42, idx2, vals2)
+    assert np.array_equal(idx2[:n2], idx[:n2])
+
+
 def test_cp_als_matches_reference(gpu, golden):
     """fit history within 1e-10 absolute, factors within 1e-8 relative."""
     z, meta = golden
