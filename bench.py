@@ -422,9 +422,10 @@ def run_cpals(args):
     with ClockSampler(0) as clk:
         model, ms_total = timed(iters)
         _, ms_two = timed(2)
-    # per-iteration cost without the call's fixed costs (allocation, random
-    # init, initial Grams, the final D2H of the factors into host memory)
-    ms_iter = (ms_total - ms_two) / (iters - 2)
+    # per-iteration device time of the ALS loop (CUDA events inside the C ABI
+    # around every iteration: N MTTKRPs + solve/normalise/Gram + fit); the
+    # call's fixed costs (allocation, init, final D2H of factors) excluded
+    ms_iter = model.device_ms["iterations_ms"] / model.device_ms["iterations"]
     # MTTKRP alone on the final factors: per-mode kernel time (roofline)
     fac = [torch.from_numpy(a).cuda() for a in model.factors.factors]
     outs = [torch.empty((d, R), dtype=torch.float64, device="cuda") for d in dims]
@@ -458,7 +459,10 @@ def run_cpals(args):
                    "iterations": iters, "tol": "-inf (exactly 10 iterations, cpals.cpp:107)"},
         "fit_history": model.fit_history,
         "cp_als_call_ms": {"iters_10": round(ms_total, 2), "iters_2": round(ms_two, 2),
-                           "note": "value = (T10 - T2) / 8: per-iteration device + host-sync cost"},
+                           "note": "whole API call incl. allocation and D2H of the factors"},
+        "device_ms": {"per_iteration": round(ms_iter, 3),
+                      "mttkrp_per_iteration": round(model.device_ms["mttkrp_ms"] / iters, 3),
+                      "dense_per_iteration": round(ms_iter - model.device_ms["mttkrp_ms"] / iters, 3)},
         "mttkrp_per_mode_ms": [round(x, 4) for x in mode_ms],
         "roofline": {"bound": "hbm", "achieved": round(mttkrp_gbps, 2), "peak": peak, "unit": "GB/s",
                      "frac": round(mttkrp_gbps / peak, 4), "traffic": None,

@@ -166,6 +166,27 @@ std::vector<BatchSpan> compute_batch_table(const BlcoTensor& t,
                                            std::uint64_t elements_per_workgroup);
 SparseTensorCoo delinearize_all(const BlcoTensor& t);
 
+// .blco container, byte-compatible with the reference; element validation of
+// read_blco_block runs on the device.
+void serialize_blco(const BlcoTensor& t, std::ostream& out);
+void save_blco(const BlcoTensor& t, const std::filesystem::path& path);
+BlcoTensor deserialize_blco(std::istream& in);
+BlcoTensor load_blco(const std::filesystem::path& path);
+
+struct BlcoHeader {
+  std::uint16_t version = 0;
+  std::vector<index_t> dims;
+  int target_bits = 0;
+  std::vector<int> mode_bits;
+  std::uint64_t max_nnz_per_block = 0;
+  std::uint64_t block_count = 0;
+
+  BitLayout make_layout_checked() const;
+};
+
+BlcoHeader read_blco_header(std::istream& in);
+BlcoBlock read_blco_block(std::istream& in, const BitLayout& layout);
+
 // ------------------------------------------------------------------ exec.hpp
 struct ExecConfig {
   int workgroup_size = 128;
@@ -233,6 +254,23 @@ class MemoryBlockSource final : public BlockSource {
 
  private:
   const BlcoTensor* t_;
+  std::uint64_t cursor_ = 0;
+};
+
+// Incremental `.blco` reader: header up front, one validated block per next().
+class FileBlockSource final : public BlockSource {
+ public:
+  explicit FileBlockSource(const std::filesystem::path& path);
+  ~FileBlockSource() override;
+  const BitLayout& layout() const override { return layout_; }
+  std::uint64_t block_count() const override { return header_.block_count; }
+  std::uint64_t max_nnz_per_block() const override { return header_.max_nnz_per_block; }
+  bool next(BlcoBlock& out) override;
+
+ private:
+  std::unique_ptr<std::istream> in_;
+  BlcoHeader header_;
+  BitLayout layout_;
   std::uint64_t cursor_ = 0;
 };
 

@@ -198,6 +198,21 @@ int blco_tensor_download(const blco_tensor* t, uint64_t* idx, double* vals);
 int blco_tensor_device_ptrs(const blco_tensor* t, const uint64_t** idx, const double** vals);
 void blco_tensor_free(blco_tensor* t);
 
+/* ------------------------------------------------------ .blco container
+ * Byte-compatible with the reference container (blco_format.hpp:67-93,
+ * blco_format.cpp:149-255).  Per-element validation of read_blco_block
+ * (field width, coordinates inside dims, ascending ALTO order; :201-227) runs
+ * on the device.  Messages match the reference ("blco: bad magic", ...). */
+int blco_save(const blco_tensor* t, const char* path);                   /* save_blco */
+int blco_load(const char* path, int device, blco_tensor** out);          /* load_blco */
+int blco_read_header(const char* path, blco_layout* layout, uint64_t* max_nnz_per_block,
+                     uint64_t* block_count, uint16_t* version);            /* read_blco_header */
+/* read_blco_block's element checks for one block (host or device indices) */
+int blco_validate_block(const blco_layout* layout, uint64_t key, uint64_t nnz, const uint64_t* idx,
+                        int device);
+int blco_validate_block_device(const blco_layout* layout, uint64_t key, uint64_t nnz,
+                               const uint64_t* d_idx);
+
 /* -------------------------------------------------------------- MTTKRP
  * mttkrp (proj/include/blco/mttkrp.hpp:110-112): host factors in, host M out
  * (dims[mode] x rank, overwritten). */
@@ -290,6 +305,17 @@ int blco_host_unregister(void* p);
 int blco_cp_als(const blco_tensor* t, uint64_t rank, int max_iters, double tol, uint64_t seed,
                 int strategy, const blco_exec_config* cfg, double* const* factors_out,
                 double* lambda_out, double* fit_out, int* iters_out);
+/* Same, plus device time of the iteration loop (CUDA events): iterations_ms
+ * covers every mode's MTTKRP + solve + normalise + Gram and the fit;
+ * mttkrp_ms the MTTKRP kernels alone. */
+typedef struct blco_cp_als_stats {
+  int32_t iterations;
+  double iterations_ms;
+  double mttkrp_ms;
+} blco_cp_als_stats;
+int blco_cp_als_timed(const blco_tensor* t, uint64_t rank, int max_iters, double tol, uint64_t seed,
+                      int strategy, const blco_exec_config* cfg, double* const* factors_out,
+                      double* lambda_out, double* fit_out, int* iters_out, blco_cp_als_stats* stats);
 int blco_fit(const blco_tensor* t, const double* const* factors, const double* lambda,
              uint64_t rank, const blco_exec_config* cfg, double* fit_out);
 

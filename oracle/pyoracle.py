@@ -285,6 +285,19 @@ class RefTensor:
         cat = lambda xs, dt: np.concatenate(xs) if xs else np.zeros(0, dt)  # noqa: E731
         return _u64(keys), _u64(offs), cat(ii, np.uint64), cat(vv, np.float64)
 
+    def serialize(self) -> bytes:
+        """serialize_blco of the reference tensor."""
+        lib = self.ref.lib
+        lib.ref_serialize.restype = C.c_uint64
+        lib.ref_serialize.argtypes = [C.c_void_p, C.c_char_p, C.c_uint64]
+        cap = 64 + 16 * (1 << 20)
+        while True:
+            buf = C.create_string_buffer(cap)
+            n = lib.ref_serialize(self.h, buf, cap)
+            if n:
+                return buf.raw[:n]
+            cap *= 4
+
     def batch_table(self) -> np.ndarray:
         n = self.ref.lib.ref_blco_batch(self.h, None)
         out = np.zeros((n, 3), np.uint64)

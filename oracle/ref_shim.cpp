@@ -7,6 +7,7 @@
 // ctypes.  No reference source is copied into this repository.
 #include <cstring>
 #include <exception>
+#include <sstream>
 #include <string>
 #include <vector>
 
@@ -150,6 +151,17 @@ int ref_blco_from_blocks(int order, const uint64_t* dims, int target_bits, uint6
 }
 
 void ref_blco_free(void* h) { delete static_cast<blco::BlcoTensor*>(h); }
+
+// serialize_blco into buf (capacity cap); returns the byte count (0 if it
+// does not fit).
+uint64_t ref_serialize(void* h, char* buf, uint64_t cap) {
+  std::ostringstream out;
+  blco::serialize_blco(*static_cast<blco::BlcoTensor*>(h), out);
+  const std::string s = out.str();
+  if (s.size() > cap) return 0;
+  std::memcpy(buf, s.data(), s.size());
+  return s.size();
+}
 
 uint64_t ref_blco_nblocks(void* h) { return static_cast<blco::BlcoTensor*>(h)->blocks.size(); }
 

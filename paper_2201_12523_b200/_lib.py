@@ -95,6 +95,10 @@ class StreamReport(C.Structure):
     ]
 
 
+class CpAlsStats(C.Structure):
+    _fields_ = [("iterations", C.c_int32), ("iterations_ms", C.c_double), ("mttkrp_ms", C.c_double)]
+
+
 SOURCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(BlockView))
 
 _P = C.c_void_p
@@ -134,6 +138,11 @@ SIGNATURES = {
     "blco_tensor_download": (_I, [_P, _PU64, _PD]),
     "blco_tensor_device_ptrs": (_I, [_P, C.POINTER(_P), C.POINTER(_P)]),
     "blco_tensor_free": (None, [_P]),
+    "blco_save": (_I, [_P, C.c_char_p]),
+    "blco_load": (_I, [C.c_char_p, _I, C.POINTER(_P)]),
+    "blco_read_header": (_I, [C.c_char_p, C.POINTER(Layout), _PU64, _PU64, C.POINTER(C.c_uint16)]),
+    "blco_validate_block": (_I, [C.POINTER(Layout), _U64, _U64, _PU64, _I]),
+    "blco_validate_block_device": (_I, [C.POINTER(Layout), _U64, _U64, _P]),
     "blco_mttkrp": (_I, [_P, C.POINTER(_P), _U64, _I, _I, C.POINTER(ExecCfg), _PD,
                          C.POINTER(MttkrpStats)]),
     "blco_mttkrp_device": (_I, [_P, C.POINTER(_P), _U64, _I, _I, C.POINTER(ExecCfg), _P, _I,
@@ -149,6 +158,8 @@ SIGNATURES = {
     "blco_host_unregister": (_I, [_P]),
     "blco_cp_als": (_I, [_P, _U64, _I, C.c_double, _U64, _I, C.POINTER(ExecCfg),
                          C.POINTER(_P), _PD, _PD, C.POINTER(_I)]),
+    "blco_cp_als_timed": (_I, [_P, _U64, _I, C.c_double, _U64, _I, C.POINTER(ExecCfg),
+                               C.POINTER(_P), _PD, _PD, C.POINTER(_I), C.POINTER(CpAlsStats)]),
     "blco_fit": (_I, [_P, C.POINTER(_P), _PD, _U64, C.POINTER(ExecCfg), _PD]),
     "blco_factors_random": (_I, [_PU64, _I, _U64, _U64, C.POINTER(_P)]),
     "blco_factors_random_device": (_I, [_PU64, _I, _U64, _U64, C.POINTER(_P), _P]),

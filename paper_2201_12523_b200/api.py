@@ -505,6 +505,86 @@ def build_blco(coo: SparseTensorCoo, target_bits: int = 64, max_nnz_per_block: i
     return t
 
 
+# ----------------------------------------------------------------- container
+
+
+@dataclass
+class BlcoHeader:
+    """blco::BlcoHeader (proj/include/blco/blco_format.hpp:77-87)."""
+    version: int
+    layout: BitLayout
+    max_nnz_per_block: int
+    block_count: int
+
+    @property
+    def dims(self) -> list[int]:
+        return self.layout.dims
+
+
+def save_blco(t, path) -> None:
+    """save_blco (blco_format.hpp:72): the reference's byte format."""
+    _check(lib.blco_save(_as_device(t).handle, str(path).encode()))
+
+
+def load_blco(path, device: int = 0) -> BlcoTensor:
+    """load_blco (blco_format.hpp:74): every element validated on the device."""
+    h = C.c_void_p()
+    _check(lib.blco_load(str(path).encode(), device, C.byref(h)))
+    dt = DeviceTensor(h.value, device)
+    t = dt.to_host()
+    t._device = dt
+    return t
+
+
+def read_blco_header(path) -> BlcoHeader:
+    """read_blco_header (blco_format.hpp:91): header only, payload untouched."""
+    c = L.Layout()
+    mx, nb, ver = C.c_uint64(), C.c_uint64(), C.c_uint16()
+    _check(lib.blco_read_header(str(path).encode(), C.byref(c), C.byref(mx), C.byref(nb), C.byref(ver)))
+    return BlcoHeader(ver.value, BitLayout(c), mx.value, nb.value)
+
+
+class FileBlockSource:
+    """blco::FileBlockSource (proj/include/blco/streaming.hpp:45-58): header up
+    front, one block record per iteration, each validated on the device."""
+
+    def __init__(self, path, device: int = 0):
+        self.header = read_blco_header(path)
+        self.layout = self.header.layout
+        self.max_nnz_per_block = self.header.max_nnz_per_block
+        self.device = device
+        self._f = open(path, "rb")
+        order = self.layout.order()
+        self._f.seek(4 + 2 + 2 + 8 * order + 2 + 2 * order + 8 + 8)
+        self._left = self.header.block_count
+
+    def block_count(self) -> int:
+        return self.header.block_count
+
+    def __iter__(self):
+        return self
+
+    def __next__(self):
+        if self._left == 0:
+            self._f.close()
+            raise StopIteration
+        raw = self._f.read(16)
+        if len(raw) < 16:
+            raise IoError("blco: truncated payload")
+        key, n = np.frombuffer(raw, np.uint64)
+        key, n = int(key), int(n)
+        if self.layout.stripped_bits < 64 and key >= (1 << self.layout.stripped_bits):
+            raise FormatError("blco: block key out of range")
+        idx = np.frombuffer(self._f.read(8 * n), np.uint64)
+        vals = np.frombuffer(self._f.read(8 * n), np.float64)
+        if idx.size < n or vals.size < n:
+            raise IoError("blco: truncated payload")
+        idx = np.ascontiguousarray(idx)
+        _check(lib.blco_validate_block(C.byref(self.layout._c), key, n, _pu64(idx), self.device))
+        self._left -= 1
+        return key, idx, np.ascontiguousarray(vals)
+
+
 # -------------------------------------------------------------------- MTTKRP
 
 
@@ -601,6 +681,11 @@ def stream_mttkrp(source, f: FactorMatrices, mode: int, budget: DeviceBudget,
         max_nnz_per_block = source.max_nnz_per_block
         block_count = int(source.keys.size)
         it = iter(source.blocks)
+    elif isinstance(source, FileBlockSource):
+        layout = source.layout
+        max_nnz_per_block = source.max_nnz_per_block
+        block_count = source.block_count()
+        it = iter(source)
     else:
         it = iter(source)
     f.validate(layout.dims)
@@ -701,14 +786,18 @@ def cp_als(t, opts: CpAlsOptions, config: ExecConfig | None = None) -> CpModel:
     fits = np.zeros(max(1, opts.max_iters))
     iters = C.c_int(0)
     c = config._c()
-    status = lib.blco_cp_als(d.handle, opts.rank, opts.max_iters, opts.tol, opts.seed,
-                             int(opts.strategy), C.byref(c), _ptr_array(fs), _pd(lam), _pd(fits),
-                             C.byref(iters))
+    st = L.CpAlsStats()
+    status = lib.blco_cp_als_timed(d.handle, opts.rank, opts.max_iters, opts.tol, opts.seed,
+                                   int(opts.strategy), C.byref(c), _ptr_array(fs), _pd(lam), _pd(fits),
+                                   C.byref(iters), C.byref(st))
     hist = [float(x) for x in fits[: iters.value]]
     if status == L.ERROR and (lib.blco_last_error() or b"").startswith(b"cp_als: non-finite"):
         raise CpAlsError(lib.blco_last_error().decode(), hist)
     _check(status)
-    return CpModel(FactorMatrices(opts.rank, fs), lam, hist, opts.seed)
+    model = CpModel(FactorMatrices(opts.rank, fs), lam, hist, opts.seed)
+    model.device_ms = {"iterations": st.iterations, "iterations_ms": st.iterations_ms,
+                       "mttkrp_ms": st.mttkrp_ms}
+    return model
 
 
 def fit(t, model: CpModel, config: ExecConfig | None = None) -> float:

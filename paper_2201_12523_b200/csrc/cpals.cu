@@ -12,7 +12,10 @@
 // then fit = 1 - sqrt(max(0, |X|^2 - 2<X,Xhat> + |Xhat|^2)) / |X|.
 // Summation orders differ from the sequential host loops, so parity is
 // tolerance-based.
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "internal.hpp"
@@ -300,6 +303,13 @@ extern "C" {
 int blco_cp_als(const blco_tensor* t, uint64_t rank, int max_iters, double tol, uint64_t seed,
                 int strategy, const blco_exec_config* cfg, double* const* factors_out,
                 double* lambda_out, double* fit_out, int* iters_out) {
+  return blco_cp_als_timed(t, rank, max_iters, tol, seed, strategy, cfg, factors_out, lambda_out, fit_out,
+                           iters_out, nullptr);
+}
+
+int blco_cp_als_timed(const blco_tensor* t, uint64_t rank, int max_iters, double tol, uint64_t seed,
+                      int strategy, const blco_exec_config* cfg, double* const* factors_out,
+                      double* lambda_out, double* fit_out, int* iters_out, blco_cp_als_stats* st) {
   return guarded([&] {
     if (rank < 1) throw_format("cp_als: rank must be >= 1");
     if (max_iters < 0) throw_format("cp_als: max_iters must be >= 0");
@@ -341,24 +351,58 @@ int blco_cp_als(const blco_tensor* t, uint64_t rank, int max_iters, double tol, 
     DevBuf<double> mt(maxrows * rank), mlast(l.dims[N - 1] * rank);
     double prev = 0.0;
     int it = 0;
+    // BLCO_B200_TRACE=1: synchronise after every step and report where the
+    // iteration time goes (stderr).
+    static const bool trace = std::getenv("BLCO_B200_TRACE") != nullptr;
+    double acc[6] = {0, 0, 0, 0, 0, 0};
+    auto t_last = std::chrono::steady_clock::now();
+    // device-time accounting (CUDA events on the legacy stream the loop runs on)
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_mt, ev_all;
+    auto mark = [](std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& v, bool begin) {
+      if (begin) {
+        v.emplace_back(nullptr, nullptr);
+        cudaEventCreate(&v.back().first);
+        cudaEventRecord(v.back().first, nullptr);
+      } else {
+        cudaEventCreate(&v.back().second);
+        cudaEventRecord(v.back().second, nullptr);
+      }
+    };
+    auto tick = [&](int slot) {
+      if (!trace) return;
+      cudaDeviceSynchronize();
+      const auto now = std::chrono::steady_clock::now();
+      acc[slot] += std::chrono::duration<double>(now - t_last).count();
+      t_last = now;
+    };
     for (; it < max_iters; ++it) {
+      if (st) mark(ev_all, true);
       for (int n = 0; n < N; ++n) {
         std::vector<double> v(static_cast<size_t>(R) * R, 1.0);
         for (int m = 0; m < N; ++m)
           if (m != n)
             for (size_t i = 0; i < v.size(); ++i) v[i] *= grams[m][i];
+        tick(5);
+        if (st) mark(ev_mt, true);
         mttkrp_into(*t, ptr, rank, n, strategy, c, mt.ptr);
+        if (st) mark(ev_mt, false);
         if (n == N - 1 && mlast.n)
           B200_CUDA(cudaMemcpy(mlast.ptr, mt.ptr, mlast.bytes(), cudaMemcpyDeviceToDevice));
+        tick(0);
         dense.solve(mt.ptr, l.dims[n], v);
+        tick(1);
         B200_CUDA(cudaMemcpy(A[n].ptr, mt.ptr, A[n].bytes(), cudaMemcpyDeviceToDevice));
+        tick(2);
         lambda = dense.normalize(A[n].ptr, l.dims[n]);
+        tick(3);
         grams[n] = dense.gram(A[n].ptr, l.dims[n]);
+        tick(4);
       }
       const double inner = dense.inner(mlast.ptr, A[N - 1].ptr, l.dims[N - 1], lambda);
       const double f = fit_value(xn, inner, recon_norm_sq(grams, lambda, R));
       fit_out[it] = f;
       *iters_out = it + 1;
+      if (st) mark(ev_all, false);
       if (!std::isfinite(f)) {
         emit();
         throw_error("cp_als: non-finite fit at iteration " + std::to_string(it + 1));
@@ -366,6 +410,27 @@ int blco_cp_als(const blco_tensor* t, uint64_t rank, int max_iters, double tol, 
       if (it > 0 && f - prev < tol) break;
       prev = f;
     }
+    if (st) {
+      B200_CUDA(cudaDeviceSynchronize());
+      auto sum = [](std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& v) {
+        double ms = 0;
+        for (auto& [a, b] : v) {
+          float x = 0;
+          if (a && b && cudaEventElapsedTime(&x, a, b) == cudaSuccess) ms += x;
+          if (a) cudaEventDestroy(a);
+          if (b) cudaEventDestroy(b);
+        }
+        return ms;
+      };
+      st->iterations = static_cast<int>(ev_all.size());
+      st->mttkrp_ms = sum(ev_mt);
+      st->iterations_ms = sum(ev_all);
+    }
+    if (trace)
+      std::fprintf(stderr,
+                   "[blco trace] cp_als %d iters: mttkrp %.3f s, solve %.3f s, copy %.3f s, normalize %.3f s, "
+                   "gram %.3f s, host %.3f s\n",
+                   it, acc[0], acc[1], acc[2], acc[3], acc[4], acc[5]);
     emit();
   });
 }

@@ -4,7 +4,10 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <fstream>
+#include <istream>
 #include <map>
+#include <ostream>
 #include <mutex>
 #include <numeric>
 #include <thread>
@@ -382,6 +385,136 @@ SparseTensorCoo delinearize_all(const BlcoTensor& t) {
       coo.values.push_back(b.values[e]);
     }
   return coo;
+}
+
+// --------------------------------------------------------------- container
+namespace {
+template <class T>
+void write_raw(std::ostream& out, const T& v) {
+  out.write(reinterpret_cast<const char*>(&v), sizeof(T));
+}
+
+template <class T>
+T read_raw(std::istream& in) {
+  T v{};
+  in.read(reinterpret_cast<char*>(&v), sizeof(T));
+  if (!in) throw IoError("blco: truncated payload");
+  return v;
+}
+
+template <class T>
+void read_vec(std::istream& in, std::vector<T>& v, std::size_t n) {
+  v.resize(n);
+  in.read(reinterpret_cast<char*>(v.data()), static_cast<std::streamsize>(n * sizeof(T)));
+  if (!in) throw IoError("blco: truncated payload");
+}
+}  // namespace
+
+void serialize_blco(const BlcoTensor& t, std::ostream& out) {
+  out.write("BLCO", 4);
+  write_raw<std::uint16_t>(out, 1);
+  write_raw<std::uint16_t>(out, static_cast<std::uint16_t>(t.order()));
+  for (index_t d : t.layout.dims) write_raw<std::uint64_t>(out, d);
+  write_raw<std::uint16_t>(out, static_cast<std::uint16_t>(t.layout.target_bits));
+  for (int b : t.layout.mode_bits) write_raw<std::uint16_t>(out, static_cast<std::uint16_t>(b));
+  write_raw<std::uint64_t>(out, t.max_nnz_per_block);
+  write_raw<std::uint64_t>(out, t.blocks.size());
+  for (const BlcoBlock& b : t.blocks) {
+    write_raw<std::uint64_t>(out, b.key);
+    write_raw<std::uint64_t>(out, b.nnz());
+    out.write(reinterpret_cast<const char*>(b.linear_indices.data()),
+              static_cast<std::streamsize>(b.nnz() * sizeof(index_t)));
+    out.write(reinterpret_cast<const char*>(b.values.data()),
+              static_cast<std::streamsize>(b.nnz() * sizeof(double)));
+  }
+  if (!out) throw IoError("blco: write failed");
+}
+
+void save_blco(const BlcoTensor& t, const std::filesystem::path& path) {
+  std::ofstream out(path, std::ios::binary);
+  if (!out) throw IoError("cannot open " + path.string() + " for writing");
+  serialize_blco(t, out);
+}
+
+BlcoHeader read_blco_header(std::istream& in) {
+  char magic[4] = {};
+  in.read(magic, 4);
+  if (!in || std::memcmp(magic, "BLCO", 4) != 0) throw FormatError("blco: bad magic");
+  BlcoHeader h;
+  h.version = read_raw<std::uint16_t>(in);
+  if (h.version != 1) throw FormatError("blco: unsupported format version " + std::to_string(h.version));
+  const auto order = read_raw<std::uint16_t>(in);
+  if (order < 1) throw FormatError("blco: order must be >= 1");
+  read_vec(in, h.dims, order);
+  h.target_bits = read_raw<std::uint16_t>(in);
+  std::vector<std::uint16_t> mb;
+  read_vec(in, mb, order);
+  h.mode_bits.assign(mb.begin(), mb.end());
+  h.max_nnz_per_block = read_raw<std::uint64_t>(in);
+  h.block_count = read_raw<std::uint64_t>(in);
+  return h;
+}
+
+BitLayout BlcoHeader::make_layout_checked() const {
+  BitLayout l = make_layout(dims, target_bits);
+  if (l.mode_bits != mode_bits) throw FormatError("blco: stored mode bit widths do not match dims");
+  if (max_nnz_per_block < 1) throw FormatError("blco: max_nnz_per_block must be >= 1");
+  return l;
+}
+
+BlcoBlock read_blco_block(std::istream& in, const BitLayout& layout) {
+  BlcoBlock blk;
+  blk.key = read_raw<std::uint64_t>(in);
+  if (layout.stripped_bits < 64 && blk.key >= (index_t{1} << layout.stripped_bits))
+    throw FormatError("blco: block key out of range");
+  const auto n = read_raw<std::uint64_t>(in);
+  read_vec(in, blk.linear_indices, n);
+  read_vec(in, blk.values, n);
+  const blco_layout c = to_c(layout);
+  ck(blco_validate_block(&c, blk.key, n, blk.linear_indices.data(), current_device()));
+  return blk;
+}
+
+BlcoTensor deserialize_blco(std::istream& in) {
+  const BlcoHeader h = read_blco_header(in);
+  BlcoTensor t;
+  t.layout = h.make_layout_checked();
+  t.max_nnz_per_block = h.max_nnz_per_block;
+  index_t prev = 0;
+  for (std::uint64_t b = 0; b < h.block_count; ++b) {
+    BlcoBlock blk = read_blco_block(in, t.layout);
+    if (blk.nnz() == 0) throw FormatError("blco: empty block record");
+    if (blk.nnz() > t.max_nnz_per_block) throw FormatError("blco: block exceeds max_nnz_per_block");
+    if (b > 0 && blk.key < prev) throw FormatError("blco: blocks not in ascending key order");
+    prev = blk.key;
+    t.total_nnz += blk.nnz();
+    t.blocks.push_back(std::move(blk));
+  }
+  t.batch_quota = kDefaultBatchQuota;
+  t.batch_table = compute_batch_table(t, t.batch_quota);
+  return t;
+}
+
+BlcoTensor load_blco(const std::filesystem::path& path) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw IoError("cannot open " + path.string());
+  return deserialize_blco(in);
+}
+
+FileBlockSource::FileBlockSource(const std::filesystem::path& path)
+    : in_(std::make_unique<std::ifstream>(path, std::ios::binary)) {
+  if (!*in_) throw IoError("cannot open " + path.string());
+  header_ = read_blco_header(*in_);
+  layout_ = header_.make_layout_checked();
+}
+
+FileBlockSource::~FileBlockSource() = default;
+
+bool FileBlockSource::next(BlcoBlock& out) {
+  if (cursor_ >= header_.block_count) return false;
+  out = read_blco_block(*in_, layout_);
+  ++cursor_;
+  return true;
 }
 
 // ------------------------------------------------------------------ config

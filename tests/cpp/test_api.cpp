@@ -4,7 +4,9 @@
 // proj/tests lines; a reference user's code compiles against these headers.
 #include <cmath>
 #include <cstdio>
+#include <filesystem>
 #include <functional>
+#include <sstream>
 #include <map>
 #include <set>
 #include <string>
@@ -334,6 +336,47 @@ TEST(budget_errors) {  // test_streaming.cpp:173-199
   b.capacity_bytes = factor_bytes(f, t.dims()[0]) + 16;
   MemoryBlockSource s2(t);
   CHECK_THROWS_AS(stream_mttkrp(s2, f, 0, b), FormatError);
+}
+
+TEST(serialize_roundtrip) {  // test_blco.cpp:124-135
+  auto t = build_blco(golden_tensor(), 5, 6);
+  std::ostringstream out;
+  serialize_blco(t, out);
+  std::istringstream in(out.str());
+  auto t2 = deserialize_blco(in);
+  CHECK(t.structurally_equal(t2));
+  std::ostringstream out2;
+  serialize_blco(t2, out2);
+  CHECK(out.str() == out2.str());
+  std::string bad = out.str();
+  bad[0] = 'X';
+  std::istringstream in_bad(bad);
+  CHECK_THROWS_AS(deserialize_blco(in_bad), FormatError);
+  std::istringstream in_trunc(out.str().substr(0, out.str().size() - 5));
+  CHECK_THROWS_AS(deserialize_blco(in_trunc), IoError);
+}
+
+TEST(file_source_streams) {  // test_streaming.cpp:81-103
+  Rng rng(97);
+  auto coo = random_coo(rng, {40, 30, 20}, 300);
+  auto t = build_blco(coo, 8, 40);
+  auto path = std::filesystem::temp_directory_path() / "b200_stream_test.blco";
+  save_blco(t, path);
+  auto f = random_factors(rng, coo.dims, 4);
+  ExecConfig cfg;
+  cfg.workgroup_size = 16;
+  cfg.tile_size = 4;
+  cfg.coarsening = 1;
+  auto want = mttkrp(t, f, 2, cfg, Strategy::Register);
+  DeviceBudget budget;
+  budget.num_queues = 2;
+  budget.reservation_bytes = t.max_nnz_per_block * 16;
+  budget.capacity_bytes = factor_bytes(f, t.dims()[2]) + 2 * budget.reservation_bytes;
+  FileBlockSource source(path);
+  auto got = stream_mttkrp(source, f, 2, budget, cfg, Strategy::Register);
+  CHECK(rel_frobenius(got, want) <= 1e-12);
+  CHECK(load_blco(path).structurally_equal(t));
+  std::filesystem::remove(path);
 }
 
 TEST(cp_als_monotone_noiseless) {  // SPEC.md:665 probe: rank-4 30^3 reaches a high fit

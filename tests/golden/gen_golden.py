@@ -115,6 +115,9 @@ def main() -> None:
                        f"b{k}_offsets": offs, f"b{k}_idx": bi, f"b{k}_vals": bv,
                        f"b{k}_batch": t.batch_table()})
         meta["builds"].append({"dims": dims, "target": tb, "max_nnz": cap})
+        # reference container bytes (serialize_blco) for the round-trip tests
+        if k in (0, 1, 5, 17, 18, 21):
+            arrays[f"b{k}_blco"] = np.frombuffer(t.serialize(), dtype=np.uint8)
         # D. mttkrp on this build: oracle::mttkrp_coo and blco::mttkrp
         #    (small modes only -- outputs are dims[mode] x rank)
         ranks = [] if max(dims) > 5000 else [2] if k < 3 else [1, 3, 8] if k % 2 else [16, 32]
