@@ -11,18 +11,15 @@
 // Device design:
 //   K1 k_encode   : one thread per element; ALTO (lo, hi) via a constant-memory
 //                   interleave map, re-encoded index via shift/mask.
-//   K2 sort       : CUB onesweep LSD radix sort of the 64-bit low ALTO word
-//                   carrying a 32-bit element id, then (total_bits > 64 only) a
-//                   stable sort of the high word -- LSD stability makes the
-//                   pair sort equal to a 128-bit sort.  Keys are unique unless
-//                   the input has duplicates, so any correct sort reproduces
-//                   std::stable_sort's order.
+//   K2 sort       : hand-written stable LSD radix sort (primitives.cu) of the
+//                   64-bit low ALTO word carrying a 32-bit element id, then
+//                   (total_bits > 64 only) a stable sort of the high word --
+//                   LSD stability makes the pair sort equal to a 128-bit
+//                   sort.  Keys are unique unless the input has duplicates, so
+//                   any correct sort reproduces std::stable_sort's order.
 //   K3 k_runs     : adjacent compare on the sorted ALTO words -> duplicate
-//                   flag + key-run starts (compacted with CUB select); the
-//                   host chunks the (few) runs; k_gather places idx/values.
-#include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_select.cuh>
-#include <thrust/iterator/counting_iterator.h>
+//                   flag + key-run starts (stable compaction, primitives.cu);
+//                   the host chunks the (few) runs; k_gather places idx/values.
 
 #include <algorithm>
 #include <chrono>
@@ -136,6 +133,12 @@ __global__ void k_encode(EncodeParams p, uint64_t nnz, const uint32_t* __restric
     reenc[e] = r;
     perm[e] = static_cast<uint32_t>(e);
   }
+}
+
+__global__ void k_iota(uint32_t* __restrict__ out, uint64_t n) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    out[i] = static_cast<uint32_t>(i);
 }
 
 template <class T>
@@ -306,44 +309,51 @@ void build_from_device_coo(blco_tensor& t, DevBuf<uint32_t>& coords, DevBuf<doub
   check_launch("k_encode");
   coords.reset();
 
-  // K2: LSD radix sort (low word, then high word), payload = element id.
+  // K2: stable LSD radix sort (low word, then high word), payload = element id
+  // (primitives.cu).  keys_out / perm_out receive the sorted low word and the
+  // final order.
   DevBuf<uint64_t> keys_out(nnz);
   DevBuf<uint32_t> perm_out(nnz);
-  size_t tmp_bytes = 0;
   const int lo_bits = std::max(1, std::min(64, l.total_bits));
-  B200_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, lo.ptr, keys_out.ptr, perm.ptr,
-                                            perm_out.ptr, nnz, 0, lo_bits, s));
-  DevBuf<unsigned char> tmp(tmp_bytes);
-  B200_CUDA(cub::DeviceRadixSort::SortPairs(tmp.ptr, tmp_bytes, lo.ptr, keys_out.ptr, perm.ptr,
-                                            perm_out.ptr, nnz, 0, lo_bits, s));
-  count_launch();
-  // sorted_lo = keys_out, order = perm_out
+  {
+    bool alt = false;
+    radix_sort_pairs<uint64_t>(lo.ptr, keys_out.ptr, perm.ptr, perm_out.ptr, nnz, 0, lo_bits, s, &alt);
+    if (!alt) {  // result still in (lo, perm): move it into (keys_out, perm_out)
+      std::swap(lo.ptr, keys_out.ptr);
+      std::swap(perm.ptr, perm_out.ptr);
+    }
+  }
   DevBuf<uint64_t> sorted_hi;
   if (wide) {
-    DevBuf<uint64_t> hi_g(nnz);
-    k_gather<uint64_t><<<grid_for(nnz, 4), kThreads, 0, s>>>(hi.ptr, perm_out.ptr, hi_g.ptr, nnz);
+    // high words in the low-word order, then a stable sort on them
+    sorted_hi.alloc(nnz);
+    k_gather<uint64_t><<<grid_for(nnz, 4), kThreads, 0, s>>>(hi.ptr, perm_out.ptr, sorted_hi.ptr, nnz);
     count_launch();
     check_launch("k_gather(hi)");
-    sorted_hi.alloc(nnz);
-    const int hi_bits = l.total_bits - 64;
-    size_t tb2 = 0;
-    B200_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb2, hi_g.ptr, sorted_hi.ptr, perm_out.ptr,
-                                              perm.ptr, nnz, 0, hi_bits, s));
-    if (tb2 > tmp.n) tmp.alloc(tb2);
-    B200_CUDA(cub::DeviceRadixSort::SortPairs(tmp.ptr, tb2, hi_g.ptr, sorted_hi.ptr, perm_out.ptr,
-                                              perm.ptr, nnz, 0, hi_bits, s));
+    // keep the sorted low word alongside: sort (hi, position) pairs, then
+    // gather both the element ids and the low words through the positions
+    DevBuf<uint32_t> pos(nnz), pos_alt(nnz);
+    k_iota<<<grid_for(nnz, 4), kThreads, 0, s>>>(pos.ptr, nnz);
     count_launch();
-    // final order in perm; re-gather the low word in that order
-    k_gather<uint64_t><<<grid_for(nnz, 4), kThreads, 0, s>>>(lo.ptr, perm.ptr, keys_out.ptr, nnz);
-    count_launch();
-    check_launch("k_gather(lo)");
-    std::swap(perm.ptr, perm_out.ptr);  // perm_out := final order
+    bool alt = false;
+    radix_sort_pairs<uint64_t>(sorted_hi.ptr, hi.ptr, pos.ptr, pos_alt.ptr, nnz, 0, l.total_bits - 64, s, &alt);
+    if (alt) {
+      std::swap(sorted_hi.ptr, hi.ptr);
+      std::swap(pos.ptr, pos_alt.ptr);
+    }
+    k_gather<uint32_t><<<grid_for(nnz, 4), kThreads, 0, s>>>(perm_out.ptr, pos.ptr, perm.ptr, nnz);
+    k_gather<uint64_t><<<grid_for(nnz, 4), kThreads, 0, s>>>(keys_out.ptr, pos.ptr, lo.ptr, nnz);
+    count_launch(2);
+    check_launch("k_gather(order)");
+    std::swap(perm.ptr, perm_out.ptr);
+    std::swap(lo.ptr, keys_out.ptr);
   }
+  lo.reset();
   hi.reset();
+  perm.reset();
   B200_CUDA(cudaStreamSynchronize(s));
   if (stats) stats->sort_seconds = secs(t0);
 
-  DevBuf<unsigned char>* tmp_ptr = &tmp;
   if (dedup_target) {
     // Candidates are sorted by (ALTO, candidate id): the first of each equal
     // run is the earliest draw.  Keep the dedup_target earliest unique draws.
@@ -352,22 +362,13 @@ void build_from_device_coo(blco_tensor& t, DevBuf<uint32_t>& coords, DevBuf<doub
                                                          nnz, f.ptr, perm_out.ptr, UINT32_MAX);
     count_launch();
     check_launch("k_first_of_run");
-    DevBuf<uint32_t> ids(nnz), ids_sorted(nnz);
-    DevBuf<uint64_t> cnt(1);
-    size_t sb = 0;
-    B200_CUDA(cub::DeviceSelect::Flagged(nullptr, sb, perm_out.ptr, f.ptr, ids.ptr, cnt.ptr, nnz, s));
-    if (sb > tmp_ptr->n) tmp_ptr->alloc(sb);
-    B200_CUDA(cub::DeviceSelect::Flagged(tmp_ptr->ptr, sb, perm_out.ptr, f.ptr, ids.ptr, cnt.ptr, nnz, s));
-    count_launch();
-    uint64_t uniq = 0;
-    B200_CUDA(cudaMemcpy(&uniq, cnt.ptr, 8, cudaMemcpyDeviceToHost));
+    DevBuf<uint32_t> ids(nnz), ids_alt(nnz), dummy(nnz), dummy_alt(nnz);
+    const uint64_t uniq = select_flagged<uint32_t>(perm_out.ptr, f.ptr, nnz, ids.ptr, s);
     if (uniq < dedup_target) throw Status(kRetryDraws, "synth: not enough unique draws");
-    B200_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, sb, ids.ptr, ids_sorted.ptr, uniq, 0, 32, s));
-    if (sb > tmp_ptr->n) tmp_ptr->alloc(sb);
-    B200_CUDA(cub::DeviceRadixSort::SortKeys(tmp_ptr->ptr, sb, ids.ptr, ids_sorted.ptr, uniq, 0, 32, s));
-    count_launch();
+    bool alt = false;
+    radix_sort_pairs<uint32_t>(ids.ptr, ids_alt.ptr, dummy.ptr, dummy_alt.ptr, uniq, 0, 32, s, &alt);
     uint32_t last = 0;
-    B200_CUDA(cudaMemcpy(&last, ids_sorted.ptr + (dedup_target - 1), 4, cudaMemcpyDeviceToHost));
+    B200_CUDA(cudaMemcpy(&last, (alt ? ids_alt.ptr : ids.ptr) + (dedup_target - 1), 4, cudaMemcpyDeviceToHost));
     k_first_of_run<<<grid_for(nnz, 4), kThreads, 0, s>>>(keys_out.ptr, wide ? sorted_hi.ptr : nullptr,
                                                          nnz, f.ptr, perm_out.ptr, last);
     count_launch();
@@ -375,13 +376,9 @@ void build_from_device_coo(blco_tensor& t, DevBuf<uint32_t>& coords, DevBuf<doub
     // compact (lo, hi, perm) through the selection, preserving ALTO order
     DevBuf<uint64_t> lo2(dedup_target), hi2(wide ? dedup_target : 0);
     DevBuf<uint32_t> perm2(dedup_target);
-    B200_CUDA(cub::DeviceSelect::Flagged(nullptr, sb, keys_out.ptr, f.ptr, lo2.ptr, cnt.ptr, nnz, s));
-    if (sb > tmp_ptr->n) tmp_ptr->alloc(sb);
-    B200_CUDA(cub::DeviceSelect::Flagged(tmp_ptr->ptr, sb, keys_out.ptr, f.ptr, lo2.ptr, cnt.ptr, nnz, s));
-    B200_CUDA(cub::DeviceSelect::Flagged(tmp_ptr->ptr, sb, perm_out.ptr, f.ptr, perm2.ptr, cnt.ptr, nnz, s));
-    if (wide)
-      B200_CUDA(cub::DeviceSelect::Flagged(tmp_ptr->ptr, sb, sorted_hi.ptr, f.ptr, hi2.ptr, cnt.ptr, nnz, s));
-    count_launch(wide ? 3 : 2);
+    select_flagged<uint64_t>(keys_out.ptr, f.ptr, nnz, lo2.ptr, s);
+    select_flagged<uint32_t>(perm_out.ptr, f.ptr, nnz, perm2.ptr, s);
+    if (wide) select_flagged<uint64_t>(sorted_hi.ptr, f.ptr, nnz, hi2.ptr, s);
     keys_out = std::move(lo2);
     sorted_hi = std::move(hi2);
     perm_out = std::move(perm2);
@@ -405,16 +402,7 @@ void build_from_device_coo(blco_tensor& t, DevBuf<uint32_t>& coords, DevBuf<doub
   if (dup) throw_format("blco: duplicate coordinate tuple in input");
 
   DevBuf<uint64_t> run_starts(nnz);
-  DevBuf<uint64_t> nsel(1);
-  size_t sb = 0;
-  thrust::counting_iterator<uint64_t> iota(0);
-  B200_CUDA(cub::DeviceSelect::Flagged(nullptr, sb, iota, flags.ptr, run_starts.ptr, nsel.ptr, nnz, s));
-  if (sb > tmp.n) tmp.alloc(sb);
-  B200_CUDA(cub::DeviceSelect::Flagged(tmp.ptr, sb, iota, flags.ptr, run_starts.ptr, nsel.ptr, nnz, s));
-  count_launch();
-  uint64_t nruns = 0;
-  B200_CUDA(cudaMemcpyAsync(&nruns, nsel.ptr, sizeof nruns, cudaMemcpyDeviceToHost, s));
-  B200_CUDA(cudaStreamSynchronize(s));
+  const uint64_t nruns = select_flagged<uint64_t>(nullptr, flags.ptr, nnz, run_starts.ptr, s);
   std::vector<uint64_t> starts(nruns);
   B200_CUDA(cudaMemcpy(starts.data(), run_starts.ptr, nruns * sizeof(uint64_t), cudaMemcpyDeviceToHost));
   // block key of each run, read off the sorted ALTO words at the run start
@@ -639,7 +627,7 @@ int blco_synth_alto_chunk(const uint64_t* dims, int order, uint64_t chunk, uint6
     const uint64_t lo = static_cast<uint64_t>(space * chunk / nchunks);
     DeviceGuard dg(device);
     cudaStream_t s = 0;
-    DevBuf<uint64_t> alto(ncand), alto_s(ncand), out_idx(ncand), nsel(1);
+    DevBuf<uint64_t> alto(ncand), alto_s(ncand), out_idx(ncand);
     DevBuf<uint32_t> ids(ncand), ids_s(ncand), ids_sel(ncand);
     DevBuf<uint8_t> flag(ncand);
     DevBuf<double> out_val(ncand);
@@ -650,33 +638,21 @@ int blco_synth_alto_chunk(const uint64_t* dims, int order, uint64_t chunk, uint6
                                                         ids.ptr, flag.ptr);
     count_launch();
     check_launch("k_alto_cand");
-    size_t sb = 0;
-    B200_CUDA(cub::DeviceSelect::Flagged(nullptr, sb, alto.ptr, flag.ptr, alto_s.ptr, nsel.ptr, ncand, s));
-    DevBuf<unsigned char> tmp(sb);
-    B200_CUDA(cub::DeviceSelect::Flagged(tmp.ptr, sb, alto.ptr, flag.ptr, alto_s.ptr, nsel.ptr, ncand, s));
-    B200_CUDA(cub::DeviceSelect::Flagged(tmp.ptr, sb, ids.ptr, flag.ptr, ids_s.ptr, nsel.ptr, ncand, s));
-    count_launch(2);
-    uint64_t nv = 0;
-    B200_CUDA(cudaMemcpy(&nv, nsel.ptr, 8, cudaMemcpyDeviceToHost));
+    const uint64_t nv = select_flagged<uint64_t>(alto.ptr, flag.ptr, ncand, alto_s.ptr, s);
+    select_flagged<uint32_t>(ids.ptr, flag.ptr, ncand, ids_s.ptr, s);
     // 2. ALTO order (stable: equal keys keep candidate order)
-    size_t tb = 0;
-    B200_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, alto_s.ptr, alto.ptr, ids_s.ptr, ids.ptr, nv, 0,
-                                              l.total_bits, s));
-    if (tb > tmp.n) tmp.alloc(tb);
-    B200_CUDA(cub::DeviceRadixSort::SortPairs(tmp.ptr, tb, alto_s.ptr, alto.ptr, ids_s.ptr, ids.ptr, nv, 0,
-                                              l.total_bits, s));
-    count_launch();
+    bool alt = false;
+    radix_sort_pairs<uint64_t>(alto_s.ptr, alto.ptr, ids_s.ptr, ids.ptr, nv, 0, l.total_bits, s, &alt);
+    if (!alt) {
+      std::swap(alto_s.ptr, alto.ptr);
+      std::swap(ids_s.ptr, ids.ptr);
+    }
     // 3. duplicates: keep the first (earliest) candidate of each equal run
     k_first_of_run<<<grid_for(nv, 4), kThreads, 0, s>>>(alto.ptr, nullptr, nv, flag.ptr, ids.ptr, UINT32_MAX);
     count_launch();
     check_launch("k_first_of_run");
-    B200_CUDA(cub::DeviceSelect::Flagged(nullptr, sb, alto.ptr, flag.ptr, alto_s.ptr, nsel.ptr, nv, s));
-    if (sb > tmp.n) tmp.alloc(sb);
-    B200_CUDA(cub::DeviceSelect::Flagged(tmp.ptr, sb, alto.ptr, flag.ptr, alto_s.ptr, nsel.ptr, nv, s));
-    B200_CUDA(cub::DeviceSelect::Flagged(tmp.ptr, sb, ids.ptr, flag.ptr, ids_sel.ptr, nsel.ptr, nv, s));
-    count_launch(2);
-    uint64_t n = 0;
-    B200_CUDA(cudaMemcpy(&n, nsel.ptr, 8, cudaMemcpyDeviceToHost));
+    const uint64_t n = select_flagged<uint64_t>(alto.ptr, flag.ptr, nv, alto_s.ptr, s);
+    select_flagged<uint32_t>(ids.ptr, flag.ptr, nv, ids_sel.ptr, s);
     alto = std::move(alto_s);
     if (n) {
       k_alto_finish<<<grid_for(n, 2), kThreads, 0, s>>>(ep, seed, chunk * ncand, n, alto.ptr, ids_sel.ptr,

@@ -153,6 +153,17 @@ struct MttkrpLaunch {
   int stash_slots = 0;                     // out
 };
 
+// primitives.cu: hand-written sort / scan / compaction (construction path)
+void scan_exclusive_u64(const uint64_t* in, uint64_t* out, uint64_t n, cudaStream_t s);
+// Stable LSD sort on bits [begin_bit, end_bit); the result lands in the
+// *_alt buffers iff *result_in_alt.
+template <class K>
+void radix_sort_pairs(K* keys, K* keys_alt, uint32_t* vals, uint32_t* vals_alt, uint64_t n, int begin_bit,
+                      int end_bit, cudaStream_t s, bool* result_in_alt);
+// Stable compaction; in == nullptr writes the element indices.  Returns count.
+template <class T>
+uint64_t select_flagged(const T* in, const uint8_t* flags, uint64_t n, T* out, cudaStream_t s);
+
 KernelView view_of(const blco_tensor& t);
 void mttkrp_enqueue(MttkrpLaunch& a);
 void merge_copies_enqueue(const double* copies, uint64_t elems, int ncopies, double* out,

@@ -1,0 +1,252 @@
+// primitives.cu -- hand-written device primitives for BLCO construction:
+// a stable LSD radix sort of (key, u32 payload) pairs, an exclusive scan and a
+// flagged compaction.  They replace CUB on the construction path (K2/K3);
+// CUB's DeviceRadixSort stays only as the cross-check in the GPU tests.
+//
+// Radix sort, per 8-bit digit pass over tiles of 4096 elements (256 threads x
+// 16 items, striped: item s of thread t is element s*256 + t of the tile):
+//   k_digit_hist : per-tile 256-bin histogram -> hist[digit * ntiles + tile]
+//   scan         : exclusive scan of hist (digit-major) -> global offsets
+//   k_digit_scatter : stable in-tile ranks (warp __match_any_sync + per-warp
+//                  digit counts in shared memory, 16 position-ordered steps),
+//                  scatter key and payload to offset[digit][tile] + rank.
+// HBM traffic per pass: keys+payload read twice, written once.
+#include <algorithm>
+
+#include "internal.hpp"
+
+namespace b200 {
+namespace {
+
+constexpr int kSortThreads = 256;
+constexpr int kSortItems = 16;
+constexpr int kSortTile = kSortThreads * kSortItems;  // 4096
+constexpr int kDigits = 256;
+constexpr int kScanItems = 16;
+constexpr int kScanTile = 256 * kScanItems;
+
+template <class K>
+__global__ void __launch_bounds__(kSortThreads) k_digit_hist(const K* __restrict__ keys, uint64_t n, int shift,
+                                                           uint32_t dmask, uint64_t ntiles,
+                                                           uint64_t* __restrict__ hist) {
+  __shared__ uint32_t h[kDigits];
+  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    h[threadIdx.x] = 0;
+    __syncthreads();
+    const uint64_t base = tile * kSortTile;
+#pragma unroll
+    for (int s = 0; s < kSortItems; ++s) {
+      const uint64_t e = base + s * kSortThreads + threadIdx.x;
+      if (e < n) atomicAdd(&h[static_cast<uint32_t>(keys[e] >> shift) & dmask], 1u);
+    }
+    __syncthreads();
+    hist[static_cast<uint64_t>(threadIdx.x) * ntiles + tile] = h[threadIdx.x];
+    __syncthreads();
+  }
+}
+
+template <class K>
+__global__ void __launch_bounds__(kSortThreads) k_digit_scatter(const K* __restrict__ keys_in,
+                                                              const uint32_t* __restrict__ vals_in, uint64_t n,
+                                                              int shift, uint32_t dmask, uint64_t ntiles,
+                                                              const uint64_t* __restrict__ offsets,
+                                                              K* __restrict__ keys_out,
+                                                              uint32_t* __restrict__ vals_out) {
+  __shared__ uint32_t wcnt[kSortThreads / 32][kDigits];  // per-warp digit counts of one step
+  __shared__ uint64_t run[kDigits];                        // running position per digit
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    run[threadIdx.x] = offsets[static_cast<uint64_t>(threadIdx.x) * ntiles + tile];
+    const uint64_t base = tile * kSortTile;
+    for (int s = 0; s < kSortItems; ++s) {
+      for (int w = 0; w < kSortThreads / 32; ++w) wcnt[w][threadIdx.x] = 0;
+      __syncthreads();
+      const uint64_t e = base + s * kSortThreads + threadIdx.x;
+      const bool ok = e < n;
+      K key{};
+      uint32_t val = 0;
+      if (ok) {
+        key = keys_in[e];
+        val = vals_in[e];
+      }
+      const uint32_t d = ok ? static_cast<uint32_t>(key >> shift) & dmask : kDigits;  // kDigits: none
+      const unsigned peers = __match_any_sync(0xffffffffu, d);
+      const uint32_t wrank = __popc(peers & ((1u << lane) - 1u));
+      if (ok && wrank == 0) wcnt[warp][d] = __popc(peers);
+      __syncthreads();
+      if (ok) {
+        uint64_t pos = run[d] + wrank;
+        for (int w = 0; w < warp; ++w) pos += wcnt[w][d];
+        keys_out[pos] = key;
+        vals_out[pos] = val;
+      }
+      __syncthreads();
+      uint32_t step = 0;
+      for (int w = 0; w < kSortThreads / 32; ++w) step += wcnt[w][threadIdx.x];
+      run[threadIdx.x] += step;
+    }
+    __syncthreads();
+  }
+}
+
+// Exclusive scan of u64 values, chunk by chunk; chunk totals to sums.
+__global__ void __launch_bounds__(256) k_scan_chunks(const uint64_t* __restrict__ in, uint64_t* __restrict__ out,
+                                                   uint64_t n, uint64_t* __restrict__ sums) {
+  __shared__ uint64_t warp_tot[8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t base = blockIdx.x * uint64_t(kScanTile) + threadIdx.x * uint64_t(kScanItems);
+  uint64_t v[kScanItems], run = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    v[i] = base + i < n ? in[base + i] : 0;
+    const uint64_t x = v[i];
+    v[i] = run;
+    run += x;
+  }
+  uint64_t x = run;
+#pragma unroll
+  for (int dd = 1; dd < 32; dd <<= 1) {
+    const uint64_t y = __shfl_up_sync(0xffffffffu, x, dd);
+    if (lane >= dd) x += y;
+  }
+  if (lane == 31) warp_tot[warp] = x;
+  __syncthreads();
+  uint64_t woff = 0;
+  for (int w = 0; w < warp; ++w) woff += warp_tot[w];
+  const uint64_t toff = woff + x - run;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i)
+    if (base + i < n) out[base + i] = toff + v[i];
+  if (threadIdx.x == 255) sums[blockIdx.x] = woff + x;
+}
+
+__global__ void k_add_chunk_offsets(uint64_t* __restrict__ out, uint64_t n, const uint64_t* __restrict__ offs) {
+  const uint64_t add = offs[blockIdx.x];
+  const uint64_t base = blockIdx.x * uint64_t(kScanTile);
+  for (int i = threadIdx.x; i < kScanTile; i += blockDim.x)
+    if (base + i < n) out[base + i] += add;
+}
+
+// Per-tile flag counts for compaction.
+__global__ void __launch_bounds__(256) k_flag_counts(const uint8_t* __restrict__ flags, uint64_t n,
+                                                   uint64_t* __restrict__ counts) {
+  __shared__ uint32_t c;
+  if (threadIdx.x == 0) c = 0;
+  __syncthreads();
+  const uint64_t base = blockIdx.x * uint64_t(kScanTile);
+  uint32_t mine = 0;
+  for (int i = threadIdx.x; i < kScanTile; i += blockDim.x)
+    if (base + i < n) mine += flags[base + i] != 0;
+  for (int dd = 16; dd > 0; dd >>= 1) mine += __shfl_down_sync(0xffffffffu, mine, dd);
+  if ((threadIdx.x & 31) == 0 && mine) atomicAdd(&c, mine);
+  __syncthreads();
+  if (threadIdx.x == 0) counts[blockIdx.x] = c;
+}
+
+// Stable compaction of a tile: warp ballots give in-warp order, warps are
+// visited in order, 16 position-ordered steps per tile.
+template <class T>
+__global__ void __launch_bounds__(256) k_compact(const T* __restrict__ in, const uint8_t* __restrict__ flags,
+                                               uint64_t n, const uint64_t* __restrict__ offs,
+                                               T* __restrict__ out) {
+  __shared__ uint32_t wtot[8];
+  __shared__ uint64_t run;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) run = offs[blockIdx.x];
+  const uint64_t base = blockIdx.x * uint64_t(kScanTile);
+  for (int s = 0; s < kScanTile / 256; ++s) {
+    const uint64_t e = base + s * 256 + threadIdx.x;
+    const bool f = e < n && flags[e];
+    const unsigned b = __ballot_sync(0xffffffffu, f);
+    if (lane == 0) wtot[warp] = __popc(b);
+    __syncthreads();
+    uint64_t pos = run + __popc(b & ((1u << lane) - 1u));
+    for (int w = 0; w < warp; ++w) pos += wtot[w];
+    if (f) out[pos] = in ? in[e] : static_cast<T>(e);  // in == nullptr: write the index
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t t = 0;
+      for (int w = 0; w < 8; ++w) t += wtot[w];
+      run += t;
+    }
+    __syncthreads();
+  }
+}
+
+unsigned grid_cap(uint64_t n) { return static_cast<unsigned>(std::min<uint64_t>(std::max<uint64_t>(n, 1), 1u << 30)); }
+
+}  // namespace
+
+// exclusive scan (u64) of n values, in -> out (may alias)
+void scan_exclusive_u64(const uint64_t* in, uint64_t* out, uint64_t n, cudaStream_t s) {
+  if (!n) return;
+  const uint64_t chunks = (n + kScanTile - 1) / kScanTile;
+  DevBuf<uint64_t> sums(chunks), sums_scan(chunks);
+  k_scan_chunks<<<grid_cap(chunks), 256, 0, s>>>(in, out, n, sums.ptr);
+  count_launch();
+  check_launch("k_scan_chunks");
+  if (chunks > 1) {
+    scan_exclusive_u64(sums.ptr, sums_scan.ptr, chunks, s);
+    k_add_chunk_offsets<<<grid_cap(chunks), 256, 0, s>>>(out, n, sums_scan.ptr);
+    count_launch();
+    check_launch("k_add_chunk_offsets");
+  }
+}
+
+template <class K>
+void radix_sort_pairs(K* keys, K* keys_alt, uint32_t* vals, uint32_t* vals_alt, uint64_t n, int begin_bit,
+                      int end_bit, cudaStream_t s, bool* result_in_alt) {
+  *result_in_alt = false;
+  if (n <= 1 || end_bit <= begin_bit) return;
+  const uint64_t ntiles = (n + kSortTile - 1) / kSortTile;
+  DevBuf<uint64_t> hist(ntiles * kDigits);
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(ntiles, static_cast<uint64_t>(nsm) * 8));
+  K *kin = keys, *kout = keys_alt;
+  uint32_t *vin = vals, *vout = vals_alt;
+  for (int shift = begin_bit; shift < end_bit; shift += 8) {
+    const int bits = std::min(8, end_bit - shift);
+    const uint32_t dmask = (1u << bits) - 1u;
+    k_digit_hist<K><<<grid, kSortThreads, 0, s>>>(kin, n, shift, dmask, ntiles, hist.ptr);
+    count_launch();
+    check_launch("k_digit_hist");
+    scan_exclusive_u64(hist.ptr, hist.ptr, ntiles * kDigits, s);
+    k_digit_scatter<K><<<grid, kSortThreads, 0, s>>>(kin, vin, n, shift, dmask, ntiles, hist.ptr, kout, vout);
+    count_launch();
+    check_launch("k_digit_scatter");
+    std::swap(kin, kout);
+    std::swap(vin, vout);
+    *result_in_alt = !*result_in_alt;
+  }
+}
+
+template void radix_sort_pairs<uint64_t>(uint64_t*, uint64_t*, uint32_t*, uint32_t*, uint64_t, int, int,
+                                         cudaStream_t, bool*);
+template void radix_sort_pairs<uint32_t>(uint32_t*, uint32_t*, uint32_t*, uint32_t*, uint64_t, int, int,
+                                         cudaStream_t, bool*);
+
+template <class T>
+uint64_t select_flagged(const T* in, const uint8_t* flags, uint64_t n, T* out, cudaStream_t s) {
+  if (!n) return 0;
+  const uint64_t chunks = (n + kScanTile - 1) / kScanTile;
+  DevBuf<uint64_t> counts(chunks), offs(chunks + 1);
+  k_flag_counts<<<grid_cap(chunks), 256, 0, s>>>(flags, n, counts.ptr);
+  count_launch();
+  check_launch("k_flag_counts");
+  scan_exclusive_u64(counts.ptr, offs.ptr, chunks, s);
+  k_compact<T><<<grid_cap(chunks), 256, 0, s>>>(in, flags, n, offs.ptr, out);
+  count_launch();
+  check_launch("k_compact");
+  uint64_t last_off = 0, last_cnt = 0;
+  B200_CUDA(cudaMemcpyAsync(&last_off, offs.ptr + chunks - 1, 8, cudaMemcpyDeviceToHost, s));
+  B200_CUDA(cudaMemcpyAsync(&last_cnt, counts.ptr + chunks - 1, 8, cudaMemcpyDeviceToHost, s));
+  B200_CUDA(cudaStreamSynchronize(s));
+  return last_off + last_cnt;
+}
+
+template uint64_t select_flagged<uint64_t>(const uint64_t*, const uint8_t*, uint64_t, uint64_t*, cudaStream_t);
+template uint64_t select_flagged<uint32_t>(const uint32_t*, const uint8_t*, uint64_t, uint32_t*, cudaStream_t);
+
+}  // namespace b200
