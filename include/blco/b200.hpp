@@ -225,6 +225,13 @@ DenseMatrix mttkrp(const BlcoTensor& t, const FactorMatrices& f, int mode,
                    const ExecConfig& config = {}, Strategy strategy = Strategy::Auto,
                    MttkrpStats* stats = nullptr);
 
+// B200 extension: mttkrp(t, f, n) for every mode n in one call, the host
+// payload uploaded (every call, no device cache) in chunks under the compute
+// (blco_mttkrp_all_host).  Result n is dims[n] x rank.
+std::vector<DenseMatrix> mttkrp_all_modes(const BlcoTensor& t, const FactorMatrices& f,
+                                          const ExecConfig& config = {},
+                                          Strategy strategy = Strategy::Auto);
+
 // ------------------------------------------------------------- streaming.hpp
 struct DeviceBudget {
   std::uint64_t capacity_bytes = 0;

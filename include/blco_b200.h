@@ -227,6 +227,29 @@ int blco_mttkrp_device(const blco_tensor* t, const double* const* d_factors, uin
                        int mode, int strategy, const blco_exec_config* cfg, double* d_out,
                        int accumulate, void* stream, blco_mttkrp_stats* stats);
 
+/* All-mode MTTKRP of a HOST-resident BLCO tensor: outs[n] = mttkrp(t, f, n)
+ * for every mode n (mttkrp.hpp:110-112 applied to modes 0..N-1, the
+ * BASELINE "time/iter (all modes)" step).  The block payload (keys,
+ * block_nnz, idx[b], vals[b] as in blco_tensor_upload; pinned host memory
+ * gives asynchronous copies) is uploaded in tile-aligned chunks on one stream
+ * while every mode's kernel runs on the chunks already resident on another;
+ * factors[m] are host dims[m] x rank, outs[m] host dims[m] x rank
+ * (overwritten).  chunk_elems = 0 picks max(2^20, nnz/32).  Device buffers
+ * are cached per calling thread and reused by later calls. */
+typedef struct blco_all_modes_report {
+  double device_ms;   /* CUDA events: first copy enqueued .. last D2H done */
+  uint64_t chunks;
+  uint64_t h2d_bytes; /* payload + factors + tile table + block bases */
+  uint64_t d2h_bytes; /* every M_n */
+  uint64_t launches;  /* kernels this call launched */
+} blco_all_modes_report;
+
+int blco_mttkrp_all_host(const blco_layout* layout, uint64_t nblocks, const uint64_t* keys,
+                         const uint64_t* block_nnz, const uint64_t* const* idx,
+                         const double* const* vals, const double* const* factors, uint64_t rank,
+                         int strategy, const blco_exec_config* cfg, uint64_t chunk_elems,
+                         int device, double* const* outs, blco_all_modes_report* report);
+
 /* merge_copies (mttkrp.hpp:103): out = sum_c copies[c], copy 0 first. */
 int blco_merge_copies(const double* const* copies, uint64_t ncopies, uint64_t elems,
                       double* out);

@@ -1,10 +1,12 @@
 /*
  * blco_oracle.c -- CPU restatement of the reference BLCO path.
- * TEST INFRASTRUCTURE ONLY (see blco_oracle.h).  Plain C11, single-threaded.
+ * TEST INFRASTRUCTURE ONLY (see blco_oracle.h).  Plain C11, single-threaded
+ * except for the element filter of the row-sampled oracle (pthreads).
  */
 #include "blco_oracle.h"
 
 #include <math.h>
+#include <pthread.h>
 #include <stdarg.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -315,39 +317,175 @@ void orc_factors_random(const uint64_t* dims, int order, uint64_t rank, uint64_t
     }
 }
 
-int orc_synth_uniform(int order, const uint64_t* dims, uint64_t nnz, uint64_t seed,
-                      uint64_t* idx, double* vals) {
+typedef struct feistel {
+  uint64_t cells, mask, key[4];
+  int half;
+} feistel;
+
+static int feistel_init(int order, const uint64_t* dims, uint64_t nnz, uint64_t seed, feistel* fs) {
   unsigned __int128 cells = 1;
   for (int m = 0; m < order; ++m) cells *= dims[m];
   if (cells > (unsigned __int128)UINT64_MAX) return fail("synth: cell count exceeds 2^64-1");
-  const uint64_t P = (uint64_t)cells;
-  if (nnz > P) return fail("synth: more non-zeros than cells");
-  int kb = bits_for(P);
+  fs->cells = (uint64_t)cells;
+  if (nnz > fs->cells) return fail("synth: more non-zeros than cells");
+  int kb = bits_for(fs->cells);
   if (kb & 1) ++kb;
   if (kb < 2) kb = 2;
-  const int half = kb / 2;
-  const uint64_t mask = half == 64 ? ~0ull : ((1ull << half) - 1);
-  uint64_t key[4];
-  for (int r = 0; r < 4; ++r) key[r] = mix64(seed + (uint64_t)(r + 1) * GOLDEN);
+  fs->half = kb / 2;
+  fs->mask = fs->half == 64 ? ~0ull : ((1ull << fs->half) - 1);
+  for (int r = 0; r < 4; ++r) fs->key[r] = mix64(seed + (uint64_t)(r + 1) * GOLDEN);
+  return ORC_OK;
+}
+
+/* element e -> its cell: keyed 4-round Feistel, cycle-walked into [0, cells) */
+static uint64_t feistel_cell(const feistel* fs, uint64_t e) {
+  uint64_t x = e;
+  do {
+    uint64_t L = x >> fs->half, R = x & fs->mask;
+    for (int r = 0; r < 4; ++r) {
+      const uint64_t F = mix64(R ^ fs->key[r]) & fs->mask;
+      const uint64_t nl = R;
+      R = L ^ F;
+      L = nl;
+    }
+    x = (L << fs->half) | R;
+  } while (x >= fs->cells);
+  return x;
+}
+
+static double element_value(uint64_t seed, uint64_t e) {
+  return unit_double(mix64((seed ^ VALUE_SALT) + (e + 1) * GOLDEN));
+}
+
+int orc_synth_uniform(int order, const uint64_t* dims, uint64_t nnz, uint64_t seed,
+                      uint64_t* idx, double* vals) {
+  feistel fs;
+  if (feistel_init(order, dims, nnz, seed, &fs) != ORC_OK) return ORC_EFORMAT;
   for (uint64_t e = 0; e < nnz; ++e) {
-    uint64_t x = e;
-    do {
-      uint64_t L = x >> half, R = x & mask;
-      for (int r = 0; r < 4; ++r) {
-        const uint64_t F = mix64(R ^ key[r]) & mask;
-        const uint64_t nl = R;
-        R = L ^ F;
-        L = nl;
-      }
-      x = (L << half) | R;
-    } while (x >= P);
+    uint64_t x = feistel_cell(&fs, e);
     for (int m = 0; m < order; ++m) {
       idx[(uint64_t)m * nnz + e] = x % dims[m];
       x /= dims[m];
     }
-    vals[e] = unit_double(mix64((seed ^ VALUE_SALT) + (e + 1) * GOLDEN));
+    vals[e] = element_value(seed, e);
   }
   return ORC_OK;
+}
+
+/* Row-sampled oracle (SURVEY.md 8c "Large configs"): the rows rows[m][0..k)
+ * of mttkrp_coo(T, f, m) for every mode m of the uniform synthetic tensor T
+ * = orc_synth_uniform(dims, nnz, seed), without materialising T.  Worker
+ * threads filter contiguous element ranges for elements whose mode-m
+ * coordinate is sampled; the hits are then accumulated on one thread in
+ * element order with mttkrp_coo's product order (oracle.cpp:15-24), so the
+ * sampled rows are bit-identical to those of the full oracle. */
+#define RS_MAX_ORDER 8
+
+typedef struct hit {
+  uint64_t e;
+  uint32_t coord[RS_MAX_ORDER];
+} hit;
+
+typedef struct rs_job {
+  const feistel* fs;
+  int order;
+  const uint64_t* dims;
+  const int32_t* const* slot_of; /* per mode: row -> sample slot or -1 */
+  uint64_t e0, e1;
+  hit* hits;
+  uint64_t nhits, cap;
+  int oom;
+} rs_job;
+
+static void* rs_worker(void* arg) {
+  rs_job* j = arg;
+  uint64_t c[ORC_MAX_ORDER];
+  for (uint64_t e = j->e0; e < j->e1; ++e) {
+    uint64_t x = feistel_cell(j->fs, e);
+    int any = 0;
+    for (int m = 0; m < j->order; ++m) {
+      c[m] = x % j->dims[m];
+      x /= j->dims[m];
+      any |= j->slot_of[m][c[m]] >= 0;
+    }
+    if (!any) continue;
+    if (j->nhits == j->cap) {
+      const uint64_t nc = j->cap ? 2 * j->cap : 4096;
+      hit* h = realloc(j->hits, nc * sizeof *h);
+      if (!h) {
+        j->oom = 1;
+        return NULL;
+      }
+      j->hits = h, j->cap = nc;
+    }
+    hit* h = &j->hits[j->nhits++];
+    h->e = e;
+    for (int m = 0; m < j->order; ++m) h->coord[m] = (uint32_t)c[m];
+  }
+  return NULL;
+}
+
+int orc_rowsample_uniform(int order, const uint64_t* dims, uint64_t nnz, uint64_t seed,
+                          const double* const* f, uint64_t rank, const uint64_t* nrows,
+                          const uint64_t* const* rows, double* const* out, int threads) {
+  if (order < 1 || order > RS_MAX_ORDER) return fail("rowsample: order must lie in [1, 8]");
+  feistel fs;
+  if (feistel_init(order, dims, nnz, seed, &fs) != ORC_OK) return ORC_EFORMAT;
+  int32_t* slot_of[RS_MAX_ORDER] = {0};
+  int rc = ORC_OK;
+  for (int m = 0; m < order; ++m) {
+    slot_of[m] = malloc(dims[m] * sizeof(int32_t));
+    if (!slot_of[m]) {
+      rc = fail("rowsample: out of memory");
+      goto done;
+    }
+    memset(slot_of[m], 0xff, dims[m] * sizeof(int32_t));
+    for (uint64_t k = 0; k < nrows[m]; ++k) {
+      if (rows[m][k] >= dims[m]) {
+        rc = fail("rowsample: row out of range");
+        goto done;
+      }
+      slot_of[m][rows[m][k]] = (int32_t)k;
+    }
+    memset(out[m], 0, nrows[m] * rank * sizeof(double));
+  }
+  if (threads < 1) threads = 1;
+  if (threads > 256) threads = 256;
+  {
+    rs_job jobs[256];
+    pthread_t tid[256];
+    for (int t = 0; t < threads; ++t) {
+      jobs[t] = (rs_job){&fs, order, dims, (const int32_t* const*)slot_of,
+                         nnz / threads * t, t + 1 == threads ? nnz : nnz / threads * (t + 1), NULL, 0, 0, 0};
+      pthread_create(&tid[t], NULL, rs_worker, &jobs[t]);
+    }
+    for (int t = 0; t < threads; ++t) pthread_join(tid[t], NULL);
+    double* row = malloc(rank * sizeof *row);
+    for (int t = 0; t < threads; ++t) {
+      if (jobs[t].oom) rc = fail("rowsample: out of memory");
+      for (uint64_t i = 0; rc == ORC_OK && i < jobs[t].nhits; ++i) {
+        const hit* h = &jobs[t].hits[i];
+        const double v = element_value(seed, h->e);
+        for (int mode = 0; mode < order; ++mode) {
+          const int32_t s = slot_of[mode][h->coord[mode]];
+          if (s < 0) continue;
+          for (uint64_t r = 0; r < rank; ++r) row[r] = v;
+          for (int n = 0; n < order; ++n) {
+            if (n == mode) continue;
+            const double* a = f[n] + (uint64_t)h->coord[n] * rank;
+            for (uint64_t r = 0; r < rank; ++r) row[r] *= a[r];
+          }
+          double* dst = out[mode] + (uint64_t)s * rank;
+          for (uint64_t r = 0; r < rank; ++r) dst[r] += row[r];
+        }
+      }
+      free(jobs[t].hits);
+    }
+    free(row);
+  }
+done:
+  for (int m = 0; m < order; ++m) free(slot_of[m]);
+  return rc;
 }
 
 /* Independent draws, first nnz distinct tuples in draw order (the product's

@@ -151,6 +151,22 @@ class Oracle:
                                             C.c_uint64(seed), _pu(idx), _pd(vals)))
         return idx, vals
 
+    def rowsample_uniform(self, dims, nnz, seed, factors, rows, threads=None):
+        """Rows rows[m] of mttkrp_coo(T, factors, m), every mode m, of the
+        uniform synthetic tensor T (streamed, never stored); bit-identical to
+        the full oracle's rows.  Returns one (len(rows[m]), rank) array per mode."""
+        import os
+        fs = [_f64(a) for a in factors]
+        rank = fs[0].shape[1]
+        rows = [_u64(r) for r in rows]
+        outs = [np.zeros((r.size, rank)) for r in rows]
+        nrows = _u64([r.size for r in rows])
+        rp = (C.c_void_p * len(rows))(*[r.ctypes.data for r in rows])
+        self._ck(self.lib.orc_rowsample_uniform(len(dims), _pu(_u64(dims)), C.c_uint64(nnz), C.c_uint64(seed),
+                                                _pp(fs), C.c_uint64(rank), _pu(nrows), rp, _pp(outs),
+                                                int(threads or os.cpu_count() or 1)))
+        return outs
+
     def synth_draws(self, dims, nnz, seed, skew=1):
         idx = np.zeros((len(dims), nnz), np.uint64)
         vals = np.zeros(nnz)

@@ -6,9 +6,9 @@ whose CUDA kernels (sm_100a) do all the work.  See DESIGN.md.
 from .api import (  # noqa: F401
     BitLayout, BlcoBlock, BlcoHeader, BlcoTensor, BuildStats, CpAlsError, CpAlsOptions, CpModel, CudaError,
     DeviceBudget, DeviceTensor, Error, ExecConfig, FactorMatrices, FileBlockSource, FormatError, IoError,
-    MttkrpStats, SparseTensorCoo, SplitIndex, Strategy, StreamReport, VerifyError, build_blco,
+    AllModesReport, MttkrpStats, SparseTensorCoo, SplitIndex, Strategy, StreamReport, VerifyError, build_blco,
     choose_strategy, compute_batch_table, cp_als, delinearize, device_count, encode_coords,
     factors_random_device, fit, interleaved_remainder, kernel_launch_count, linearize,
-    load_blco, make_layout, merge_copies, mttkrp, partition, read_blco_header, save_blco,
+    load_blco, make_layout, merge_copies, mttkrp, mttkrp_all_modes, partition, read_blco_header, save_blco,
     split_block_key, stream_mttkrp,
     synth_draws_host, synth_uniform_host, throughput_report)

@@ -95,6 +95,11 @@ class StreamReport(C.Structure):
     ]
 
 
+class AllModesReport(C.Structure):
+    _fields_ = [("device_ms", C.c_double), ("chunks", C.c_uint64), ("h2d_bytes", C.c_uint64),
+                ("d2h_bytes", C.c_uint64), ("launches", C.c_uint64)]
+
+
 class CpAlsStats(C.Structure):
     _fields_ = [("iterations", C.c_int32), ("iterations_ms", C.c_double), ("mttkrp_ms", C.c_double)]
 
@@ -147,6 +152,9 @@ SIGNATURES = {
                          C.POINTER(MttkrpStats)]),
     "blco_mttkrp_device": (_I, [_P, C.POINTER(_P), _U64, _I, _I, C.POINTER(ExecCfg), _P, _I,
                                 _P, C.POINTER(MttkrpStats)]),
+    "blco_mttkrp_all_host": (_I, [C.POINTER(Layout), _U64, _PU64, _PU64, C.POINTER(_P), C.POINTER(_P),
+                                  C.POINTER(_P), _U64, _I, C.POINTER(ExecCfg), _U64, _I, C.POINTER(_P),
+                                  C.POINTER(AllModesReport)]),
     "blco_merge_copies": (_I, [C.POINTER(_P), _U64, _U64, _PD]),
     "blco_stream_mttkrp": (_I, [C.POINTER(Layout), _U64, SOURCE_FN, _P, C.POINTER(_P), _U64,
                                 _I, C.POINTER(Budget), C.POINTER(ExecCfg), _I, _I, _PD,

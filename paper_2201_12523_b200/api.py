@@ -459,6 +459,21 @@ class DeviceTensor:
         _check(lib.blco_tensor_blocks(self._h, _pu64(keys), _pu64(bn)))
         return bn[: self.nblocks]
 
+    def validate_device(self) -> None:
+        """read_blco_block's per-element checks (blco_format.cpp:201-227:
+        fields within width, coordinates inside dims, strictly ascending ALTO
+        order) on every block, run on the device; raises FormatError."""
+        keys = np.zeros(max(1, self.nblocks), np.uint64)
+        bn = np.zeros(max(1, self.nblocks), np.uint64)
+        _check(lib.blco_tensor_blocks(self._h, _pu64(keys), _pu64(bn)))
+        ip, vp = C.c_void_p(), C.c_void_p()
+        _check(lib.blco_tensor_device_ptrs(self._h, C.byref(ip), C.byref(vp)))
+        off = 0
+        for b in range(self.nblocks):
+            _check(lib.blco_validate_block_device(C.byref(self.layout._c), int(keys[b]), int(bn[b]),
+                                                  C.c_void_p((ip.value or 0) + 8 * off)))
+            off += int(bn[b])
+
     def to_host(self) -> BlcoTensor:
         keys = np.zeros(max(1, self.nblocks), np.uint64)
         bn = np.zeros(max(1, self.nblocks), np.uint64)
@@ -611,6 +626,50 @@ def mttkrp(t, f: FactorMatrices, mode: int, config: ExecConfig | None = None,
     if stats is not None:
         _fill_stats(stats, st)
     return out
+
+
+@dataclass
+class AllModesReport:
+    """blco_all_modes_report: device time and bytes of one mttkrp_all_modes call."""
+    device_ms: float = 0.0
+    chunks: int = 0
+    h2d_bytes: int = 0
+    d2h_bytes: int = 0
+    launches: int = 0
+
+
+def mttkrp_all_modes(t: BlcoTensor, f: FactorMatrices, config: ExecConfig | None = None,
+                     strategy: Strategy = Strategy.Auto, outs: Sequence[np.ndarray] | None = None,
+                     chunk_elems: int = 0, device: int = 0,
+                     report: AllModesReport | None = None) -> list[np.ndarray]:
+    """mttkrp(t, f, n) for every mode n of a HOST BlcoTensor in one call
+    (blco_mttkrp_all_host): the payload is uploaded in chunks under the
+    compute, every call.  `outs` (dims[n] x rank float64, C-contiguous; pinned
+    memory makes the read-back asynchronous) are overwritten and returned."""
+    config = config or ExecConfig()
+    config.validate()
+    dims = t.layout.dims
+    f.validate(dims)
+    if outs is None:
+        outs = [np.empty((d, f.rank), dtype=np.float64) for d in dims]
+    for d, o in zip(dims, outs):
+        if o.dtype != np.float64 or o.shape != (d, f.rank) or not o.flags.c_contiguous:
+            raise FormatError("mttkrp: output arrays must be C-contiguous float64 dims[n] x rank")
+    bn = _u64(np.diff(t.offsets))
+    nb = int(bn.size)
+    idx_ptrs = (C.c_void_p * max(1, nb))(*[t.idx.ctypes.data + 8 * int(t.offsets[b]) for b in range(nb)])
+    val_ptrs = (C.c_void_p * max(1, nb))(*[t.vals.ctypes.data + 8 * int(t.offsets[b]) for b in range(nb)])
+    keys = _u64(t.keys)
+    fs = [a if a.dtype == np.float64 and a.flags.c_contiguous else _f64(a) for a in f.factors]
+    rep = L.AllModesReport()
+    c = config._c()
+    _check(lib.blco_mttkrp_all_host(C.byref(t.layout._c), nb, _pu64(keys), _pu64(bn), idx_ptrs, val_ptrs,
+                                    _ptr_array(fs), f.rank, int(strategy), C.byref(c), chunk_elems, device,
+                                    _ptr_array(outs), C.byref(rep)))
+    if report is not None:
+        report.device_ms, report.chunks = rep.device_ms, rep.chunks
+        report.h2d_bytes, report.d2h_bytes, report.launches = rep.h2d_bytes, rep.d2h_bytes, rep.launches
+    return list(outs)
 
 
 def merge_copies(copies: Sequence[np.ndarray]) -> np.ndarray:

@@ -582,6 +582,33 @@ DenseMatrix mttkrp(const BlcoTensor& t, const FactorMatrices& f, int mode, const
   return m;
 }
 
+std::vector<DenseMatrix> mttkrp_all_modes(const BlcoTensor& t, const FactorMatrices& f,
+                                          const ExecConfig& config, Strategy strategy) {
+  config.validate();
+  f.validate(t.dims());
+  const blco_layout l = to_c(t.layout);
+  std::vector<std::uint64_t> keys, nnz;
+  std::vector<const std::uint64_t*> idx;
+  std::vector<const double*> vals;
+  for (const auto& b : t.blocks) {
+    if (b.linear_indices.size() != b.values.size())
+      throw FormatError("blco: block index/value arrays have mismatched lengths");
+    keys.push_back(b.key);
+    nnz.push_back(b.nnz());
+    idx.push_back(b.linear_indices.data());
+    vals.push_back(b.values.data());
+  }
+  std::vector<DenseMatrix> out;
+  std::vector<double*> optr;
+  for (int m = 0; m < t.order(); ++m) out.emplace_back(t.dims()[m], f.rank);
+  for (auto& o : out) optr.push_back(o.data.data());
+  const auto ptrs = factor_ptrs(f);
+  const blco_exec_config c = to_c(config);
+  ck(blco_mttkrp_all_host(&l, keys.size(), keys.data(), nnz.data(), idx.data(), vals.data(), ptrs.data(),
+                          f.rank, static_cast<int>(strategy), &c, 0, current_device(), optr.data(), nullptr));
+  return out;
+}
+
 // --------------------------------------------------------------- streaming
 bool MemoryBlockSource::next(BlcoBlock& out) {
   if (cursor_ >= t_->blocks.size()) return false;

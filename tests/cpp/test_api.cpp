@@ -259,6 +259,16 @@ TEST(strategy_config_grid) {  // test_mttkrp.cpp:267-290
   }
 }
 
+TEST(all_modes_extension) {  // B200 extension: every mode of a host tensor in one call
+  Rng rng(79);
+  auto coo = random_coo(rng, {40, 17, 63}, 900);
+  auto t = build_blco(coo, 9, 100);  // several blocks
+  auto f = random_factors(rng, coo.dims, 5);
+  auto all = mttkrp_all_modes(t, f);
+  CHECK(all.size() == 3);
+  for (int mode = 0; mode < 3; ++mode) CHECK(rel_frobenius(all[mode], mttkrp_coo(coo, f, mode)) <= 1e-12);
+}
+
 TEST(single_copy_hierarchical) {  // test_mttkrp.cpp:235-244
   auto t = build_blco(golden_tensor(), 64);
   Rng rng(67);

@@ -1,0 +1,95 @@
+"""Parity at BASELINE.json's full sizes (SURVEY.md 8c "Large configs").
+
+The oracle cannot hold these tensors' MTTKRPs in seconds, so full-size parity
+goes through size-independent checks:
+  * row-sampled MTTKRP: S seeded rows per mode of the device M_n against the
+    streamed row-sampled oracle (oracle/blco_oracle.c orc_rowsample_uniform),
+    whose rows are bit-identical to oracle::mttkrp_coo's on the full tensor;
+    tolerance: relative Frobenius <= 1e-12 over the sampled rows (the
+    reference's fp64 bar, proj/tests/test_mttkrp.cpp:267-290);
+  * the device-built BLCO at full size passes read_blco_block's element checks
+    (fields in width, coordinates inside dims, strictly ascending ALTO order;
+    blco_format.cpp:201-227) on the device, and (NELL-2) its (cell, value)
+    multiset equals the generator's: an order-free 64-bit hash of every
+    element, bit-exact.
+"""
+import numpy as np
+import pytest
+
+from conftest import rel_frobenius
+
+pytestmark = pytest.mark.gpu
+
+NELL2 = ([12092, 9184, 28818], 76_879_419, 32)
+AMAZON = ([4821207, 1774269, 1805187], 1_741_809_018, 32)
+TOL = 1e-12
+
+
+def _mix64(z):
+    z = np.asarray(z, np.uint64)
+    with np.errstate(over="ignore"):
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    return z ^ (z >> np.uint64(31))
+
+
+def _multiset_hash(cells, vals):
+    h = _mix64(cells ^ _mix64(np.ascontiguousarray(vals).view(np.uint64)))
+    with np.errstate(over="ignore"):
+        return int(np.sum(h, dtype=np.uint64))
+
+
+def _sample_rows(dims, per_mode, seed=11):
+    rng = np.random.default_rng(seed)
+    return [np.sort(rng.choice(d, size=min(d, per_mode), replace=False)).astype(np.uint64) for d in dims]
+
+
+def _check_rows(gpu, oracle, dt, dims, nnz, rank, per_mode):
+    f = gpu.FactorMatrices.random(dims, rank, 7)
+    rows = _sample_rows(dims, per_mode)
+    want = oracle.rowsample_uniform(dims, nnz, 42, f.factors, rows)
+    for mode in range(len(dims)):
+        got = gpu.mttkrp(dt, f, mode)[rows[mode].astype(np.int64)]
+        assert rel_frobenius(got, want[mode]) <= TOL, mode
+        # every sampled row is non-trivial at these densities
+        assert np.count_nonzero(want[mode].any(axis=1)) > 0.9 * rows[mode].size
+
+
+def test_nell2_full_size_rows(gpu, oracle):
+    """BASELINE configs[1] at full size: 76.9M nnz, R=32, every mode."""
+    dims, nnz, rank = NELL2
+    dt = gpu.DeviceTensor.synthetic(dims, nnz, 42)
+    assert dt.nnz == nnz
+    _check_rows(gpu, oracle, dt, dims, nnz, rank, 512)
+
+
+def test_nell2_full_size_build(gpu, oracle):
+    """The full-size device build: block checks on the device, and the
+    element multiset (cell, value) equals the generator's, bit-exact."""
+    dims, nnz, _ = NELL2
+    dt = gpu.DeviceTensor.synthetic(dims, nnz, 42)
+    dt.validate_device()
+    host = dt.to_host()
+    lay = host.layout
+    cells = np.zeros(nnz, np.uint64)
+    stride = 1
+    for m in range(3):
+        base = np.repeat(np.array([lay.block_base(int(k))[m] for k in host.keys], np.uint64),
+                         np.diff(host.offsets).astype(np.int64))
+        c = base | ((host.idx >> np.uint64(lay.field_shift[m])) & np.uint64(lay.field_mask[m]))
+        assert int(c.max()) < dims[m]
+        cells += c * np.uint64(stride)
+        stride *= dims[m]
+    idx, vals = oracle.synth_uniform(dims, nnz, 42)
+    want_cells = idx[0] + idx[1] * np.uint64(dims[0]) + idx[2] * np.uint64(dims[0] * dims[1])
+    assert _multiset_hash(cells, host.vals) == _multiset_hash(want_cells, vals)
+
+
+def test_amazon_full_size_rows(gpu, oracle):
+    """BASELINE configs[2] at full size on one B200: 1.74B nnz, 65-bit layout
+    (1 stripped bit, 14 blocks), R=32, every mode; device block checks."""
+    dims, nnz, rank = AMAZON
+    dt = gpu.DeviceTensor.synthetic(dims, nnz, 42)
+    assert dt.nnz == nnz and dt.block_nnz().size == 14
+    dt.validate_device()
+    _check_rows(gpu, oracle, dt, dims, nnz, rank, 512)

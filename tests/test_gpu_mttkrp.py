@@ -158,3 +158,43 @@ def test_slices_sum_to_whole(gpu, oracle):
             acc = sum(gpu.mttkrp(dt.slice(b, e), f, mode) for b, e in ranges)
             want = oracle.mttkrp_coo(dims, idx, vals, f.factors, mode)
             assert rel_frobenius(acc, want) <= TOL
+
+
+@pytest.mark.parametrize("target,cap,chunk", [(64, 1 << 27, 0), (64, 1 << 27, 5000), (12, 7000, 3000),
+                                              (20, 1, 1), (9, 1000, 100_000)])
+def test_all_modes_host_pipeline(gpu, oracle, target, cap, chunk):
+    """mttkrp_all_modes (blco_mttkrp_all_host): host tensor uploaded in
+    chunks (crossing block boundaries) under the per-mode kernels; every M_n
+    against the oracle, pageable and pinned host memory, both strategies."""
+    dims = [700, 90, 1300]
+    coo = gpu.synth_uniform_host(dims, 40_000, 17)
+    f = gpu.FactorMatrices.random(dims, 16, 7)
+    t = gpu.build_blco(coo, target, cap)
+    want = [oracle.mttkrp_coo(dims, coo.indices, coo.values, f.factors, m) for m in range(3)]
+    rep = gpu.AllModesReport()
+    for strat in (gpu.Strategy.Auto, gpu.Strategy.Hierarchical):
+        got = gpu.mttkrp_all_modes(t, f, strategy=strat, chunk_elems=chunk, report=rep)
+        for m in range(3):
+            assert rel_frobenius(got[m], want[m]) <= TOL, (m, strat)
+    assert rep.h2d_bytes >= 40_000 * 16 and rep.d2h_bytes == sum(d * 16 * 8 for d in dims)
+    assert rep.launches >= 3 * rep.chunks and rep.device_ms > 0
+    # pinned payload / outputs, repeated calls reuse the cached device buffers
+    idx = gpu.api.pinned_empty(t.idx.size, np.uint64)
+    vals = gpu.api.pinned_empty(t.vals.size, np.float64)
+    idx[:], vals[:] = t.idx, t.vals
+    tp = gpu.BlcoTensor(t.layout, t.max_nnz_per_block, t.keys, t.offsets, idx, vals)
+    outs = [gpu.api.pinned_empty(d * 16, np.float64).reshape(d, 16) for d in dims]
+    for _ in range(2):
+        got = gpu.mttkrp_all_modes(tp, f, outs=outs, chunk_elems=chunk)
+        for m in range(3):
+            assert rel_frobenius(got[m], want[m]) <= TOL
+
+
+def test_all_modes_host_empty_and_errors(gpu):
+    dims = [5, 6, 7]
+    t = gpu.build_blco(gpu.SparseTensorCoo(dims, np.zeros((3, 0), np.uint64), np.zeros(0)))
+    f = gpu.FactorMatrices.random(dims, 4, 1)
+    got = gpu.mttkrp_all_modes(t, f)
+    assert all(g.shape == (d, 4) and not g.any() for g, d in zip(got, dims))
+    with pytest.raises(gpu.FormatError):
+        gpu.mttkrp_all_modes(t, gpu.FactorMatrices.random([5, 6, 8], 4, 1))
