@@ -312,6 +312,16 @@ int blco_stream_mttkrp(const blco_layout* layout, uint64_t max_nnz_per_block,
                        const blco_exec_config* cfg, int strategy, int device, double* out,
                        blco_stream_report* report);
 
+/* B200 extension: the blocks stream once and every mode's MTTKRP runs on each
+ * resident block (outs[m] = dims[m] x rank, host).  The resident set adds all
+ * N outputs to the factors; same budget rules and report as above, with
+ * compute intervals covering the N kernels of a block. */
+int blco_stream_mttkrp_all(const blco_layout* layout, uint64_t max_nnz_per_block,
+                           blco_block_source_fn next, void* ctx, const double* const* factors,
+                           uint64_t rank, const blco_device_budget* budget,
+                           const blco_exec_config* cfg, int strategy, int device, double* const* outs,
+                           blco_stream_report* report);
+
 void blco_set_error(int status, const char* msg);
 
 /* Pinned host memory for stream sources (true async H2D); pageable source

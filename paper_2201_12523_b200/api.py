@@ -732,6 +732,23 @@ def stream_mttkrp(source, f: FactorMatrices, mode: int, budget: DeviceBudget,
     ``source`` is a host BlcoTensor (MemoryBlockSource) or an iterator of
     (key, idx, vals) blocks together with ``layout`` / ``max_nnz_per_block``.
     """
+    return _stream(source, f, mode, budget, config, strategy, report, device, layout, max_nnz_per_block,
+                   block_count)
+
+
+def stream_mttkrp_all_modes(source, f: FactorMatrices, budget: DeviceBudget,
+                            config: ExecConfig | None = None, strategy: Strategy = Strategy.Auto,
+                            report: StreamReport | None = None, device: int = 0,
+                            layout: BitLayout | None = None, max_nnz_per_block: int | None = None,
+                            block_count: int | None = None) -> list[np.ndarray]:
+    """B200 extension of stream_mttkrp: the blocks cross the host link once and
+    every mode's MTTKRP runs on each resident block (blco_stream_mttkrp_all).
+    Returns [M_0, ..., M_{N-1}]."""
+    return _stream(source, f, None, budget, config, strategy, report, device, layout, max_nnz_per_block,
+                   block_count)
+
+
+def _stream(source, f, mode, budget, config, strategy, report, device, layout, max_nnz_per_block, block_count):
     config = config or ExecConfig()
     config.validate()
     stable = isinstance(source, BlcoTensor)  # MemoryBlockSource: views outlive the call
@@ -748,7 +765,7 @@ def stream_mttkrp(source, f: FactorMatrices, mode: int, budget: DeviceBudget,
     else:
         it = iter(source)
     f.validate(layout.dims)
-    if mode < 0 or mode >= layout.order():
+    if mode is not None and (mode < 0 or mode >= layout.order()):
         raise FormatError("stream: mode out of range")
     keep: list = []
     err: list = []
@@ -772,7 +789,8 @@ def stream_mttkrp(source, f: FactorMatrices, mode: int, budget: DeviceBudget,
 
     cb = L.SOURCE_FN(pull)
     fs = [_f64(a) for a in f.factors]
-    out = np.zeros((layout.dims[mode], f.rank))
+    modes = range(layout.order()) if mode is None else [mode]
+    outs = [np.zeros((layout.dims[m], f.rank)) for m in modes]
     cap = max(1, block_count or 4096)
     bq = (C.c_int32 * cap)()
     tl = (L.StreamEvent * (2 * cap))()
@@ -782,9 +800,14 @@ def stream_mttkrp(source, f: FactorMatrices, mode: int, budget: DeviceBudget,
     b = L.Budget(budget.capacity_bytes, budget.num_queues, budget.reservation_bytes,
                  budget.injected_transfer_latency_s)
     c = config._c()
-    status = lib.blco_stream_mttkrp(C.byref(layout._c), max_nnz_per_block or 0, cb, None,
-                                    _ptr_array(fs), f.rank, mode, C.byref(b), C.byref(c),
-                                    int(strategy), device, _pd(out), C.byref(r))
+    if mode is None:
+        status = lib.blco_stream_mttkrp_all(C.byref(layout._c), max_nnz_per_block or 0, cb, None,
+                                            _ptr_array(fs), f.rank, C.byref(b), C.byref(c),
+                                            int(strategy), device, _ptr_array(outs), C.byref(r))
+    else:
+        status = lib.blco_stream_mttkrp(C.byref(layout._c), max_nnz_per_block or 0, cb, None,
+                                        _ptr_array(fs), f.rank, mode, C.byref(b), C.byref(c),
+                                        int(strategy), device, _pd(outs[0]), C.byref(r))
     if err:
         raise err[0]
     _check(status)
@@ -797,7 +820,7 @@ def stream_mttkrp(source, f: FactorMatrices, mode: int, budget: DeviceBudget,
         report.timeline = [StreamEventRec("transfer" if tl[i].kind == 0 else "compute", tl[i].queue,
                                           tl[i].block, tl[i].begin_s, tl[i].end_s)
                            for i in range(min(r.timeline_count, 2 * cap))]
-    return out
+    return outs[0] if mode is not None else outs
 
 
 # -------------------------------------------------------------------- CP-ALS

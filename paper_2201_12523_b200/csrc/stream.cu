@@ -77,36 +77,37 @@ bool is_pinned(const void* p) {
   return a.type == cudaMemoryTypeHost;
 }
 
-}  // namespace
-}  // namespace b200
-
-using namespace b200;
-
-extern "C" int blco_stream_mttkrp(const blco_layout* layout, uint64_t max_nnz_per_block,
-                                  blco_block_source_fn next, void* ctx,
-                                  const double* const* factors, uint64_t rank, int mode,
-                                  const blco_device_budget* budget, const blco_exec_config* cfg,
-                                  int strategy, int device, double* out,
-                                  blco_stream_report* report) {
-  return guarded([&] {
+// Streams the blocks once and runs MTTKRP for every mode in modes[] on each
+// resident block (one mode: stream_mttkrp; all modes: the all-mode
+// extension, which moves the tensor over the host link once per iteration).
+void stream_impl(const blco_layout* layout, uint64_t max_nnz_per_block, blco_block_source_fn next,
+                 void* ctx, const double* const* factors, uint64_t rank, const std::vector<int>& modes,
+                 const blco_device_budget* budget, const blco_exec_config* cfg, int strategy_in,
+                 int device, double* const* outs, blco_stream_report* report) {
+  {
     blco_exec_config c;
     if (cfg) c = *cfg; else blco_exec_config_default(&c);
     if (blco_exec_config_validate(&c) != BLCO_OK) throw_format(blco_last_error());
     const blco_layout& l = *layout;
     check_device_layout(l);
     if (rank < 1) throw_format("factors: rank must be >= 1");
-    if (mode < 0 || mode >= l.order) throw_format("stream: mode out of range");
+    for (int mode : modes)
+      if (mode < 0 || mode >= l.order) throw_format("stream: mode out of range");
     if (budget->num_queues < 1) throw_format("stream: num_queues must be >= 1");
-    if (strategy == BLCO_STRATEGY_AUTO) strategy = blco_choose_strategy(l.dims[mode], &c);
-    const bool hier = strategy == BLCO_STRATEGY_HIERARCHICAL;
-    const uint64_t out_rows = l.dims[mode];
-    const uint64_t out_elems = out_rows * rank;
+    const int NM = static_cast<int>(modes.size());
+    std::vector<int> strat(NM);
+    std::vector<bool> hier(NM);
+    std::vector<uint64_t> out_elems(NM);
     const int C = std::max(1, c.num_factor_copies);
-
-    // Resident set: factors + output (+ copies), streaming.cpp:117-124.
+    // Resident set: factors + outputs (+ copies), streaming.cpp:117-124.
     uint64_t pinned = 0;
     for (int m = 0; m < l.order; ++m) pinned += l.dims[m] * rank * sizeof(double);
-    pinned += out_elems * sizeof(double) * (hier ? C : 1);
+    for (int k = 0; k < NM; ++k) {
+      strat[k] = strategy_in == BLCO_STRATEGY_AUTO ? blco_choose_strategy(l.dims[modes[k]], &c) : strategy_in;
+      hier[k] = strat[k] == BLCO_STRATEGY_HIERARCHICAL;
+      out_elems[k] = l.dims[modes[k]] * rank;
+      pinned += out_elems[k] * sizeof(double) * (hier[k] ? C : 1);
+    }
     if (pinned > budget->capacity_bytes)
       throw_format("stream: factor matrices and output (" + std::to_string(pinned) +
                    " bytes) exceed device capacity " + std::to_string(budget->capacity_bytes));
@@ -129,9 +130,13 @@ extern "C" int blco_stream_mttkrp(const blco_layout* layout, uint64_t max_nnz_pe
       if (df[m].n) B200_CUDA(cudaMemcpy(df[m].ptr, factors[m], df[m].bytes(), cudaMemcpyHostToDevice));
       fptr[m] = df[m].ptr;
     }
-    DevBuf<double> dout(out_elems), copies(hier ? out_elems * C : 0);
-    if (dout.n) B200_CUDA(cudaMemset(dout.ptr, 0, dout.bytes()));
-    if (copies.n) B200_CUDA(cudaMemset(copies.ptr, 0, copies.bytes()));
+    std::vector<DevBuf<double>> dout(NM), copies(NM);
+    for (int k = 0; k < NM; ++k) {
+      dout[k].alloc(out_elems[k]);
+      copies[k].alloc(hier[k] ? out_elems[k] * C : 0);
+      if (dout[k].n) B200_CUDA(cudaMemset(dout[k].ptr, 0, dout[k].bytes()));
+      if (copies[k].n) B200_CUDA(cudaMemset(copies[k].ptr, 0, copies[k].bytes()));
+    }
     DevBuf<uint8_t> dmode(BLCO_MAX_BITS), dbit(BLCO_MAX_BITS);
     DevBuf<int32_t> drem(BLCO_MAX_ORDER);
     B200_CUDA(cudaMemcpy(dmode.ptr, l.imap_mode, BLCO_MAX_BITS, cudaMemcpyHostToDevice));
@@ -209,24 +214,26 @@ extern "C" int blco_stream_mttkrp(const blco_layout* layout, uint64_t max_nnz_pe
           B200_CUDA(cudaEventSynchronize(tr.e));
 
         B200_CUDA(cudaEventRecord(cp.b, q.stream));
-        MttkrpLaunch a{};
-        a.view.layout = &l;
-        a.view.tiles = q.tiles.ptr;
-        a.view.ntiles = (bv.nnz + tile - 1) / tile;
-        a.view.elem_end = bv.nnz;
-        a.view.idx = q.idx.ptr;
-        a.view.vals = q.vals.ptr;
-        a.view.block_base = q.base.ptr;
-        a.factors = fptr.data();
-        a.rank = rank;
-        a.mode = mode;
-        a.strategy = strategy;
-        a.cfg = c;
-        a.out = dout.ptr;
-        a.accumulate = 1;
-        a.stream = q.stream;
-        a.hier_copies = hier ? copies.ptr : nullptr;
-        mttkrp_enqueue(a);
+        for (int k = 0; k < NM; ++k) {
+          MttkrpLaunch a{};
+          a.view.layout = &l;
+          a.view.tiles = q.tiles.ptr;
+          a.view.ntiles = (bv.nnz + tile - 1) / tile;
+          a.view.elem_end = bv.nnz;
+          a.view.idx = q.idx.ptr;
+          a.view.vals = q.vals.ptr;
+          a.view.block_base = q.base.ptr;
+          a.factors = fptr.data();
+          a.rank = rank;
+          a.mode = modes[k];
+          a.strategy = strat[k];
+          a.cfg = c;
+          a.out = dout[k].ptr;
+          a.accumulate = 1;
+          a.stream = q.stream;
+          a.hier_copies = hier[k] ? copies[k].ptr : nullptr;
+          mttkrp_enqueue(a);
+        }
         B200_CUDA(cudaEventRecord(cp.e, q.stream));
         bytes += bbytes;
         ++ordinal;
@@ -248,10 +255,12 @@ extern "C" int blco_stream_mttkrp(const blco_layout* layout, uint64_t max_nnz_pe
       B200_CUDA(cudaStreamWaitEvent(qs[0].stream, done, 0));
       cudaEventDestroy(done);
     }
-    if (hier) merge_copies_enqueue(copies.ptr, out_elems, C, dout.ptr, 1, qs[0].stream);
+    for (int k = 0; k < NM; ++k)
+      if (hier[k]) merge_copies_enqueue(copies[k].ptr, out_elems[k], C, dout[k].ptr, 1, qs[0].stream);
     B200_CUDA(cudaEventRecord(stop, qs[0].stream));
     B200_CUDA(cudaStreamSynchronize(qs[0].stream));
-    if (out_elems) B200_CUDA(cudaMemcpy(out, dout.ptr, dout.bytes(), cudaMemcpyDeviceToHost));
+    for (int k = 0; k < NM; ++k)
+      if (out_elems[k]) B200_CUDA(cudaMemcpy(outs[k], dout[k].ptr, dout[k].bytes(), cudaMemcpyDeviceToHost));
 
     if (report) {
       float total_ms = 0;
@@ -289,6 +298,38 @@ extern "C" int blco_stream_mttkrp(const blco_layout* layout, uint64_t max_nnz_pe
     cudaEventDestroy(start);
     cudaEventDestroy(stop);
     for (auto& q : qs) cudaStreamDestroy(q.stream);
+  }
+}
+
+}  // namespace
+}  // namespace b200
+
+using namespace b200;
+
+extern "C" int blco_stream_mttkrp(const blco_layout* layout, uint64_t max_nnz_per_block,
+                                  blco_block_source_fn next, void* ctx,
+                                  const double* const* factors, uint64_t rank, int mode,
+                                  const blco_device_budget* budget, const blco_exec_config* cfg,
+                                  int strategy, int device, double* out,
+                                  blco_stream_report* report) {
+  return guarded([&] {
+    stream_impl(layout, max_nnz_per_block, next, ctx, factors, rank, std::vector<int>{mode}, budget, cfg,
+                strategy, device, &out, report);
+  });
+}
+
+extern "C" int blco_stream_mttkrp_all(const blco_layout* layout, uint64_t max_nnz_per_block,
+                                      blco_block_source_fn next, void* ctx,
+                                      const double* const* factors, uint64_t rank,
+                                      const blco_device_budget* budget, const blco_exec_config* cfg,
+                                      int strategy, int device, double* const* outs,
+                                      blco_stream_report* report) {
+  return guarded([&] {
+    if (!layout) throw_format("stream: null layout");
+    std::vector<int> modes(layout->order);
+    for (int m = 0; m < layout->order; ++m) modes[m] = m;
+    stream_impl(layout, max_nnz_per_block, next, ctx, factors, rank, modes, budget, cfg, strategy, device,
+                outs, report);
   });
 }
 
