@@ -7,12 +7,12 @@
 // and every M_n in host memory on return.
 //
 // Pipeline (two CUDA streams, one device):
-//   copy stream   : H2D of the payload (idx, vals) in tile-aligned chunks,
-//                   one event per chunk;
-//   compute stream: H2D of factors / tile table / block bases, zero M_n, then
-//                   per chunk c: wait(event c), K4 for every mode over the
-//                   chunk's tiles (accumulating into M_n), and finally D2H of
-//                   every M_n.
+//   copy stream   : H2D of factors / tile table / block bases (one event),
+//                   then the payload (idx, vals) in tile-aligned chunks, one
+//                   event per chunk;
+//   compute stream: zero M_n, wait(tables), then per chunk c: wait(event c),
+//                   K4 for every mode over the chunk's tiles (accumulating
+//                   into M_n), and finally D2H of every M_n.
 // The link is the bound (16 B/nnz over PCIe/C2C against ~9 ms of compute for
 // NELL-2), so the step costs ~ H2D(payload) + one chunk's compute + D2H(M).
 // Each chunk's idx/vals are re-read by the N mode launches right after they
@@ -29,8 +29,10 @@ namespace {
 struct AllModeCtx {
   int device = -1;
   cudaStream_t copy = nullptr, comp = nullptr;
-  cudaEvent_t start = nullptr, stop = nullptr;
+  cudaEvent_t start = nullptr, stop = nullptr, tables = nullptr;
   std::vector<cudaEvent_t> chunk_ev;
+  void* host_stage = nullptr;  // pinned staging of the tile table + block bases
+  size_t host_cap = 0;
   DevBuf<uint64_t> idx;
   DevBuf<double> vals;
   DevBuf<uint32_t> base;
@@ -42,6 +44,11 @@ struct AllModeCtx {
     chunk_ev.clear();
     if (start) cudaEventDestroy(start);
     if (stop) cudaEventDestroy(stop);
+    if (tables) cudaEventDestroy(tables);
+    if (host_stage) cudaFreeHost(host_stage);
+    host_stage = nullptr;
+    host_cap = 0;
+    tables = nullptr;
     if (copy) cudaStreamDestroy(copy);
     if (comp) cudaStreamDestroy(comp);
     start = stop = nullptr;
@@ -74,6 +81,7 @@ AllModeCtx& context(int device) {
     B200_CUDA(cudaStreamCreateWithFlags(&c.comp, cudaStreamNonBlocking));
     B200_CUDA(cudaEventCreate(&c.start));
     B200_CUDA(cudaEventCreate(&c.stop));
+    B200_CUDA(cudaEventCreateWithFlags(&c.tables, cudaEventDisableTiming));
     c.device = device;
   }
   return c;
@@ -146,9 +154,39 @@ extern "C" int blco_mttkrp_all_host(const blco_layout* layout, uint64_t nblocks,
     }
     uint64_t h2d = 0, d2h = 0, launches0 = g_launches.load();
 
+    // Staging of the small tables in pinned memory, so every copy below is
+    // asynchronous.  Everything the kernels need besides the payload goes
+    // first on the copy stream: copies of one direction are served in issue
+    // order by the copy engine, so anything queued behind the payload chunks
+    // would hold the first kernel back until the whole payload had landed.
+    const size_t tile_bytes = ht.size() * sizeof(TileDesc), base_bytes = hbase.size() * 4;
+    if (x.host_cap < tile_bytes + base_bytes) {
+      if (x.host_stage) cudaFreeHost(x.host_stage);
+      x.host_stage = nullptr;
+      x.host_cap = 0;
+      B200_CUDA(cudaHostAlloc(&x.host_stage, tile_bytes + base_bytes, cudaHostAllocPortable));
+      x.host_cap = tile_bytes + base_bytes;
+    }
     B200_CUDA(cudaEventRecord(x.start, x.comp));
-    B200_CUDA(cudaStreamWaitEvent(x.copy, x.start, 0));
-    // payload chunks on the copy stream
+    B200_CUDA(cudaStreamWaitEvent(x.copy, x.start, 0));  // the previous call's D2H / kernels are done
+    std::memcpy(x.host_stage, ht.data(), tile_bytes);
+    std::memcpy(static_cast<char*>(x.host_stage) + tile_bytes, hbase.data(), base_bytes);
+    std::vector<const double*> fptr(N);
+    for (int m = 0; m < N; ++m) {
+      const uint64_t n = l.dims[m] * rank;
+      B200_CUDA(cudaMemcpyAsync(x.fac[m].ptr, factors[m], n * 8, cudaMemcpyHostToDevice, x.copy));
+      B200_CUDA(cudaMemsetAsync(x.out[m].ptr, 0, n * 8, x.comp));
+      fptr[m] = x.fac[m].ptr;
+      h2d += n * 8;
+    }
+    if (!ht.empty()) {
+      B200_CUDA(cudaMemcpyAsync(x.tiles.ptr, x.host_stage, tile_bytes, cudaMemcpyHostToDevice, x.copy));
+      B200_CUDA(cudaMemcpyAsync(x.base.ptr, static_cast<char*>(x.host_stage) + tile_bytes, base_bytes,
+                                cudaMemcpyHostToDevice, x.copy));
+      h2d += tile_bytes + base_bytes;
+    }
+    B200_CUDA(cudaEventRecord(x.tables, x.copy));
+    // payload chunks
     for (size_t k = 0; k < chunks.size(); ++k) {
       const uint64_t e0 = ht[chunks[k].first].start;
       const uint64_t e1 = ht[chunks[k].second - 1].start + ht[chunks[k].second - 1].count;
@@ -163,21 +201,7 @@ extern "C" int blco_mttkrp_all_host(const blco_layout* layout, uint64_t nblocks,
       }
       B200_CUDA(cudaEventRecord(x.chunk_ev[k], x.copy));
     }
-    // factors, tables, zeroed outputs on the compute stream
-    std::vector<const double*> fptr(N);
-    for (int m = 0; m < N; ++m) {
-      const uint64_t n = l.dims[m] * rank;
-      B200_CUDA(cudaMemcpyAsync(x.fac[m].ptr, factors[m], n * 8, cudaMemcpyHostToDevice, x.comp));
-      B200_CUDA(cudaMemsetAsync(x.out[m].ptr, 0, n * 8, x.comp));
-      fptr[m] = x.fac[m].ptr;
-      h2d += n * 8;
-    }
-    if (!ht.empty()) {
-      B200_CUDA(cudaMemcpyAsync(x.tiles.ptr, ht.data(), ht.size() * sizeof(TileDesc), cudaMemcpyHostToDevice,
-                                x.comp));
-      B200_CUDA(cudaMemcpyAsync(x.base.ptr, hbase.data(), hbase.size() * 4, cudaMemcpyHostToDevice, x.comp));
-      h2d += ht.size() * sizeof(TileDesc) + hbase.size() * 4;
-    }
+    B200_CUDA(cudaStreamWaitEvent(x.comp, x.tables, 0));
     std::vector<int> strat(N);
     for (int m = 0; m < N; ++m)
       strat[m] = strategy == BLCO_STRATEGY_AUTO ? blco_choose_strategy(l.dims[m], &c) : strategy;

@@ -33,6 +33,29 @@ def test_streamed_equals_in_memory(gpu):  # test_streaming.cpp:21-52
         assert rep.bytes_streamed == t.total_nnz * 16
 
 
+def test_streamed_all_modes(gpu, oracle):
+    """stream_mttkrp_all_modes: blocks cross the link once, every mode's M
+    equals the oracle; the resident set counts all N outputs."""
+    dims = [50, 40, 60]
+    coo, t = small_tensor(gpu, dims, 600, 83, 8, 64)
+    f = gpu.FactorMatrices.random(dims, 4, 1)
+    want = [oracle.mttkrp_coo(dims, coo.indices, coo.values, f.factors, m) for m in range(3)]
+    outs_bytes = sum(d * 4 * 8 for d in dims)
+    for queues in (1, 3):
+        for strat in (gpu.Strategy.Register, gpu.Strategy.Hierarchical):
+            b = gpu.DeviceBudget(num_queues=queues, reservation_bytes=t.max_nnz_per_block * 16)
+            b.capacity_bytes = sum(a.size * 8 for a in f.factors) + outs_bytes + queues * b.reservation_bytes
+            rep = gpu.StreamReport()
+            got = gpu.stream_mttkrp_all_modes(t, f, b, strategy=strat, report=rep)
+            for m in range(3):
+                assert rel_frobenius(got[m], want[m]) <= 1e-12, (queues, strat, m)
+            assert rep.blocks == t.keys.size and rep.bytes_streamed == t.total_nnz * 16
+            assert rep.peak_resident_bytes <= b.capacity_bytes
+    b.capacity_bytes -= 8  # one output short of the resident set
+    with pytest.raises(gpu.FormatError):
+        gpu.stream_mttkrp_all_modes(t, f, b, strategy=gpu.Strategy.Register)
+
+
 def test_streaming_matches_reference_stream(gpu, golden):
     z, meta = golden
     for j, ent in enumerate(meta["streams"]):
