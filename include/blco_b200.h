@@ -129,6 +129,11 @@ typedef struct blco_mttkrp_stats {
   uint64_t commit_events;
   uint64_t scalar_adds;
   float kernel_ms; /* device time of the MTTKRP kernel(s), CUDA events */
+  /* sorted register kernel only: SM cycles summed over CTAs in the
+   * processing phase (load, decode, group by row) and over warps in the
+   * computing phase (gather, multiply, commit) */
+  uint64_t processing_cycles;
+  uint64_t computing_cycles;
 } blco_mttkrp_stats;
 
 /* BuildStats (proj/include/blco/blco_format.hpp:49-54), device stage times */

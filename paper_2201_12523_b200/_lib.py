@@ -50,6 +50,8 @@ class MttkrpStats(C.Structure):
         ("commit_events", C.c_uint64),
         ("scalar_adds", C.c_uint64),
         ("kernel_ms", C.c_float),
+        ("processing_cycles", C.c_uint64),
+        ("computing_cycles", C.c_uint64),
     ]
 
 

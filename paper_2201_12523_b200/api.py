@@ -121,6 +121,8 @@ class MttkrpStats:
     commit_events: int = 0
     scalar_adds: int = 0
     kernel_ms: float = 0.0
+    processing_cycles: int = 0  # sorted register kernel: SM cycles, summed over CTAs
+    computing_cycles: int = 0   # ... and over warps
 
 
 @dataclass
@@ -509,6 +511,8 @@ def _fill_stats(stats: MttkrpStats, st: L.MttkrpStats) -> None:
     stats.commit_events = st.commit_events
     stats.scalar_adds = st.scalar_adds
     stats.kernel_ms = st.kernel_ms
+    stats.processing_cycles = st.processing_cycles
+    stats.computing_cycles = st.computing_cycles
 
 
 def build_blco(coo: SparseTensorCoo, target_bits: int = 64, max_nnz_per_block: int = 1 << 27,

@@ -58,7 +58,9 @@ struct Params {
   int stash_slots;
   uint32_t shift[N];
   uint64_t mask[N];
-  unsigned long long* counters;  // [segments, stash flushes, commit lanes] or null
+  // [segments, stash flushes, commit lanes, processing-phase cycles (per
+  // CTA), computing-phase cycles (per warp)] or null
+  unsigned long long* counters;
 };
 
 // ------------------------------------------------------------ staging layout
@@ -129,7 +131,7 @@ struct Row {
 // positions so simultaneous LDS of the groups fall in disjoint banks.
 // Products accumulate in registers along a run of equal target rows and
 // commit once per run (and at the end of the group's range).
-template <int N, int LPE, int CPL, bool FULL, bool HIER>
+template <int N, int LPE, int CPL, bool FULL, bool HIER, int U = kUnroll>
 __device__ __forceinline__ void compute_range(const Params<N>& p, const Stage<N> st, int lo0, int wn,
                                               int lane, int col0, double* __restrict__ copy_out,
                                               double* stash, uint32_t* tags,
@@ -154,21 +156,21 @@ __device__ __forceinline__ void compute_range(const Params<N>& p, const Stage<N>
   for (int c = 0; c < CPL; ++c) acc[c] = 0.0;
 
   constexpr int NO = N > 1 ? N - 1 : 1;
-  for (int t0 = 0; t0 < span; t0 += kUnroll) {
-    bool ok[kUnroll];
-    double v[kUnroll];
-    uint32_t w[kUnroll][NW];
-    Row<CPL> rows[kUnroll][NO];
+  for (int t0 = 0; t0 < span; t0 += U) {
+    bool ok[U];
+    double v[U];
+    uint32_t w[U][NW];
+    Row<CPL> rows[U][NO];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
+    for (int u = 0; u < U; ++u) {
       const int j = lo + t0 + u;
       ok[u] = j < hi;
       st.get(ok[u] ? j : lo0, v[u], w[u]);
     }
-    const int jn = lo + t0 + kUnroll;
+    const int jn = lo + t0 + U;
     const uint32_t next_row = jn < hi ? st.row(jn) : 0xffffffffu;
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u)
+    for (int u = 0; u < U; ++u)
 #pragma unroll
       for (int k = 0; k < N - 1; ++k)
         if (ok[u] && (FULL || ncol_ok > 0)) {
@@ -178,7 +180,7 @@ __device__ __forceinline__ void compute_range(const Params<N>& p, const Stage<N>
             rows[u][k].v[c] = (FULL || c < ncol_ok) ? __ldg(rp + col + c * LPE) : 0.0;
         }
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
+    for (int u = 0; u < U; ++u) {
       if (!ok[u]) continue;
 #pragma unroll
       for (int c = 0; c < CPL; ++c) {
@@ -188,7 +190,7 @@ __device__ __forceinline__ void compute_range(const Params<N>& p, const Stage<N>
         acc[c] = __dadd_rn(acc[c], prod);
       }
       const uint32_t row = w[u][N - 1];
-      const uint32_t nrow = u + 1 < kUnroll ? (ok[u + 1] ? w[u + 1][N - 1] : 0xffffffffu) : next_row;
+      const uint32_t nrow = u + 1 < U ? (ok[u + 1] ? w[u + 1][N - 1] : 0xffffffffu) : next_row;
       if (nrow != row) {
         if constexpr (HIER) {
           const uint32_t slot = row % static_cast<uint32_t>(p.stash_slots);
@@ -392,21 +394,28 @@ __device__ __forceinline__ Stage<N> cta_stage(unsigned char* dyn) {
                   reinterpret_cast<uint4*>(dyn), kTileElems};
 }
 
-template <int N, int LPE, int CPL, bool FULL, bool STATS>
-__global__ void __launch_bounds__(kCtaThreads) k_mttkrp_sorted(Params<N> p) {
+template <int N, int LPE, int CPL, bool FULL, bool STATS, int U = kUnroll, int MINB = 1>
+__global__ void __launch_bounds__(kCtaThreads, MINB) k_mttkrp_sorted(Params<N> p) {
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ BucketShared bs;
   const Stage<N> st = cta_stage<N>(dyn);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const TileDesc td = p.tiles[blockIdx.x];
   unsigned long long segs = STATS ? 0 : ~0ull, commits = 0, flushes = 0;
+  long long t0 = STATS ? clock64() : 0;
   const uint32_t cnt = process_cta<N>(p, td, st, bs, segs);
+  long long t1 = STATS ? clock64() : 0;
   const int lo0 = warp * kWarpElems;
   const int wn = static_cast<int>(cnt) > lo0 ? min(kWarpElems, static_cast<int>(cnt) - lo0) : 0;
   if (wn > 0)
-    compute_range<N, LPE, CPL, FULL, false>(p, st, lo0, wn, lane, blockIdx.y * LPE * CPL, p.out, nullptr,
+    compute_range<N, LPE, CPL, FULL, false, U>(p, st, lo0, wn, lane, blockIdx.y * LPE * CPL, p.out, nullptr,
                                             nullptr, commits, flushes);
   if constexpr (STATS) {
+    const long long t2 = clock64();
+    if (lane == 0) {
+      if (threadIdx.x == 0) atomicAdd(&p.counters[3], static_cast<unsigned long long>(t1 - t0));
+      atomicAdd(&p.counters[4], static_cast<unsigned long long>(t2 - t1));
+    }
     unsigned long long s = blockIdx.y == 0 ? segs : 0, c = commits;
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) {
@@ -664,8 +673,8 @@ void run(MttkrpLaunch& a, blco_mttkrp_stats* stats) {
   Workspace& ws = workspace();
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (stats) {
-    if (ws.counters.n < 3) ws.counters.alloc(3);
-    B200_CUDA(cudaMemsetAsync(ws.counters.ptr, 0, 3 * sizeof(unsigned long long), a.stream));
+    if (ws.counters.n < 5) ws.counters.alloc(5);
+    B200_CUDA(cudaMemsetAsync(ws.counters.ptr, 0, 5 * sizeof(unsigned long long), a.stream));
     a.counters = ws.counters.ptr;
     B200_CUDA(cudaEventCreate(&e0));
     B200_CUDA(cudaEventCreate(&e1));
@@ -674,7 +683,7 @@ void run(MttkrpLaunch& a, blco_mttkrp_stats* stats) {
   mttkrp_enqueue(a);
   if (!stats) return;
   B200_CUDA(cudaEventRecord(e1, a.stream));
-  unsigned long long h[3] = {0, 0, 0};
+  unsigned long long h[5] = {0, 0, 0, 0, 0};
   B200_CUDA(cudaMemcpyAsync(h, ws.counters.ptr, sizeof h, cudaMemcpyDeviceToHost, a.stream));
   B200_CUDA(cudaStreamSynchronize(a.stream));
   float ms = 0;
@@ -695,6 +704,8 @@ void run(MttkrpLaunch& a, blco_mttkrp_stats* stats) {
     stats->scalar_adds = h[0] * a.rank;
   }
   stats->kernel_ms = ms;
+  stats->processing_cycles = h[3];
+  stats->computing_cycles = h[4];
 }
 
 }  // namespace
