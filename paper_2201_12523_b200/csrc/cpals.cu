@@ -6,9 +6,10 @@
 //   M = MTTKRP(X, n)                           (device, mttkrp.cu)
 //   A_n = M V^-1 via Cholesky of V, Tikhonov escalation on failure
 //                                              (factorisation on host, the
-//                                               I_n row solves on device)
-//   lambda = column 2-norms, A_n /= lambda     (device reductions)
-//   Gram(A_n)                                  (device)
+//                                               I_n row solves on device,
+//                                               fused with Gram(A_n))
+//   lambda = sqrt(diag Gram), A_n /= lambda     (device, fused with the
+//                                               fit's inner product)
 // then fit = 1 - sqrt(max(0, |X|^2 - 2<X,Xhat> + |Xhat|^2)) / |X|.
 // Summation orders differ from the sequential host loops, so parity is
 // tolerance-based.
@@ -25,73 +26,165 @@ namespace {
 
 constexpr int kT = 256;
 
-// Forward/back substitution of every row of M against L (R x R lower).
-template <int RMAX>
-__global__ void k_solve_rows(double* __restrict__ a, uint64_t rows, int R,
-                             const double* __restrict__ L) {
-  __shared__ double sl[RMAX * RMAX];
-  for (int i = threadIdx.x; i < R * R; i += blockDim.x) sl[i] = L[i];
-  __syncthreads();
-  for (uint64_t row = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; row < rows;
-       row += uint64_t(gridDim.x) * blockDim.x) {
-    double b[RMAX];
-    double* p = a + row * R;
+// Fused epilogue pass 1 (solve_normal + the Gram of the solution,
+// dense_kernels.cpp:68-92 and :8-21): A = M V^-1 row by row with V = L L^T,
+// and G += A^T A (upper triangle) on the same staged rows.  A CTA stages ROWS
+// rows of M through shared memory with coalesced loads (row stride R+1
+// doubles, so a thread's own row is conflict-free), solves one row per
+// thread in registers, stores the rows to A coalesced, and accumulates the
+// R(R+1)/2 pair sums of the chunk in registers (one pair set per thread),
+// flushed with one atomic per pair at the end.  diag(G) is the column
+// sum-of-squares normalize_columns needs (cpals.cpp:51-61), so the
+// separate norm pass disappears and Gram(A / lambda) = G_ij / (l_i l_j).
+constexpr int kSolveThreads = 128;
+
+template <int RM>
+constexpr int solve_rows() {
+  return 4096 / RM < kSolveThreads ? 4096 / RM : kSolveThreads;
+}
+
+// L (R x R lower, the diagonal replaced by 1 / L_ii) as a kernel parameter:
+// with R == RM every L_ik index is a compile-time constant and the solve's
+// DFMAs read it straight from the constant bank (no shared-memory traffic).
+template <int RM>
+struct LParam {
+  double v[RM * RM];
+};
+
+template <int RM, bool EXACT>
+__device__ __forceinline__ double lget(const LParam<EXACT ? RM : 1>& lp, const double* sl, int R, int i, int k) {
+  if constexpr (EXACT) return lp.v[i * RM + k];
+  else return sl[i * R + k];
+}
+
+template <int RM, bool EXACT>
+__global__ void __launch_bounds__(kSolveThreads) k_solve_gram(const double* __restrict__ m, double* __restrict__ a,
+                                                              uint64_t rows, int R,
+                                                              const __grid_constant__ LParam<EXACT ? RM : 1> lp,
+                                                              const double* __restrict__ L, double* __restrict__ g) {
+  constexpr int ROWS = solve_rows<RM>();
+  constexpr int W = kSolveThreads / 32;
+  // Gram lane blocking: lane owns AI rows x AJ columns of a GI x GJ block of G
+  // (the whole R x R for RM <= 32, with the warps splitting the staged rows;
+  // one 32 x 32 quadrant per warp for RM = 64, every warp on every row).
+  constexpr int AI = RM <= 32 ? RM / 8 : 4, AJ = RM <= 32 ? RM / 4 : 8;
+  constexpr bool QUAD = RM > 32;
+  extern __shared__ double smem[];
+  double* sl = smem;                      // R x R (generic R only)
+  // two ROWS x (R + 1) tiles (double-buffered); RR = R as a compile-time
+  // constant when R == RM, so row/column splits are shifts
+  const int RR = EXACT ? RM : R;
+  const int S = RR + 1;
+  if constexpr (!EXACT)
+    for (int i = threadIdx.x; i < R * R; i += blockDim.x) sl[i] = L[i];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int qi = QUAD ? (warp >> 1) * 32 : 0, qj = QUAD ? (warp & 1) * 32 : 0;
+  const int i0 = qi + (lane >> 2) * AI, j0 = qj + (lane & 3) * AJ;
+  double gacc[AI][AJ];
 #pragma unroll
-    for (int i = 0; i < RMAX; ++i)
-      if (i < R) b[i] = p[i];
+  for (int x = 0; x < AI; ++x)
 #pragma unroll
-    for (int i = 0; i < RMAX; ++i) {
-      if (i >= R) break;
-      double s = b[i];
+    for (int y = 0; y < AJ; ++y) gacc[x][y] = 0.0;
+
+  // cp.async prefetch of the CTA's next chunk into the other buffer while
+  // this chunk is solved (8-byte copies: the padded row stride is odd)
+  const uint64_t step = uint64_t(gridDim.x) * ROWS;
+  auto prefetch = [&](uint64_t base, double* dst) {
+    if (base < rows) {
+      const int n = static_cast<int>((rows - base < uint64_t(ROWS) ? rows - base : ROWS) * R);
+      constexpr int PER = ROWS * RM / kSolveThreads;
 #pragma unroll
-      for (int k = 0; k < RMAX; ++k)
-        if (k < i) s -= sl[i * R + k] * b[k];
-      b[i] = s / sl[i * R + i];
+      for (int j = 0; j < PER; ++j) {
+        const int k = threadIdx.x + j * kSolveThreads;
+        if (k < n) {
+          const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst + (k / RR) * S + k % RR));
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(m + base * R + k) : "memory");
+        }
+      }
     }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  double* const tile0 = smem + RM * RM;
+  prefetch(blockIdx.x * uint64_t(ROWS), tile0);
+  int buf = 0;
+  for (uint64_t r0 = blockIdx.x * uint64_t(ROWS); r0 < rows; r0 += step, buf ^= 1) {
+    const int nr = static_cast<int>(rows - r0 < uint64_t(ROWS) ? rows - r0 : ROWS);
+    double* tile = tile0 + buf * (ROWS * (RM + 1));
+    __syncthreads();  // every thread is done with the other buffer (previous chunk)
+    prefetch(r0 + step, tile0 + (buf ^ 1) * (ROWS * (RM + 1)));
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    __syncthreads();
+    if (static_cast<int>(threadIdx.x) < nr) {
+      double b[RM];
+      double* row = tile + threadIdx.x * S;
 #pragma unroll
-    for (int ii = RMAX - 1; ii >= 0; --ii) {
-      if (ii >= R) continue;
-      double s = b[ii];
+      for (int i = 0; i < RM; ++i)
+        if (i < RR) b[i] = row[i];
 #pragma unroll
-      for (int k = 0; k < RMAX; ++k)
-        if (k > ii && k < R) s -= sl[k * R + ii] * b[k];
-      b[ii] = s / sl[ii * R + ii];
+      for (int i = 0; i < RM; ++i) {
+        if (i < RR) {
+          double x = b[i];
+#pragma unroll
+          for (int k = 0; k < i; ++k) x -= lget<RM, EXACT>(lp, sl, R, i, k) * b[k];
+          b[i] = x * lget<RM, EXACT>(lp, sl, R, i, i);
+        }
+      }
+#pragma unroll
+      for (int ii = RM - 1; ii >= 0; --ii) {
+        if (ii < RR) {
+          double x = b[ii];
+#pragma unroll
+          for (int k = ii + 1; k < RM; ++k)
+            if (k < RR) x -= lget<RM, EXACT>(lp, sl, R, k, ii) * b[k];
+          b[ii] = x * lget<RM, EXACT>(lp, sl, R, ii, ii);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < RM; ++i)
+        if (i < RR) row[i] = b[i];
     }
+    __syncthreads();
+    for (int k = threadIdx.x; k < nr * RR; k += blockDim.x) a[r0 * RR + k] = tile[(k / RR) * S + k % RR];
+    for (int r = QUAD ? 0 : warp; r < nr; r += QUAD ? 1 : W) {
+      const double* t = tile + r * S;
+      double xi[AI], yj[AJ];
 #pragma unroll
-    for (int i = 0; i < RMAX; ++i)
-      if (i < R) p[i] = b[i];
+      for (int x = 0; x < AI; ++x) xi[x] = t[min(i0 + x, R - 1)];
+#pragma unroll
+      for (int y = 0; y < AJ; ++y) yj[y] = t[min(j0 + y, R - 1)];
+#pragma unroll
+      for (int x = 0; x < AI; ++x)
+#pragma unroll
+        for (int y = 0; y < AJ; ++y) gacc[x][y] += xi[x] * yj[y];
+    }
   }
-}
-
-// out[r] += sum_i a[i, r]^2 (one partial per CTA, then atomics).
-__global__ void k_col_sumsq(const double* __restrict__ a, uint64_t rows, int R,
-                            double* __restrict__ out) {
-  extern __shared__ double part[];
-  for (int i = threadIdx.x; i < R; i += blockDim.x) part[i] = 0.0;
-  __syncthreads();
-  const uint64_t n = rows * R;
-  // thread t handles column (t % R) of rows t/R, t/R + blockDim/R, ...
-  const int per = blockDim.x / R;
-  const int c = threadIdx.x % R;
-  double s = 0.0;
-  if (static_cast<int>(threadIdx.x) < per * R)
-    for (uint64_t row = blockIdx.x * uint64_t(per) + threadIdx.x / R; row < rows;
-         row += uint64_t(gridDim.x) * per) {
-      const double x = a[row * R + c];
-      s += x * x;
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+#pragma unroll
+  for (int x = 0; x < AI; ++x)
+#pragma unroll
+    for (int y = 0; y < AJ; ++y) {
+      const int gi = i0 + x, gj = j0 + y;
+      if (gi < R && gj < R && gj >= gi) atomicAdd(&g[gi * R + gj], gacc[x][y]);
     }
-  (void)n;
-  atomicAdd(&part[c], s);
-  __syncthreads();
-  for (int i = threadIdx.x; i < R; i += blockDim.x) atomicAdd(&out[i], part[i]);
 }
 
-__global__ void k_scale_cols(double* __restrict__ a, uint64_t rows, int R,
-                             const double* __restrict__ lambda) {
+// Fused epilogue pass 2: A /= lambda column-wise (cpals.cpp:59-60) and, for
+// the last mode, the fit's <X, Xhat> = sum m[i,r] lambda[r] A[i,r]
+// (cpals.cpp:36-44) on the normalised A.
+__global__ void k_scale_inner(double* __restrict__ a, uint64_t rows, int R, const double* __restrict__ lambda,
+                              const double* __restrict__ m, double* __restrict__ inner) {
   const uint64_t n = rows * R;
+  double s = 0.0;
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
-       i += uint64_t(gridDim.x) * blockDim.x)
-    a[i] /= lambda[i % R];
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const double l = lambda[(R & (R - 1)) == 0 ? i & (R - 1) : i % R];
+    const double x = a[i] * (1.0 / l);
+    a[i] = x;
+    if (m) s += m[i] * l * x;
+  }
+  if (!m) return;
+  for (int d = 16; d > 0; d >>= 1) s += __shfl_down_sync(0xffffffffu, s, d);
+  if ((threadIdx.x & 31) == 0) atomicAdd(inner, s);
 }
 
 // G (R x R, upper triangle) += A^T A.  Each CTA stages chunks of rows in
@@ -145,6 +238,8 @@ __global__ void k_sumsq(const double* __restrict__ v, uint64_t n, double* __rest
   if ((threadIdx.x & 31) == 0) atomicAdd(out, s);
 }
 
+bool exact_rank(int R) { return R == 16 || R == 32; }
+
 unsigned grid_of(uint64_t n) {
   return static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>((n + kT - 1) / kT, 148 * 16)));
 }
@@ -191,7 +286,12 @@ struct Dense {
     return g;
   }
 
-  void solve(double* m, uint64_t rows, const std::vector<double>& v) {
+  // A = M V^-1 (Cholesky with Tikhonov escalation, dense_kernels.cpp:68-92),
+  // then normalize_columns (cpals.cpp:51-61); returns lambda and leaves the
+  // Gram of the normalised A in gram_out.  For the last mode (m_inner set)
+  // also returns <X, Xhat> through *inner.  Two passes over A.
+  std::vector<double> solve_normalize(const double* m, double* a, uint64_t rows, const std::vector<double>& v,
+                                      std::vector<double>& gram_out, const double* m_inner, double* inner) {
     double trace = 0.0;
     for (int i = 0; i < R; ++i) trace += v[i * R + i];
     const double unit = trace > 0.0 ? trace / R : 1.0;
@@ -200,37 +300,56 @@ struct Dense {
     for (double lam = 1e-12 * unit; !ok && lam <= 1e-3 * unit * (1.0 + 1e-9); lam *= 10.0)
       ok = cholesky(v, R, lam, Lh);
     if (!ok) throw_error("solve_normal: matrix singular after maximal diagonal shift");
-    B200_CUDA(cudaMemcpy(L.ptr, Lh.data(), Lh.size() * 8, cudaMemcpyHostToDevice));
-    if (!rows) return;
-    if (R <= 16) k_solve_rows<16><<<grid_of(rows), kT>>>(m, rows, R, L.ptr);
-    else if (R <= 32) k_solve_rows<32><<<grid_of(rows), kT>>>(m, rows, R, L.ptr);
-    else if (R <= 64) k_solve_rows<64><<<grid_of(rows), 128>>>(m, rows, R, L.ptr);
-    else throw_format("b200: cp_als supports rank <= 64 on the device");
-    count_launch();
-    check_launch("k_solve_rows");
-  }
-
-  std::vector<double> normalize(double* a, uint64_t rows) {
-    double* lam = scratch.ptr + static_cast<size_t>(R) * R;
-    B200_CUDA(cudaMemset(lam, 0, R * 8));
+    B200_CUDA(cudaMemset(scratch.ptr, 0, static_cast<size_t>(R) * R * 8));
     if (rows) {
-      k_col_sumsq<<<grid_of(rows * R), kT, R * sizeof(double)>>>(a, rows, R, lam);
+      auto launch = [&](auto kern, auto lp_tag, int rm, int rows_per, bool exact) {
+        using LP = decltype(lp_tag);
+        LP lp{};
+        if (exact)
+          for (int i = 0; i < R * R; ++i) lp.v[i] = i % (R + 1) == 0 ? 1.0 / Lh[i] : Lh[i];
+        const size_t smem = (static_cast<size_t>(rm) * rm + 2 * static_cast<size_t>(rows_per) * (rm + 1)) * 8;
+        B200_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        int per_sm = 1;
+        B200_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSolveThreads, smem));
+        const unsigned grid = static_cast<unsigned>(
+            std::min<uint64_t>((rows + rows_per - 1) / rows_per, 148ull * std::max(1, per_sm)));
+        kern<<<grid, kSolveThreads, smem>>>(m, a, rows, R, lp, L.ptr, scratch.ptr);
+      };
+      if (!exact_rank(R)) {  // generic R: L (diagonal inverted) through shared memory
+        std::vector<double> inv(Lh);
+        for (int i = 0; i < R; ++i) inv[i * R + i] = 1.0 / Lh[i * R + i];
+        B200_CUDA(cudaMemcpy(L.ptr, inv.data(), inv.size() * 8, cudaMemcpyHostToDevice));
+      }
+      if (R == 16) launch(k_solve_gram<16, true>, LParam<16>{}, 16, solve_rows<16>(), true);
+      else if (R == 32) launch(k_solve_gram<32, true>, LParam<32>{}, 32, solve_rows<32>(), true);
+      else if (R < 16) launch(k_solve_gram<16, false>, LParam<1>{}, 16, solve_rows<16>(), false);
+      else if (R < 32) launch(k_solve_gram<32, false>, LParam<1>{}, 32, solve_rows<32>(), false);
+      else if (R <= 64) launch(k_solve_gram<64, false>, LParam<1>{}, 64, solve_rows<64>(), false);
+      else throw_format("b200: cp_als supports rank <= 64 on the device");
       count_launch();
-      check_launch("k_col_sumsq");
+      check_launch("k_solve_gram");
     }
-    std::vector<double> h(R);
-    B200_CUDA(cudaMemcpy(h.data(), lam, R * 8, cudaMemcpyDeviceToHost));
-    for (auto& x : h) {
-      x = std::sqrt(x);
-      if (x == 0.0) x = 1.0;  // cpals.cpp:58
+    std::vector<double> g(static_cast<size_t>(R) * R);
+    B200_CUDA(cudaMemcpy(g.data(), scratch.ptr, g.size() * 8, cudaMemcpyDeviceToHost));
+    std::vector<double> lam(R);
+    for (int r = 0; r < R; ++r) {
+      lam[r] = std::sqrt(g[r * R + r]);
+      if (lam[r] == 0.0) lam[r] = 1.0;  // cpals.cpp:58
     }
-    B200_CUDA(cudaMemcpy(lam, h.data(), R * 8, cudaMemcpyHostToDevice));
+    gram_out.assign(static_cast<size_t>(R) * R, 0.0);
+    for (int i = 0; i < R; ++i)
+      for (int j = i; j < R; ++j) gram_out[i * R + j] = gram_out[j * R + i] = g[i * R + j] / (lam[i] * lam[j]);
+    double* dlam = scratch.ptr + static_cast<size_t>(R) * R;
+    double* dinner = dlam + R;
+    B200_CUDA(cudaMemcpy(dlam, lam.data(), R * 8, cudaMemcpyHostToDevice));
+    if (m_inner) B200_CUDA(cudaMemset(dinner, 0, 8));
     if (rows) {
-      k_scale_cols<<<grid_of(rows * R), kT>>>(a, rows, R, lam);
+      k_scale_inner<<<grid_of(rows * R), kT>>>(a, rows, R, dlam, m_inner, dinner);
       count_launch();
-      check_launch("k_scale_cols");
+      check_launch("k_scale_inner");
     }
-    return h;
+    if (m_inner) B200_CUDA(cudaMemcpy(inner, dinner, 8, cudaMemcpyDeviceToHost));
+    return lam;
   }
 
   double inner(const double* m, const double* a, uint64_t rows, const std::vector<double>& lambda) {
@@ -348,13 +467,13 @@ int blco_cp_als_timed(const blco_tensor* t, uint64_t rank, int max_iters, double
     for (int m = 0; m < N; ++m) grams[m] = dense.gram(A[m].ptr, l.dims[m]);
     uint64_t maxrows = 0;
     for (int m = 0; m < N; ++m) maxrows = std::max<uint64_t>(maxrows, l.dims[m]);
-    DevBuf<double> mt(maxrows * rank), mlast(l.dims[N - 1] * rank);
+    DevBuf<double> mt(maxrows * rank);
     double prev = 0.0;
     int it = 0;
     // BLCO_B200_TRACE=1: synchronise after every step and report where the
     // iteration time goes (stderr).
     static const bool trace = std::getenv("BLCO_B200_TRACE") != nullptr;
-    double acc[6] = {0, 0, 0, 0, 0, 0};
+    double acc[3] = {0, 0, 0};
     auto t_last = std::chrono::steady_clock::now();
     // device-time accounting (CUDA events on the legacy stream the loop runs on)
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_mt, ev_all;
@@ -377,28 +496,23 @@ int blco_cp_als_timed(const blco_tensor* t, uint64_t rank, int max_iters, double
     };
     for (; it < max_iters; ++it) {
       if (st) mark(ev_all, true);
+      double inner = 0.0;
       for (int n = 0; n < N; ++n) {
         std::vector<double> v(static_cast<size_t>(R) * R, 1.0);
         for (int m = 0; m < N; ++m)
           if (m != n)
             for (size_t i = 0; i < v.size(); ++i) v[i] *= grams[m][i];
-        tick(5);
+        tick(2);
         if (st) mark(ev_mt, true);
         mttkrp_into(*t, ptr, rank, n, strategy, c, mt.ptr);
         if (st) mark(ev_mt, false);
-        if (n == N - 1 && mlast.n)
-          B200_CUDA(cudaMemcpy(mlast.ptr, mt.ptr, mlast.bytes(), cudaMemcpyDeviceToDevice));
         tick(0);
-        dense.solve(mt.ptr, l.dims[n], v);
+        // A_n = normalise(M V^-1) straight into A_n; M of the last mode stays
+        // in mt for the fit's inner product
+        lambda = dense.solve_normalize(mt.ptr, A[n].ptr, l.dims[n], v, grams[n], n == N - 1 ? mt.ptr : nullptr,
+                                       &inner);
         tick(1);
-        B200_CUDA(cudaMemcpy(A[n].ptr, mt.ptr, A[n].bytes(), cudaMemcpyDeviceToDevice));
-        tick(2);
-        lambda = dense.normalize(A[n].ptr, l.dims[n]);
-        tick(3);
-        grams[n] = dense.gram(A[n].ptr, l.dims[n]);
-        tick(4);
       }
-      const double inner = dense.inner(mlast.ptr, A[N - 1].ptr, l.dims[N - 1], lambda);
       const double f = fit_value(xn, inner, recon_norm_sq(grams, lambda, R));
       fit_out[it] = f;
       *iters_out = it + 1;
@@ -427,10 +541,8 @@ int blco_cp_als_timed(const blco_tensor* t, uint64_t rank, int max_iters, double
       st->iterations_ms = sum(ev_all);
     }
     if (trace)
-      std::fprintf(stderr,
-                   "[blco trace] cp_als %d iters: mttkrp %.3f s, solve %.3f s, copy %.3f s, normalize %.3f s, "
-                   "gram %.3f s, host %.3f s\n",
-                   it, acc[0], acc[1], acc[2], acc[3], acc[4], acc[5]);
+      std::fprintf(stderr, "[blco trace] cp_als %d iters: mttkrp %.3f s, solve+normalize+gram %.3f s, host %.3f s\n",
+                   it, acc[0], acc[1], acc[2]);
     emit();
   });
 }
