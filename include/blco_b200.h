@@ -99,7 +99,10 @@ uint64_t blco_batch_table(const uint64_t* block_nnz, uint64_t nblocks, uint64_t 
  * (DESIGN.md), num_compute_units feeds choose_strategy exactly as in
  * proj/src/mttkrp.cpp:17-21, num_factor_copies is honoured by the
  * hierarchical kernel, stash_slots is a lower bound on the shared-memory
- * stash, deterministic/num_threads have no device meaning. */
+ * stash, num_threads has no device meaning.  deterministic != 0 selects the
+ * fixed-order kernels of determ.cu (bit-identical results run to run, and
+ * across block splits of the same tensor; device-resident tensors only, the
+ * streamed paths reject it, nnz < 2^32, rank <= 256). */
 typedef struct blco_exec_config {
   int32_t workgroup_size;
   int32_t tile_size;

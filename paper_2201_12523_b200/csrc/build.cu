@@ -486,6 +486,7 @@ void finalize_tensor(blco_tensor& t) {
   }
   std::lock_guard<std::mutex> g(t.mu);
   t.tiles.clear();
+  t.det.clear();
 }
 
 const TileDesc* tile_table(const blco_tensor& t, uint32_t tile_elems, uint64_t* ntiles) {

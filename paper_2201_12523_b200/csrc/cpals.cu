@@ -159,13 +159,43 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve_gram(const double* __re
     }
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
+  // one R x R partial slot per warp (zeroed by the caller), summed in slot
+  // order by k_reduce_ordered: the Gram does not depend on atomic order
+  double* slot = g + (static_cast<uint64_t>(blockIdx.x) * W + warp) * R * R;
 #pragma unroll
   for (int x = 0; x < AI; ++x)
 #pragma unroll
     for (int y = 0; y < AJ; ++y) {
       const int gi = i0 + x, gj = j0 + y;
-      if (gi < R && gj < R && gj >= gi) atomicAdd(&g[gi * R + gj], gacc[x][y]);
+      if (gi < R && gj < R && gj >= gi) slot[gi * R + gj] = gacc[x][y];
     }
+}
+
+__device__ __forceinline__ double block_sum(double v);
+
+// out[w] = sum_p parts[p * width + w] with a fixed reduction tree: one CTA
+// per column, thread t adds slots t, t + blockDim, ... in order, then the
+// fixed-shape block_sum.  The result depends only on the partials.
+__global__ void k_reduce_ordered(const double* __restrict__ parts, uint64_t nparts, int width,
+                                 double* __restrict__ out) {
+  const int w = blockIdx.x;
+  double s = 0.0;
+  for (uint64_t q = threadIdx.x; q < nparts; q += blockDim.x) s += parts[q * width + w];
+  s = block_sum(s);
+  if (threadIdx.x == 0) out[w] = s;
+}
+
+// Fixed-order block sum of one value per thread: warp shuffle tree, then
+// thread 0 adds the warps' sums in warp order and returns the total.
+__device__ __forceinline__ double block_sum(double v) {
+  __shared__ double ws[32];
+  for (int d = 16; d > 0; d >>= 1) v += __shfl_down_sync(0xffffffffu, v, d);
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += ws[w];
+  return t;
 }
 
 // Fused epilogue pass 2: A /= lambda column-wise (cpals.cpp:59-60) and, for
@@ -183,8 +213,8 @@ __global__ void k_scale_inner(double* __restrict__ a, uint64_t rows, int R, cons
     if (m) s += m[i] * l * x;
   }
   if (!m) return;
-  for (int d = 16; d > 0; d >>= 1) s += __shfl_down_sync(0xffffffffu, s, d);
-  if ((threadIdx.x & 31) == 0) atomicAdd(inner, s);
+  s = block_sum(s);
+  if (threadIdx.x == 0) inner[blockIdx.x] = s;  // per-block partial, reduced in block order
 }
 
 // G (R x R, upper triangle) += A^T A.  Each CTA stages chunks of rows in
@@ -214,7 +244,7 @@ __global__ void k_gram(const double* __restrict__ a, uint64_t rows, int R,
   }
   __syncthreads();
   for (int p = threadIdx.x; p < pairs; p += blockDim.x)
-    if (p % R >= p / R) atomicAdd(&g[p], gpart[p]);
+    g[static_cast<uint64_t>(blockIdx.x) * pairs + p] = p % R >= p / R ? gpart[p] : 0.0;
 }
 
 // sum_{i,r} m[i,r] * lambda[r] * a[i,r]
@@ -225,8 +255,8 @@ __global__ void k_inner(const double* __restrict__ m, const double* __restrict__
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
        i += uint64_t(gridDim.x) * blockDim.x)
     s += m[i] * lambda[i % R] * a[i];
-  for (int d = 16; d > 0; d >>= 1) s += __shfl_down_sync(0xffffffffu, s, d);
-  if ((threadIdx.x & 31) == 0) atomicAdd(out, s);
+  s = block_sum(s);
+  if (threadIdx.x == 0) out[blockIdx.x] = s;
 }
 
 __global__ void k_sumsq(const double* __restrict__ v, uint64_t n, double* __restrict__ out) {
@@ -234,8 +264,8 @@ __global__ void k_sumsq(const double* __restrict__ v, uint64_t n, double* __rest
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
        i += uint64_t(gridDim.x) * blockDim.x)
     s += v[i] * v[i];
-  for (int d = 16; d > 0; d >>= 1) s += __shfl_down_sync(0xffffffffu, s, d);
-  if ((threadIdx.x & 31) == 0) atomicAdd(out, s);
+  s = block_sum(s);
+  if (threadIdx.x == 0) out[blockIdx.x] = s;
 }
 
 bool exact_rank(int R) { return R == 16 || R == 32; }
@@ -261,26 +291,44 @@ bool cholesky(const std::vector<double>& v, int r, double shift, std::vector<dou
   return true;
 }
 
+// Every reduction of the epilogue writes per-CTA (or per-warp) partials that
+// k_reduce_ordered sums in a fixed order, so CP-ALS is bit-reproducible given
+// bit-reproducible MTTKRPs (ExecConfig::deterministic).
 struct Dense {
   int R;
-  cudaStream_t s = nullptr;
-  DevBuf<double> L, scratch;  // scratch: R*R gram / R lambda / 1 scalar
+  DevBuf<double> L, small;  // small: R x R reduced Gram | R lambda | 1 scalar
+  DevBuf<double> parts;     // partial slots (grown on demand)
 
-  explicit Dense(int r) : R(r), L(static_cast<size_t>(r) * r), scratch(static_cast<size_t>(r) * r + r + 1) {}
+  explicit Dense(int r) : R(r), L(static_cast<size_t>(r) * r), small(static_cast<size_t>(r) * r + r + 1) {}
+
+  double* slots(uint64_t n) {
+    if (parts.n < n) parts.alloc(n);
+    return parts.ptr;
+  }
+  // sum nslots partials of `width` values in slot order into small[0..width)
+  void reduce(uint64_t nslots, int width) {
+    k_reduce_ordered<<<width, 256>>>(parts.ptr, nslots, width, small.ptr);
+    count_launch();
+    check_launch("k_reduce_ordered");
+  }
+  std::vector<double> fetch(int width) {
+    std::vector<double> h(width);
+    B200_CUDA(cudaMemcpy(h.data(), small.ptr, width * 8, cudaMemcpyDeviceToHost));
+    return h;
+  }
 
   std::vector<double> gram(const double* a, uint64_t rows) {
-    B200_CUDA(cudaMemset(scratch.ptr, 0, static_cast<size_t>(R) * R * 8));
-    if (rows) {
-      const size_t smem = (static_cast<size_t>(R) * R + kGramChunk * R) * sizeof(double);
-      if (smem > 48 * 1024)
-        B200_CUDA(cudaFuncSetAttribute(k_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-      const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((rows + kGramChunk - 1) / kGramChunk, 148 * 8));
-      k_gram<<<grid, kT, smem>>>(a, rows, R, scratch.ptr);
-      count_launch();
-      check_launch("k_gram");
-    }
-    std::vector<double> g(static_cast<size_t>(R) * R);
-    B200_CUDA(cudaMemcpy(g.data(), scratch.ptr, g.size() * 8, cudaMemcpyDeviceToHost));
+    const int RR = R * R;
+    if (!rows) return std::vector<double>(RR, 0.0);
+    const size_t smem = (static_cast<size_t>(RR) + kGramChunk * R) * sizeof(double);
+    if (smem > 48 * 1024)
+      B200_CUDA(cudaFuncSetAttribute(k_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((rows + kGramChunk - 1) / kGramChunk, 148 * 8));
+    k_gram<<<grid, kT, smem>>>(a, rows, R, slots(uint64_t(grid) * RR));
+    count_launch();
+    check_launch("k_gram");
+    reduce(grid, RR);
+    std::vector<double> g = fetch(RR);
     for (int i = 0; i < R; ++i)
       for (int j = 0; j < i; ++j) g[i * R + j] = g[j * R + i];
     return g;
@@ -300,20 +348,29 @@ struct Dense {
     for (double lam = 1e-12 * unit; !ok && lam <= 1e-3 * unit * (1.0 + 1e-9); lam *= 10.0)
       ok = cholesky(v, R, lam, Lh);
     if (!ok) throw_error("solve_normal: matrix singular after maximal diagonal shift");
-    B200_CUDA(cudaMemset(scratch.ptr, 0, static_cast<size_t>(R) * R * 8));
+    const int RR = R * R;
+    std::vector<double> g(RR, 0.0);
     if (rows) {
       auto launch = [&](auto kern, auto lp_tag, int rm, int rows_per, bool exact) {
         using LP = decltype(lp_tag);
         LP lp{};
         if (exact)
-          for (int i = 0; i < R * R; ++i) lp.v[i] = i % (R + 1) == 0 ? 1.0 / Lh[i] : Lh[i];
+          for (int i = 0; i < RR; ++i) lp.v[i] = i % (R + 1) == 0 ? 1.0 / Lh[i] : Lh[i];
         const size_t smem = (static_cast<size_t>(rm) * rm + 2 * static_cast<size_t>(rows_per) * (rm + 1)) * 8;
         B200_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         int per_sm = 1;
         B200_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSolveThreads, smem));
         const unsigned grid = static_cast<unsigned>(
             std::min<uint64_t>((rows + rows_per - 1) / rows_per, 148ull * std::max(1, per_sm)));
-        kern<<<grid, kSolveThreads, smem>>>(m, a, rows, R, lp, L.ptr, scratch.ptr);
+        const uint64_t nslots = uint64_t(grid) * (kSolveThreads / 32);
+        double* sl = slots(nslots * RR);
+        // R <= 32: every warp writes the whole upper triangle of its slot (the
+        // lower one is never read); R = 64: each warp owns one quadrant
+        if (rm > 32) B200_CUDA(cudaMemsetAsync(sl, 0, nslots * RR * 8, nullptr));
+        kern<<<grid, kSolveThreads, smem>>>(m, a, rows, R, lp, L.ptr, sl);
+        count_launch();
+        check_launch("k_solve_gram");
+        reduce(nslots, RR);
       };
       if (!exact_rank(R)) {  // generic R: L (diagonal inverted) through shared memory
         std::vector<double> inv(Lh);
@@ -326,56 +383,62 @@ struct Dense {
       else if (R < 32) launch(k_solve_gram<32, false>, LParam<1>{}, 32, solve_rows<32>(), false);
       else if (R <= 64) launch(k_solve_gram<64, false>, LParam<1>{}, 64, solve_rows<64>(), false);
       else throw_format("b200: cp_als supports rank <= 64 on the device");
-      count_launch();
-      check_launch("k_solve_gram");
+      g = fetch(RR);
     }
-    std::vector<double> g(static_cast<size_t>(R) * R);
-    B200_CUDA(cudaMemcpy(g.data(), scratch.ptr, g.size() * 8, cudaMemcpyDeviceToHost));
     std::vector<double> lam(R);
     for (int r = 0; r < R; ++r) {
       lam[r] = std::sqrt(g[r * R + r]);
       if (lam[r] == 0.0) lam[r] = 1.0;  // cpals.cpp:58
     }
-    gram_out.assign(static_cast<size_t>(R) * R, 0.0);
+    gram_out.assign(RR, 0.0);
     for (int i = 0; i < R; ++i)
       for (int j = i; j < R; ++j) gram_out[i * R + j] = gram_out[j * R + i] = g[i * R + j] / (lam[i] * lam[j]);
-    double* dlam = scratch.ptr + static_cast<size_t>(R) * R;
-    double* dinner = dlam + R;
+    double* dlam = small.ptr + RR;
     B200_CUDA(cudaMemcpy(dlam, lam.data(), R * 8, cudaMemcpyHostToDevice));
-    if (m_inner) B200_CUDA(cudaMemset(dinner, 0, 8));
+    if (m_inner) *inner = 0.0;
     if (rows) {
-      k_scale_inner<<<grid_of(rows * R), kT>>>(a, rows, R, dlam, m_inner, dinner);
+      const unsigned grid = grid_of(rows * R);
+      double* part = m_inner ? slots(grid) : nullptr;
+      k_scale_inner<<<grid, kT>>>(a, rows, R, dlam, m_inner, part);
       count_launch();
       check_launch("k_scale_inner");
+      if (m_inner) {
+        k_reduce_ordered<<<1, 256>>>(part, grid, 1, small.ptr + RR + R);
+        count_launch();
+        check_launch("k_reduce_ordered");
+        B200_CUDA(cudaMemcpy(inner, small.ptr + RR + R, 8, cudaMemcpyDeviceToHost));
+      }
     }
-    if (m_inner) B200_CUDA(cudaMemcpy(inner, dinner, 8, cudaMemcpyDeviceToHost));
     return lam;
   }
 
   double inner(const double* m, const double* a, uint64_t rows, const std::vector<double>& lambda) {
-    double* lam = scratch.ptr + static_cast<size_t>(R) * R;
-    double* out = lam + R;
+    if (!rows) return 0.0;
+    double* lam = small.ptr + R * R;
     B200_CUDA(cudaMemcpy(lam, lambda.data(), R * 8, cudaMemcpyHostToDevice));
-    B200_CUDA(cudaMemset(out, 0, 8));
-    if (rows) {
-      k_inner<<<grid_of(rows * R), kT>>>(m, a, rows, R, lam, out);
-      count_launch();
-      check_launch("k_inner");
-    }
+    const unsigned grid = grid_of(rows * R);
+    k_inner<<<grid, kT>>>(m, a, rows, R, lam, slots(grid));
+    count_launch();
+    check_launch("k_inner");
+    k_reduce_ordered<<<1, 256>>>(parts.ptr, grid, 1, lam + R);
+    count_launch();
+    check_launch("k_reduce_ordered");
     double h = 0;
-    B200_CUDA(cudaMemcpy(&h, out, 8, cudaMemcpyDeviceToHost));
+    B200_CUDA(cudaMemcpy(&h, lam + R, 8, cudaMemcpyDeviceToHost));
     return h;
   }
 };
 
 double tensor_norm_sq(const blco_tensor& t) {
-  DevBuf<double> out(1);
-  B200_CUDA(cudaMemset(out.ptr, 0, 8));
-  if (t.nnz) {
-    k_sumsq<<<grid_of(t.nnz), kT>>>(t.vals.ptr, t.nnz, out.ptr);
-    count_launch();
-    check_launch("k_sumsq");
-  }
+  if (!t.nnz) return 0.0;
+  const unsigned grid = grid_of(t.nnz);
+  DevBuf<double> part(grid), out(1);
+  k_sumsq<<<grid, kT>>>(t.vals.ptr, t.nnz, part.ptr);
+  count_launch();
+  check_launch("k_sumsq");
+  k_reduce_ordered<<<1, 256>>>(part.ptr, grid, 1, out.ptr);
+  count_launch();
+  check_launch("k_reduce_ordered");
   double h = 0;
   B200_CUDA(cudaMemcpy(&h, out.ptr, 8, cudaMemcpyDeviceToHost));
   return h;
@@ -401,6 +464,7 @@ void mttkrp_into(const blco_tensor& t, const std::vector<const double*>& f, uint
                  int strategy, const blco_exec_config& cfg, double* out) {
   MttkrpLaunch a{};
   a.view = view_of(t);
+  a.tensor = &t;
   a.factors = f.data();
   a.rank = R;
   a.mode = mode;

@@ -105,6 +105,16 @@ struct TileDesc {
 };
 static_assert(sizeof(TileDesc) == 16, "TileDesc must stay 16 bytes");
 
+// Deterministic-mode index of one mode (determ.cu): element ids sorted
+// stably by target row, rows split into chunks, long rows' partial slots.
+struct DetIndex {
+  DevBuf<uint32_t> perm;
+  DevBuf<uint64_t> chunk_begin, block_off;
+  DevBuf<uint32_t> chunk_count, chunk_row, chunk_part;
+  DevBuf<uint32_t> multi_row, multi_first, multi_nparts;
+  uint64_t nparts = 0;
+};
+
 }  // namespace b200
 
 // ------------------------------------------------------- the opaque tensor
@@ -121,6 +131,8 @@ struct blco_tensor {
   // tile tables keyed by tile size, built lazily
   mutable std::mutex mu;
   mutable std::map<uint32_t, b200::DevBuf<b200::TileDesc>> tiles;
+  // deterministic-mode indices keyed by mode, built lazily
+  mutable std::map<int, b200::DetIndex> det;
 
   uint64_t nblocks() const { return keys.size(); }
 };
@@ -147,6 +159,7 @@ struct MttkrpLaunch {
   double* out;  // device, dims[mode] x rank
   int accumulate;
   cudaStream_t stream;
+  const blco_tensor* tensor = nullptr;     // set for device-resident tensors (deterministic mode)
   double* hier_copies = nullptr;           // persistent copies (caller merges)
   unsigned long long* counters = nullptr;  // stats counters or null
   uint64_t workgroups = 0;                 // out
@@ -166,6 +179,7 @@ uint64_t select_flagged(const T* in, const uint8_t* flags, uint64_t n, T* out, c
 
 KernelView view_of(const blco_tensor& t);
 void mttkrp_enqueue(MttkrpLaunch& a);
+void det_mttkrp_enqueue(const blco_tensor& t, MttkrpLaunch& a);
 void merge_copies_enqueue(const double* copies, uint64_t elems, int ncopies, double* out,
                           int accumulate, cudaStream_t s);
 uint32_t mttkrp_tile_elems();

@@ -712,6 +712,13 @@ void run(MttkrpLaunch& a, blco_mttkrp_stats* stats) {
 
 void mttkrp_enqueue(MttkrpLaunch& a) {
   if (a.rank < 1) throw_format("factors: rank must be >= 1");
+  if (a.cfg.deterministic) {
+    // fixed summation order (determ.cu); needs the device tensor's cache
+    if (!a.tensor)
+      throw_format("b200: deterministic mode needs a device-resident tensor (not the streamed paths)");
+    det_mttkrp_enqueue(*a.tensor, a);
+    return;
+  }
   switch (a.view.layout->order) {
     case 1: return launch_order<1>(a);
     case 2: return launch_order<2>(a);
@@ -741,6 +748,7 @@ int blco_mttkrp_device(const blco_tensor* t, const double* const* d_factors, uin
     DeviceGuard dg(t->device);
     MttkrpLaunch a{};
     a.view = view_of(*t);
+    a.tensor = t;
     a.factors = d_factors;
     a.rank = rank;
     a.mode = mode;
@@ -773,6 +781,7 @@ int blco_mttkrp(const blco_tensor* t, const double* const* factors, uint64_t ran
     DevBuf<double> dout(elems);
     MttkrpLaunch a{};
     a.view = view_of(*t);
+    a.tensor = t;
     a.factors = ptrs.data();
     a.rank = rank;
     a.mode = mode;

@@ -198,3 +198,39 @@ def test_all_modes_host_empty_and_errors(gpu):
     assert all(g.shape == (d, 4) and not g.any() for g, d in zip(got, dims))
     with pytest.raises(gpu.FormatError):
         gpu.mttkrp_all_modes(t, gpu.FactorMatrices.random([5, 6, 8], 4, 1))
+
+
+@pytest.mark.parametrize("dims,nnz,rank", [([700, 90, 1300], 40_000, 16), ([24, 3000, 50], 200_000, 32),
+                                           ([40, 50, 30, 20], 30_000, 33), ([300, 200], 20_000, 100),
+                                           ([5000], 3000, 8)])
+def test_deterministic_mode(gpu, oracle, dims, nnz, rank):
+    """ExecConfig::deterministic (exec.hpp:22; exec.cpp:78-86): a fixed
+    summation order on the device.  Within 1e-12 of the oracle; bit-identical
+    across runs and across block splits / key widths of the same tensor (the
+    ALTO element order does not depend on them); rows longer than one chunk
+    (2048 elements) go through the ordered partial combine."""
+    coo = gpu.synth_uniform_host(dims, nnz, 5)
+    f = gpu.FactorMatrices.random(dims, rank, 9)
+    det = gpu.ExecConfig(deterministic=True)
+    t64 = gpu.build_blco(coo, 64)
+    tsplit = gpu.build_blco(coo, max(1, sum(int(d - 1).bit_length() for d in dims) - 3), 1000)
+    assert tsplit.keys.size > 1
+    for mode in range(len(dims)):
+        want = oracle.mttkrp_coo(dims, coo.indices, coo.values, f.factors, mode)
+        a = gpu.mttkrp(t64, f, mode, det)
+        assert rel_frobenius(a, want) <= TOL
+        assert np.array_equal(a, gpu.mttkrp(t64, f, mode, det))
+        assert np.array_equal(a, gpu.mttkrp(tsplit, f, mode, det, gpu.Strategy.Hierarchical))
+
+
+def test_deterministic_rejected_on_streamed_paths(gpu):
+    dims = [50, 40, 60]
+    coo = gpu.synth_uniform_host(dims, 600, 3)
+    t = gpu.build_blco(coo, 64)
+    f = gpu.FactorMatrices.random(dims, 4, 1)
+    det = gpu.ExecConfig(deterministic=True)
+    with pytest.raises(gpu.FormatError, match="deterministic"):
+        gpu.mttkrp_all_modes(t, f, det)
+    b = gpu.DeviceBudget(capacity_bytes=1 << 30, num_queues=2, reservation_bytes=1 << 20)
+    with pytest.raises(gpu.FormatError, match="deterministic"):
+        gpu.stream_mttkrp(t, f, 0, b, det)

@@ -164,3 +164,21 @@ def test_cp_als_zero_iters_and_errors(gpu):
     assert all(np.array_equal(a, b) for a, b in zip(m.factors.factors, ref.factors))
     with pytest.raises(gpu.FormatError):
         gpu.cp_als(t, gpu.CpAlsOptions(rank=0))
+
+
+def test_cp_als_deterministic_is_bit_reproducible(gpu, golden):
+    """ExecConfig::deterministic: fixed-order MTTKRP (determ.cu) plus the
+    epilogue's fixed-order reductions make two CP-ALS runs bit-identical,
+    and they stay within the reference tolerance."""
+    z, meta = golden
+    ent = meta["cpals"][0]
+    dims = ent["dims"]
+    t = gpu.build_blco(gpu.SparseTensorCoo(dims, z["c0_in_idx"], z["c0_in_vals"]))
+    opts = gpu.CpAlsOptions(rank=ent["rank"], max_iters=ent["iters"], tol=ent["tol"], seed=ent["seed"])
+    det = gpu.ExecConfig(deterministic=True)
+    a = gpu.cp_als(t, opts, det)
+    b = gpu.cp_als(t, opts, det)
+    assert a.fit_history == b.fit_history
+    for m in range(len(dims)):
+        assert np.array_equal(a.factors.factors[m], b.factors.factors[m])
+    assert np.max(np.abs(np.array(a.fit_history) - z["c0_fit"])) <= 1e-10
