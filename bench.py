@@ -103,10 +103,24 @@ class ClockSampler:
 
 
 def dist_env():
+    """(world, rank, device).  BLCO_B200_ONE_DEVICE=1 puts every rank on
+    cuda:0 (with BLCO_B200_DIST_BACKEND=gloo) so the N > 1 code paths can be
+    exercised on a one-GPU box; timings from such a run mean nothing."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("BLCO_B200_ONE_DEVICE") == "1":
+        local = 0
     return world, rank, local
+
+
+def dist_init(torch, dev):
+    import torch.distributed as dist
+    backend = os.environ.get("BLCO_B200_DIST_BACKEND", "nccl")
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+    else:
+        dist.init_process_group(backend)
 
 
 # --------------------------------------------------------- CPU reference
@@ -190,7 +204,7 @@ def run_ours(args, world, rank_id, local):
     torch.cuda.set_device(dev)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        dist_init(torch, dev)
     stream = torch.cuda.current_stream()
     sptr = stream.cuda_stream
 
@@ -206,7 +220,8 @@ def run_ours(args, world, rank_id, local):
         ranges = b.partition(full.block_nnz(), 1024, world)
         lo, hi = ranges[rank_id]
         dt = full.slice(lo, hi, dev)
-        del full
+        if not args.check:
+            del full
     else:
         dt = full
     local_nnz = dt.nnz
@@ -320,9 +335,17 @@ def run_ours(args, world, rank_id, local):
                   "nnz_per_s": round(nnz / build_s, 1)},
         "segments_mode0": stats.segments,
     }
+    if args.check:
+        # the summed partials of the last step against the whole tensor on this device
+        errs = []
+        for m in range(N):
+            ref = torch.zeros((dims[m], R), dtype=torch.float64, device=f"cuda:{dev}")
+            full.mttkrp_device(fptr, R, m, ref.data_ptr(), strategy, cfg, stream=sptr)
+            torch.cuda.synchronize()
+            errs.append(float(torch.linalg.norm(outs[m] - ref) / torch.linalg.norm(ref)))
+        result["check"] = {"rel_frobenius_vs_single_device": errs, "ranks": world}
     if not args.no_e2e:
-        result["e2e"] = e2e_run(b, torch, dt if world == 1 else dt, dims, R, N, nnz if world == 1 else local_nnz,
-                                args, dev, world)
+        result["e2e"] = e2e_run(b, torch, dt, dims, R, N, nnz, args, dev, world)
     if rank_id == 0 and world == 1 and not args.no_cpu_baseline and args.config in ("cfg1", "nell2"):
         try:
             gbps, info = reference_sample_run(dims, nnz, R, steps=2, warmup=1)
@@ -342,9 +365,12 @@ def run_ours(args, world, rank_id, local):
 
 def e2e_run(b, torch, dt, dims, R, N, nnz, args, dev, world):
     """Same metric through the public host API (mttkrp_all_modes ->
-    blco_mttkrp_all_host): every step uploads the BLCO payload from pinned
-    host memory in chunks under the compute, uploads the host factors and
-    reads every M_n back into host memory."""
+    blco_mttkrp_all_host): every step uploads the (rank's) BLCO payload from
+    pinned host memory in chunks under the compute, uploads the host factors
+    and reads every M_n back into pinned host memory.  With N > 1 ranks the
+    outputs stay on the device, are summed with an NCCL all-reduce per mode,
+    and every rank reads the summed M_n back.  Wall clock per step, max over
+    ranks (the API call returns after its outputs are written)."""
     host = dt.to_host()
     idx = b.api.pinned_empty(host.idx.size, np.uint64)
     vals = b.api.pinned_empty(host.vals.size, np.float64)
@@ -362,26 +388,46 @@ def e2e_run(b, torch, dt, dims, R, N, nnz, args, dev, world):
     cfg = b.ExecConfig(num_compute_units=torch.cuda.get_device_properties(dev).multi_processor_count)
     strategy = b.Strategy[args.strategy]
     rep = b.AllModesReport()
+    if world > 1:
+        import torch.distributed as dist
+        douts = [torch.empty((d, R), dtype=torch.float64, device=f"cuda:{dev}") for d in dims]
+        touts = [torch.from_numpy(o) for o in outs]
 
     def step():
-        b.mttkrp_all_modes(ht, f, cfg, strategy, outs=outs, device=dev, report=rep)
-        return rep.device_ms
+        if world == 1:
+            b.mttkrp_all_modes(ht, f, cfg, strategy, outs=outs, device=dev, report=rep)
+            return
+        b.mttkrp_all_modes(ht, f, cfg, strategy, device=dev, report=rep, device_outs=[o.data_ptr() for o in douts])
+        works = [dist.all_reduce(o, async_op=True) for o in douts]
+        for w, o, t in zip(works, douts, touts):
+            w.wait()
+            t.copy_(o, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
 
     for _ in range(max(1, min(args.warmup, 3))):
         step()
     torch.cuda.synchronize()
     n = max(1, min(args.steps, 10))
+    if world > 1:
+        dist.barrier()
     w0 = time.perf_counter()
-    dev_ms = [step() for _ in range(n)]
+    for _ in range(n):
+        step()
     wall_ms = (time.perf_counter() - w0) * 1e3 / n
-    ms = sum(dev_ms) / n
+    if world > 1:
+        t = torch.tensor([wall_ms], dtype=torch.float64, device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        wall_ms = float(t.item())
     bpe = bytes_per_elem(N, R)
-    return {"value": round(nnz * N * bpe / (ms * 1e-3) / 1e9, 2), "unit": "GB/s", "ms_per_step": round(ms, 3),
-            "wall_ms_per_step": round(wall_ms, 3), "steps": n,
-            "h2d_bytes_per_step": int(rep.h2d_bytes), "d2h_bytes_per_step": int(rep.d2h_bytes),
+    d2h = sum(d * R * 8 for d in dims)
+    return {"value": round(nnz * N * bpe / (wall_ms * 1e-3) / 1e9, 2), "unit": "GB/s",
+            "ms_per_step": round(wall_ms, 3), "api_device_ms_per_call": round(rep.device_ms, 3), "steps": n,
+            "h2d_bytes_per_step": int(rep.h2d_bytes), "d2h_bytes_per_step": int(d2h),
             "chunks": int(rep.chunks), "launches_per_step": int(rep.launches),
+            "timing": "host wall clock per step (synchronous API), max over ranks",
             "path": "mttkrp_all_modes (blco_mttkrp_all_host): pinned host payload uploaded in chunks under "
-                    "the all-mode kernels, host factors in, host M_n out; CUDA events around each call"}
+                    "the all-mode kernels, host factors in, M_n out to pinned host memory"
+                    + ("" if world == 1 else " after an NCCL all-reduce of the ranks' device partials")}
 
 
 # ------------------------------------------------------------ reference arm
@@ -487,21 +533,33 @@ STREAM_CONFIGS = {
                       "host memory), R=32, out-of-memory streaming, DeviceBudget{24 GiB, 4 queues, 2 GiB}"),
     "reddit_stream_small": ([8211298, 176962, 8116559], 600_000_000, 32, 8,
                             "synthetic Reddit-shaped, 0.6B nnz (9.6 GB pinned), R=32, streamed, 24 GiB budget"),
+    "reddit_stream_tiny": ([8211298, 176962, 8116559], 20_000_000, 32, 4,
+                           "synthetic Reddit-shaped, 20M nnz, R=32, streamed (multi-rank plumbing test size)"),
 }
 
 
-def run_stream(args):
-    """stream_mttkrp (proj/src/streaming.cpp:103-309) over pinned host blocks."""
+def run_stream(args, world, rank_id, local):
+    """stream_mttkrp (proj/src/streaming.cpp:103-309) over pinned host blocks.
+
+    One all-mode step = every block crosses the host link once and all N
+    modes run on it while resident (stream_mttkrp_all_modes).  With N > 1
+    ranks each rank generates and streams its own
+    contiguous range of ALTO chunks over its own host link into device
+    partials, which an NCCL all-reduce per mode sums; time = max over ranks."""
     import torch
 
     import paper_2201_12523_b200 as b
 
     dims, nnz_target, R, nchunks, desc = STREAM_CONFIGS[args.config]
     N = len(dims)
-    torch.cuda.set_device(0)
+    dev = local
+    torch.cuda.set_device(dev)
+    if world > 1:
+        import torch.distributed as dist
+        dist_init(torch, dev)
     # host-link peak: best of 10 pinned 1 GiB H2D copies
     src = torch.empty(1 << 30, dtype=torch.uint8, pin_memory=True)
-    dst = torch.empty(1 << 30, dtype=torch.uint8, device="cuda")
+    dst = torch.empty(1 << 30, dtype=torch.uint8, device=f"cuda:{dev}")
     best = 0.0
     for _ in range(10):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -512,28 +570,35 @@ def run_stream(args):
         best = max(best, (1 << 30) / (e0.elapsed_time(e1) * 1e-3) / 1e9)
     del src, dst
     torch.cuda.empty_cache()
-    # generate the tensor chunk by chunk (device) into pinned host memory
+    # this rank's ALTO chunks, generated on the device into pinned host memory
+    c0, c1 = nchunks * rank_id // world, nchunks * (rank_id + 1) // world
     frac = float(np.prod(np.array(dims, dtype=np.float64))) / 2.0 ** 64
     ncand = int(nnz_target / nchunks / frac) + 1
-    cap = int(nnz_target * 1.02) + ncand
+    cap = int(nnz_target * 1.02 * (c1 - c0) / nchunks) + ncand
     t0 = time.perf_counter()
     idx = b.api.pinned_empty(cap, np.uint64)
     vals = b.api.pinned_empty(cap, np.float64)
     alloc_s = time.perf_counter() - t0
     t0 = time.perf_counter()
     off = 0
-    for c in range(nchunks):
+    for c in range(c0, c1):
         if off + ncand > cap:
             raise RuntimeError("stream bench: pinned buffer too small")
-        off += b.api.synth_alto_chunk(dims, c, nchunks, ncand, TENSOR_SEED, idx[off:], vals[off:])
+        off += b.api.synth_alto_chunk(dims, c, nchunks, ncand, TENSOR_SEED, idx[off:], vals[off:], device=dev)
     gen_s = time.perf_counter() - t0
-    total = off
+    local_nnz = off
+    total = local_nnz
+    if world > 1:
+        t = torch.tensor([local_nnz], dtype=torch.int64, device=f"cuda:{dev}")
+        dist.all_reduce(t)
+        total = int(t.item())
     bmax = 1 << 27
     layout = b.make_layout(dims, 64)
-    blocks = [(o, min(bmax, total - o)) for o in range(0, total, bmax)]
+    blocks = [(o, min(bmax, local_nnz - o)) for o in range(0, local_nnz, bmax)]
     f = b.FactorMatrices.random(dims, R, FACTOR_SEED)
     budget = b.DeviceBudget(capacity_bytes=24 << 30, num_queues=4, reservation_bytes=bmax * 16)
-    cfg = b.ExecConfig(num_compute_units=torch.cuda.get_device_properties(0).multi_processor_count)
+    cfg = b.ExecConfig(num_compute_units=torch.cuda.get_device_properties(dev).multi_processor_count)
+    douts = [torch.empty((d, R), dtype=torch.float64, device=f"cuda:{dev}") for d in dims] if world > 1 else None
 
     def source():
         for o, n in blocks:
@@ -541,52 +606,78 @@ def run_stream(args):
 
     def one_all():
         rep = b.StreamReport()
-        b.stream_mttkrp_all_modes(source(), f, budget, cfg, report=rep, layout=layout, max_nnz_per_block=bmax,
-                                  block_count=len(blocks))
-        return rep
+        w0 = time.perf_counter()
+        if world == 1:
+            b.stream_mttkrp_all_modes(source(), f, budget, cfg, report=rep, layout=layout, max_nnz_per_block=bmax,
+                                      block_count=len(blocks), device=dev)
+        else:
+            b.stream_mttkrp_all_modes(source(), f, budget, cfg, report=rep, layout=layout, max_nnz_per_block=bmax,
+                                      block_count=len(blocks), device=dev, device_outs=[o.data_ptr() for o in douts])
+            for o in douts:
+                dist.all_reduce(o)
+            torch.cuda.synchronize()
+        return rep, time.perf_counter() - w0
 
     def one(mode):
         rep = b.StreamReport()
         b.stream_mttkrp(source(), f, mode, budget, cfg, report=rep, layout=layout, max_nnz_per_block=bmax,
-                        block_count=len(blocks))
+                        block_count=len(blocks), device=dev)
         return rep
 
     one_all()  # warm-up (allocations, clocks)
     steps = max(1, min(args.steps, 3))
-    with ClockSampler(0) as clk:
-        reps = [one_all() for _ in range(steps)]
-    per_mode = [one(m) for m in range(N)]  # the reference's per-mode API, for comparison
+    if world > 1:
+        dist.barrier()
+    with ClockSampler(dev) as clk:
+        runs = [one_all() for _ in range(steps)]
+    reps = [r for r, _ in runs]
+    # device-timed stream (events inside the library) for N = 1; with N > 1
+    # the step also holds the NCCL reduction, so host wall time, max over ranks
+    step_s = statistics.mean(r.total_seconds for r in reps) if world == 1 else statistics.mean(w for _, w in runs)
+    if world > 1:
+        t = torch.tensor([step_s], dtype=torch.float64, device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        step_s = float(t.item())
+    per_mode = [one(m) for m in range(N)] if world == 1 else []  # the reference's per-mode API, for comparison
     overall = [r.overall_gbps for r in reps]
-    total_s = statistics.mean(r.total_seconds for r in reps)
     bpe = bytes_per_elem(N, R)
-    value = total * N * bpe / total_s / 1e9
-    print(json.dumps({
+    value = total * N * bpe / step_s / 1e9
+    result = {
         "metric": "out-of-memory MTTKRP all-mode throughput (algorithmic B_elem bytes / time), host-link bound",
-        "value": round(value, 2), "unit": "GB/s", "n_gpus": 1, "steps": steps, "warmup": 1,
-        "ms_per_step": round(total_s * 1e3, 2), "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic uniform (ALTO-chunked generator, seeded)",
-        "config": {"workload": desc, "dims": dims, "nnz": total, "rank": R, "blocks": len(blocks),
+        "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": steps, "warmup": 1,
+        "ms_per_step": round(step_s * 1e3, 2), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic uniform (ALTO-chunked generator, seeded)",
+        "config": {"workload": desc, "dims": dims, "nnz": total, "rank": R, "blocks_per_rank": len(blocks),
                    "budget": {"capacity_bytes": 24 << 30, "num_queues": 4, "reservation_bytes": bmax * 16},
                    "step": "stream_mttkrp_all_modes: every block crosses the host link once, all N modes "
-                           "computed on it while resident"},
-        "stream": {"overall_gbps_per_step": [round(x, 2) for x in overall],
-                   "compute_gbps_per_step": [round(r.compute_gbps, 2) for r in reps],
+                           "computed on it while resident"
+                           + ("" if world == 1 else "; ranks stream disjoint ALTO chunk ranges over their own "
+                                                    "links, NCCL all-reduce of M per mode")},
+        "stream": {"overall_gbps_per_step_rank0": [round(x, 2) for x in overall],
+                   "compute_gbps_per_step_rank0": [round(r.compute_gbps, 2) for r in reps],
                    "h2d_peak_gbps": round(best, 2),
-                   "link_fraction_per_step": [round(x / best, 4) for x in overall],
-                   "bytes_streamed_per_step": reps[0].bytes_streamed,
+                   "link_fraction_per_step_rank0": [round(x / best, 4) for x in overall],
+                   "bytes_streamed_per_step_rank0": reps[0].bytes_streamed,
                    "peak_resident_bytes": reps[0].peak_resident_bytes,
                    "transfer_busy_s": [round(r.transfer_busy_seconds, 3) for r in reps],
-                   "compute_busy_s": [round(r.compute_busy_seconds, 3) for r in reps],
-                   "per_mode_api": {"total_s": round(sum(r.total_seconds for r in per_mode), 3),
-                                    "overall_gbps_per_mode": [round(r.overall_gbps, 2) for r in per_mode],
-                                    "note": "stream_mttkrp once per mode (the reference API): the tensor "
-                                            "crosses the link N times"}},
+                   "compute_busy_s": [round(r.compute_busy_seconds, 3) for r in reps]},
         "roofline": {"bound": "host-link", "achieved": round(statistics.mean(overall), 2), "peak": round(best, 2),
                      "unit": "GB/s", "frac": round(statistics.mean(overall) / best, 4), "traffic": None,
                      "kernel": "H2D cudaMemcpyAsync (BLCO blocks, 16 B/nnz) overlapped with k_mttkrp_sorted x N"},
         "clocks": clk.summary(),
         "generate": {"pinned_alloc_s": round(alloc_s, 2), "generate_s": round(gen_s, 2)},
-    }), flush=True)
+    }
+    if per_mode:
+        result["stream"]["per_mode_api"] = {
+            "total_s": round(sum(r.total_seconds for r in per_mode), 3),
+            "overall_gbps_per_mode": [round(r.overall_gbps, 2) for r in per_mode],
+            "note": "stream_mttkrp once per mode (the reference API): the tensor crosses the link N times"}
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank_id == 0:
+        print(json.dumps(result), flush=True)
 
 
 def run_reference(args, world, rank_id):
@@ -640,16 +731,19 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-step-s", type=float, default=4.0)
+    ap.add_argument("--check", action="store_true",
+                    help="compare the step's (reduced) M_n with a single-device MTTKRP of the whole tensor")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
     world, rank_id, local = dist_env()
     if args.config in STREAM_CONFIGS:
         if args.impl == "reference":
-            print(json.dumps({"impl": "reference", "unavailable": "reference stream_mttkrp over 4.69B nnz "
-                              "needs ~330 GB host RAM to build"}), flush=True)
-        elif rank_id == 0:
-            run_stream(args)
+            if rank_id == 0:
+                print(json.dumps({"impl": "reference", "unavailable": "reference stream_mttkrp over 4.69B nnz "
+                                  "needs ~330 GB host RAM to build"}), flush=True)
+        else:
+            run_stream(args, world, rank_id, local)
         return
     if args.config in ALS_CONFIGS:
         if args.impl == "reference":

@@ -242,8 +242,10 @@ int blco_mttkrp_device(const blco_tensor* t, const double* const* d_factors, uin
  * gives asynchronous copies) is uploaded in tile-aligned chunks on one stream
  * while every mode's kernel runs on the chunks already resident on another;
  * factors[m] are host dims[m] x rank, outs[m] host dims[m] x rank
- * (overwritten).  chunk_elems = 0 picks max(2^20, nnz/32).  Device buffers
- * are cached per calling thread and reused by later calls. */
+ * (overwritten), or device pointers on `device` when outs_on_device != 0
+ * (multi-GPU callers reduce them with NCCL).  chunk_elems = 0 picks
+ * max(2^20, nnz/32).  Device buffers are cached per calling thread and
+ * reused by later calls.  Returns after the outputs are written. */
 typedef struct blco_all_modes_report {
   double device_ms;   /* CUDA events: first copy enqueued .. last D2H done */
   uint64_t chunks;
@@ -256,7 +258,8 @@ int blco_mttkrp_all_host(const blco_layout* layout, uint64_t nblocks, const uint
                          const uint64_t* block_nnz, const uint64_t* const* idx,
                          const double* const* vals, const double* const* factors, uint64_t rank,
                          int strategy, const blco_exec_config* cfg, uint64_t chunk_elems,
-                         int device, double* const* outs, blco_all_modes_report* report);
+                         int device, double* const* outs, int outs_on_device,
+                         blco_all_modes_report* report);
 
 /* merge_copies (mttkrp.hpp:103): out = sum_c copies[c], copy 0 first. */
 int blco_merge_copies(const double* const* copies, uint64_t ncopies, uint64_t elems,
@@ -323,12 +326,14 @@ int blco_stream_mttkrp(const blco_layout* layout, uint64_t max_nnz_per_block,
 /* B200 extension: the blocks stream once and every mode's MTTKRP runs on each
  * resident block (outs[m] = dims[m] x rank, host).  The resident set adds all
  * N outputs to the factors; same budget rules and report as above, with
- * compute intervals covering the N kernels of a block. */
+ * compute intervals covering the N kernels of a block.  outs_on_device != 0:
+ * outs[m] are device pointers on `device` (multi-GPU streaming: each rank
+ * streams its own blocks, then the partial M_m are summed with NCCL). */
 int blco_stream_mttkrp_all(const blco_layout* layout, uint64_t max_nnz_per_block,
                            blco_block_source_fn next, void* ctx, const double* const* factors,
                            uint64_t rank, const blco_device_budget* budget,
                            const blco_exec_config* cfg, int strategy, int device, double* const* outs,
-                           blco_stream_report* report);
+                           int outs_on_device, blco_stream_report* report);
 
 void blco_set_error(int status, const char* msg);
 

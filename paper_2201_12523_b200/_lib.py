@@ -155,14 +155,14 @@ SIGNATURES = {
     "blco_mttkrp_device": (_I, [_P, C.POINTER(_P), _U64, _I, _I, C.POINTER(ExecCfg), _P, _I,
                                 _P, C.POINTER(MttkrpStats)]),
     "blco_mttkrp_all_host": (_I, [C.POINTER(Layout), _U64, _PU64, _PU64, C.POINTER(_P), C.POINTER(_P),
-                                  C.POINTER(_P), _U64, _I, C.POINTER(ExecCfg), _U64, _I, C.POINTER(_P),
+                                  C.POINTER(_P), _U64, _I, C.POINTER(ExecCfg), _U64, _I, C.POINTER(_P), _I,
                                   C.POINTER(AllModesReport)]),
     "blco_merge_copies": (_I, [C.POINTER(_P), _U64, _U64, _PD]),
     "blco_stream_mttkrp": (_I, [C.POINTER(Layout), _U64, SOURCE_FN, _P, C.POINTER(_P), _U64,
                                 _I, C.POINTER(Budget), C.POINTER(ExecCfg), _I, _I, _PD,
                                 C.POINTER(StreamReport)]),
     "blco_stream_mttkrp_all": (_I, [C.POINTER(Layout), _U64, SOURCE_FN, _P, C.POINTER(_P), _U64,
-                                    C.POINTER(Budget), C.POINTER(ExecCfg), _I, _I, C.POINTER(_P),
+                                    C.POINTER(Budget), C.POINTER(ExecCfg), _I, _I, C.POINTER(_P), _I,
                                     C.POINTER(StreamReport)]),
     "blco_set_error": (None, [_I, C.c_char_p]),
     "blco_host_alloc_pinned": (_P, [_U64]),

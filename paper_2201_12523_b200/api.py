@@ -645,7 +645,8 @@ class AllModesReport:
 def mttkrp_all_modes(t: BlcoTensor, f: FactorMatrices, config: ExecConfig | None = None,
                      strategy: Strategy = Strategy.Auto, outs: Sequence[np.ndarray] | None = None,
                      chunk_elems: int = 0, device: int = 0,
-                     report: AllModesReport | None = None) -> list[np.ndarray]:
+                     report: AllModesReport | None = None,
+                     device_outs: Sequence[int] | None = None) -> list[np.ndarray] | None:
     """mttkrp(t, f, n) for every mode n of a HOST BlcoTensor in one call
     (blco_mttkrp_all_host): the payload is uploaded in chunks under the
     compute, every call.  `outs` (dims[n] x rank float64, C-contiguous; pinned
@@ -654,11 +655,17 @@ def mttkrp_all_modes(t: BlcoTensor, f: FactorMatrices, config: ExecConfig | None
     config.validate()
     dims = t.layout.dims
     f.validate(dims)
-    if outs is None:
-        outs = [np.empty((d, f.rank), dtype=np.float64) for d in dims]
-    for d, o in zip(dims, outs):
-        if o.dtype != np.float64 or o.shape != (d, f.rank) or not o.flags.c_contiguous:
-            raise FormatError("mttkrp: output arrays must be C-contiguous float64 dims[n] x rank")
+    if device_outs is not None:  # device pointers (dims[n] x rank doubles on `device`)
+        if len(device_outs) != len(dims):
+            raise FormatError("mttkrp: one output pointer per mode required")
+        optr = (C.c_void_p * len(dims))(*[int(x) for x in device_outs])
+    else:
+        if outs is None:
+            outs = [np.empty((d, f.rank), dtype=np.float64) for d in dims]
+        for d, o in zip(dims, outs):
+            if o.dtype != np.float64 or o.shape != (d, f.rank) or not o.flags.c_contiguous:
+                raise FormatError("mttkrp: output arrays must be C-contiguous float64 dims[n] x rank")
+        optr = _ptr_array(outs)
     bn = _u64(np.diff(t.offsets))
     nb = int(bn.size)
     idx_ptrs = (C.c_void_p * max(1, nb))(*[t.idx.ctypes.data + 8 * int(t.offsets[b]) for b in range(nb)])
@@ -669,11 +676,11 @@ def mttkrp_all_modes(t: BlcoTensor, f: FactorMatrices, config: ExecConfig | None
     c = config._c()
     _check(lib.blco_mttkrp_all_host(C.byref(t.layout._c), nb, _pu64(keys), _pu64(bn), idx_ptrs, val_ptrs,
                                     _ptr_array(fs), f.rank, int(strategy), C.byref(c), chunk_elems, device,
-                                    _ptr_array(outs), C.byref(rep)))
+                                    optr, int(device_outs is not None), C.byref(rep)))
     if report is not None:
         report.device_ms, report.chunks = rep.device_ms, rep.chunks
         report.h2d_bytes, report.d2h_bytes, report.launches = rep.h2d_bytes, rep.d2h_bytes, rep.launches
-    return list(outs)
+    return None if device_outs is not None else list(outs)
 
 
 def merge_copies(copies: Sequence[np.ndarray]) -> np.ndarray:
@@ -744,15 +751,18 @@ def stream_mttkrp_all_modes(source, f: FactorMatrices, budget: DeviceBudget,
                             config: ExecConfig | None = None, strategy: Strategy = Strategy.Auto,
                             report: StreamReport | None = None, device: int = 0,
                             layout: BitLayout | None = None, max_nnz_per_block: int | None = None,
-                            block_count: int | None = None) -> list[np.ndarray]:
+                            block_count: int | None = None,
+                            device_outs: Sequence[int] | None = None) -> list[np.ndarray] | None:
     """B200 extension of stream_mttkrp: the blocks cross the host link once and
     every mode's MTTKRP runs on each resident block (blco_stream_mttkrp_all).
-    Returns [M_0, ..., M_{N-1}]."""
+    Returns [M_0, ..., M_{N-1}], or writes them to `device_outs` (device
+    pointers on `device`, for an NCCL reduction across ranks) and returns None."""
     return _stream(source, f, None, budget, config, strategy, report, device, layout, max_nnz_per_block,
-                   block_count)
+                   block_count, device_outs)
 
 
-def _stream(source, f, mode, budget, config, strategy, report, device, layout, max_nnz_per_block, block_count):
+def _stream(source, f, mode, budget, config, strategy, report, device, layout, max_nnz_per_block, block_count,
+            device_outs=None):
     config = config or ExecConfig()
     config.validate()
     stable = isinstance(source, BlcoTensor)  # MemoryBlockSource: views outlive the call
@@ -794,7 +804,7 @@ def _stream(source, f, mode, budget, config, strategy, report, device, layout, m
     cb = L.SOURCE_FN(pull)
     fs = [_f64(a) for a in f.factors]
     modes = range(layout.order()) if mode is None else [mode]
-    outs = [np.zeros((layout.dims[m], f.rank)) for m in modes]
+    outs = [] if device_outs is not None else [np.zeros((layout.dims[m], f.rank)) for m in modes]
     cap = max(1, block_count or 4096)
     bq = (C.c_int32 * cap)()
     tl = (L.StreamEvent * (2 * cap))()
@@ -805,9 +815,12 @@ def _stream(source, f, mode, budget, config, strategy, report, device, layout, m
                  budget.injected_transfer_latency_s)
     c = config._c()
     if mode is None:
+        optr = ((C.c_void_p * len(modes))(*[int(x) for x in device_outs]) if device_outs is not None
+                else _ptr_array(outs))
         status = lib.blco_stream_mttkrp_all(C.byref(layout._c), max_nnz_per_block or 0, cb, None,
                                             _ptr_array(fs), f.rank, C.byref(b), C.byref(c),
-                                            int(strategy), device, _ptr_array(outs), C.byref(r))
+                                            int(strategy), device, optr, int(device_outs is not None),
+                                            C.byref(r))
     else:
         status = lib.blco_stream_mttkrp(C.byref(layout._c), max_nnz_per_block or 0, cb, None,
                                         _ptr_array(fs), f.rank, mode, C.byref(b), C.byref(c),
@@ -824,6 +837,8 @@ def _stream(source, f, mode, budget, config, strategy, report, device, layout, m
         report.timeline = [StreamEventRec("transfer" if tl[i].kind == 0 else "compute", tl[i].queue,
                                           tl[i].block, tl[i].begin_s, tl[i].end_s)
                            for i in range(min(r.timeline_count, 2 * cap))]
+    if device_outs is not None:
+        return None
     return outs[0] if mode is not None else outs
 
 

@@ -97,7 +97,7 @@ extern "C" int blco_mttkrp_all_host(const blco_layout* layout, uint64_t nblocks,
                                     const double* const* vals, const double* const* factors,
                                     uint64_t rank, int strategy, const blco_exec_config* cfg,
                                     uint64_t chunk_elems, int device, double* const* outs,
-                                    blco_all_modes_report* report) {
+                                    int outs_on_device, blco_all_modes_report* report) {
   return guarded([&] {
     blco_exec_config c;
     if (cfg) c = *cfg; else blco_exec_config_default(&c);
@@ -229,8 +229,12 @@ extern "C" int blco_mttkrp_all_host(const blco_layout* layout, uint64_t nblocks,
     }
     for (int m = 0; m < N; ++m) {
       const uint64_t n = l.dims[m] * rank;
-      B200_CUDA(cudaMemcpyAsync(outs[m], x.out[m].ptr, n * 8, cudaMemcpyDeviceToHost, x.comp));
-      d2h += n * 8;
+      if (outs_on_device) {
+        B200_CUDA(cudaMemcpyAsync(outs[m], x.out[m].ptr, n * 8, cudaMemcpyDeviceToDevice, x.comp));
+      } else {
+        B200_CUDA(cudaMemcpyAsync(outs[m], x.out[m].ptr, n * 8, cudaMemcpyDeviceToHost, x.comp));
+        d2h += n * 8;
+      }
     }
     B200_CUDA(cudaEventRecord(x.stop, x.comp));
     B200_CUDA(cudaStreamSynchronize(x.comp));

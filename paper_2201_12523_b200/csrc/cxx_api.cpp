@@ -605,7 +605,7 @@ std::vector<DenseMatrix> mttkrp_all_modes(const BlcoTensor& t, const FactorMatri
   const auto ptrs = factor_ptrs(f);
   const blco_exec_config c = to_c(config);
   ck(blco_mttkrp_all_host(&l, keys.size(), keys.data(), nnz.data(), idx.data(), vals.data(), ptrs.data(),
-                          f.rank, static_cast<int>(strategy), &c, 0, current_device(), optr.data(), nullptr));
+                          f.rank, static_cast<int>(strategy), &c, 0, current_device(), optr.data(), 0, nullptr));
   return out;
 }
 

@@ -83,7 +83,7 @@ bool is_pinned(const void* p) {
 void stream_impl(const blco_layout* layout, uint64_t max_nnz_per_block, blco_block_source_fn next,
                  void* ctx, const double* const* factors, uint64_t rank, const std::vector<int>& modes,
                  const blco_device_budget* budget, const blco_exec_config* cfg, int strategy_in,
-                 int device, double* const* outs, blco_stream_report* report) {
+                 int device, double* const* outs, bool outs_on_device, blco_stream_report* report) {
   {
     blco_exec_config c;
     if (cfg) c = *cfg; else blco_exec_config_default(&c);
@@ -260,7 +260,9 @@ void stream_impl(const blco_layout* layout, uint64_t max_nnz_per_block, blco_blo
     B200_CUDA(cudaEventRecord(stop, qs[0].stream));
     B200_CUDA(cudaStreamSynchronize(qs[0].stream));
     for (int k = 0; k < NM; ++k)
-      if (out_elems[k]) B200_CUDA(cudaMemcpy(outs[k], dout[k].ptr, dout[k].bytes(), cudaMemcpyDeviceToHost));
+      if (out_elems[k])
+        B200_CUDA(cudaMemcpy(outs[k], dout[k].ptr, dout[k].bytes(),
+                             outs_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost));
 
     if (report) {
       float total_ms = 0;
@@ -314,7 +316,7 @@ extern "C" int blco_stream_mttkrp(const blco_layout* layout, uint64_t max_nnz_pe
                                   blco_stream_report* report) {
   return guarded([&] {
     stream_impl(layout, max_nnz_per_block, next, ctx, factors, rank, std::vector<int>{mode}, budget, cfg,
-                strategy, device, &out, report);
+                strategy, device, &out, false, report);
   });
 }
 
@@ -323,13 +325,13 @@ extern "C" int blco_stream_mttkrp_all(const blco_layout* layout, uint64_t max_nn
                                       const double* const* factors, uint64_t rank,
                                       const blco_device_budget* budget, const blco_exec_config* cfg,
                                       int strategy, int device, double* const* outs,
-                                      blco_stream_report* report) {
+                                      int outs_on_device, blco_stream_report* report) {
   return guarded([&] {
     if (!layout) throw_format("stream: null layout");
     std::vector<int> modes(layout->order);
     for (int m = 0; m < layout->order; ++m) modes[m] = m;
     stream_impl(layout, max_nnz_per_block, next, ctx, factors, rank, modes, budget, cfg, strategy, device,
-                outs, report);
+                outs, outs_on_device != 0, report);
   });
 }
 

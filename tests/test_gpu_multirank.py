@@ -1,0 +1,55 @@
+"""The N > 1 code paths of bench.py (span partition + per-rank kernels +
+overlapped all-reduce of M; multi-rank e2e; multi-rank all-mode streaming)
+run under torchrun with two ranks.  The box has one GPU, so both ranks share
+cuda:0 and reduce over gloo (BLCO_B200_ONE_DEVICE, BLCO_B200_DIST_BACKEND):
+the plumbing is the one NCCL runs on an 8-GPU node; the timings are
+meaningless and not asserted.  --check compares the ranks' summed M_n with a
+single-device MTTKRP of the whole tensor (relative Frobenius <= 1e-12)."""
+import json
+import os
+import socket
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def _port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _torchrun(args, timeout=600):
+    env = dict(os.environ, BLCO_B200_ONE_DEVICE="1", BLCO_B200_DIST_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()), str(ROOT / "bench.py"), "--gpus", "2",
+           *args]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=timeout)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]  # rank 0 alone prints
+    return json.loads(lines[0])
+
+
+def test_two_rank_all_mode_step(gpu):
+    d = _torchrun(["--config", "cfg1", "--steps", "2", "--warmup", "3", "--no-cpu-baseline", "--check"])
+    assert d["n_gpus"] == 2 and d["value"] > 0
+    assert max(d["check"]["rel_frobenius_vs_single_device"]) <= 1e-12
+    assert d["e2e"]["value"] > 0 and "all-reduce" in d["e2e"]["path"]
+
+
+def test_two_rank_reference_arm_prints_once(gpu):
+    d = _torchrun(["--config", "cfg1", "--impl", "reference", "--steps", "1", "--warmup", "1",
+                   "--ref-step-s", "0.2"])
+    assert d["impl"] == "reference"
+
+
+def test_two_rank_all_mode_streaming(gpu):
+    d = _torchrun(["--config", "reddit_stream_tiny", "--steps", "1"])
+    assert d["n_gpus"] == 2 and d["value"] > 0
+    assert d["config"]["nnz"] > 19_000_000 and "all-reduce" in d["config"]["step"]
