@@ -3,14 +3,15 @@
 // flagged compaction.  They replace CUB on the construction path (K2/K3);
 // CUB's DeviceRadixSort stays only as the cross-check in the GPU tests.
 //
-// Radix sort, per 8-bit digit pass over tiles of 4096 elements (256 threads x
-// 16 items, striped: item s of thread t is element s*256 + t of the tile):
+// Radix sort, per 8-bit digit pass over tiles of 2048 elements (256 threads x
+// 8 items):
 //   k_digit_hist : per-tile 256-bin histogram -> hist[digit * ntiles + tile]
 //   scan         : exclusive scan of hist (digit-major) -> global offsets
-//   k_digit_scatter : stable in-tile ranks (warp __match_any_sync + per-warp
-//                  digit counts in shared memory, 16 position-ordered steps),
-//                  scatter key and payload to offset[digit][tile] + rank.
-// HBM traffic per pass: keys+payload read twice, written once.
+//   k_digit_scatter : stable in-tile ranks (warp __match_any_sync against
+//                  per-warp digit histograms), one block scan, the tile
+//                  sorted by digit in shared memory, then written out as
+//                  coalesced digit runs at offset[digit][tile].
+// HBM traffic per pass: keys read twice, payload once, both written once.
 #include <algorithm>
 
 #include "internal.hpp"
@@ -19,8 +20,8 @@ namespace b200 {
 namespace {
 
 constexpr int kSortThreads = 256;
-constexpr int kSortItems = 16;
-constexpr int kSortTile = kSortThreads * kSortItems;  // 4096
+constexpr int kSortItems = 8;
+constexpr int kSortTile = kSortThreads * kSortItems;  // 2048
 constexpr int kDigits = 256;
 constexpr int kScanItems = 16;
 constexpr int kScanTile = 256 * kScanItems;
@@ -45,6 +46,17 @@ __global__ void __launch_bounds__(kSortThreads) k_digit_hist(const K* __restrict
   }
 }
 
+// Stable scatter of one tile, staged through shared memory so the global
+// writes are digit runs (coalesced) instead of one random store per element:
+//   1. warp w ranks its 256 elements (w*256 + i*32 + lane, i = 0..7, i.e.
+//      in element order) with __match_any_sync against a per-warp digit
+//      histogram in shared memory -- no block barrier per item;
+//   2. one block scan over (digit, warp) gives each element's position in
+//      the tile sorted by digit (stable: digit, then warp, then item, lane);
+//   3. keys and payloads are scattered into shared memory at those
+//      positions, then written out in position order: position p of digit d
+//      goes to offsets[d][tile] + (p - tile_start[d]), so neighbouring
+//      threads write neighbouring addresses.
 template <class K>
 __global__ void __launch_bounds__(kSortThreads) k_digit_scatter(const K* __restrict__ keys_in,
                                                               const uint32_t* __restrict__ vals_in, uint64_t n,
@@ -52,38 +64,86 @@ __global__ void __launch_bounds__(kSortThreads) k_digit_scatter(const K* __restr
                                                               const uint64_t* __restrict__ offsets,
                                                               K* __restrict__ keys_out,
                                                               uint32_t* __restrict__ vals_out) {
-  __shared__ uint32_t wcnt[kSortThreads / 32][kDigits];  // per-warp digit counts of one step
-  __shared__ uint64_t run[kDigits];                        // running position per digit
+  constexpr int W = kSortThreads / 32;
+  __shared__ uint32_t whist[W][kDigits];   // per-warp digit counts -> tile positions
+  __shared__ uint32_t dstart[kDigits];     // first tile position of each digit
+  __shared__ uint64_t gbase[kDigits];      // global offset of the digit's run for this tile
+  __shared__ uint32_t wsum[W];
+  extern __shared__ __align__(16) unsigned char stage_raw[];  // the tile, sorted by digit
+  K* skeys = reinterpret_cast<K*>(stage_raw);
+  uint32_t* svals = reinterpret_cast<uint32_t*>(stage_raw + sizeof(K) * kSortTile);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    run[threadIdx.x] = offsets[static_cast<uint64_t>(threadIdx.x) * ntiles + tile];
     const uint64_t base = tile * kSortTile;
-    for (int s = 0; s < kSortItems; ++s) {
-      for (int w = 0; w < kSortThreads / 32; ++w) wcnt[w][threadIdx.x] = 0;
-      __syncthreads();
-      const uint64_t e = base + s * kSortThreads + threadIdx.x;
-      const bool ok = e < n;
-      K key{};
-      uint32_t val = 0;
-      if (ok) {
-        key = keys_in[e];
-        val = vals_in[e];
+    const int cnt = static_cast<int>(n - base < uint64_t(kSortTile) ? n - base : kSortTile);
+    for (int w = 0; w < W; ++w) whist[w][threadIdx.x] = 0;
+    gbase[threadIdx.x] = offsets[static_cast<uint64_t>(threadIdx.x) * ntiles + tile];
+    __syncthreads();
+    K key[kSortItems];
+    uint32_t val[kSortItems], rank[kSortItems];
+    uint32_t dig[kSortItems];
+#pragma unroll
+    for (int i = 0; i < kSortItems; ++i) {
+      const int e = warp * (32 * kSortItems) + i * 32 + lane;
+      const bool ok = e < cnt;
+      key[i] = ok ? keys_in[base + e] : K{};
+      val[i] = ok ? vals_in[base + e] : 0u;
+      dig[i] = ok ? static_cast<uint32_t>(key[i] >> shift) & dmask : kDigits;
+    }
+#pragma unroll
+    for (int i = 0; i < kSortItems; ++i) {
+      const unsigned peers = __match_any_sync(0xffffffffu, dig[i]);
+      const uint32_t before = __popc(peers & ((1u << lane) - 1u));
+      uint32_t prior = 0;
+      if (dig[i] < kDigits) prior = whist[warp][dig[i]];
+      __syncwarp();
+      rank[i] = prior + before;
+      if (dig[i] < kDigits && before == 0) whist[warp][dig[i]] = prior + __popc(peers);
+      __syncwarp();
+    }
+    __syncthreads();
+    // exclusive scan over (digit, warp) in digit-major order: thread t owns digit t
+    uint32_t tot = 0;
+    uint32_t mine[W];
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      mine[w] = tot;
+      tot += whist[w][threadIdx.x];
+    }
+    uint32_t x = tot;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+      if (lane >= d) x += y;
+    }
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();
+    uint32_t woff = 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) woff += w < warp ? wsum[w] : 0;
+    const uint32_t start = woff + x - tot;
+    dstart[threadIdx.x] = start;
+#pragma unroll
+    for (int w = 0; w < W; ++w) whist[w][threadIdx.x] = start + mine[w];
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < kSortItems; ++i)
+      if (dig[i] < kDigits) {
+        const uint32_t pos = whist[warp][dig[i]] + rank[i];
+        skeys[pos] = key[i];
+        svals[pos] = val[i];
       }
-      const uint32_t d = ok ? static_cast<uint32_t>(key >> shift) & dmask : kDigits;  // kDigits: none
-      const unsigned peers = __match_any_sync(0xffffffffu, d);
-      const uint32_t wrank = __popc(peers & ((1u << lane) - 1u));
-      if (ok && wrank == 0) wcnt[warp][d] = __popc(peers);
-      __syncthreads();
-      if (ok) {
-        uint64_t pos = run[d] + wrank;
-        for (int w = 0; w < warp; ++w) pos += wcnt[w][d];
-        keys_out[pos] = key;
-        vals_out[pos] = val;
+    __syncthreads();
+#pragma unroll 4
+    for (int i = 0; i < kSortItems; ++i) {
+      const int p = i * kSortThreads + threadIdx.x;
+      if (p < cnt) {
+        const K k = skeys[p];
+        const uint32_t d = static_cast<uint32_t>(k >> shift) & dmask;
+        const uint64_t g = gbase[d] + (p - dstart[d]);
+        keys_out[g] = k;
+        vals_out[g] = svals[p];
       }
-      __syncthreads();
-      uint32_t step = 0;
-      for (int w = 0; w < kSortThreads / 32; ++w) step += wcnt[w][threadIdx.x];
-      run[threadIdx.x] += step;
     }
     __syncthreads();
   }
@@ -213,7 +273,10 @@ void radix_sort_pairs(K* keys, K* keys_alt, uint32_t* vals, uint32_t* vals_alt, 
     count_launch();
     check_launch("k_digit_hist");
     scan_exclusive_u64(hist.ptr, hist.ptr, ntiles * kDigits, s);
-    k_digit_scatter<K><<<grid, kSortThreads, 0, s>>>(kin, vin, n, shift, dmask, ntiles, hist.ptr, kout, vout);
+    constexpr size_t stage = (sizeof(K) + sizeof(uint32_t)) * kSortTile;
+    B200_CUDA(cudaFuncSetAttribute(k_digit_scatter<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(stage)));
+    k_digit_scatter<K><<<grid, kSortThreads, stage, s>>>(kin, vin, n, shift, dmask, ntiles, hist.ptr, kout, vout);
     count_launch();
     check_launch("k_digit_scatter");
     std::swap(kin, kout);
