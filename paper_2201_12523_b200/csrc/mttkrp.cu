@@ -596,14 +596,8 @@ void launch_cfg(MttkrpLaunch& a) {
       return;
     }
     auto kern = stats ? k_mttkrp_sorted<N, LPE, CPL, FULL, true> : k_mttkrp_sorted<N, LPE, CPL, FULL, false>;
-    // BLCO_B200_SMEM_PAD (bytes, experiments): extra dynamic shared memory,
-    // i.e. fewer resident CTAs per SM
-    static const size_t pad = [] {
-      const char* e = std::getenv("BLCO_B200_SMEM_PAD");
-      return e ? static_cast<size_t>(std::atoll(e)) : size_t{0};
-    }();
-    set_smem(kern, tile_stage + pad);
-    kern<<<grid, kCtaThreads, tile_stage + pad, a.stream>>>(p);
+    set_smem(kern, tile_stage);
+    kern<<<grid, kCtaThreads, tile_stage, a.stream>>>(p);
     count_launch();
     check_launch("k_mttkrp_sorted");
     return;
