@@ -136,6 +136,7 @@ extern "C" int blco_mttkrp_all_host(const blco_layout* layout, uint64_t nblocks,
     }
 
     DeviceGuard dg(device);
+    NvtxRange nv("mttkrp all modes (host pipeline)");
     AllModeCtx& x = context(device);
     grow(x.idx, nnz);
     grow(x.vals, nnz);

@@ -300,6 +300,7 @@ void build_from_device_coo(blco_tensor& t, DevBuf<uint32_t>& coords, DevBuf<doub
     return;
   }
   const bool wide = l.total_bits > 64;
+  NvtxRange nv_sort("blco build: encode + sort");
   DevBuf<uint64_t> lo(nnz), hi(wide ? nnz : 0), reenc(nnz);
   DevBuf<uint32_t> perm(nnz);
   const EncodeParams ep = encode_params(l);
@@ -387,6 +388,7 @@ void build_from_device_coo(blco_tensor& t, DevBuf<uint32_t>& coords, DevBuf<doub
   }
 
   // K3: key runs, duplicate check.
+  NvtxRange nv_blocks("blco build: key runs + blocks");
   t0 = std::chrono::steady_clock::now();
   DevBuf<uint8_t> flags(nnz);
   DevBuf<unsigned> dflag(1);
@@ -429,6 +431,7 @@ void build_from_device_coo(blco_tensor& t, DevBuf<uint32_t>& coords, DevBuf<doub
   if (stats) stats->block_seconds = secs(t0);
 
   // Re-encoded indices and values in ALTO order.
+  NvtxRange nv_gather("blco build: gather payload");
   t0 = std::chrono::steady_clock::now();
   flags.reset();
   keys_out.reset();

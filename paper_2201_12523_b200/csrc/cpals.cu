@@ -559,6 +559,7 @@ int blco_cp_als_timed(const blco_tensor* t, uint64_t rank, int max_iters, double
       t_last = now;
     };
     for (; it < max_iters; ++it) {
+      NvtxRange nv("cp_als iteration");
       if (st) mark(ev_all, true);
       double inner = 0.0;
       for (int n = 0; n < N; ++n) {

@@ -11,9 +11,21 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "blco_b200.h"
 
 namespace b200 {
+
+// NVTX range for the stages of the path (build, MTTKRP launches, streamed
+// blocks, ALS iterations), visible to nsys / ncu --nvtx.  Header-only NVTX3:
+// a no-op unless a tool is attached.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // ------------------------------------------------------------------ errors
 // Internal code throws Status; the C ABI converts to (code, message).

@@ -711,6 +711,9 @@ void run(MttkrpLaunch& a, blco_mttkrp_stats* stats) {
 }  // namespace
 
 void mttkrp_enqueue(MttkrpLaunch& a) {
+  static const char* const names[8] = {"mttkrp mode 0", "mttkrp mode 1", "mttkrp mode 2", "mttkrp mode 3",
+                                        "mttkrp mode 4", "mttkrp mode 5", "mttkrp mode 6", "mttkrp mode 7"};
+  NvtxRange nv(a.mode >= 0 && a.mode < 8 ? names[a.mode] : "mttkrp");
   if (a.rank < 1) throw_format("factors: rank must be >= 1");
   if (a.cfg.deterministic) {
     // fixed summation order (determ.cu); needs the device tensor's cache

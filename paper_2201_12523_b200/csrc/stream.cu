@@ -190,6 +190,7 @@ void stream_impl(const blco_layout* layout, uint64_t max_nnz_per_block, blco_blo
           B200_CUDA(cudaMemcpy(q.tiles.ptr, h.data(), h.size() * sizeof(TileDesc), cudaMemcpyHostToDevice));
           q.capacity = cap;
         }
+        NvtxRange nv("stream: block transfer + compute");
         Interval tr{0, qi, ordinal, nullptr, nullptr}, cp{1, qi, ordinal, nullptr, nullptr};
         B200_CUDA(cudaEventCreate(&tr.b));
         B200_CUDA(cudaEventCreate(&tr.e));

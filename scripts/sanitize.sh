@@ -1,0 +1,30 @@
+# compute-sanitizer over small workloads of every kernel family (SURVEY.md 5:
+# memcheck / racecheck / synccheck on configs 1 and 4, small).  Output -> gpurun_out/.
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+cat > /tmp/san_work.py <<'PY'
+import sys
+sys.path.insert(0, ".")
+import numpy as np
+import paper_2201_12523_b200 as b
+dims = [120, 90, 150]
+coo = b.synth_uniform_host(dims, 30000, 3)
+t = b.build_blco(coo, 12, 5000)                      # device build, several blocks
+f = b.FactorMatrices.random(dims, 32, 7)
+for m in range(3):
+    b.mttkrp(t, f, m)                                  # register path
+    b.mttkrp(t, f, m, strategy=b.Strategy.Hierarchical)
+    b.mttkrp(t, f, m, b.ExecConfig(deterministic=True))
+b.mttkrp_all_modes(t, f, chunk_elems=4096)             # host pipeline
+bud = b.DeviceBudget(capacity_bytes=1 << 28, num_queues=2, reservation_bytes=t.max_nnz_per_block * 16)
+b.stream_mttkrp_all_modes(t, f, bud)                   # streaming
+d4 = [40, 50, 30, 20]
+t4 = b.DeviceTensor.synthetic_draws(d4, 20000, 42, 4)  # config-4 style draws
+b.cp_als(t4, b.CpAlsOptions(rank=16, max_iters=2, tol=-1e300, seed=7))
+print("sanitize workload done")
+PY
+for tool in memcheck racecheck synccheck; do
+  timeout 1200 compute-sanitizer --tool $tool --error-exitcode 9 python /tmp/san_work.py > gpurun_out/sanitize_$tool.log 2>&1
+  echo "$tool rc=$?" >> gpurun_out/sanitize_$tool.log
+  tail -3 gpurun_out/sanitize_$tool.log
+done

@@ -24,10 +24,10 @@ def _port():
         return s.getsockname()[1]
 
 
-def _torchrun(args, timeout=600):
+def _torchrun(args, timeout=600, world=2):
     env = dict(os.environ, BLCO_B200_ONE_DEVICE="1", BLCO_B200_DIST_BACKEND="gloo")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
-           "--master-addr", "127.0.0.1", "--master-port", str(_port()), str(ROOT / "bench.py"), "--gpus", "2",
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()), str(ROOT / "bench.py"), "--gpus", str(world),
            *args]
     r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=timeout)
     assert r.returncode == 0, r.stderr[-3000:]
@@ -36,9 +36,11 @@ def _torchrun(args, timeout=600):
     return json.loads(lines[0])
 
 
-def test_two_rank_all_mode_step(gpu):
-    d = _torchrun(["--config", "cfg1", "--steps", "2", "--warmup", "3", "--no-cpu-baseline", "--check"])
-    assert d["n_gpus"] == 2 and d["value"] > 0
+@pytest.mark.parametrize("world", [2, 3])
+def test_multi_rank_all_mode_step(gpu, world):
+    """G ranks vs G = 1 (SURVEY.md 4 "multi-node without a cluster")."""
+    d = _torchrun(["--config", "cfg1", "--steps", "2", "--warmup", "3", "--no-cpu-baseline", "--check"], world=world)
+    assert d["n_gpus"] == world and d["value"] > 0
     assert max(d["check"]["rel_frobenius_vs_single_device"]) <= 1e-12
     assert d["e2e"]["value"] > 0 and "all-reduce" in d["e2e"]["path"]
 
