@@ -335,6 +335,8 @@ def run_ours(args, world, rank_id, local):
                   "nnz_per_s": round(nnz / build_s, 1)},
         "segments_mode0": stats.segments,
     }
+    if world == 1 and not args.no_fp32:
+        result["fp32_variant"] = fp32_variant(b, torch, dt, dims, R, N, nnz, fac, outs, cfg, sptr, dev, args)
     if args.check:
         # the summed partials of the last step against the whole tensor on this device
         errs = []
@@ -361,6 +363,41 @@ def run_ours(args, world, rank_id, local):
         dist.destroy_process_group()
     if rank_id == 0:
         print(json.dumps(result), flush=True)
+
+
+def fp32_variant(b, torch, dt, dims, R, N, nnz, fac, outs, cfg, sptr, dev, args):
+    """The fp32 variant: same tensor (fp64 values), fp32
+    factors/products/output; reported beside the fp64 headline, never as it.
+    Bytes per element per mode: 8 (index) + 8 (value) + N*R*4."""
+    f32 = [a.float() for a in fac]
+    o32 = [torch.empty((d, R), dtype=torch.float32, device=f"cuda:{dev}") for d in dims]
+    fp = [a.data_ptr() for a in f32]
+    stream = torch.cuda.current_stream()
+    for _ in range(2):
+        for m in range(N):
+            dt.mttkrp_device_f32(fp, R, m, o32[m].data_ptr(), cfg, stream=sptr)
+    torch.cuda.synchronize()
+    steps = max(3, min(args.steps, 10))
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(N)]
+    tot = [0.0] * N
+    for _ in range(steps):
+        for m in range(N):
+            ev[m][0].record(stream)
+            dt.mttkrp_device_f32(fp, R, m, o32[m].data_ptr(), cfg, stream=sptr)
+            ev[m][1].record(stream)
+        torch.cuda.synchronize()
+        for m in range(N):
+            tot[m] += ev[m][0].elapsed_time(ev[m][1])
+    per_mode = [x / steps for x in tot]
+    ms = sum(per_mode)
+    # accuracy against the fp64 kernel's result of the last timed step (same factors)
+    err = [float(torch.linalg.norm(o32[m].double() - outs[m]) / torch.linalg.norm(outs[m])) for m in range(N)]
+    bpe = 16 + N * R * 4
+    return {"ms_per_step": round(ms, 4), "per_mode_ms": [round(x, 4) for x in per_mode],
+            "value": round(nnz * N * bpe / (ms * 1e-3) / 1e9, 2), "unit": "GB/s",
+            "bytes_per_elem_per_mode": bpe, "rel_frobenius_vs_fp64": err, "tolerance": 1e-5,
+            "note": "fp32 factors/products/output over the fp64-valued BLCO tensor; kernel time, inputs "
+                    "resident; not the headline (the reference computes in fp64)"}
 
 
 def e2e_run(b, torch, dt, dims, R, N, nnz, args, dev, world):
@@ -730,6 +767,7 @@ def main():
     ap.add_argument("--strategy", choices=["Auto", "Register", "Hierarchical"], default="Auto")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-fp32", action="store_true", help="skip the fp32 variant line item")
     ap.add_argument("--ref-step-s", type=float, default=4.0)
     ap.add_argument("--check", action="store_true",
                     help="compare the step's (reduced) M_n with a single-device MTTKRP of the whole tensor")

@@ -235,6 +235,16 @@ int blco_mttkrp_device(const blco_tensor* t, const double* const* d_factors, uin
                        int mode, int strategy, const blco_exec_config* cfg, double* d_out,
                        int accumulate, void* stream, blco_mttkrp_stats* stats);
 
+/* fp32 variant: fp32 factors, products and output over
+ * the same fp64-valued BLCO tensor (values rounded to fp32 per element);
+ * register strategy only, no deterministic mode.  Tolerance 1e-5 relative
+ * Frobenius against the fp64 oracle.  Device (d_*, stream, accumulate as in
+ * blco_mttkrp_device) and host (factors in, out overwritten) entries. */
+int blco_mttkrp_device_f32(const blco_tensor* t, const float* const* d_factors, uint64_t rank, int mode,
+                           const blco_exec_config* cfg, float* d_out, int accumulate, void* stream);
+int blco_mttkrp_f32(const blco_tensor* t, const float* const* factors, uint64_t rank, int mode,
+                    const blco_exec_config* cfg, float* out);
+
 /* All-mode MTTKRP of a HOST-resident BLCO tensor: outs[n] = mttkrp(t, f, n)
  * for every mode n (mttkrp.hpp:110-112 applied to modes 0..N-1, the
  * BASELINE "time/iter (all modes)" step).  The block payload (keys,

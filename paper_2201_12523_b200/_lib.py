@@ -157,6 +157,8 @@ SIGNATURES = {
     "blco_mttkrp_all_host": (_I, [C.POINTER(Layout), _U64, _PU64, _PU64, C.POINTER(_P), C.POINTER(_P),
                                   C.POINTER(_P), _U64, _I, C.POINTER(ExecCfg), _U64, _I, C.POINTER(_P), _I,
                                   C.POINTER(AllModesReport)]),
+    "blco_mttkrp_device_f32": (_I, [_P, C.POINTER(_P), _U64, _I, C.POINTER(ExecCfg), _P, _I, _P]),
+    "blco_mttkrp_f32": (_I, [_P, C.POINTER(_P), _U64, _I, C.POINTER(ExecCfg), _P]),
     "blco_merge_copies": (_I, [C.POINTER(_P), _U64, _U64, _PD]),
     "blco_stream_mttkrp": (_I, [C.POINTER(Layout), _U64, SOURCE_FN, _P, C.POINTER(_P), _U64,
                                 _I, C.POINTER(Budget), C.POINTER(ExecCfg), _I, _I, _PD,

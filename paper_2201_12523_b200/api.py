@@ -488,6 +488,14 @@ class DeviceTensor:
         return BlcoTensor(self.layout, self.max_nnz_per_block, keys[: self.nblocks].copy(), offs,
                           idx, vals)
 
+    def mttkrp_device_f32(self, d_factors: Sequence[int], rank: int, mode: int, d_out: int,
+                          config: ExecConfig | None = None, accumulate: bool = False, stream: int = 0) -> None:
+        """fp32 variant on device pointers (blco_mttkrp_device_f32), enqueued on `stream`."""
+        c = (config or ExecConfig())._c()
+        fp = (C.c_void_p * len(d_factors))(*d_factors)
+        _check(lib.blco_mttkrp_device_f32(self._h, fp, rank, mode, C.byref(c), C.c_void_p(d_out),
+                                          int(accumulate), C.c_void_p(stream)))
+
     def mttkrp_device(self, d_factors: Sequence[int], rank: int, mode: int, d_out: int,
                       strategy: Strategy = Strategy.Auto, config: ExecConfig | None = None,
                       accumulate: bool = False, stream: int = 0,
@@ -501,6 +509,26 @@ class DeviceTensor:
                                       C.byref(st) if stats is not None else None))
         if stats is not None:
             _fill_stats(stats, st)
+
+
+def mttkrp_f32(t, f, mode: int, config: ExecConfig | None = None) -> np.ndarray:
+    """fp32 variant (blco_mttkrp_f32): factors as float32 (a FactorMatrices is
+    converted), output dims[mode] x rank float32; 1e-5 relative Frobenius
+    against the fp64 oracle."""
+    config = config or ExecConfig()
+    config.validate()
+    dims = t.layout.dims
+    fs = [np.ascontiguousarray(a, dtype=np.float32) for a in (f.factors if isinstance(f, FactorMatrices) else f)]
+    rank = fs[0].shape[1]
+    if len(fs) != len(dims) or any(a.shape != (d, rank) for a, d in zip(fs, dims)):
+        raise FormatError("factors: shapes do not match the tensor")
+    if mode < 0 or mode >= len(dims):
+        raise FormatError(f"mttkrp: mode {mode + 1} out of range for order {len(dims)}")
+    d = _as_device(t)
+    out = np.zeros((dims[mode], rank), dtype=np.float32)
+    c = config._c()
+    _check(lib.blco_mttkrp_f32(d.handle, _ptr_array(fs), rank, mode, C.byref(c), C.c_void_p(out.ctypes.data)))
+    return out
 
 
 def _fill_stats(stats: MttkrpStats, st: L.MttkrpStats) -> None:

@@ -141,7 +141,10 @@ __device__ __forceinline__ void compute_range(const Params<N>& p, const Stage<N>
   constexpr int NW = 4 * Stage<N>::NM;
   const int g = lane / LPE, q = lane % LPE;
   int h = wn / G;
-  if (G > 1 && h > 1) h = (h & ~3) | 1;
+  if (G > 1 && h > 1) {
+    h = (h & ~3) | 1;                   // group starts in disjoint banks ...
+    if ((G - 1) * h > wn) h = wn / G;   // ... unless that overruns the warp's range (G = 8)
+  }
   const int lo = lo0 + g * h;
   const int hi = g == G - 1 ? lo0 + wn : lo0 + (g + 1) * h;
   const int span = max(h, wn - (G - 1) * h);
@@ -427,6 +430,128 @@ __global__ void __launch_bounds__(kCtaThreads, MINB) k_mttkrp_sorted(Params<N> p
   }
 }
 
+// ------------------------------------------------ fp32 variant (register)
+// The same processing phase (CTA bucket grouping, fp64 values staged), with
+// fp32 factors, products and output (SURVEY.md 8c/8d "fp32 variant": 1e-5
+// relative Frobenius against the fp64 oracle; B_elem = 8 + 4 + N*R*4).
+// Lane q of a group owns V adjacent columns (V*q .. V*q+V-1, then + V*LPE per
+// chunk c), so a 32-float row is one 128-byte access of a 16-lane group and a
+// commit is one vector RED (atomicAdd on float2), both a single L1 wavefront.
+// Products are formed in the oracle's order: value (rounded to fp32) first,
+// then the non-target modes ascending.
+template <int N>
+struct ParamsF32 {
+  Params<N> base;            // payload, tiles, decode tables (processing phase)
+  const float* factors[N];   // non-target modes, ascending
+  float* out;
+};
+
+template <int V>
+struct VecF;
+template <>
+struct VecF<1> {
+  using type = float;
+  static __device__ __forceinline__ float get(const type& x, int) { return x; }
+};
+template <>
+struct VecF<2> {
+  using type = float2;
+  static __device__ __forceinline__ float get(const type& x, int i) { return i ? x.y : x.x; }
+};
+
+template <int N, int LPE, int V, int CPL, bool FULL>
+__device__ __forceinline__ void compute_range_f32(const ParamsF32<N>& p, const Stage<N> st, int lo0, int wn,
+                                                  int lane, int col0) {
+  using VT = typename VecF<V>::type;
+  constexpr int G = 32 / LPE;
+  constexpr int NW = 4 * Stage<N>::NM;
+  constexpr int NO = N > 1 ? N - 1 : 1;
+  const int g = lane / LPE, q = lane % LPE;
+  int h = wn / G;
+  if (G > 1 && h > 1) {
+    h = (h & ~3) | 1;                   // group starts in disjoint banks ...
+    if ((G - 1) * h > wn) h = wn / G;   // ... unless that overruns the warp's range (G = 8)
+  }
+  const int lo = lo0 + g * h;
+  const int hi = g == G - 1 ? lo0 + wn : lo0 + (g + 1) * h;
+  const int span = max(h, wn - (G - 1) * h);
+  const int R = p.base.rank;
+  bool cok[CPL];
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) cok[c] = FULL || col0 + V * (q + LPE * c) < R;
+  float acc[CPL][V];
+#pragma unroll
+  for (int c = 0; c < CPL; ++c)
+#pragma unroll
+    for (int v = 0; v < V; ++v) acc[c][v] = 0.0f;
+  for (int t0 = 0; t0 < span; t0 += kUnroll) {
+    bool ok[kUnroll];
+    double val[kUnroll];
+    uint32_t w[kUnroll][NW];
+    VT rows[kUnroll][NO][CPL];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int j = lo + t0 + u;
+      ok[u] = j < hi;
+      st.get(ok[u] ? j : lo0, val[u], w[u]);
+    }
+    const int jn = lo + t0 + kUnroll;
+    const uint32_t next_row = jn < hi ? st.row(jn) : 0xffffffffu;
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u)
+#pragma unroll
+      for (int k = 0; k < N - 1; ++k)
+#pragma unroll
+        for (int c = 0; c < CPL; ++c)
+          if (ok[u] && cok[c])
+            rows[u][k][c] = __ldg(reinterpret_cast<const VT*>(p.factors[k] + static_cast<uint64_t>(w[u][k]) * R +
+                                                              col0 + V * (q + LPE * c)));
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      if (!ok[u]) continue;
+      const float vf = __double2float_rn(val[u]);
+#pragma unroll
+      for (int c = 0; c < CPL; ++c)
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          float prod = vf;
+#pragma unroll
+          for (int k = 0; k < N - 1; ++k) prod = __fmul_rn(prod, VecF<V>::get(rows[u][k][c], v));
+          acc[c][v] = __fadd_rn(acc[c][v], prod);
+        }
+      const uint32_t row = w[u][N - 1];
+      const uint32_t nrow = u + 1 < kUnroll ? (ok[u + 1] ? w[u + 1][N - 1] : 0xffffffffu) : next_row;
+      if (nrow != row) {
+#pragma unroll
+        for (int c = 0; c < CPL; ++c)
+          if (cok[c]) {
+            float* o = p.out + static_cast<uint64_t>(row) * R + col0 + V * (q + LPE * c);
+            if constexpr (V == 2) atomicAdd(reinterpret_cast<float2*>(o), make_float2(acc[c][0], acc[c][1]));
+            else atomicAdd(o, acc[c][0]);
+          }
+#pragma unroll
+        for (int c = 0; c < CPL; ++c)
+#pragma unroll
+          for (int v = 0; v < V; ++v) acc[c][v] = 0.0f;
+      }
+    }
+  }
+}
+
+template <int N, int LPE, int V, int CPL, bool FULL>
+__global__ void __launch_bounds__(kCtaThreads) k_mttkrp_sorted_f32(ParamsF32<N> p) {
+  extern __shared__ __align__(16) unsigned char dyn[];
+  __shared__ BucketShared bs;
+  const Stage<N> st = cta_stage<N>(dyn);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const TileDesc td = p.base.tiles[blockIdx.x];
+  unsigned long long segs = ~0ull;
+  const uint32_t cnt = process_cta<N>(p.base, td, st, bs, segs);
+  const int lo0 = warp * kWarpElems;
+  const int wn = static_cast<int>(cnt) > lo0 ? min(kWarpElems, static_cast<int>(cnt) - lo0) : 0;
+  if (wn > 0) compute_range_f32<N, LPE, V, CPL, FULL>(p, st, lo0, wn, lane, blockIdx.y * LPE * V * CPL);
+}
+
 // Persistent CTAs; dynamic shared memory = tile stage + stash (slots x R
 // doubles + tags).
 template <int N, int LPE, int CPL, bool FULL, bool STATS>
@@ -657,6 +782,62 @@ void launch_order(MttkrpLaunch& a) {
   }
 }
 
+template <int N, int LPE, int V, int CPL, bool FULL>
+void launch_f32_cfg(const KernelView& v, const float* const* factors, uint64_t rank, int mode, float* out,
+                    cudaStream_t s) {
+  const blco_layout& l = *v.layout;
+  ParamsF32<N> p{};
+  p.base.tiles = v.tiles;
+  p.base.ntiles = v.ntiles;
+  p.base.elem_end = v.elem_end;
+  p.base.idx = v.idx;
+  p.base.val = v.vals;
+  p.base.block_base = v.block_base;
+  for (int m = 0, k = 0; m < N; ++m) {
+    if (m != mode) p.factors[k++] = factors[m];
+    p.base.shift[m] = static_cast<uint32_t>(l.field_shift[m]);
+    p.base.mask[m] = l.field_mask[m];
+  }
+  p.base.mode = mode;
+  p.base.rank = static_cast<int>(rank);
+  p.out = out;
+  if (v.ntiles == 0) return;
+  const unsigned ychunks = static_cast<unsigned>((rank + LPE * V * CPL - 1) / (LPE * V * CPL));
+  const size_t stage = stage_bytes<N>(kTileElems);
+  auto kern = k_mttkrp_sorted_f32<N, LPE, V, CPL, FULL>;
+  set_smem(kern, stage);
+  kern<<<dim3(static_cast<unsigned>(v.ntiles), ychunks), kCtaThreads, stage, s>>>(p);
+  count_launch();
+  check_launch("k_mttkrp_sorted_f32");
+}
+
+template <int N>
+void launch_f32_order(const KernelView& v, const float* const* f, uint64_t rank, int mode, float* out,
+                      cudaStream_t s) {
+  switch (rank) {
+    case 8: return launch_f32_cfg<N, 4, 2, 1, true>(v, f, rank, mode, out, s);
+    case 16: return launch_f32_cfg<N, 8, 2, 1, true>(v, f, rank, mode, out, s);
+    case 32: return launch_f32_cfg<N, 16, 2, 1, true>(v, f, rank, mode, out, s);
+    case 64: return launch_f32_cfg<N, 32, 2, 1, true>(v, f, rank, mode, out, s);
+    default: return launch_f32_cfg<N, 32, 1, 1, false>(v, f, rank, mode, out, s);
+  }
+}
+
+void mttkrp_f32_enqueue(const KernelView& v, const float* const* f, uint64_t rank, int mode, float* out,
+                        cudaStream_t s) {
+  switch (v.layout->order) {
+    case 1: return launch_f32_order<1>(v, f, rank, mode, out, s);
+    case 2: return launch_f32_order<2>(v, f, rank, mode, out, s);
+    case 3: return launch_f32_order<3>(v, f, rank, mode, out, s);
+    case 4: return launch_f32_order<4>(v, f, rank, mode, out, s);
+    case 5: return launch_f32_order<5>(v, f, rank, mode, out, s);
+    case 6: return launch_f32_order<6>(v, f, rank, mode, out, s);
+    case 7: return launch_f32_order<7>(v, f, rank, mode, out, s);
+    case 8: return launch_f32_order<8>(v, f, rank, mode, out, s);
+    default: throw_format("b200: order above the device limit");
+  }
+}
+
 void validate_call(const blco_tensor* t, uint64_t rank, int mode, const blco_exec_config* cfg) {
   if (!t) throw_format("mttkrp: null tensor");
   if (blco_exec_config_validate(cfg) != BLCO_OK) throw_format(blco_last_error());
@@ -761,6 +942,47 @@ int blco_mttkrp_device(const blco_tensor* t, const double* const* d_factors, uin
     a.accumulate = accumulate;
     a.stream = static_cast<cudaStream_t>(stream);
     run(a, stats);
+  });
+}
+
+int blco_mttkrp_device_f32(const blco_tensor* t, const float* const* d_factors, uint64_t rank, int mode,
+                           const blco_exec_config* cfg, float* d_out, int accumulate, void* stream) {
+  return guarded([&] {
+    blco_exec_config c;
+    if (cfg) c = *cfg; else blco_exec_config_default(&c);
+    validate_call(t, rank, mode, &c);
+    if (c.deterministic) throw_format("b200: the fp32 variant has no deterministic mode");
+    DeviceGuard dg(t->device);
+    NvtxRange nv("mttkrp fp32");
+    const KernelView v = view_of(*t);
+    const uint64_t elems = t->layout.dims[mode] * rank;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (!accumulate && elems) B200_CUDA(cudaMemsetAsync(d_out, 0, elems * sizeof(float), s));
+    mttkrp_f32_enqueue(v, d_factors, rank, mode, d_out, s);
+  });
+}
+
+int blco_mttkrp_f32(const blco_tensor* t, const float* const* factors, uint64_t rank, int mode,
+                    const blco_exec_config* cfg, float* out) {
+  return guarded([&] {
+    blco_exec_config c;
+    if (cfg) c = *cfg; else blco_exec_config_default(&c);
+    validate_call(t, rank, mode, &c);
+    if (c.deterministic) throw_format("b200: the fp32 variant has no deterministic mode");
+    DeviceGuard dg(t->device);
+    const blco_layout& l = t->layout;
+    std::vector<DevBuf<float>> df(l.order);
+    std::vector<const float*> ptrs(l.order);
+    for (int m = 0; m < l.order; ++m) {
+      df[m].alloc(l.dims[m] * rank);
+      if (df[m].n) B200_CUDA(cudaMemcpy(df[m].ptr, factors[m], df[m].bytes(), cudaMemcpyHostToDevice));
+      ptrs[m] = df[m].ptr;
+    }
+    const uint64_t elems = l.dims[mode] * rank;
+    DevBuf<float> dout(elems);
+    if (elems) B200_CUDA(cudaMemset(dout.ptr, 0, dout.bytes()));
+    mttkrp_f32_enqueue(view_of(*t), ptrs.data(), rank, mode, dout.ptr, nullptr);
+    if (elems) B200_CUDA(cudaMemcpy(out, dout.ptr, dout.bytes(), cudaMemcpyDeviceToHost));
   });
 }
 

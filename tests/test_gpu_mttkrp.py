@@ -234,3 +234,26 @@ def test_deterministic_rejected_on_streamed_paths(gpu):
     b = gpu.DeviceBudget(capacity_bytes=1 << 30, num_queues=2, reservation_bytes=1 << 20)
     with pytest.raises(gpu.FormatError, match="deterministic"):
         gpu.stream_mttkrp(t, f, 0, b, det)
+
+
+@pytest.mark.parametrize("dims,nnz,rank", [([700, 90, 1300], 40_000, 32), ([700, 90, 1300], 40_000, 16),
+                                           ([40, 50, 30, 20], 30_000, 64), ([300, 200], 20_000, 8),
+                                           ([60, 70, 80], 20_000, 33), ([24, 3000, 50], 100_000, 32)])
+def test_fp32_variant(gpu, oracle, dims, nnz, rank):
+    """fp32 factors / products / output: relative Frobenius
+    <= 1e-5 against the fp64 oracle, every mode, device and host entries."""
+    import torch
+    coo = gpu.synth_uniform_host(dims, nnz, 13)
+    f = gpu.FactorMatrices.random(dims, rank, 7)
+    t = gpu.build_blco(coo, 64)
+    d = t.device()
+    fd = [torch.from_numpy(a.astype(np.float32)).cuda() for a in f.factors]
+    for mode in range(len(dims)):
+        want = oracle.mttkrp_coo(dims, coo.indices, coo.values, f.factors, mode)
+        got = gpu.mttkrp_f32(t, f, mode)
+        assert got.dtype == np.float32 and rel_frobenius(got, want) <= 1e-5, mode
+        out = torch.full((dims[mode], rank), 1.0, dtype=torch.float32, device="cuda")
+        d.mttkrp_device_f32([a.data_ptr() for a in fd], rank, mode, out.data_ptr(), accumulate=True,
+                            stream=torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        assert rel_frobenius(out.cpu().numpy() - 1.0, want) <= 1e-5
