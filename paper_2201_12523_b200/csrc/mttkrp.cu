@@ -66,37 +66,78 @@ struct Params {
 // ------------------------------------------------------------ staging layout
 // A staged element is its value plus its coordinates packed as u32 words:
 // words 0..N-2 hold the non-target modes (ascending), word N-1 the target row.
-// The words live structure-of-arrays in uint4 planes so one LDS.128 fetches
-// four of them; NM = ceil(N/4) planes.
+//   N <= 3 ("packed"): one 16-byte record {value, w0, w1} per element (one
+//     LDS.128 in the computing phase) plus a u32 row plane, read four rows at
+//     a time with LDS.128 when the warp is two lane groups.  Measured LSU
+//     costs: LDS.128 = 2 wavefronts and LDS.64/LDS.32 = 1 per
+//     warp instruction, so the record + row plane cost 1.25 wavefronts per
+//     element instead of 1.6 for separate value / coordinate planes.
+//   N >= 4: value f64[W] plus uint4 planes of the words (NM = ceil(N/4)).
 template <int N>
 struct Stage {
   static constexpr int NM = (N + 3) / 4;
-  double* val;   // [W]
-  uint4* meta;   // [NM][W]
+  static constexpr bool kPacked = N <= 3;
+  static constexpr int kRowPad = 8;  // row plane over-read by the 4-row loads
+  double* val;     // [W] (general layout)
+  uint4* meta;     // general: [NM][W]; packed: records [W]
+  uint32_t* rows;  // packed: [W + kRowPad]
   int W;
 
   __device__ __forceinline__ void put(int j, double v, const uint32_t (&w)[4 * NM]) const {
-    val[j] = v;
+    if constexpr (kPacked) {
+      const uint64_t b = static_cast<uint64_t>(__double_as_longlong(v));
+      meta[j] = make_uint4(static_cast<uint32_t>(b), static_cast<uint32_t>(b >> 32), N > 1 ? w[0] : 0u,
+                           N > 2 ? w[1] : 0u);
+      rows[j] = w[N - 1];
+    } else {
+      val[j] = v;
 #pragma unroll
-    for (int q = 0; q < NM; ++q) meta[q * W + j] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+      for (int q = 0; q < NM; ++q) meta[q * W + j] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+    }
   }
+  // Packed layout: fills the value and the non-target words; the row word
+  // (w[N-1]) comes from row() / rows4().
   __device__ __forceinline__ void get(int j, double& v, uint32_t (&w)[4 * NM]) const {
-    v = val[j];
+    if constexpr (kPacked) {
+      const uint4 x = meta[j];
+      v = __longlong_as_double(static_cast<long long>((static_cast<uint64_t>(x.y) << 32) | x.x));
+      if constexpr (N > 1) w[0] = x.z;
+      if constexpr (N > 2) w[1] = x.w;
+    } else {
+      v = val[j];
 #pragma unroll
-    for (int q = 0; q < NM; ++q) {
-      const uint4 x = meta[q * W + j];
-      w[4 * q] = x.x, w[4 * q + 1] = x.y, w[4 * q + 2] = x.z, w[4 * q + 3] = x.w;
+      for (int q = 0; q < NM; ++q) {
+        const uint4 x = meta[q * W + j];
+        w[4 * q] = x.x, w[4 * q + 1] = x.y, w[4 * q + 2] = x.z, w[4 * q + 3] = x.w;
+      }
     }
   }
   __device__ __forceinline__ uint32_t row(int j) const {
-    const uint32_t* plane = reinterpret_cast<const uint32_t*>(meta + ((N - 1) / 4) * W);
-    return plane[4 * j + (N - 1) % 4];
+    if constexpr (kPacked) {
+      return rows[j];
+    } else {
+      const uint32_t* plane = reinterpret_cast<const uint32_t*>(meta + ((N - 1) / 4) * W);
+      return plane[4 * j + (N - 1) % 4];
+    }
   }
+  // rows j .. j+3 (j % 4 == 0), packed layout only
+  __device__ __forceinline__ uint4 rows4(int j) const { return *reinterpret_cast<const uint4*>(rows + j); }
 };
 
 template <int N>
 constexpr size_t stage_bytes(int W) {
-  return static_cast<size_t>(W) * (sizeof(double) + Stage<N>::NM * sizeof(uint4));
+  return Stage<N>::kPacked ? static_cast<size_t>(W) * sizeof(uint4) + (W + Stage<N>::kRowPad) * sizeof(uint32_t)
+                           : static_cast<size_t>(W) * (sizeof(double) + Stage<N>::NM * sizeof(uint4));
+}
+
+// A stage of W elements carved from `base` (16-byte aligned).
+template <int N>
+__device__ __forceinline__ Stage<N> make_stage(unsigned char* base, int W) {
+  if constexpr (Stage<N>::kPacked)
+    return Stage<N>{nullptr, reinterpret_cast<uint4*>(base), reinterpret_cast<uint32_t*>(base + W * sizeof(uint4)), W};
+  else
+    return Stage<N>{reinterpret_cast<double*>(base + Stage<N>::NM * sizeof(uint4) * W), reinterpret_cast<uint4*>(base),
+                    nullptr, W};
 }
 
 // Decodes one element into packed words (non-target modes ascending, row last).
@@ -140,10 +181,17 @@ __device__ __forceinline__ void compute_range(const Params<N>& p, const Stage<N>
   constexpr int G = 32 / LPE;
   constexpr int NW = 4 * Stage<N>::NM;
   const int g = lane / LPE, q = lane % LPE;
+  // Two lane groups with the packed stage: group starts 4 (mod 8) apart, so
+  // the groups' 16-byte records and 4-row loads sit in disjoint banks and
+  // every batch starts 4-aligned.  Otherwise 1 (mod 4) apart.
+  constexpr bool kRows4 = Stage<N>::kPacked && G == 2 && U == 4;
   int h = wn / G;
-  if (G > 1 && h > 1) {
-    h = (h & ~3) | 1;                   // group starts in disjoint banks ...
-    if ((G - 1) * h > wn) h = wn / G;   // ... unless that overruns the warp's range (G = 8)
+  if constexpr (kRows4) {
+    h = h >= 4 ? (h & ~7) | 4 : 0;  // disjoint banks, 4-aligned group starts ...
+    if (h > wn) h = (wn / 2) & ~3;   // ... without overrunning the range
+  } else if (G > 1 && h > 1) {
+    h = (h & ~3) | 1;                 // disjoint banks ...
+    if ((G - 1) * h > wn) h = wn / G;  // ... without overrunning the range (G = 8)
   }
   const int lo = lo0 + g * h;
   const int hi = g == G - 1 ? lo0 + wn : lo0 + (g + 1) * h;
@@ -169,6 +217,13 @@ __device__ __forceinline__ void compute_range(const Params<N>& p, const Stage<N>
       const int j = lo + t0 + u;
       ok[u] = j < hi;
       st.get(ok[u] ? j : lo0, v[u], w[u]);
+    }
+    if constexpr (kRows4) {
+      const uint4 r4 = st.rows4(lo + t0);
+      w[0][N - 1] = r4.x, w[1][N - 1] = r4.y, w[2][N - 1] = r4.z, w[3][N - 1] = r4.w;
+    } else if constexpr (Stage<N>::kPacked) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) w[u][N - 1] = st.row(ok[u] ? lo + t0 + u : lo0);
     }
     const int jn = lo + t0 + U;
     const uint32_t next_row = jn < hi ? st.row(jn) : 0xffffffffu;
@@ -374,8 +429,7 @@ __global__ void __launch_bounds__(kCtaThreads) k_mttkrp_warp(Params<N> p) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const size_t per_warp = stage_bytes<N>(kWarpElems);
   unsigned char* mine = dyn + warp * per_warp;
-  const Stage<N> st{reinterpret_cast<double*>(mine + Stage<N>::NM * sizeof(uint4) * kWarpElems),
-                    reinterpret_cast<uint4*>(mine), kWarpElems};
+  const Stage<N> st = make_stage<N>(mine, kWarpElems);
   const TileDesc td = p.tiles[blockIdx.x];
   unsigned long long segs = 0, commits = 0, flushes = 0;
   const int wn = process_warp<N>(p, td, warp, lane, st, segs);
@@ -393,8 +447,7 @@ __global__ void __launch_bounds__(kCtaThreads) k_mttkrp_warp(Params<N> p) {
 
 template <int N>
 __device__ __forceinline__ Stage<N> cta_stage(unsigned char* dyn) {
-  return Stage<N>{reinterpret_cast<double*>(dyn + Stage<N>::NM * sizeof(uint4) * kTileElems),
-                  reinterpret_cast<uint4*>(dyn), kTileElems};
+  return make_stage<N>(dyn, kTileElems);
 }
 
 template <int N, int LPE, int CPL, bool FULL, bool STATS, int U = kUnroll, int MINB = 1>
@@ -494,6 +547,7 @@ __device__ __forceinline__ void compute_range_f32(const ParamsF32<N>& p, const S
       const int j = lo + t0 + u;
       ok[u] = j < hi;
       st.get(ok[u] ? j : lo0, val[u], w[u]);
+      if constexpr (Stage<N>::kPacked) w[u][N - 1] = st.row(ok[u] ? j : lo0);
     }
     const int jn = lo + t0 + kUnroll;
     const uint32_t next_row = jn < hi ? st.row(jn) : 0xffffffffu;
