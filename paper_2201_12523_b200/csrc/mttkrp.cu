@@ -281,6 +281,116 @@ __device__ __forceinline__ void compute_range(const Params<N>& p, const Stage<N>
   }
 }
 
+// Register-path computing phase for an exact rank (FULL: R == LPE * CPL,
+// one column chunk) over the packed stage -- the hot configuration.  The same
+// arithmetic and commit rule as compute_range, with the per-element overhead
+// stripped: the row stride is a compile-time constant, the lane's column
+// offset is folded into per-mode base pointers once, and every batch but the
+// group's last runs without element masks.
+template <int N, int LPE, int CPL, int U>
+__device__ __forceinline__ void compute_range_fast(const Params<N>& p, const Stage<N> st, int lo0, int wn, int lane,
+                                                   double* __restrict__ out, unsigned long long& commits) {
+  constexpr int G = 32 / LPE;
+  constexpr int NW = 4 * Stage<N>::NM;
+  constexpr int NO = N > 1 ? N - 1 : 1;
+  constexpr int RF = LPE * CPL;
+  constexpr bool kRows4 = G == 2 && U == 4;
+  const int g = lane / LPE, q = lane % LPE;
+  int h = wn / G;
+  if constexpr (kRows4) {
+    h = h >= 4 ? (h & ~7) | 4 : 0;
+    if (h > wn) h = (wn / 2) & ~3;
+  } else if (G > 1 && h > 1) {
+    h = (h & ~3) | 1;
+    if ((G - 1) * h > wn) h = wn / G;
+  }
+  const int lo = lo0 + g * h;
+  const int n = (g == G - 1 ? wn - (G - 1) * h : h);  // my elements: [lo, lo + n)
+  const double* fb[NO];
+#pragma unroll
+  for (int k = 0; k < N - 1; ++k) fb[k] = p.factors[k] + q;
+  double* const ob = out + q;
+  double acc[CPL];
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) acc[c] = 0.0;
+
+  auto consume = [&](const double (&v)[U], const uint32_t (&w)[U][NW], const Row<CPL> (&rows)[U][NO],
+                     uint32_t next_row, int valid) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (u < valid) {
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+          double prod = v[u];
+#pragma unroll
+          for (int k = 0; k < N - 1; ++k) prod = __dmul_rn(prod, rows[u][k].v[c]);
+          acc[c] = __dadd_rn(acc[c], prod);
+        }
+        const uint32_t row = w[u][N - 1];
+        const uint32_t nrow = u + 1 < valid ? w[u + 1][N - 1] : next_row;
+        if (nrow != row) {
+          double* o = ob + static_cast<uint64_t>(row) * RF;
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) atomicAdd(o + c * LPE, acc[c]);
+          ++commits;
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) acc[c] = 0.0;
+        }
+      }
+    }
+  };
+
+  const int nfull = n / U;
+  for (int b = 0; b < nfull; ++b) {
+    const int j0 = lo + b * U;
+    double v[U];
+    uint32_t w[U][NW];
+    Row<CPL> rows[U][NO];
+#pragma unroll
+    for (int u = 0; u < U; ++u) st.get(j0 + u, v[u], w[u]);
+    if constexpr (kRows4) {
+      const uint4 r4 = st.rows4(j0);
+      w[0][N - 1] = r4.x, w[1][N - 1] = r4.y, w[2][N - 1] = r4.z, w[3][N - 1] = r4.w;
+    } else {
+#pragma unroll
+      for (int u = 0; u < U; ++u) w[u][N - 1] = st.row(j0 + u);
+    }
+    const uint32_t next_row = j0 + U < lo + n ? st.row(j0 + U) : 0xffffffffu;
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int k = 0; k < N - 1; ++k) {
+        const double* rp = fb[k] + static_cast<uint64_t>(w[u][k]) * RF;
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) rows[u][k].v[c] = __ldg(rp + c * LPE);
+      }
+    consume(v, w, rows, next_row, U);
+  }
+  const int rem = n - nfull * U;
+  if (rem > 0) {
+    const int j0 = lo + nfull * U;
+    double v[U];
+    uint32_t w[U][NW];
+    Row<CPL> rows[U][NO];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = u < rem ? j0 + u : j0;
+      st.get(j, v[u], w[u]);
+      w[u][N - 1] = st.row(j);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int k = 0; k < N - 1; ++k)
+        if (u < rem) {
+          const double* rp = fb[k] + static_cast<uint64_t>(w[u][k]) * RF;
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) rows[u][k].v[c] = __ldg(rp + c * LPE);
+        }
+    consume(v, w, rows, 0xffffffffu, rem);
+  }
+}
+
 __device__ __forceinline__ uint32_t tile_count(const TileDesc& td, uint64_t elem_end) {
   const uint64_t room = td.start >= elem_end ? 0 : elem_end - td.start;
   return room < td.count ? static_cast<uint32_t>(room) : td.count;
@@ -463,9 +573,13 @@ __global__ void __launch_bounds__(kCtaThreads, MINB) k_mttkrp_sorted(Params<N> p
   long long t1 = STATS ? clock64() : 0;
   const int lo0 = warp * kWarpElems;
   const int wn = static_cast<int>(cnt) > lo0 ? min(kWarpElems, static_cast<int>(cnt) - lo0) : 0;
-  if (wn > 0)
-    compute_range<N, LPE, CPL, FULL, false, U>(p, st, lo0, wn, lane, blockIdx.y * LPE * CPL, p.out, nullptr,
-                                            nullptr, commits, flushes);
+  if (wn > 0) {
+    if constexpr (FULL && Stage<N>::kPacked && U == 4)
+      compute_range_fast<N, LPE, CPL, U>(p, st, lo0, wn, lane, p.out, commits);
+    else
+      compute_range<N, LPE, CPL, FULL, false, U>(p, st, lo0, wn, lane, blockIdx.y * LPE * CPL, p.out, nullptr,
+                                              nullptr, commits, flushes);
+  }
   if constexpr (STATS) {
     const long long t2 = clock64();
     if (lane == 0) {
