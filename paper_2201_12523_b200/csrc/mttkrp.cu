@@ -706,6 +706,105 @@ __device__ __forceinline__ void compute_range_f32(const ParamsF32<N>& p, const S
   }
 }
 
+// Lean fp32 computing phase for an exact rank (R == LPE * V), packed stage.
+template <int N, int LPE, int V>
+__device__ __forceinline__ void compute_range_f32_fast(const ParamsF32<N>& p, const Stage<N> st, int lo0, int wn,
+                                                       int lane) {
+  using VT = typename VecF<V>::type;
+  constexpr int G = 32 / LPE;
+  constexpr int NW = 4 * Stage<N>::NM;
+  constexpr int NO = N > 1 ? N - 1 : 1;
+  constexpr int RF = LPE * V;
+  constexpr int U = kUnroll;
+  constexpr bool kRows4 = G == 2 && U == 4;
+  const int g = lane / LPE, q = lane % LPE;
+  int h = wn / G;
+  if constexpr (kRows4) {
+    h = h >= 4 ? (h & ~7) | 4 : 0;
+    if (h > wn) h = (wn / 2) & ~3;
+  } else if (G > 1 && h > 1) {
+    h = (h & ~3) | 1;
+    if ((G - 1) * h > wn) h = wn / G;
+  }
+  const int lo = lo0 + g * h;
+  const int n = (g == G - 1 ? wn - (G - 1) * h : h);
+  const float* fb[NO];
+#pragma unroll
+  for (int k = 0; k < N - 1; ++k) fb[k] = p.factors[k] + V * q;
+  float* const ob = p.out + V * q;
+  float acc[V];
+#pragma unroll
+  for (int x = 0; x < V; ++x) acc[x] = 0.0f;
+
+  auto consume = [&](const double (&v)[U], const uint32_t (&w)[U][NW], const VT (&rows)[U][NO],
+                     uint32_t next_row, int valid) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (u < valid) {
+        const float vf = __double2float_rn(v[u]);
+#pragma unroll
+        for (int x = 0; x < V; ++x) {
+          float prod = vf;
+#pragma unroll
+          for (int k = 0; k < N - 1; ++k) prod = __fmul_rn(prod, VecF<V>::get(rows[u][k], x));
+          acc[x] = __fadd_rn(acc[x], prod);
+        }
+        const uint32_t row = w[u][N - 1];
+        const uint32_t nrow = u + 1 < valid ? w[u + 1][N - 1] : next_row;
+        if (nrow != row) {
+          float* o = ob + static_cast<uint64_t>(row) * RF;
+          if constexpr (V == 2) atomicAdd(reinterpret_cast<float2*>(o), make_float2(acc[0], acc[1]));
+          else atomicAdd(o, acc[0]);
+#pragma unroll
+          for (int x = 0; x < V; ++x) acc[x] = 0.0f;
+        }
+      }
+    }
+  };
+  const int nfull = n / U;
+  for (int b = 0; b < nfull; ++b) {
+    const int j0 = lo + b * U;
+    double v[U];
+    uint32_t w[U][NW];
+    VT rows[U][NO];
+#pragma unroll
+    for (int u = 0; u < U; ++u) st.get(j0 + u, v[u], w[u]);
+    if constexpr (kRows4) {
+      const uint4 r4 = st.rows4(j0);
+      w[0][N - 1] = r4.x, w[1][N - 1] = r4.y, w[2][N - 1] = r4.z, w[3][N - 1] = r4.w;
+    } else {
+#pragma unroll
+      for (int u = 0; u < U; ++u) w[u][N - 1] = st.row(j0 + u);
+    }
+    const uint32_t next_row = j0 + U < lo + n ? st.row(j0 + U) : 0xffffffffu;
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int k = 0; k < N - 1; ++k)
+        rows[u][k] = __ldg(reinterpret_cast<const VT*>(fb[k] + static_cast<uint64_t>(w[u][k]) * RF));
+    consume(v, w, rows, next_row, U);
+  }
+  const int rem = n - nfull * U;
+  if (rem > 0) {
+    const int j0 = lo + nfull * U;
+    double v[U];
+    uint32_t w[U][NW];
+    VT rows[U][NO];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = u < rem ? j0 + u : j0;
+      st.get(j, v[u], w[u]);
+      w[u][N - 1] = st.row(j);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int k = 0; k < N - 1; ++k)
+        if (u < rem) rows[u][k] = __ldg(reinterpret_cast<const VT*>(fb[k] + static_cast<uint64_t>(w[u][k]) * RF));
+    consume(v, w, rows, 0xffffffffu, rem);
+  }
+}
+
 template <int N, int LPE, int V, int CPL, bool FULL>
 __global__ void __launch_bounds__(kCtaThreads) k_mttkrp_sorted_f32(ParamsF32<N> p) {
   extern __shared__ __align__(16) unsigned char dyn[];
@@ -717,7 +816,12 @@ __global__ void __launch_bounds__(kCtaThreads) k_mttkrp_sorted_f32(ParamsF32<N> 
   const uint32_t cnt = process_cta<N>(p.base, td, st, bs, segs);
   const int lo0 = warp * kWarpElems;
   const int wn = static_cast<int>(cnt) > lo0 ? min(kWarpElems, static_cast<int>(cnt) - lo0) : 0;
-  if (wn > 0) compute_range_f32<N, LPE, V, CPL, FULL>(p, st, lo0, wn, lane, blockIdx.y * LPE * V * CPL);
+  if (wn > 0) {
+    if constexpr (FULL && CPL == 1 && Stage<N>::kPacked)
+      compute_range_f32_fast<N, LPE, V>(p, st, lo0, wn, lane);
+    else
+      compute_range_f32<N, LPE, V, CPL, FULL>(p, st, lo0, wn, lane, blockIdx.y * LPE * V * CPL);
+  }
 }
 
 // Persistent CTAs; dynamic shared memory = tile stage + stash (slots x R
