@@ -59,15 +59,19 @@ class ClockSampler:
               "clocks_event_reasons.sw_power_cap")
     NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
-    def __init__(self, device: int):
+    def __init__(self, device: int, period_ms: int | None = None):
         self.device = device
         self.proc = None
+        self.period_ms = period_ms or int(os.environ.get("BLCO_B200_CLOCK_MS", "100"))
 
     def __enter__(self):
+        if self.period_ms <= 0:  # BLCO_B200_CLOCK_MS=0: no sampling (interference checks only)
+            return self
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "100",
-                 "-i", str(self.device)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms",
+                 str(self.period_ms), "-i", str(self.device)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
         time.sleep(0.3)

@@ -257,3 +257,35 @@ def test_fp32_variant(gpu, oracle, dims, nnz, rank):
                             stream=torch.cuda.current_stream().cuda_stream)
         torch.cuda.synchronize()
         assert rel_frobenius(out.cpu().numpy() - 1.0, want) <= 1e-5
+
+
+def test_warp_variant_subprocess(gpu):
+    """BLCO_B200_VARIANT=warp (the paper's 32-element __match_any_sync tiles,
+    read once per process) against the oracle in a fresh process."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    code = """
+import sys
+sys.path.insert(0, '.'); sys.path.insert(0, 'oracle')
+import numpy as np
+import paper_2201_12523_b200 as b
+from pyoracle import Oracle
+o = Oracle()
+worst = 0.0
+for dims, rank in (([700, 90, 1300], 32), ([40, 50, 30, 20], 16), ([300, 200], 33)):
+    coo = b.synth_uniform_host(dims, 20000, 3)
+    f = b.FactorMatrices.random(dims, rank, 7)
+    t = b.build_blco(coo, 64)
+    for m in range(len(dims)):
+        want = o.mttkrp_coo(dims, coo.indices, coo.values, f.factors, m)
+        got = b.mttkrp(t, f, m, strategy=b.Strategy.Register)
+        worst = max(worst, float(np.sqrt(((got - want) ** 2).sum() / (want ** 2).sum())))
+print(worst)
+"""
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=300,
+                       env=dict(os.environ, BLCO_B200_VARIANT="warp"))
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert float(r.stdout.strip().splitlines()[-1]) <= TOL
