@@ -43,25 +43,23 @@ constexpr int solve_rows() {
   return 4096 / RM < kSolveThreads ? 4096 / RM : kSolveThreads;
 }
 
-// L (R x R lower, the diagonal replaced by 1 / L_ii) as a kernel parameter:
-// with R == RM every L_ik index is a compile-time constant and the solve's
-// DFMAs read it straight from the constant bank (no shared-memory traffic).
-template <int RM>
-struct LParam {
-  double v[RM * RM];
-};
+// L (R x R lower, the diagonal replaced by 1 / L_ii) in constant memory,
+// copied device-to-device from the Cholesky kernel's output: with R == RM
+// every L_ik index is a compile-time constant and the solve's DFMAs read it
+// straight from the constant bank (no shared-memory traffic).  One ALS runs
+// per device at a time (cp_als is synchronous on the legacy stream).
+__constant__ double c_L[32 * 32];
 
 template <int RM, bool EXACT>
-__device__ __forceinline__ double lget(const LParam<EXACT ? RM : 1>& lp, const double* sl, int R, int i, int k) {
-  if constexpr (EXACT) return lp.v[i * RM + k];
+__device__ __forceinline__ double lget(const double* sl, int R, int i, int k) {
+  if constexpr (EXACT) return c_L[i * RM + k];
   else return sl[i * R + k];
 }
 
 template <int RM, bool EXACT>
 __global__ void __launch_bounds__(kSolveThreads) k_solve_gram(const double* __restrict__ m, double* __restrict__ a,
-                                                              uint64_t rows, int R,
-                                                              const __grid_constant__ LParam<EXACT ? RM : 1> lp,
-                                                              const double* __restrict__ L, double* __restrict__ g) {
+                                                              uint64_t rows, int R, const double* __restrict__ L,
+                                                              double* __restrict__ g) {
   constexpr int ROWS = solve_rows<RM>();
   constexpr int W = kSolveThreads / 32;
   // Gram lane blocking: lane owns AI rows x AJ columns of a GI x GJ block of G
@@ -125,8 +123,8 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve_gram(const double* __re
         if (i < RR) {
           double x = b[i];
 #pragma unroll
-          for (int k = 0; k < i; ++k) x -= lget<RM, EXACT>(lp, sl, R, i, k) * b[k];
-          b[i] = x * lget<RM, EXACT>(lp, sl, R, i, i);
+          for (int k = 0; k < i; ++k) x -= lget<RM, EXACT>(sl, R, i, k) * b[k];
+          b[i] = x * lget<RM, EXACT>(sl, R, i, i);
         }
       }
 #pragma unroll
@@ -135,8 +133,8 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve_gram(const double* __re
           double x = b[ii];
 #pragma unroll
           for (int k = ii + 1; k < RM; ++k)
-            if (k < RR) x -= lget<RM, EXACT>(lp, sl, R, k, ii) * b[k];
-          b[ii] = x * lget<RM, EXACT>(lp, sl, R, ii, ii);
+            if (k < RR) x -= lget<RM, EXACT>(sl, R, k, ii) * b[k];
+          b[ii] = x * lget<RM, EXACT>(sl, R, ii, ii);
         }
       }
 #pragma unroll
@@ -196,6 +194,105 @@ __device__ __forceinline__ double block_sum(double v) {
   if (threadIdx.x == 0)
     for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += ws[w];
   return t;
+}
+
+// ---------------------------------------------------------------- R x R work
+// The small dense steps of an ALS mode run on the device so an iteration is
+// enqueued without host round trips (one read of the fit per iteration).
+// Each restates the host arithmetic of dense_kernels.cpp / cpals.cpp in the
+// same operation order with explicitly rounded operations, so it matches the
+// host restatement bit for bit.
+
+// V = hadamard_{m != n} grams[m] (cpals.cpp:86-90), then
+// cholesky(V + shift I) with the Tikhonov escalation of solve_normal
+// (dense_kernels.cpp:33-56, :72-80).  L_out gets L with its diagonal
+// replaced by 1 / L_ii; status[0] = 1 when every shift failed.
+__global__ void k_small_prep(const double* __restrict__ grams, int N, int n, int R, double* __restrict__ L_out,
+                             int* __restrict__ status) {
+  extern __shared__ double sm[];
+  double* V = sm;          // R x R
+  double* L = sm + R * R;  // R x R
+  __shared__ int fail;
+  __shared__ double shift;
+  const int RR = R * R;
+  for (int i = threadIdx.x; i < RR; i += blockDim.x) {
+    double v = 1.0;
+    for (int m = 0; m < N; ++m)
+      if (m != n) v = __dmul_rn(v, grams[static_cast<size_t>(m) * RR + i]);
+    V[i] = v;
+  }
+  __syncthreads();
+  double unit = 1.0;
+  if (threadIdx.x == 0) {
+    double trace = 0.0;
+    for (int i = 0; i < R; ++i) trace = __dadd_rn(trace, V[i * R + i]);
+    unit = trace > 0.0 ? __ddiv_rn(trace, static_cast<double>(R)) : 1.0;
+    shift = 0.0;
+  }
+  for (int attempt = 0;; ++attempt) {
+    if (threadIdx.x == 0) fail = 0;
+    __syncthreads();
+    for (int j = 0; j < R; ++j) {
+      if (threadIdx.x == 0) {
+        double x = __dadd_rn(V[j * R + j], shift);
+        for (int k = 0; k < j; ++k) x = __dsub_rn(x, __dmul_rn(L[j * R + k], L[j * R + k]));
+        if (!(x > 0.0) || !isfinite(x)) fail = 1;
+        L[j * R + j] = __dsqrt_rn(x);
+      }
+      __syncthreads();
+      for (int i = j + 1 + threadIdx.x; i < R; i += blockDim.x) {
+        double x = V[i * R + j];
+        for (int k = 0; k < j; ++k) x = __dsub_rn(x, __dmul_rn(L[i * R + k], L[j * R + k]));
+        L[i * R + j] = __ddiv_rn(x, L[j * R + j]);
+      }
+      __syncthreads();
+    }
+    if (!fail) break;
+    // escalation: 0, then 1e-12 * unit, x10 each step, up to 1e-3 * unit
+    if (threadIdx.x == 0) shift = attempt == 0 ? 1e-12 * unit : shift * 10.0;
+    __syncthreads();
+    if (!(shift <= 1e-3 * unit * (1.0 + 1e-9))) {
+      if (threadIdx.x == 0) status[0] = 1;
+      return;
+    }
+  }
+  for (int i = threadIdx.x; i < RR; i += blockDim.x) {
+    const int r = i / R, c = i % R;
+    L_out[i] = c > r ? 0.0 : (r == c ? __ddiv_rn(1.0, L[i]) : L[i]);
+  }
+}
+
+// lambda = sqrt(diag G) (0 -> 1, cpals.cpp:57-58); gram_out = G / (l l^T).
+__global__ void k_small_norm(const double* __restrict__ G, int R, double* __restrict__ gram_out,
+                             double* __restrict__ lam) {
+  __shared__ double l[64];
+  for (int r = threadIdx.x; r < R; r += blockDim.x) {
+    double x = __dsqrt_rn(G[r * R + r]);
+    l[r] = x == 0.0 ? 1.0 : x;
+    lam[r] = l[r];
+  }
+  __syncthreads();
+  for (int p = threadIdx.x; p < R * R; p += blockDim.x) {
+    const int i = p / R, j = p % R;
+    const int a = i < j ? i : j, b = i < j ? j : i;  // the upper triangle holds the sums
+    gram_out[p] = __ddiv_rn(G[a * R + b], __dmul_rn(l[a], l[b]));
+  }
+}
+
+// fit (cpals.cpp:113-129): |Xhat|^2 = sum_rc prod_m gram_m[r,c] l_r l_c.
+__global__ void k_small_fit(const double* __restrict__ grams, int N, int R, const double* __restrict__ lam,
+                            const double* __restrict__ inner, double xn, double* __restrict__ fit_out) {
+  if (threadIdx.x != 0) return;
+  const int RR = R * R;
+  double hat = 0.0;
+  for (int r = 0; r < R; ++r)
+    for (int c = 0; c < R; ++c) {
+      double full = 1.0;
+      for (int m = 0; m < N; ++m) full = __dmul_rn(full, grams[static_cast<size_t>(m) * RR + r * R + c]);
+      hat = __dadd_rn(hat, __dmul_rn(__dmul_rn(full, lam[r]), lam[c]));
+    }
+  const double resid = fmax(0.0, __dadd_rn(__dsub_rn(xn, __dmul_rn(2.0, inner[0])), hat));
+  fit_out[0] = __dsub_rn(1.0, __ddiv_rn(__dsqrt_rn(resid), __dsqrt_rn(xn)));
 }
 
 // Fused epilogue pass 2: A /= lambda column-wise (cpals.cpp:59-60) and, for
@@ -299,7 +396,14 @@ struct Dense {
   DevBuf<double> L, small;  // small: R x R reduced Gram | R lambda | 1 scalar
   DevBuf<double> parts;     // partial slots (grown on demand)
 
-  explicit Dense(int r) : R(r), L(static_cast<size_t>(r) * r), small(static_cast<size_t>(r) * r + r + 1) {}
+  // parts is sized up front for the largest reduction of a call (the solve's
+  // per-warp Gram slots at full occupancy), so no iteration reallocates --
+  // a cudaFree/cudaMalloc inside the loop stalls the queued kernels.
+  explicit Dense(int r) : R(r), L(static_cast<size_t>(r) * r), small(static_cast<size_t>(r) * r + r + 1) {
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+    slots(std::max<uint64_t>(uint64_t(nsm) * 32 * (kSolveThreads / 32) * r * r, uint64_t(148) * 16 * 4));
+  }
 
   double* slots(uint64_t n) {
     if (parts.n < n) parts.alloc(n);
@@ -322,7 +426,7 @@ struct Dense {
     if (!rows) return std::vector<double>(RR, 0.0);
     const size_t smem = (static_cast<size_t>(RR) + kGramChunk * R) * sizeof(double);
     if (smem > 48 * 1024)
-      B200_CUDA(cudaFuncSetAttribute(k_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      ensure_dyn_smem(reinterpret_cast<const void*>(k_gram), smem);
     const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((rows + kGramChunk - 1) / kGramChunk, 148 * 8));
     k_gram<<<grid, kT, smem>>>(a, rows, R, slots(uint64_t(grid) * RR));
     count_launch();
@@ -334,32 +438,37 @@ struct Dense {
     return g;
   }
 
-  // A = M V^-1 (Cholesky with Tikhonov escalation, dense_kernels.cpp:68-92),
-  // then normalize_columns (cpals.cpp:51-61); returns lambda and leaves the
-  // Gram of the normalised A in gram_out.  For the last mode (m_inner set)
-  // also returns <X, Xhat> through *inner.  Two passes over A.
-  std::vector<double> solve_normalize(const double* m, double* a, uint64_t rows, const std::vector<double>& v,
-                                      std::vector<double>& gram_out, const double* m_inner, double* inner) {
-    double trace = 0.0;
-    for (int i = 0; i < R; ++i) trace += v[i * R + i];
-    const double unit = trace > 0.0 ? trace / R : 1.0;
-    std::vector<double> Lh;
-    bool ok = cholesky(v, R, 0.0, Lh);
-    for (double lam = 1e-12 * unit; !ok && lam <= 1e-3 * unit * (1.0 + 1e-9); lam *= 10.0)
-      ok = cholesky(v, R, lam, Lh);
-    if (!ok) throw_error("solve_normal: matrix singular after maximal diagonal shift");
+  // One ALS mode's dense steps, enqueued on the legacy stream without host
+  // round trips: V and its Cholesky factor (with Tikhonov escalation,
+  // dense_kernels.cpp:68-92) on the device, A = M V^-1 fused with Gram(A),
+  // then normalize_columns (cpals.cpp:51-61): lambda and the Gram of the
+  // normalised A_n stay on the device (dgrams[n], dlam).  For the last mode
+  // (m_inner set) also <X, Xhat> into *dinner.  status[0] is set when V stays
+  // singular after the maximal shift.
+  void solve_normalize(const double* m, double* a, uint64_t rows, double* dgrams, int N, int n, double* dlam,
+                       int* dstatus, const double* m_inner, double* dinner) {
     const int RR = R * R;
-    std::vector<double> g(RR, 0.0);
+    // BLCO_B200_ALS_PROBE=1: device time of each step of this epilogue (stderr)
+    static const bool probe = std::getenv("BLCO_B200_ALS_PROBE") != nullptr;
+    cudaEvent_t pe[6] = {};
+    auto pmark = [&](int k) {
+      if (!probe) return;
+      cudaEventCreate(&pe[k]);
+      cudaEventRecord(pe[k], nullptr);
+    };
+    pmark(0);
+    k_small_prep<<<1, 256, 2 * RR * sizeof(double)>>>(dgrams, N, n, R, L.ptr, dstatus);
+    count_launch();
+    check_launch("k_small_prep");
+    pmark(1);
+    if (exact_rank(R))
+      B200_CUDA(cudaMemcpyToSymbolAsync(c_L, L.ptr, RR * sizeof(double), 0, cudaMemcpyDeviceToDevice, nullptr));
+    pmark(2);
     if (rows) {
-      auto launch = [&](auto kern, auto lp_tag, int rm, int rows_per, bool exact) {
-        using LP = decltype(lp_tag);
-        LP lp{};
-        if (exact)
-          for (int i = 0; i < RR; ++i) lp.v[i] = i % (R + 1) == 0 ? 1.0 / Lh[i] : Lh[i];
+      auto launch = [&](auto kern, int rm, int rows_per) {
         const size_t smem = (static_cast<size_t>(rm) * rm + 2 * static_cast<size_t>(rows_per) * (rm + 1)) * 8;
-        B200_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        int per_sm = 1;
-        B200_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSolveThreads, smem));
+        ensure_dyn_smem(reinterpret_cast<const void*>(kern), smem);
+        const int per_sm = blocks_per_sm(reinterpret_cast<const void*>(kern), kSolveThreads, smem);
         const unsigned grid = static_cast<unsigned>(
             std::min<uint64_t>((rows + rows_per - 1) / rows_per, 148ull * std::max(1, per_sm)));
         const uint64_t nslots = uint64_t(grid) * (kSolveThreads / 32);
@@ -367,35 +476,25 @@ struct Dense {
         // R <= 32: every warp writes the whole upper triangle of its slot (the
         // lower one is never read); R = 64: each warp owns one quadrant
         if (rm > 32) B200_CUDA(cudaMemsetAsync(sl, 0, nslots * RR * 8, nullptr));
-        kern<<<grid, kSolveThreads, smem>>>(m, a, rows, R, lp, L.ptr, sl);
+        kern<<<grid, kSolveThreads, smem>>>(m, a, rows, R, L.ptr, sl);
         count_launch();
         check_launch("k_solve_gram");
         reduce(nslots, RR);
       };
-      if (!exact_rank(R)) {  // generic R: L (diagonal inverted) through shared memory
-        std::vector<double> inv(Lh);
-        for (int i = 0; i < R; ++i) inv[i * R + i] = 1.0 / Lh[i * R + i];
-        B200_CUDA(cudaMemcpy(L.ptr, inv.data(), inv.size() * 8, cudaMemcpyHostToDevice));
-      }
-      if (R == 16) launch(k_solve_gram<16, true>, LParam<16>{}, 16, solve_rows<16>(), true);
-      else if (R == 32) launch(k_solve_gram<32, true>, LParam<32>{}, 32, solve_rows<32>(), true);
-      else if (R < 16) launch(k_solve_gram<16, false>, LParam<1>{}, 16, solve_rows<16>(), false);
-      else if (R < 32) launch(k_solve_gram<32, false>, LParam<1>{}, 32, solve_rows<32>(), false);
-      else if (R <= 64) launch(k_solve_gram<64, false>, LParam<1>{}, 64, solve_rows<64>(), false);
+      if (R == 16) launch(k_solve_gram<16, true>, 16, solve_rows<16>());
+      else if (R == 32) launch(k_solve_gram<32, true>, 32, solve_rows<32>());
+      else if (R < 16) launch(k_solve_gram<16, false>, 16, solve_rows<16>());
+      else if (R < 32) launch(k_solve_gram<32, false>, 32, solve_rows<32>());
+      else if (R <= 64) launch(k_solve_gram<64, false>, 64, solve_rows<64>());
       else throw_format("b200: cp_als supports rank <= 64 on the device");
-      g = fetch(RR);
+    } else {
+      B200_CUDA(cudaMemsetAsync(small.ptr, 0, RR * sizeof(double), nullptr));
     }
-    std::vector<double> lam(R);
-    for (int r = 0; r < R; ++r) {
-      lam[r] = std::sqrt(g[r * R + r]);
-      if (lam[r] == 0.0) lam[r] = 1.0;  // cpals.cpp:58
-    }
-    gram_out.assign(RR, 0.0);
-    for (int i = 0; i < R; ++i)
-      for (int j = i; j < R; ++j) gram_out[i * R + j] = gram_out[j * R + i] = g[i * R + j] / (lam[i] * lam[j]);
-    double* dlam = small.ptr + RR;
-    B200_CUDA(cudaMemcpy(dlam, lam.data(), R * 8, cudaMemcpyHostToDevice));
-    if (m_inner) *inner = 0.0;
+    pmark(3);
+    k_small_norm<<<1, 256>>>(small.ptr, R, dgrams + static_cast<size_t>(n) * RR, dlam);
+    count_launch();
+    check_launch("k_small_norm");
+    if (m_inner) B200_CUDA(cudaMemsetAsync(dinner, 0, sizeof(double), nullptr));
     if (rows) {
       const unsigned grid = grid_of(rows * R);
       double* part = m_inner ? slots(grid) : nullptr;
@@ -403,13 +502,20 @@ struct Dense {
       count_launch();
       check_launch("k_scale_inner");
       if (m_inner) {
-        k_reduce_ordered<<<1, 256>>>(part, grid, 1, small.ptr + RR + R);
+        k_reduce_ordered<<<1, 256>>>(part, grid, 1, dinner);
         count_launch();
         check_launch("k_reduce_ordered");
-        B200_CUDA(cudaMemcpy(inner, small.ptr + RR + R, 8, cudaMemcpyDeviceToHost));
       }
     }
-    return lam;
+    pmark(4);
+    if (probe) {
+      cudaEventSynchronize(pe[4]);
+      float t[4];
+      for (int k = 0; k < 4; ++k) cudaEventElapsedTime(&t[k], pe[k], pe[k + 1]);
+      std::fprintf(stderr, "[als probe] mode %d rows %llu: prep %.3f symbol %.3f solve+gram %.3f norm+scale %.3f ms\n",
+                   n, static_cast<unsigned long long>(rows), t[0], t[1], t[2], t[3]);
+      for (int k = 0; k < 5; ++k) cudaEventDestroy(pe[k]);
+    }
   }
 
   double inner(const double* m, const double* a, uint64_t rows, const std::vector<double>& lambda) {
@@ -527,17 +633,25 @@ int blco_cp_als_timed(const blco_tensor* t, uint64_t rank, int max_iters, double
     const double xn = tensor_norm_sq(*t);
     if (xn == 0.0) throw_format("cp_als: zero-norm tensor");
     Dense dense(R);
-    std::vector<std::vector<double>> grams(N);
-    for (int m = 0; m < N; ++m) grams[m] = dense.gram(A[m].ptr, l.dims[m]);
+    const int RR = R * R;
+    // Grams, lambda, <X, Xhat>, fit and the singular flag live on the device
+    DevBuf<double> dgrams(static_cast<size_t>(N) * RR), dlam(R), dinner(1), dfit(std::max(1, max_iters));
+    DevBuf<int> dstatus(1);
+    B200_CUDA(cudaMemset(dstatus.ptr, 0, sizeof(int)));
+    for (int m = 0; m < N; ++m) {
+      const std::vector<double> g = dense.gram(A[m].ptr, l.dims[m]);
+      B200_CUDA(cudaMemcpy(dgrams.ptr + static_cast<size_t>(m) * RR, g.data(), RR * sizeof(double),
+                           cudaMemcpyHostToDevice));
+    }
     uint64_t maxrows = 0;
     for (int m = 0; m < N; ++m) maxrows = std::max<uint64_t>(maxrows, l.dims[m]);
     DevBuf<double> mt(maxrows * rank);
     double prev = 0.0;
     int it = 0;
-    // BLCO_B200_TRACE=1: synchronise after every step and report where the
+    // BLCO_B200_TRACE=1: synchronise around the MTTKRPs and report where the
     // iteration time goes (stderr).
     static const bool trace = std::getenv("BLCO_B200_TRACE") != nullptr;
-    double acc[3] = {0, 0, 0};
+    double acc[2] = {0, 0};
     auto t_last = std::chrono::steady_clock::now();
     // device-time accounting (CUDA events on the legacy stream the loop runs on)
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_mt, ev_all;
@@ -558,37 +672,43 @@ int blco_cp_als_timed(const blco_tensor* t, uint64_t rank, int max_iters, double
       acc[slot] += std::chrono::duration<double>(now - t_last).count();
       t_last = now;
     };
+    auto fetch_lambda = [&] { B200_CUDA(cudaMemcpy(lambda.data(), dlam.ptr, R * sizeof(double), cudaMemcpyDeviceToHost)); };
     for (; it < max_iters; ++it) {
       NvtxRange nv("cp_als iteration");
       if (st) mark(ev_all, true);
-      double inner = 0.0;
       for (int n = 0; n < N; ++n) {
-        std::vector<double> v(static_cast<size_t>(R) * R, 1.0);
-        for (int m = 0; m < N; ++m)
-          if (m != n)
-            for (size_t i = 0; i < v.size(); ++i) v[i] *= grams[m][i];
-        tick(2);
+        tick(1);
         if (st) mark(ev_mt, true);
         mttkrp_into(*t, ptr, rank, n, strategy, c, mt.ptr);
         if (st) mark(ev_mt, false);
         tick(0);
         // A_n = normalise(M V^-1) straight into A_n; M of the last mode stays
         // in mt for the fit's inner product
-        lambda = dense.solve_normalize(mt.ptr, A[n].ptr, l.dims[n], v, grams[n], n == N - 1 ? mt.ptr : nullptr,
-                                       &inner);
-        tick(1);
+        dense.solve_normalize(mt.ptr, A[n].ptr, l.dims[n], dgrams.ptr, N, n, dlam.ptr, dstatus.ptr,
+                              n == N - 1 ? mt.ptr : nullptr, dinner.ptr);
       }
-      const double f = fit_value(xn, inner, recon_norm_sq(grams, lambda, R));
+      k_small_fit<<<1, 32>>>(dgrams.ptr, N, R, dlam.ptr, dinner.ptr, xn, dfit.ptr + it);
+      count_launch();
+      check_launch("k_small_fit");
+      if (st) mark(ev_all, false);
+      // the iteration's one host round trip: its fit and the singular flag
+      double f = 0;
+      int singular = 0;
+      B200_CUDA(cudaMemcpy(&f, dfit.ptr + it, sizeof(double), cudaMemcpyDeviceToHost));
+      B200_CUDA(cudaMemcpy(&singular, dstatus.ptr, sizeof(int), cudaMemcpyDeviceToHost));
+      tick(1);
+      if (singular) throw_error("solve_normal: matrix singular after maximal diagonal shift");
       fit_out[it] = f;
       *iters_out = it + 1;
-      if (st) mark(ev_all, false);
       if (!std::isfinite(f)) {
+        fetch_lambda();
         emit();
         throw_error("cp_als: non-finite fit at iteration " + std::to_string(it + 1));
       }
       if (it > 0 && f - prev < tol) break;
       prev = f;
     }
+    fetch_lambda();
     if (st) {
       B200_CUDA(cudaDeviceSynchronize());
       auto sum = [](std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& v) {
@@ -606,8 +726,8 @@ int blco_cp_als_timed(const blco_tensor* t, uint64_t rank, int max_iters, double
       st->iterations_ms = sum(ev_all);
     }
     if (trace)
-      std::fprintf(stderr, "[blco trace] cp_als %d iters: mttkrp %.3f s, solve+normalize+gram %.3f s, host %.3f s\n",
-                   it, acc[0], acc[1], acc[2]);
+      std::fprintf(stderr, "[blco trace] cp_als %d iters: mttkrp %.3f s, dense epilogue + fit %.3f s\n", it, acc[0],
+                   acc[1]);
     emit();
   });
 }

@@ -5,6 +5,9 @@
 // encode/decode functions at :71-124; batch spans follow
 // proj/src/blco_format.cpp:136-147.
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <string>
 
 #include "internal.hpp"
@@ -35,6 +38,35 @@ void check_launch(const char* what) {
   if (e != cudaSuccess)
     throw Status(BLCO_ECUDA, std::string("cuda: launch of ") + what + " failed: " +
                                  cudaGetErrorString(e));
+}
+
+namespace {
+std::mutex g_attr_mu;
+std::map<std::pair<int, const void*>, size_t> g_smem_granted;
+std::map<std::tuple<int, const void*, int, size_t>, int> g_occupancy;
+}  // namespace
+
+void ensure_dyn_smem(const void* kernel, size_t bytes) {
+  int dev = 0;
+  B200_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> g(g_attr_mu);
+  size_t& have = g_smem_granted[{dev, kernel}];
+  if (bytes <= have) return;
+  B200_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
+  have = bytes;
+}
+
+int blocks_per_sm(const void* kernel, int threads, size_t dyn_smem) {
+  int dev = 0;
+  B200_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> g(g_attr_mu);
+  auto key = std::make_tuple(dev, kernel, threads, dyn_smem);
+  auto it = g_occupancy.find(key);
+  if (it != g_occupancy.end()) return it->second;
+  int n = 0;
+  B200_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, threads, dyn_smem));
+  g_occupancy[key] = n;
+  return n;
 }
 
 int bits_for_extent(uint64_t extent) { return extent <= 1 ? 0 : 64 - __builtin_clzll(extent - 1); }

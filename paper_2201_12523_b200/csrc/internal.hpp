@@ -56,6 +56,13 @@ int guarded(F&& f) {
   }
 }
 
+// Kernel attribute helpers, cached per (device, kernel): cudaFuncSetAttribute
+// is only called when a kernel needs more dynamic shared memory than it was
+// last granted, and occupancy queries are answered from the cache, so the
+// hot enqueue paths make no attribute calls in steady state.
+void ensure_dyn_smem(const void* kernel, size_t bytes);
+int blocks_per_sm(const void* kernel, int threads, size_t dyn_smem);
+
 extern std::atomic<uint64_t> g_launches;
 inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 void check_launch(const char* what);

@@ -945,7 +945,7 @@ bool use_warp_variant() {
 
 template <class K>
 void set_smem(K kern, size_t dyn) {
-  B200_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn)));
+  ensure_dyn_smem(reinterpret_cast<const void*>(kern), dyn);
 }
 
 template <int N, int LPE, int CPL, bool FULL>
@@ -1018,9 +1018,7 @@ void launch_cfg(MttkrpLaunch& a) {
   const size_t dyn = tile_stage + slots * per_slot + 16;
   auto kern = stats ? k_mttkrp_hier<N, LPE, CPL, FULL, true> : k_mttkrp_hier<N, LPE, CPL, FULL, false>;
   set_smem(kern, dyn);
-  int per_sm = 0;
-  B200_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kCtaThreads, dyn));
-  per_sm = std::max(per_sm, 1);
+  const int per_sm = std::max(blocks_per_sm(reinterpret_cast<const void*>(kern), kCtaThreads, dyn), 1);
   const uint64_t grid = std::min<uint64_t>(p.ntiles, static_cast<uint64_t>(nsm) * per_sm);
   a.workgroups = grid;
   const int C = std::max(1, a.cfg.num_factor_copies);

@@ -274,8 +274,7 @@ void radix_sort_pairs(K* keys, K* keys_alt, uint32_t* vals, uint32_t* vals_alt, 
     check_launch("k_digit_hist");
     scan_exclusive_u64(hist.ptr, hist.ptr, ntiles * kDigits, s);
     constexpr size_t stage = (sizeof(K) + sizeof(uint32_t)) * kSortTile;
-    B200_CUDA(cudaFuncSetAttribute(k_digit_scatter<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(stage)));
+    ensure_dyn_smem(reinterpret_cast<const void*>(k_digit_scatter<K>), stage);
     k_digit_scatter<K><<<grid, kSortThreads, stage, s>>>(kin, vin, n, shift, dmask, ntiles, hist.ptr, kout, vout);
     count_launch();
     check_launch("k_digit_scatter");
