@@ -371,23 +371,6 @@ unsigned grid_of(uint64_t n) {
   return static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>((n + kT - 1) / kT, 148 * 16)));
 }
 
-// dense_kernels.cpp:35-56 restated (host, R x R).
-bool cholesky(const std::vector<double>& v, int r, double shift, std::vector<double>& L) {
-  L.assign(static_cast<size_t>(r) * r, 0.0);
-  for (int i = 0; i < r; ++i)
-    for (int j = 0; j <= i; ++j) {
-      double s = v[i * r + j] + (i == j ? shift : 0.0);
-      for (int k = 0; k < j; ++k) s -= L[i * r + k] * L[j * r + k];
-      if (i == j) {
-        if (!(s > 0.0) || !std::isfinite(s)) return false;
-        L[i * r + i] = std::sqrt(s);
-      } else {
-        L[i * r + j] = s / L[j * r + j];
-      }
-    }
-  return true;
-}
-
 // Every reduction of the epilogue writes per-CTA (or per-warp) partials that
 // k_reduce_ordered sums in a fixed order, so CP-ALS is bit-reproducible given
 // bit-reproducible MTTKRPs (ExecConfig::deterministic).
