@@ -313,6 +313,14 @@ DenseMatrix stream_mttkrp(BlockSource& source, const FactorMatrices& f, int mode
                           const DeviceBudget& budget, const ExecConfig& config = {},
                           Strategy strategy = Strategy::Auto, StreamReport* report = nullptr);
 
+// B200 extension: every block crosses the host link once and all N modes are
+// computed on it (blco_stream_mttkrp_all).  Result n is dims[n] x rank; the
+// resident set adds all N outputs to the factors.
+std::vector<DenseMatrix> stream_mttkrp_all_modes(BlockSource& source, const FactorMatrices& f,
+                                                 const DeviceBudget& budget, const ExecConfig& config = {},
+                                                 Strategy strategy = Strategy::Auto,
+                                                 StreamReport* report = nullptr);
+
 // ----------------------------------------------------------------- cpals.hpp
 struct CpAlsOptions {
   std::size_t rank = 32;

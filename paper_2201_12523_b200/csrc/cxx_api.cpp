@@ -654,20 +654,29 @@ int pull(void* ctx, blco_block_view* out) {
 }
 }  // namespace
 
-DenseMatrix stream_mttkrp(BlockSource& source, const FactorMatrices& f, int mode,
-                          const DeviceBudget& budget, const ExecConfig& config, Strategy strategy,
-                          StreamReport* report) {
+namespace {
+// Shared by stream_mttkrp (mode >= 0) and stream_mttkrp_all_modes (mode < 0).
+std::vector<DenseMatrix> stream_impl(BlockSource& source, const FactorMatrices& f, int mode,
+                                     const DeviceBudget& budget, const ExecConfig& config, Strategy strategy,
+                                     StreamReport* report) {
   config.validate();
   const BitLayout& layout = source.layout();
   f.validate(layout.dims);
-  if (mode < 0 || mode >= layout.order()) throw FormatError("stream: mode out of range");
+  if (mode >= layout.order()) throw FormatError("stream: mode out of range");
   const blco_layout l = to_c(layout);
   const blco_exec_config c = to_c(config);
   const blco_device_budget b{budget.capacity_bytes, budget.num_queues, budget.reservation_bytes,
                              budget.injected_transfer_latency_s};
   SourceCtx ctx{&source, dynamic_cast<MemoryBlockSource*>(&source), {}, nullptr};
   const auto ptrs = factor_ptrs(f);
-  DenseMatrix m(layout.dims[mode], f.rank);
+  std::vector<DenseMatrix> outs;
+  std::vector<double*> optr;
+  if (mode >= 0) {
+    outs.emplace_back(layout.dims[mode], f.rank);
+  } else {
+    for (int m = 0; m < layout.order(); ++m) outs.emplace_back(layout.dims[m], f.rank);
+  }
+  for (auto& o : outs) optr.push_back(o.data.data());
   const std::uint64_t nb = source.block_count();
   std::vector<int32_t> bq(nb);
   std::vector<blco_stream_event> tl(2 * nb);
@@ -676,9 +685,11 @@ DenseMatrix stream_mttkrp(BlockSource& source, const FactorMatrices& f, int mode
   r.block_queue_capacity = nb;
   r.timeline = tl.data();
   r.timeline_capacity = tl.size();
-  const int status = blco_stream_mttkrp(&l, source.max_nnz_per_block(), pull, &ctx, ptrs.data(),
-                                        f.rank, mode, &b, &c, static_cast<int>(strategy),
-                                        current_device(), m.data.data(), &r);
+  const int status =
+      mode >= 0 ? blco_stream_mttkrp(&l, source.max_nnz_per_block(), pull, &ctx, ptrs.data(), f.rank, mode, &b, &c,
+                                     static_cast<int>(strategy), current_device(), optr[0], &r)
+                : blco_stream_mttkrp_all(&l, source.max_nnz_per_block(), pull, &ctx, ptrs.data(), f.rank, &b, &c,
+                                         static_cast<int>(strategy), current_device(), optr.data(), 0, &r);
   if (ctx.error) std::rethrow_exception(ctx.error);
   ck(status);
   if (report) {
@@ -697,7 +708,20 @@ DenseMatrix stream_mttkrp(BlockSource& source, const FactorMatrices& f, int mode
                                                               : StreamEvent::Kind::Compute,
                                              tl[i].queue, tl[i].block, tl[i].begin_s, tl[i].end_s});
   }
-  return m;
+  return outs;
+}
+}  // namespace
+
+DenseMatrix stream_mttkrp(BlockSource& source, const FactorMatrices& f, int mode, const DeviceBudget& budget,
+                          const ExecConfig& config, Strategy strategy, StreamReport* report) {
+  if (mode < 0) throw FormatError("stream: mode out of range");
+  return std::move(stream_impl(source, f, mode, budget, config, strategy, report)[0]);
+}
+
+std::vector<DenseMatrix> stream_mttkrp_all_modes(BlockSource& source, const FactorMatrices& f,
+                                                 const DeviceBudget& budget, const ExecConfig& config,
+                                                 Strategy strategy, StreamReport* report) {
+  return stream_impl(source, f, -1, budget, config, strategy, report);
 }
 
 // ------------------------------------------------------------------- cp-als

@@ -269,6 +269,22 @@ TEST(all_modes_extension) {  // B200 extension: every mode of a host tensor in o
   for (int mode = 0; mode < 3; ++mode) CHECK(rel_frobenius(all[mode], mttkrp_coo(coo, f, mode)) <= 1e-12);
 }
 
+TEST(streamed_all_modes_extension) {  // B200 extension of test_streaming.cpp:21-52
+  Rng rng(83);
+  auto coo = random_coo(rng, {50, 40, 60}, 600);
+  auto t = build_blco(coo, 8, 64);
+  auto f = random_factors(rng, coo.dims, 4);
+  DeviceBudget b;
+  b.num_queues = 2;
+  b.reservation_bytes = t.max_nnz_per_block * 16;
+  b.capacity_bytes = 2 * b.reservation_bytes + (50 + 40 + 60) * 4 * 8 * 2;
+  MemoryBlockSource src(t);
+  StreamReport rep;
+  auto all = stream_mttkrp_all_modes(src, f, b, {}, Strategy::Register, &rep);
+  CHECK(all.size() == 3 && rep.blocks == t.blocks.size());
+  for (int mode = 0; mode < 3; ++mode) CHECK(rel_frobenius(all[mode], mttkrp_coo(coo, f, mode)) <= 1e-12);
+}
+
 TEST(single_copy_hierarchical) {  // test_mttkrp.cpp:235-244
   auto t = build_blco(golden_tensor(), 64);
   Rng rng(67);
