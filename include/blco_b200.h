@@ -254,8 +254,9 @@ int blco_mttkrp_f32(const blco_tensor* t, const float* const* factors, uint64_t 
  * factors[m] are host dims[m] x rank, outs[m] host dims[m] x rank
  * (overwritten), or device pointers on `device` when outs_on_device != 0
  * (multi-GPU callers reduce them with NCCL).  chunk_elems = 0 picks
- * max(2^20, nnz/32).  Device buffers are cached per calling thread and
- * reused by later calls.  Returns after the outputs are written. */
+ * max(2^20, nnz/32), shrinking geometrically over the last chunks.
+ * Device buffers are cached per calling thread and reused by later calls.
+ * Returns after the outputs are written. */
 typedef struct blco_all_modes_report {
   double device_ms;   /* CUDA events: first copy enqueued .. last D2H done */
   uint64_t chunks;

@@ -125,13 +125,24 @@ extern "C" int blco_mttkrp_all_host(const blco_layout* layout, uint64_t nblocks,
     for (uint64_t b = 0; b < nblocks; ++b)
       for (int m = 0; m < N; ++m)
         hbase[b * N + m] = static_cast<uint32_t>(key_upper(l, m, keys[b]) << l.rem_bits[m]);
-    if (chunk_elems == 0) chunk_elems = std::max<uint64_t>(uint64_t{1} << 20, (nnz + 31) / 32);
-    // chunk = run of whole tiles holding ~chunk_elems elements
+    // chunk = run of whole tiles holding ~chunk_elems elements.  With the
+    // automatic size the last chunks shrink geometrically (down to 2^16
+    // elements): only the final chunk's kernels run after the last byte has
+    // crossed the link, so a small tail keeps the step close to the link time.
+    const bool auto_chunks = chunk_elems == 0;
+    if (auto_chunks) chunk_elems = std::max<uint64_t>(uint64_t{1} << 20, (nnz + 31) / 32);
     std::vector<std::pair<uint64_t, uint64_t>> chunks;  // tile ranges
+    uint64_t done = 0;
     for (uint64_t t0 = 0; t0 < ht.size();) {
+      uint64_t target = chunk_elems;
+      if (auto_chunks) {
+        const uint64_t left = nnz - done;
+        while (target > (uint64_t{1} << 16) && target > left / 2) target /= 2;
+      }
       uint64_t t1 = t0, e = 0;
-      while (t1 < ht.size() && (t1 == t0 || e + ht[t1].count <= chunk_elems)) e += ht[t1++].count;
+      while (t1 < ht.size() && (t1 == t0 || e + ht[t1].count <= target)) e += ht[t1++].count;
       chunks.emplace_back(t0, t1);
+      done += e;
       t0 = t1;
     }
 
