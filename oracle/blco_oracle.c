@@ -425,6 +425,57 @@ static void* rs_worker(void* arg) {
   return NULL;
 }
 
+/* Row-sampled mttkrp_coo over an in-memory COO (idx mode-major): rows
+ * rows[m][0..nrows[m]) of every mode, one pass in COO order with the oracle's
+ * product order (oracle.cpp:15-24), so the rows are bit-identical to
+ * orc_mttkrp_coo's. */
+int orc_rowsample_coo(int order, const uint64_t* dims, uint64_t nnz, const uint64_t* idx, const double* vals,
+                      const double* const* f, uint64_t rank, const uint64_t* nrows,
+                      const uint64_t* const* rows, double* const* out) {
+  if (order < 1 || order > ORC_MAX_ORDER) return fail("rowsample: bad order");
+  int32_t* slot_of[ORC_MAX_ORDER] = {0};
+  int rc = ORC_OK;
+  double* row = malloc(rank * sizeof *row);
+  for (int m = 0; m < order; ++m) {
+    slot_of[m] = malloc(dims[m] * sizeof(int32_t));
+    if (!slot_of[m] || !row) {
+      rc = fail("rowsample: out of memory");
+      goto done;
+    }
+    memset(slot_of[m], 0xff, dims[m] * sizeof(int32_t));
+    for (uint64_t k = 0; k < nrows[m]; ++k) {
+      if (rows[m][k] >= dims[m]) {
+        rc = fail("rowsample: row out of range");
+        goto done;
+      }
+      slot_of[m][rows[m][k]] = (int32_t)k;
+    }
+    memset(out[m], 0, nrows[m] * rank * sizeof(double));
+  }
+  for (uint64_t e = 0; e < nnz; ++e)
+    for (int mode = 0; mode < order; ++mode) {
+      const uint64_t c = idx[(uint64_t)mode * nnz + e];
+      if (c >= dims[mode]) {
+        rc = fail("rowsample: coordinate out of range");
+        goto done;
+      }
+      const int32_t sl = slot_of[mode][c];
+      if (sl < 0) continue;
+      for (uint64_t r = 0; r < rank; ++r) row[r] = vals[e];
+      for (int n = 0; n < order; ++n) {
+        if (n == mode) continue;
+        const double* a = f[n] + idx[(uint64_t)n * nnz + e] * rank;
+        for (uint64_t r = 0; r < rank; ++r) row[r] *= a[r];
+      }
+      double* dst = out[mode] + (uint64_t)sl * rank;
+      for (uint64_t r = 0; r < rank; ++r) dst[r] += row[r];
+    }
+done:
+  for (int m = 0; m < order; ++m) free(slot_of[m]);
+  free(row);
+  return rc;
+}
+
 int orc_rowsample_uniform(int order, const uint64_t* dims, uint64_t nnz, uint64_t seed,
                           const double* const* f, uint64_t rank, const uint64_t* nrows,
                           const uint64_t* const* rows, double* const* out, int threads) {

@@ -108,6 +108,12 @@ void orc_factors_random(const uint64_t* dims, int order, uint64_t rank, uint64_t
  * fastest) and value unit(splitmix64 output e of seed ^ VALUE_SALT). */
 int orc_synth_uniform(int order, const uint64_t* dims, uint64_t nnz, uint64_t seed,
                       uint64_t* idx, double* vals);
+/* Rows rows[m][0..nrows[m]) of mttkrp_coo over an in-memory COO, every mode,
+ * bit-identical to orc_mttkrp_coo's rows. */
+int orc_rowsample_coo(int order, const uint64_t* dims, uint64_t nnz, const uint64_t* idx, const double* vals,
+                      const double* const* f, uint64_t rank, const uint64_t* nrows,
+                      const uint64_t* const* rows, double* const* out);
+
 /* Rows rows[m][0..nrows[m]) of mttkrp_coo(T, f, m) for every mode m of
  * T = orc_synth_uniform(dims, nnz, seed), streamed (T is never stored);
  * bit-identical to the full oracle's rows (SURVEY.md 8c row-sampled oracle).

@@ -151,6 +151,21 @@ class Oracle:
                                             C.c_uint64(seed), _pu(idx), _pd(vals)))
         return idx, vals
 
+    def rowsample_coo(self, dims, idx, vals, factors, rows):
+        """Rows rows[m] of mttkrp_coo(COO, factors, m), every mode (one pass,
+        bit-identical to mttkrp_coo's rows)."""
+        idx = _u64(idx).reshape(len(dims), -1)
+        vals = _f64(vals)
+        fs = [_f64(a) for a in factors]
+        rank = fs[0].shape[1]
+        rows = [_u64(r) for r in rows]
+        outs = [np.zeros((r.size, rank)) for r in rows]
+        rp = (C.c_void_p * len(rows))(*[r.ctypes.data for r in rows])
+        self._ck(self.lib.orc_rowsample_coo(len(dims), _pu(_u64(dims)), C.c_uint64(vals.size), _pu(idx), _pd(vals),
+                                            _pp(fs), C.c_uint64(rank), _pu(_u64([r.size for r in rows])), rp,
+                                            _pp(outs)))
+        return outs
+
     def rowsample_uniform(self, dims, nnz, seed, factors, rows, threads=None):
         """Rows rows[m] of mttkrp_coo(T, factors, m), every mode m, of the
         uniform synthetic tensor T (streamed, never stored); bit-identical to

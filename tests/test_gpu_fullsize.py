@@ -93,3 +93,38 @@ def test_amazon_full_size_rows(gpu, oracle):
     assert dt.nnz == nnz and dt.block_nnz().size == 14
     dt.validate_device()
     _check_rows(gpu, oracle, dt, dims, nnz, rank, 512)
+
+
+def test_reddit_stream_chunks_rows(gpu, oracle):
+    """BASELINE configs[4] at full scale, two of the 64 ALTO chunks of the
+    Reddit-shaped generator (146M elements, 64-bit layout) streamed through a
+    capped budget with stream_mttkrp_all_modes (blocks of 2^25); sampled rows
+    of every mode against the row-sampled oracle over the decoded COO."""
+    dims, nnz_target, nchunks = [8211298, 176962, 8116559], 4_687_474_081, 64
+    frac = float(np.prod(np.array(dims, dtype=np.float64))) / 2.0 ** 64
+    ncand = int(nnz_target / nchunks / frac) + 1
+    idx = gpu.api.pinned_empty(2 * ncand, np.uint64)
+    vals = gpu.api.pinned_empty(2 * ncand, np.float64)
+    off = 0
+    for c in (0, 37):
+        off += gpu.api.synth_alto_chunk(dims, c, nchunks, ncand, 42, idx[off:], vals[off:])
+    assert off > 2 * 0.95 * nnz_target / nchunks
+    layout = gpu.make_layout(dims, 64)
+    assert layout.stripped_bits == 0
+    coords = np.empty((3, off), np.uint64)
+    for m in range(3):
+        coords[m] = (idx[:off] >> np.uint64(layout.field_shift[m])) & np.uint64(layout.field_mask[m])
+        assert int(coords[m].max()) < dims[m]
+    bmax = 1 << 25
+    blocks = [(0, idx[o:o + min(bmax, off - o)], vals[o:o + min(bmax, off - o)]) for o in range(0, off, bmax)]
+    f = gpu.FactorMatrices.random(dims, 32, 7)
+    budget = gpu.DeviceBudget(capacity_bytes=12 << 30, num_queues=3, reservation_bytes=bmax * 16)
+    rep = gpu.StreamReport()
+    got = gpu.stream_mttkrp_all_modes(iter(blocks), f, budget, report=rep, layout=layout, max_nnz_per_block=bmax,
+                                      block_count=len(blocks))
+    assert rep.blocks == len(blocks) and rep.bytes_streamed == off * 16
+    assert rep.peak_resident_bytes <= budget.capacity_bytes
+    rows = _sample_rows(dims, 512)
+    want = oracle.rowsample_coo(dims, coords, vals[:off], f.factors, rows)
+    for mode in range(3):
+        assert rel_frobenius(got[mode][rows[mode].astype(np.int64)], want[mode]) <= TOL, mode

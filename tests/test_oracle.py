@@ -219,3 +219,14 @@ def test_rowsample_equals_full_oracle_rows(oracle, reflib):
         full = oracle.mttkrp_coo(dims, idx, vals, f, m)
         assert np.array_equal(got[m], full[rows[m]])
         assert np.array_equal(got[m], reflib.mttkrp_coo(dims, idx, vals, f, m)[rows[m]])
+
+
+def test_rowsample_coo_equals_full_oracle_rows(oracle):
+    dims, nnz, rank = [120, 90, 60], 40_000, 8
+    idx, vals = oracle.synth_uniform(dims, nnz, 9)
+    f = oracle.factors_random(dims, rank, 3)
+    rng = np.random.default_rng(2)
+    rows = [np.sort(rng.choice(d, size=17, replace=False)) for d in dims]
+    got = oracle.rowsample_coo(dims, idx, vals, f, rows)
+    for m in range(3):
+        assert np.array_equal(got[m], oracle.mttkrp_coo(dims, idx, vals, f, m)[rows[m]])
