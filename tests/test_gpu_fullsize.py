@@ -128,3 +128,30 @@ def test_reddit_stream_chunks_rows(gpu, oracle):
     want = oracle.rowsample_coo(dims, coords, vals[:off], f.factors, rows)
     for mode in range(3):
         assert rel_frobenius(got[mode][rows[mode].astype(np.int64)], want[mode]) <= TOL, mode
+
+
+def test_delicious_full_size_rows(gpu, oracle):
+    """BASELINE configs[3] at full size: the Delicious-shaped power-law tensor
+    (140M distinct draws floor(I*u^4), 78-bit layout, 14 stripped bits, many
+    keyed blocks), R=16: device block checks, then sampled rows of every mode
+    of the device MTTKRP against the row-sampled oracle over the tensor's
+    decoded COO."""
+    dims, nnz, rank = [532924, 17262471, 2480308, 1443], 140_126_181, 16
+    dt = gpu.DeviceTensor.synthetic_draws(dims, nnz, 42, 4)
+    assert dt.nnz == nnz
+    dt.validate_device()
+    host = dt.to_host()
+    lay = host.layout
+    assert lay.total_bits == 78 and lay.stripped_bits == 14 and host.keys.size > 1
+    counts = np.diff(host.offsets).astype(np.int64)
+    coords = np.empty((4, nnz), np.uint64)
+    for m in range(4):
+        base = np.repeat(np.array([lay.block_base(int(k))[m] for k in host.keys], np.uint64), counts)
+        coords[m] = base | ((host.idx >> np.uint64(lay.field_shift[m])) & np.uint64(lay.field_mask[m]))
+        assert int(coords[m].max()) < dims[m]
+    f = gpu.FactorMatrices.random(dims, rank, 7)
+    rows = _sample_rows(dims, 256)
+    want = oracle.rowsample_coo(dims, coords, host.vals, f.factors, rows)
+    for mode in range(4):
+        got = gpu.mttkrp(dt, f, mode)[rows[mode].astype(np.int64)]
+        assert rel_frobenius(got, want[mode]) <= TOL, mode
