@@ -130,7 +130,17 @@ def dist_init(torch, dev):
 # --------------------------------------------------------- CPU reference
 
 
-def reference_sample_run(dims, nnz, rank, steps, warmup, target_step_s=4.0, threads=None):
+def cpu_model() -> str:
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def reference_sample_run(dims, nnz, rank, steps, warmup, target_step_s=4.0, threads=None, extra=False):
     """Times the reference's blco::mttkrp (all modes) on the host.
 
     The sample is the `S` elements of smallest ALTO index of the synthetic
@@ -183,9 +193,29 @@ def reference_sample_run(dims, nnz, rank, steps, warmup, target_step_s=4.0, thre
     bpe = bytes_per_elem(order, rank)
     step_s = sum(times) / len(times)
     gbps = S * order * bpe / step_s / 1e9
-    return gbps, {"sample_nnz": S, "step_s": step_s, "threads": threads, "setup_s": setup_s,
-                  "sample": f"first {S} elements in ALTO order of the {nnz}-nnz tensor "
-                            f"(reference build_blco on that COO subset), all {order} modes, R={rank}"}
+    info = {"sample_nnz": S, "step_s": step_s, "threads": threads, "setup_s": setup_s,
+            "sample": f"first {S} elements in ALTO order of the {nnz}-nnz tensor "
+                      f"(reference build_blco on that COO subset), all {order} modes, R={rank}"}
+    if extra:
+        # the reference anti-scales with threads, so also one
+        # thread, and the oracle::mttkrp_coo loop (1 thread) on the same sample
+        cfg1 = cfg_array(num_threads=1)
+        s0 = time.perf_counter()
+        for mode in range(order):
+            t.mttkrp(factors, mode, cfg1)
+        one_s = time.perf_counter() - s0
+        sel = np.argpartition(alto, S - 1)[:S] if S < gen_n else np.arange(gen_n)
+        sidx, svals = idx[:, sel], vals[sel]
+        s0 = time.perf_counter()
+        for mode in range(order):
+            ref.mttkrp_coo(dims, sidx, svals, factors, mode)
+        coo_s = time.perf_counter() - s0
+        info["reference_1_thread"] = {"value": round(S * order * bpe / one_s / 1e9, 4), "unit": "GB/s",
+                                      "step_s": round(one_s, 3)}
+        info["oracle_mttkrp_coo_1_thread"] = {"value": round(S * order * bpe / coo_s / 1e9, 4), "unit": "GB/s",
+                                              "step_s": round(coo_s, 3),
+                                              "note": "reference oracle::mttkrp_coo (oracle.cpp:9-26)"}
+    return gbps, info
 
 
 def make_wide(dims) -> bool:
@@ -354,10 +384,12 @@ def run_ours(args, world, rank_id, local):
         result["e2e"] = e2e_run(b, torch, dt, dims, R, N, nnz, args, dev, world)
     if rank_id == 0 and world == 1 and not args.no_cpu_baseline and args.config in ("cfg1", "nell2"):
         try:
-            gbps, info = reference_sample_run(dims, nnz, R, steps=2, warmup=1)
+            gbps, info = reference_sample_run(dims, nnz, R, steps=2, warmup=1, extra=True)
             result["cpu_baseline"] = {"value": round(gbps, 4), "unit": "GB/s", "cores": info["threads"],
                                       "kind": "reference", "sample": info["sample"],
-                                      "step_s": round(info["step_s"], 3)}
+                                      "step_s": round(info["step_s"], 3), "cpu_model": cpu_model(),
+                                      "reference_1_thread": info["reference_1_thread"],
+                                      "oracle_mttkrp_coo_1_thread": info["oracle_mttkrp_coo_1_thread"]}
         except Exception as e:  # noqa: BLE001
             result["cpu_baseline"] = {"value": None, "unit": "GB/s", "cores": None, "kind": "reference",
                                       "sample": f"failed: {e}"}
