@@ -328,13 +328,23 @@ def run_ours(args, world, rank_id, local):
     except (OSError, ValueError):
         pass
     peak = peaks.get("hbm_gbs") or 6650.0
-    traffic = None
+    traffic, binding = None, None
     prof = ROOT / "profiles" / f"ncu_{args.config}.json"
     if prof.exists():
         try:
-            per_launch = json.loads(prof.read_text()).get("dram_bytes_per_launch_all_modes") or []
+            rep = json.loads(prof.read_text())
+            per_launch = rep.get("dram_bytes_per_launch_all_modes") or []
             traffic = round(sum(per_launch) / len(per_launch)) if per_launch else None
-        except ValueError:
+            ls = rep.get("launches") or []
+            if ls:
+                avg = lambda k: round(statistics.mean(float(x.get(k, 0) or 0) for x in ls), 1)  # noqa: E731
+                l1 = avg("l1tex__throughput.avg.pct_of_peak_sustained_elapsed")
+                dram = round(100 * statistics.mean(float(x["dram_bytes"]) / float(x["gpu__time_duration.sum"])
+                                                   for x in ls) / (peak * 1e9), 1)
+                binding = {"l1tex_pct": l1, "dram_pct": dram, "lts_pct": avg("lts__throughput.avg.pct_of_peak_sustained_elapsed"),
+                           "limiter": "L1 data pipe (gathers hit L2)" if l1 > dram else "HBM",
+                           "source": f"profiles/ncu_{args.config}.json (ncu --set full)"}
+        except (ValueError, TypeError):
             traffic = None
 
     result = {
@@ -359,7 +369,7 @@ def run_ours(args, world, rank_id, local):
         "per_mode_ms": [round(statistics.mean(x), 4) for x in mode_ms],
         "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic,
-                     "kernel": "k_mttkrp_register (one launch per mode)",
+                     "kernel": "k_mttkrp_sorted (one launch per mode)", "binding": binding,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks.get("hbm_gbs") else "fallback"},
         "clocks": clk.summary(),
         "gpu_launches": launches,
