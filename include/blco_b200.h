@@ -398,6 +398,10 @@ int blco_partition(const uint64_t* block_nnz, uint64_t nblocks, uint64_t quota, 
 int blco_device_count(void);
 /* Number of kernels this library launched since load (tests/bench audit). */
 uint64_t blco_kernel_launch_count(void);
+/* Frees the calling thread's cached device buffers (the all-mode host
+ * pipeline's payload/factor/output buffers, hierarchical copies, the
+ * deterministic partials); later calls re-create them. */
+int blco_release_thread_caches(void);
 
 #ifdef __cplusplus
 }

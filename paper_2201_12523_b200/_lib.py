@@ -182,6 +182,7 @@ SIGNATURES = {
     "blco_partition": (_I, [_PU64, _U64, _U64, _I, _PU64, _PU64]),
     "blco_device_count": (_I, []),
     "blco_kernel_launch_count": (_U64, []),
+    "blco_release_thread_caches": (_I, []),
 }
 
 

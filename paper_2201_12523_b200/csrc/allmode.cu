@@ -88,6 +88,14 @@ AllModeCtx& context(int device) {
 }
 
 }  // namespace
+
+void release_allmode_cache() {
+  if (t_ctx.device >= 0) {
+    DeviceGuard g(t_ctx.device);
+    t_ctx.release();
+  }
+}
+
 }  // namespace b200
 
 using namespace b200;

@@ -585,6 +585,10 @@ int blco_cp_als_timed(const blco_tensor* t, uint64_t rank, int max_iters, double
   return guarded([&] {
     if (rank < 1) throw_format("cp_als: rank must be >= 1");
     if (max_iters < 0) throw_format("cp_als: max_iters must be >= 0");
+    // c_L (constant memory) is one per device context: ALS runs are
+    // serialised within the process
+    static std::mutex als_mu;
+    std::lock_guard<std::mutex> als_lock(als_mu);
     blco_exec_config c;
     if (cfg) c = *cfg; else blco_exec_config_default(&c);
     if (blco_exec_config_validate(&c) != BLCO_OK) throw_format(blco_last_error());

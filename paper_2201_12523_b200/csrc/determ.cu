@@ -288,6 +288,8 @@ thread_local DevBuf<double> t_partial;
 
 }  // namespace
 
+void release_det_cache() { t_partial.reset(); }
+
 void det_mttkrp_enqueue(const blco_tensor& t, MttkrpLaunch& a) {
   const DetIndex& d = det_index(t, a.mode, a.stream);
   const uint64_t elems = t.layout.dims[a.mode] * a.rank;

@@ -151,6 +151,14 @@ int blco_abi_version(void) { return 1; }
 void blco_set_error(int status, const char* msg) { set_error(status, msg ? msg : ""); }
 uint64_t blco_kernel_launch_count(void) { return g_launches.load(); }
 
+int blco_release_thread_caches(void) {
+  return guarded([] {
+    release_allmode_cache();
+    release_det_cache();
+    release_mttkrp_workspace();
+  });
+}
+
 int blco_make_layout(const uint64_t* dims, int order, int target_bits, blco_layout* out) {
   return guarded([&] { *out = make_layout(dims, order, target_bits); });
 }

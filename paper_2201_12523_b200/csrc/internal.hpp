@@ -199,6 +199,10 @@ uint64_t select_flagged(const T* in, const uint8_t* flags, uint64_t n, T* out, c
 KernelView view_of(const blco_tensor& t);
 void mttkrp_enqueue(MttkrpLaunch& a);
 void det_mttkrp_enqueue(const blco_tensor& t, MttkrpLaunch& a);
+// per-thread device caches (blco_release_thread_caches)
+void release_allmode_cache();
+void release_det_cache();
+void release_mttkrp_workspace();
 void merge_copies_enqueue(const double* copies, uint64_t elems, int ncopies, double* out,
                           int accumulate, cudaStream_t s);
 uint32_t mttkrp_tile_elems();

@@ -921,6 +921,16 @@ struct Workspace {
 };
 thread_local Workspace t_ws;
 
+}  // namespace
+
+void release_mttkrp_workspace() {
+  t_ws.copies.reset();
+  t_ws.counters.reset();
+  t_ws.device = -1;
+}
+
+namespace {
+
 // Per-thread scratch, re-created when the calling thread changes device.
 Workspace& workspace() {
   int dev = 0;

@@ -289,3 +289,20 @@ print(worst)
                        env=dict(os.environ, BLCO_B200_VARIANT="warp"))
     assert r.returncode == 0, r.stderr[-2000:]
     assert float(r.stdout.strip().splitlines()[-1]) <= TOL
+
+
+def test_release_thread_caches(gpu, oracle):
+    """blco_release_thread_caches frees the per-thread device buffers; later
+    calls re-create them and still match the oracle."""
+    dims = [200, 150, 100]
+    coo = gpu.synth_uniform_host(dims, 20_000, 4)
+    f = gpu.FactorMatrices.random(dims, 16, 2)
+    t = gpu.build_blco(coo, 64)
+    want = [oracle.mttkrp_coo(dims, coo.indices, coo.values, f.factors, m) for m in range(3)]
+    gpu.mttkrp_all_modes(t, f)
+    gpu.mttkrp(t, f, 0, gpu.ExecConfig(deterministic=True))
+    assert gpu.api.lib.blco_release_thread_caches() == 0
+    got = gpu.mttkrp_all_modes(t, f)
+    for m in range(3):
+        assert rel_frobenius(got[m], want[m]) <= TOL
+    assert rel_frobenius(gpu.mttkrp(t, f, 1, gpu.ExecConfig(deterministic=True)), want[1]) <= TOL
