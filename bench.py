@@ -618,6 +618,9 @@ STREAM_CONFIGS = {
                             "synthetic Reddit-shaped, 0.6B nnz (9.6 GB pinned), R=32, streamed, 24 GiB budget"),
     "reddit_stream_tiny": ([8211298, 176962, 8116559], 20_000_000, 32, 4,
                            "synthetic Reddit-shaped, 20M nnz, R=32, streamed (multi-rank plumbing test size)"),
+    "reddit_file_small": ([8211298, 176962, 8116559], 600_000_000, 32, 8,
+                          "synthetic Reddit-shaped, 0.6B nnz written as a .blco container (9.6 GB) and streamed "
+                          "from the file (native pinned-ring reader, device-side element checks), 24 GiB budget"),
 }
 
 
@@ -687,6 +690,28 @@ def run_stream(args, world, rank_id, local):
         for o, n in blocks:
             yield (0, idx[o:o + n], vals[o:o + n])
 
+    file_info = None
+    if "file" in args.config:
+        # the tensor as a .blco container (blco_format.cpp:149-172 layout),
+        # written from the pinned arrays; the stream then reads the file
+        import tempfile
+        fdir = os.environ.get("BLCO_B200_FILE_DIR") or tempfile.gettempdir()
+        path = os.path.join(fdir, f"bench_{args.config}_{rank_id}.blco")
+        w0 = time.perf_counter()
+        with open(path, "wb") as fh:
+            fh.write(b"BLCO" + np.array([1, N], "<u2").tobytes() + np.array(dims, "<u8").tobytes()
+                     + np.array([64], "<u2").tobytes() + np.array(layout.mode_bits, "<u2").tobytes()
+                     + np.array([bmax, len(blocks)], "<u8").tobytes())
+            for o, n in blocks:
+                fh.write(np.array([0, n], "<u8").tobytes())
+                fh.write(memoryview(idx[o:o + n]))
+                fh.write(memoryview(vals[o:o + n]))
+        file_info = {"path": path, "bytes": os.path.getsize(path), "write_s": round(time.perf_counter() - w0, 2),
+                     "note": "just written, so mostly served from the page cache"}
+
+        def source():  # noqa: F811 - the file replaces the in-memory blocks
+            return b.FileBlockSource(path, dev)
+
     def one_all():
         rep = b.StreamReport()
         w0 = time.perf_counter()
@@ -751,6 +776,12 @@ def run_stream(args, world, rank_id, local):
         "clocks": clk.summary(),
         "generate": {"pinned_alloc_s": round(alloc_s, 2), "generate_s": round(gen_s, 2)},
     }
+    if file_info:
+        result["file"] = file_info
+        try:
+            os.remove(file_info["path"])
+        except OSError:
+            pass
     if per_mode:
         result["stream"]["per_mode_api"] = {
             "total_s": round(sum(r.total_seconds for r in per_mode), 3),

@@ -273,8 +273,13 @@ class FileBlockSource final : public BlockSource {
   std::uint64_t block_count() const override { return header_.block_count; }
   std::uint64_t max_nnz_per_block() const override { return header_.max_nnz_per_block; }
   bool next(BlcoBlock& out) override;
+  // B200: stream_mttkrp on an unconsumed FileBlockSource reads the file
+  // through the native pinned-ring reader (blco_stream_mttkrp_file)
+  const std::filesystem::path& path() const { return path_; }
+  bool consumed() const { return cursor_ != 0; }
 
  private:
+  std::filesystem::path path_;
   std::unique_ptr<std::istream> in_;
   BlcoHeader header_;
   BitLayout layout_;

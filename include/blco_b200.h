@@ -346,6 +346,18 @@ int blco_stream_mttkrp_all(const blco_layout* layout, uint64_t max_nnz_per_block
                            const blco_exec_config* cfg, int strategy, int device, double* const* outs,
                            int outs_on_device, blco_stream_report* report);
 
+/* stream_mttkrp over a FileBlockSource (streaming.hpp:45-58) without a host
+ * round trip through pageable memory: a reader thread reads each block of the
+ * .blco container at `path` into a ring of pinned host slots (num_queues + 2)
+ * while earlier blocks are copied and multiplied; read_blco_block's record
+ * checks run on the host, its per-element checks on the device on the copy
+ * that is multiplied (reference messages: "blco: bad magic",
+ * "blco: truncated payload", ...).  mode >= 0: outs[0] = M_mode; mode < 0:
+ * every mode, outs[m] (host, dims[m] x rank). */
+int blco_stream_mttkrp_file(const char* path, const double* const* factors, uint64_t rank, int mode,
+                            const blco_device_budget* budget, const blco_exec_config* cfg, int strategy,
+                            int device, double* const* outs, blco_stream_report* report);
+
 void blco_set_error(int status, const char* msg);
 
 /* Pinned host memory for stream sources (true async H2D); pageable source

@@ -166,6 +166,8 @@ SIGNATURES = {
     "blco_stream_mttkrp_all": (_I, [C.POINTER(Layout), _U64, SOURCE_FN, _P, C.POINTER(_P), _U64,
                                     C.POINTER(Budget), C.POINTER(ExecCfg), _I, _I, C.POINTER(_P), _I,
                                     C.POINTER(StreamReport)]),
+    "blco_stream_mttkrp_file": (_I, [C.c_char_p, C.POINTER(_P), _U64, _I, C.POINTER(Budget), C.POINTER(ExecCfg),
+                                     _I, _I, C.POINTER(_P), C.POINTER(StreamReport)]),
     "blco_set_error": (None, [_I, C.c_char_p]),
     "blco_host_alloc_pinned": (_P, [_U64]),
     "blco_host_free_pinned": (None, [_P]),

@@ -596,6 +596,7 @@ class FileBlockSource:
     front, one block record per iteration, each validated on the device."""
 
     def __init__(self, path, device: int = 0):
+        self.path = str(path)
         self.header = read_blco_header(path)
         self.layout = self.header.layout
         self.max_nnz_per_block = self.header.max_nnz_per_block
@@ -789,6 +790,44 @@ def stream_mttkrp_all_modes(source, f: FactorMatrices, budget: DeviceBudget,
                    block_count, device_outs)
 
 
+def _fill_report(report, r, bq, tl, cap):
+    for k in ("blocks", "bytes_streamed", "total_seconds", "transfer_busy_seconds",
+              "compute_busy_seconds", "overall_gbps", "compute_gbps", "peak_resident_bytes"):
+        setattr(report, k, getattr(r, k))
+    n = min(r.blocks, cap)
+    report.block_queue = [bq[i] for i in range(n)]
+    report.timeline = [StreamEventRec("transfer" if tl[i].kind == 0 else "compute", tl[i].queue,
+                                      tl[i].block, tl[i].begin_s, tl[i].end_s)
+                       for i in range(min(r.timeline_count, 2 * cap))]
+
+
+def _stream_file(source, f, mode, budget, config, strategy, report, device):
+    """Unconsumed FileBlockSource: the native pinned-ring file reader with
+    device-side element checks (blco_stream_mttkrp_file)."""
+    layout = source.layout
+    f.validate(layout.dims)
+    if mode is not None and (mode < 0 or mode >= layout.order()):
+        raise FormatError("stream: mode out of range")
+    fs = [_f64(a) for a in f.factors]
+    modes = range(layout.order()) if mode is None else [mode]
+    outs = [np.zeros((layout.dims[m], f.rank)) for m in modes]
+    cap = max(1, source.block_count())
+    bq = (C.c_int32 * cap)()
+    tl = (L.StreamEvent * (2 * cap))()
+    r = L.StreamReport()
+    r.block_queue, r.block_queue_capacity = C.cast(bq, C.POINTER(C.c_int32)), cap
+    r.timeline, r.timeline_capacity = C.cast(tl, C.POINTER(L.StreamEvent)), 2 * cap
+    b = L.Budget(budget.capacity_bytes, budget.num_queues, budget.reservation_bytes,
+                 budget.injected_transfer_latency_s)
+    c = config._c()
+    _check(lib.blco_stream_mttkrp_file(source.path.encode(), _ptr_array(fs), f.rank, -1 if mode is None else mode,
+                                       C.byref(b), C.byref(c), int(strategy), device, _ptr_array(outs), C.byref(r)))
+    source._left = 0
+    if report is not None:
+        _fill_report(report, r, bq, tl, cap)
+    return outs[0] if mode is not None else outs
+
+
 def _stream(source, f, mode, budget, config, strategy, report, device, layout, max_nnz_per_block, block_count,
             device_outs=None):
     config = config or ExecConfig()
@@ -800,6 +839,8 @@ def _stream(source, f, mode, budget, config, strategy, report, device, layout, m
         block_count = int(source.keys.size)
         it = iter(source.blocks)
     elif isinstance(source, FileBlockSource):
+        if source._left == source.header.block_count and device_outs is None:
+            return _stream_file(source, f, mode, budget, config, strategy, report, device)
         layout = source.layout
         max_nnz_per_block = source.max_nnz_per_block
         block_count = source.block_count()

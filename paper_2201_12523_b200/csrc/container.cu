@@ -156,6 +156,27 @@ void write_header(FILE* f, const blco_layout& l, uint64_t max_nnz, uint64_t nblo
 }
 
 }  // namespace
+
+void enqueue_block_check(const blco_layout& l, uint64_t key, const uint64_t* d_idx, uint64_t n, unsigned* d_bad,
+                         cudaStream_t s) {
+  if (!n) return;
+  const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, 148 * 16));
+  k_check_block<<<grid, 256, 0, s>>>(check_params(l, key), d_idx, n, d_bad);
+  count_launch();
+  check_launch("k_check_block");
+}
+
+void throw_block_check(unsigned bad) {
+  if (bad & 1u) throw_format("blco: re-encoded index exceeds field width");
+  if (bad & 2u) throw_format("blco: element de-linearizes outside dims");
+  if (bad & 4u) throw_format("blco: elements not in ascending ALTO order");
+}
+
+BlcoFileHeader read_blco_file_header(FILE* f) {
+  const Header h = read_header(f);
+  return BlcoFileHeader{h.version, h.layout, h.max_nnz, h.nblocks};
+}
+
 }  // namespace b200
 
 using namespace b200;

@@ -502,7 +502,7 @@ BlcoTensor load_blco(const std::filesystem::path& path) {
 }
 
 FileBlockSource::FileBlockSource(const std::filesystem::path& path)
-    : in_(std::make_unique<std::ifstream>(path, std::ios::binary)) {
+    : path_(path), in_(std::make_unique<std::ifstream>(path, std::ios::binary)) {
   if (!*in_) throw IoError("cannot open " + path.string());
   header_ = read_blco_header(*in_);
   layout_ = header_.make_layout_checked();
@@ -685,11 +685,19 @@ std::vector<DenseMatrix> stream_impl(BlockSource& source, const FactorMatrices& 
   r.block_queue_capacity = nb;
   r.timeline = tl.data();
   r.timeline_capacity = tl.size();
-  const int status =
-      mode >= 0 ? blco_stream_mttkrp(&l, source.max_nnz_per_block(), pull, &ctx, ptrs.data(), f.rank, mode, &b, &c,
-                                     static_cast<int>(strategy), current_device(), optr[0], &r)
-                : blco_stream_mttkrp_all(&l, source.max_nnz_per_block(), pull, &ctx, ptrs.data(), f.rank, &b, &c,
-                                         static_cast<int>(strategy), current_device(), optr.data(), 0, &r);
+  auto* file = dynamic_cast<FileBlockSource*>(&source);
+  int status;
+  if (file && !file->consumed()) {
+    // pinned-ring reader and device-side element checks (blco_stream_mttkrp_file)
+    status = blco_stream_mttkrp_file(file->path().c_str(), ptrs.data(), f.rank, mode, &b, &c,
+                                     static_cast<int>(strategy), current_device(), optr.data(), &r);
+  } else {
+    status = mode >= 0
+                 ? blco_stream_mttkrp(&l, source.max_nnz_per_block(), pull, &ctx, ptrs.data(), f.rank, mode, &b, &c,
+                                      static_cast<int>(strategy), current_device(), optr[0], &r)
+                 : blco_stream_mttkrp_all(&l, source.max_nnz_per_block(), pull, &ctx, ptrs.data(), f.rank, &b, &c,
+                                          static_cast<int>(strategy), current_device(), optr.data(), 0, &r);
+  }
   if (ctx.error) std::rethrow_exception(ctx.error);
   ck(status);
   if (report) {

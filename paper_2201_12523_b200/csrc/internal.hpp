@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cstdio>
 #include <cstdint>
 #include <map>
 #include <mutex>
@@ -199,6 +200,18 @@ uint64_t select_flagged(const T* in, const uint8_t* flags, uint64_t n, T* out, c
 KernelView view_of(const blco_tensor& t);
 void mttkrp_enqueue(MttkrpLaunch& a);
 void det_mttkrp_enqueue(const blco_tensor& t, MttkrpLaunch& a);
+// container.cu: .blco header and the device-side element checks of
+// read_blco_block (blco_format.cpp:201-227), asynchronous: bits are ORed
+// into *d_bad (1 field width, 2 outside dims, 4 ALTO order).
+struct BlcoFileHeader {
+  uint16_t version;
+  blco_layout layout;
+  uint64_t max_nnz, nblocks;
+};
+BlcoFileHeader read_blco_file_header(FILE* f);
+void enqueue_block_check(const blco_layout& l, uint64_t key, const uint64_t* d_idx, uint64_t n, unsigned* d_bad,
+                         cudaStream_t s);
+void throw_block_check(unsigned bad);
 // per-thread device caches (blco_release_thread_caches)
 void release_allmode_cache();
 void release_det_cache();

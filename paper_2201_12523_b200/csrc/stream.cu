@@ -13,6 +13,11 @@
 #include <algorithm>
 #include <chrono>
 #include <cstring>
+#include <fcntl.h>
+#include <unistd.h>
+
+#include <condition_variable>
+#include <deque>
 #include <thread>
 
 #include "internal.hpp"
@@ -77,11 +82,39 @@ bool is_pinned(const void* p) {
   return a.type == cudaMemoryTypeHost;
 }
 
+// Where blocks come from: the caller's pull callback (BlockSource::next) or
+// the native .blco file reader below.
+struct BlockFeed {
+  virtual ~BlockFeed() = default;
+  // 1 = a block in *v, 0 = end of stream; errors throw Status
+  virtual int next(blco_block_view& v) = 0;
+  // the host->device copy of block `ordinal` is complete once `done` fires
+  virtual void transferred(uint64_t ordinal, cudaEvent_t done) {
+    (void)ordinal;
+    (void)done;
+  }
+  // run read_blco_block's element checks on the transferred copy
+  virtual bool validate() const { return false; }
+  // the engine is done pulling (called before it releases its events)
+  virtual void finish() {}
+};
+
+struct CallbackFeed final : BlockFeed {
+  blco_block_source_fn fn;
+  void* ctx;
+  CallbackFeed(blco_block_source_fn f, void* c) : fn(f), ctx(c) {}
+  int next(blco_block_view& v) override {
+    const int r = fn(ctx, &v);
+    if (r < 0) throw Status(-r, blco_last_error());
+    return r;
+  }
+};
+
 // Streams the blocks once and runs MTTKRP for every mode in modes[] on each
 // resident block (one mode: stream_mttkrp; all modes: the all-mode
 // extension, which moves the tensor over the host link once per iteration).
-void stream_impl(const blco_layout* layout, uint64_t max_nnz_per_block, blco_block_source_fn next,
-                 void* ctx, const double* const* factors, uint64_t rank, const std::vector<int>& modes,
+void stream_impl(const blco_layout* layout, uint64_t max_nnz_per_block, BlockFeed& feed,
+                 const double* const* factors, uint64_t rank, const std::vector<int>& modes,
                  const blco_device_budget* budget, const blco_exec_config* cfg, int strategy_in,
                  int device, double* const* outs, bool outs_on_device, blco_stream_report* report) {
   {
@@ -158,15 +191,15 @@ void stream_impl(const blco_layout* layout, uint64_t max_nnz_per_block, blco_blo
     std::vector<Interval> timeline;
     std::vector<int32_t> block_queue;
     std::vector<double> sleep_arg(1, budget->injected_transfer_latency_s);
+    DevBuf<unsigned> dbad(1);  // read_blco_block check bits of file-fed blocks
+    B200_CUDA(cudaMemset(dbad.ptr, 0, sizeof(unsigned)));
     uint64_t ordinal = 0, bytes = 0;
     std::string err;
     int err_code = BLCO_OK;
     try {
       for (;;) {
         blco_block_view bv{};
-        const int r = next(ctx, &bv);
-        if (r < 0) throw Status(-r, blco_last_error());
-        if (r == 0) break;
+        if (feed.next(bv) == 0) break;
         const uint64_t bbytes = bv.nnz * (sizeof(uint64_t) + sizeof(double));
         if (bbytes > reservation)
           throw_format("stream: block " + std::to_string(ordinal) + " (" + std::to_string(bbytes) +
@@ -210,6 +243,8 @@ void stream_impl(const blco_layout* layout, uint64_t max_nnz_per_block, blco_blo
         if (budget->injected_transfer_latency_s > 0)
           B200_CUDA(cudaLaunchHostFunc(q.stream, host_sleep, sleep_arg.data()));
         B200_CUDA(cudaEventRecord(tr.e, q.stream));
+        feed.transferred(ordinal, tr.e);
+        if (feed.validate()) enqueue_block_check(l, bv.key, q.idx.ptr, bv.nnz, dbad.ptr, q.stream);
         // a transient source buffer may be overwritten by the next pull
         if (bv.nnz && !(bv.flags & BLCO_BLOCK_STABLE) && (!is_pinned(bv.idx) || !is_pinned(bv.vals)))
           B200_CUDA(cudaEventSynchronize(tr.e));
@@ -244,6 +279,17 @@ void stream_impl(const blco_layout* layout, uint64_t max_nnz_per_block, blco_blo
       err_code = s.code;
     }
     for (auto& q : qs) B200_CUDA(cudaStreamSynchronize(q.stream));
+    feed.finish();
+    if (err_code == BLCO_OK && feed.validate()) {
+      unsigned bad = 0;
+      B200_CUDA(cudaMemcpy(&bad, dbad.ptr, sizeof bad, cudaMemcpyDeviceToHost));
+      try {
+        throw_block_check(bad);
+      } catch (const Status& s) {
+        err = s.what();
+        err_code = s.code;
+      }
+    }
     if (err_code != BLCO_OK) {
       for (auto& iv : timeline) cudaEventDestroy(iv.b), cudaEventDestroy(iv.e);
       for (auto& q : qs) cudaStreamDestroy(q.stream);
@@ -304,6 +350,192 @@ void stream_impl(const blco_layout* layout, uint64_t max_nnz_per_block, blco_blo
   }
 }
 
+// Native FileBlockSource (streaming.hpp:45-58, streaming.cpp:13-31): a
+// reader thread reads each block record of a .blco container straight into a
+// ring of pinned host slots while earlier blocks are copied and multiplied; a
+// slot is refilled only after the engine reports that the copy of the block
+// it held has completed.  read_blco_block's record checks (key range, empty
+// record, capacity, ascending keys; blco_format.cpp:201-238) run here, its
+// per-element checks on the device on the transferred copy -- the block
+// crosses the link once.
+class FileFeed final : public BlockFeed {
+ public:
+  FileFeed(const char* path, int device, int nslots) : device_(device), slots_(nslots) {
+    f_ = std::fopen(path, "rb");
+    if (!f_) throw Status(BLCO_EIO, std::string("cannot open ") + path);
+    try {
+      h_ = read_blco_file_header(f_);
+    } catch (...) {
+      std::fclose(f_);
+      throw;
+    }
+    fd_ = ::open(path, O_RDONLY);
+    if (fd_ < 0) {
+      std::fclose(f_);
+      throw Status(BLCO_EIO, std::string("cannot open ") + path);
+    }
+    pos_ = 4 + 2 + 2 + 8 * static_cast<uint64_t>(h_.layout.order) + 2 + 2 * static_cast<uint64_t>(h_.layout.order) +
+           8 + 8;
+    const unsigned hw = std::thread::hardware_concurrency();
+    readers_ = static_cast<int>(std::max(1u, std::min(8u, hw / 2)));
+    done_.assign(nslots, nullptr);
+    done_ordinal_.assign(nslots, ~uint64_t{0});
+    th_ = std::thread([this] { run(); });
+  }
+  ~FileFeed() override {
+    finish();
+    for (auto& sl : slots_)
+      if (sl.mem) cudaFreeHost(sl.mem);
+    if (fd_ >= 0) ::close(fd_);
+    if (f_) std::fclose(f_);
+  }
+  const BlcoFileHeader& header() const { return h_; }
+
+  int next(blco_block_view& v) override {
+    std::unique_lock<std::mutex> lk(mu_);
+    cv_.wait(lk, [&] { return !ready_.empty() || finished_; });
+    if (!ready_.empty()) {
+      v = ready_.front();
+      ready_.pop_front();
+      return 1;
+    }
+    if (err_code_ != BLCO_OK) throw Status(err_code_, err_);
+    return 0;
+  }
+  void transferred(uint64_t ordinal, cudaEvent_t done) override {
+    std::lock_guard<std::mutex> lk(mu_);
+    const size_t k = ordinal % slots_.size();
+    done_[k] = done;
+    done_ordinal_[k] = ordinal;
+    cv_.notify_all();
+  }
+  bool validate() const override { return true; }
+  void finish() override {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+      cv_.notify_all();
+    }
+    if (th_.joinable()) th_.join();
+  }
+
+ private:
+  struct Slot {
+    void* mem = nullptr;
+    size_t cap = 0;
+  };
+
+  bool read_at(void* dst, size_t bytes, uint64_t off) const {
+    auto* p = static_cast<char*>(dst);
+    while (bytes) {
+      const ssize_t r = ::pread(fd_, p, bytes, static_cast<off_t>(off));
+      if (r <= 0) return false;
+      p += r, off += static_cast<uint64_t>(r), bytes -= static_cast<size_t>(r);
+    }
+    return true;
+  }
+  bool read_parallel(void* dst, size_t bytes, uint64_t off) const {
+    const size_t piece = (bytes + readers_ - 1) / readers_;
+    if (readers_ == 1 || bytes < (size_t{8} << 20)) return read_at(dst, bytes, off);
+    std::vector<std::thread> th;
+    std::vector<char> ok(readers_, 0);
+    for (int i = 0; i < readers_; ++i) {
+      const size_t b = piece * i, e = std::min(bytes, b + piece);
+      if (b >= e) {
+        ok[i] = 1;
+        continue;
+      }
+      th.emplace_back([&, i, b, e] { ok[i] = read_at(static_cast<char*>(dst) + b, e - b, off + b); });
+    }
+    for (auto& t : th) t.join();
+    for (char x : ok)
+      if (!x) return false;
+    return true;
+  }
+
+  void fail(int code, const std::string& msg) {
+    std::lock_guard<std::mutex> lk(mu_);
+    err_code_ = code;
+    err_ = msg;
+    finished_ = true;
+    cv_.notify_all();
+  }
+
+  void run() {
+    try {
+      B200_CUDA(cudaSetDevice(device_));
+      const size_t K = slots_.size();
+      const blco_layout& l = h_.layout;
+      uint64_t prev_key = 0;
+      for (uint64_t b = 0; b < h_.nblocks; ++b) {
+        const size_t k = b % K;
+        if (b >= K) {  // the slot's previous block (b - K) must have crossed the link
+          cudaEvent_t ev = nullptr;
+          {
+            std::unique_lock<std::mutex> lk(mu_);
+            cv_.wait(lk, [&] { return stop_ || done_ordinal_[k] == b - K; });
+            if (stop_) return;
+            ev = done_[k];
+          }
+          B200_CUDA(cudaEventSynchronize(ev));
+        }
+        uint64_t rec[2];
+        if (!read_at(rec, 16, pos_)) throw Status(BLCO_EIO, "blco: truncated payload");
+        pos_ += 16;
+        const uint64_t key = rec[0], n = rec[1];
+        if (l.stripped_bits < 64 && key >= (uint64_t{1} << l.stripped_bits))
+          throw_format("blco: block key out of range");
+        if (n == 0) throw_format("blco: empty block record");
+        if (n > h_.max_nnz) throw_format("blco: block exceeds max_nnz_per_block");
+        if (b > 0 && key < prev_key) throw_format("blco: blocks not in ascending key order");
+        prev_key = key;
+        Slot& sl = slots_[k];
+        if (sl.cap < n * 16) {
+          if (sl.mem) cudaFreeHost(sl.mem);
+          sl.mem = nullptr;
+          sl.cap = 0;
+          B200_CUDA(cudaHostAlloc(&sl.mem, n * 16, cudaHostAllocPortable));
+          sl.cap = n * 16;
+        }
+        auto* idx = static_cast<uint64_t*>(sl.mem);
+        auto* vals = reinterpret_cast<double*>(idx + n);
+        // the record's idx[n] | vals[n] are contiguous in the file and in the
+        // slot: one range, read by `readers_` threads in parallel (pread)
+        if (!read_parallel(sl.mem, n * 16, pos_)) throw Status(BLCO_EIO, "blco: truncated payload");
+        pos_ += n * 16;
+        std::lock_guard<std::mutex> lk(mu_);
+        if (stop_) return;
+        ready_.push_back(blco_block_view{key, n, idx, vals, BLCO_BLOCK_STABLE});
+        cv_.notify_all();
+      }
+      std::lock_guard<std::mutex> lk(mu_);
+      finished_ = true;
+      cv_.notify_all();
+    } catch (const Status& s) {
+      fail(s.code, s.what());
+    } catch (const std::exception& e) {
+      fail(BLCO_ERROR, e.what());
+    }
+  }
+
+  FILE* f_ = nullptr;
+  int fd_ = -1;
+  uint64_t pos_ = 0;  // file offset of the next block record
+  int readers_ = 1;
+  BlcoFileHeader h_{};
+  int device_;
+  std::vector<Slot> slots_;
+  std::vector<cudaEvent_t> done_;
+  std::vector<uint64_t> done_ordinal_;
+  std::mutex mu_;
+  std::condition_variable cv_;
+  std::deque<blco_block_view> ready_;
+  bool finished_ = false, stop_ = false;
+  int err_code_ = BLCO_OK;
+  std::string err_;
+  std::thread th_;
+};
+
 }  // namespace
 }  // namespace b200
 
@@ -316,8 +548,9 @@ extern "C" int blco_stream_mttkrp(const blco_layout* layout, uint64_t max_nnz_pe
                                   int strategy, int device, double* out,
                                   blco_stream_report* report) {
   return guarded([&] {
-    stream_impl(layout, max_nnz_per_block, next, ctx, factors, rank, std::vector<int>{mode}, budget, cfg,
-                strategy, device, &out, false, report);
+    CallbackFeed feed(next, ctx);
+    stream_impl(layout, max_nnz_per_block, feed, factors, rank, std::vector<int>{mode}, budget, cfg, strategy,
+                device, &out, false, report);
   });
 }
 
@@ -331,8 +564,29 @@ extern "C" int blco_stream_mttkrp_all(const blco_layout* layout, uint64_t max_nn
     if (!layout) throw_format("stream: null layout");
     std::vector<int> modes(layout->order);
     for (int m = 0; m < layout->order; ++m) modes[m] = m;
-    stream_impl(layout, max_nnz_per_block, next, ctx, factors, rank, modes, budget, cfg, strategy, device,
-                outs, outs_on_device != 0, report);
+    CallbackFeed feed(next, ctx);
+    stream_impl(layout, max_nnz_per_block, feed, factors, rank, modes, budget, cfg, strategy, device, outs,
+                outs_on_device != 0, report);
+  });
+}
+
+extern "C" int blco_stream_mttkrp_file(const char* path, const double* const* factors, uint64_t rank, int mode,
+                                       const blco_device_budget* budget, const blco_exec_config* cfg, int strategy,
+                                       int device, double* const* outs, blco_stream_report* report) {
+  return guarded([&] {
+    if (!path) throw Status(BLCO_EIO, "cannot open (null path)");
+    if (budget->num_queues < 1) throw_format("stream: num_queues must be >= 1");
+    DeviceGuard dg(device);
+    FileFeed feed(path, device, budget->num_queues + 2);
+    const blco_layout& l = feed.header().layout;
+    std::vector<int> modes;
+    if (mode >= 0) {
+      modes.push_back(mode);
+    } else {
+      for (int m = 0; m < l.order; ++m) modes.push_back(m);
+    }
+    stream_impl(&l, feed.header().max_nnz, feed, factors, rank, modes, budget, cfg, strategy, device, outs, false,
+                report);
   });
 }
 

@@ -122,3 +122,65 @@ def test_cpp_file_source_matches(gpu):
     """FileBlockSource / save_blco / load_blco are also exercised through the
     C++ drop-in suite (tests/cpp/test_api.cpp, test_gpu_cxx.py)."""
     assert hasattr(gpu, "FileBlockSource")
+
+
+@pytest.mark.parametrize("queues", [1, 3])
+def test_native_file_stream_all_modes(gpu, oracle, tmp_path, queues):
+    """blco_stream_mttkrp_file: the .blco blocks are read into pinned ring
+    slots by a reader thread and cross the link once; every mode against
+    the oracle, and a per-mode call through the same path."""
+    dims = [60, 45, 70]
+    coo = gpu.synth_uniform_host(dims, 5000, 11)
+    t = gpu.build_blco(coo, 12, 300)
+    assert t.keys.size > 4
+    p = tmp_path / "n.blco"
+    gpu.save_blco(t, p)
+    f = gpu.FactorMatrices.random(dims, 8, 3)
+    budget = gpu.DeviceBudget(capacity_bytes=1 << 26, num_queues=queues, reservation_bytes=300 * 16)
+    rep = gpu.StreamReport()
+    got = gpu.stream_mttkrp_all_modes(gpu.FileBlockSource(p), f, budget, report=rep)
+    for m in range(3):
+        assert rel_frobenius(got[m], oracle.mttkrp_coo(dims, coo.indices, coo.values, f.factors, m)) <= 1e-12
+    assert rep.blocks == t.keys.size and rep.bytes_streamed == t.total_nnz * 16
+    assert rep.block_queue == [i % queues for i in range(t.keys.size)]
+    one = gpu.stream_mttkrp(gpu.FileBlockSource(p), f, 1, budget)
+    assert rel_frobenius(one, got[1]) <= 1e-12
+
+
+@pytest.mark.parametrize("case", ["truncated", "field_width", "order", "outside", "key_order"])
+def test_native_file_stream_rejects_corruption(gpu, tmp_path, case):
+    """read_blco_block's checks on the streamed path: record checks on the
+    host reader, element checks on the device copy (same messages)."""
+    dims = [3, 4, 4] if case == "outside" else [4, 4, 4]
+    if case == "outside":
+        t = gpu.build_blco(gpu.SparseTensorCoo(dims, np.array([[0, 2], [1, 3], [2, 3]], np.uint64), [1.0, 2.0]), 64)
+    else:
+        t = gpu.build_blco(gpu.SparseTensorCoo(dims, GI, GV), 5, 6)
+    p = tmp_path / "c.blco"
+    gpu.save_blco(t, p)
+    b = bytearray(p.read_bytes())
+    first = 4 + 2 + 2 + 3 * 8 + 2 + 3 * 2 + 8 + 8 + 16
+    if case == "truncated":
+        b = b[:-5]
+        err, msg = gpu.IoError, "truncated"
+    elif case == "field_width":
+        b[first] = 0xFF
+        err, msg = gpu.FormatError, "field width"
+    elif case == "order":
+        i0, i1 = struct.unpack_from("<QQ", b, first)
+        struct.pack_into("<QQ", b, first, i1, i0)
+        err, msg = gpu.FormatError, "ascending ALTO order"
+    elif case == "outside":
+        struct.pack_into("<Q", b, first + 8, 3)
+        err, msg = gpu.FormatError, "outside dims"
+    else:  # second block's key below the first's
+        n0 = struct.unpack_from("<Q", b, first - 8)[0]
+        second = first + 16 * n0
+        struct.pack_into("<Q", b, first - 16, 1)  # block 0 key 1
+        struct.pack_into("<Q", b, second, 0)      # block 1 key 0
+        err, msg = gpu.FormatError, "ascending key order"
+    p.write_bytes(bytes(b))
+    f = gpu.FactorMatrices.random(dims, 2, 1)
+    budget = gpu.DeviceBudget(capacity_bytes=1 << 24, num_queues=2, reservation_bytes=1 << 16)
+    with pytest.raises(err, match=msg):
+        gpu.stream_mttkrp(gpu.FileBlockSource(p), f, 0, budget)
