@@ -18,6 +18,8 @@
 
 #include <condition_variable>
 #include <deque>
+#include <map>
+#include <tuple>
 #include <thread>
 
 #include "internal.hpp"
@@ -350,6 +352,40 @@ void stream_impl(const blco_layout* layout, uint64_t max_nnz_per_block, BlockFee
   }
 }
 
+// Pinned host slots of the file reader, kept for the next call: pinning
+// gigabytes (cudaHostAlloc) costs seconds, far more than the read it serves.
+class PinnedPool {
+ public:
+  static PinnedPool& get() {
+    static PinnedPool* p = new PinnedPool;  // never destroyed: freed with the process
+    return *p;
+  }
+  // a buffer of at least `bytes` (the largest free one that fits, else new)
+  std::pair<void*, size_t> take(size_t bytes) {
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      auto it = free_.lower_bound(bytes);
+      if (it != free_.end()) {
+        auto r = std::make_pair(it->second, it->first);
+        free_.erase(it);
+        return r;
+      }
+    }
+    void* mem = nullptr;
+    B200_CUDA(cudaHostAlloc(&mem, bytes, cudaHostAllocPortable));
+    return {mem, bytes};
+  }
+  void give(void* mem, size_t bytes) {
+    if (!mem) return;
+    std::lock_guard<std::mutex> g(mu_);
+    free_.emplace(bytes, mem);
+  }
+
+ private:
+  std::mutex mu_;
+  std::multimap<size_t, void*> free_;
+};
+
 // Native FileBlockSource (streaming.hpp:45-58, streaming.cpp:13-31): a
 // reader thread reads each block record of a .blco container straight into a
 // ring of pinned host slots while earlier blocks are copied and multiplied; a
@@ -384,8 +420,7 @@ class FileFeed final : public BlockFeed {
   }
   ~FileFeed() override {
     finish();
-    for (auto& sl : slots_)
-      if (sl.mem) cudaFreeHost(sl.mem);
+    for (auto& sl : slots_) PinnedPool::get().give(sl.mem, sl.cap);
     if (fd_ >= 0) ::close(fd_);
     if (f_) std::fclose(f_);
   }
@@ -491,11 +526,13 @@ class FileFeed final : public BlockFeed {
         prev_key = key;
         Slot& sl = slots_[k];
         if (sl.cap < n * 16) {
-          if (sl.mem) cudaFreeHost(sl.mem);
+          PinnedPool::get().give(sl.mem, sl.cap);
           sl.mem = nullptr;
           sl.cap = 0;
-          B200_CUDA(cudaHostAlloc(&sl.mem, n * 16, cudaHostAllocPortable));
-          sl.cap = n * 16;
+          // at least this block, rounded up to 64 MiB so a slot is not
+          // regrown for every slightly larger block
+          const size_t want = ((n * 16 + (size_t{64} << 20) - 1) >> 26) << 26;
+          std::tie(sl.mem, sl.cap) = PinnedPool::get().take(std::max<size_t>(n * 16, std::min(want, h_.max_nnz * 16)));
         }
         auto* idx = static_cast<uint64_t*>(sl.mem);
         auto* vals = reinterpret_cast<double*>(idx + n);
