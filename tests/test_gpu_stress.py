@@ -1,0 +1,52 @@
+"""Randomised cross-path parity on the device: many small tensors of random
+order, shape, density, rank and block capacity, every MTTKRP path (register,
+hierarchical, deterministic, fp32, the all-mode host pipeline, all-mode
+streaming) against the oracle.  Targets the edge cases of the kernels' lane
+group split, tail batches and packed staging (ranges shorter than a batch,
+single-element blocks, order 1, unit-length modes, ranks around the lane
+widths)."""
+import numpy as np
+import pytest
+
+from conftest import rel_frobenius
+
+pytestmark = pytest.mark.gpu
+
+CASES = 150
+
+
+def _case(seed):
+    rng = np.random.default_rng(1000 + seed)
+    order = int(rng.integers(1, 9))
+    hi = {1: 5000, 2: 400, 3: 90}.get(order, 16)
+    dims = [int(x) for x in rng.integers(1, hi, size=order)]
+    cells = int(np.prod(dims))
+    nnz = int(min(cells, rng.integers(1, 6000)))
+    rank = int(rng.choice([1, 2, 3, 8, 15, 16, 17, 31, 32, 33, 64, 65]))
+    total_bits = sum(int(d - 1).bit_length() for d in dims)
+    target = int(rng.integers(max(1, total_bits - 6), 65)) if total_bits > 1 else 64
+    cap = int(rng.choice([1, 7, 64, 1000, 1 << 27]))
+    return dims, nnz, rank, target, cap
+
+
+@pytest.mark.parametrize("seed", range(CASES))
+def test_random_paths_match_oracle(gpu, oracle, seed):
+    dims, nnz, rank, target, cap = _case(seed)
+    coo = gpu.synth_uniform_host(dims, nnz, seed)
+    f = gpu.FactorMatrices.random(dims, rank, seed + 1)
+    t = gpu.build_blco(coo, target, cap)
+    want = [oracle.mttkrp_coo(dims, coo.indices, coo.values, f.factors, m) for m in range(len(dims))]
+    ctx = (dims, nnz, rank, target, cap)
+    for m in range(len(dims)):
+        for strat in (gpu.Strategy.Register, gpu.Strategy.Hierarchical):
+            assert rel_frobenius(gpu.mttkrp(t, f, m, strategy=strat), want[m]) <= 1e-12, (ctx, m, strat)
+        assert rel_frobenius(gpu.mttkrp(t, f, m, gpu.ExecConfig(deterministic=True)), want[m]) <= 1e-12, (ctx, m)
+        assert rel_frobenius(gpu.mttkrp_f32(t, f, m), want[m]) <= 1e-5, (ctx, m, "fp32")
+    got = gpu.mttkrp_all_modes(t, f, chunk_elems=int(np.random.default_rng(seed).integers(1, 3000)))
+    for m in range(len(dims)):
+        assert rel_frobenius(got[m], want[m]) <= 1e-12, (ctx, m, "all-modes")
+    res = min(cap, nnz) * 16
+    b = gpu.DeviceBudget(capacity_bytes=1 << 28, num_queues=2, reservation_bytes=max(res, 16))
+    got = gpu.stream_mttkrp_all_modes(t, f, b)
+    for m in range(len(dims)):
+        assert rel_frobenius(got[m], want[m]) <= 1e-12, (ctx, m, "stream")
