@@ -50,3 +50,34 @@ def test_random_paths_match_oracle(gpu, oracle, seed):
     got = gpu.stream_mttkrp_all_modes(t, f, b)
     for m in range(len(dims)):
         assert rel_frobenius(got[m], want[m]) <= 1e-12, (ctx, m, "stream")
+
+
+@pytest.mark.parametrize("seed", range(60))
+def test_random_builds_bit_exact(gpu, oracle, seed):
+    """Device build_blco against the C restatement of build_blco on random
+    shapes, including layouts wider than 64 bits (two-word sort, multi-key
+    blocking) and tiny block capacities: keys, offsets, indices, values and
+    the batch table bit-exact."""
+    rng = np.random.default_rng(7000 + seed)
+    order = int(rng.integers(1, 7))
+    wide = seed % 3 == 0
+    hi = (1 << 20) if wide else 3000
+    dims = [int(x) for x in rng.integers(1, hi, size=order)]
+    nnz = int(rng.integers(1, 20_000))
+    if np.prod(np.array(dims, dtype=object)) < 2 ** 64:
+        nnz = int(min(nnz, int(np.prod(np.array(dims, dtype=object)))))
+        coo = gpu.synth_uniform_host(dims, nnz, seed)
+    else:  # cell space beyond 2^64: the first nnz distinct uniform draws
+        idx0, vals0 = oracle.synth_draws(dims, nnz, seed, 1)
+        coo = gpu.SparseTensorCoo(dims, idx0, vals0)
+    total_bits = sum(int(d - 1).bit_length() for d in dims)
+    lo = max(1, total_bits - 64, min(64, total_bits - 12))  # stripped bits <= 64 (device limit)
+    if lo > 64 or total_bits > 128:
+        pytest.skip("layout beyond the device's 64-bit block key")
+    target = int(rng.integers(lo, 65))
+    cap = int(rng.choice([1, 5, 100, 1 << 27]))
+    t = gpu.build_blco(coo, target, cap)
+    keys, offs, idx, vals = oracle.build(dims, coo.indices, coo.values, target, cap)
+    assert np.array_equal(t.keys, keys) and np.array_equal(t.offsets, offs)
+    assert np.array_equal(t.idx, idx) and np.array_equal(t.vals, vals)
+    assert np.array_equal(t.batch_table, oracle.batch_table(np.diff(offs), 512))
