@@ -262,8 +262,18 @@ def run_ours(args, world, rank_id, local):
 
     fac = [torch.empty((d, R), dtype=torch.float64, device=f"cuda:{dev}") for d in dims]
     b.factors_random_device(dims, R, FACTOR_SEED, [a.data_ptr() for a in fac], sptr)
-    outs = [torch.empty((d, R), dtype=torch.float64, device=f"cuda:{dev}") for d in dims]
     fptr = [a.data_ptr() for a in fac]
+    rs = world > 1 and args.reduce == "reducescatter"
+    if rs:
+        # one reduce-scatter per mode leaves rank g with its row
+        # block of M_n; partials padded to world * ceil(I_n / world) rows
+        from paper_2201_12523_b200.dist import Collectives, row_shard
+        coll = Collectives()
+        pads = [row_shard(d, world, rank_id)[2] for d in dims]
+        outs = [torch.empty((world * p, R), dtype=torch.float64, device=f"cuda:{dev}") for p in pads]
+        shards = [torch.empty((p, R), dtype=torch.float64, device=f"cuda:{dev}") for p in pads]
+    else:
+        outs = [torch.empty((d, R), dtype=torch.float64, device=f"cuda:{dev}") for d in dims]
     strategy = b.Strategy[args.strategy]
     cfg = b.ExecConfig(num_compute_units=torch.cuda.get_device_properties(dev).multi_processor_count)
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{dev}")
@@ -278,7 +288,13 @@ def run_ours(args, world, rank_id, local):
             dt.mttkrp_device(fptr, R, m, outs[m].data_ptr(), strategy, cfg, accumulate=True, stream=sptr)
             if ev is not None:
                 ev[m][1].record(stream)
-            if world > 1:
+            if rs:
+                # rank g's rows of M_m reduced on NCCL's stream while the mode
+                # m+1 kernel runs (outputs are disjoint buffers)
+                w = coll.reduce_scatter(shards[m], outs[m], async_op=True)
+                if w is not None:
+                    works.append(w)
+            elif world > 1:
                 # partial M_m summed over ranks on NCCL's stream while the
                 # mode m+1 kernel runs (outputs are disjoint buffers)
                 import torch.distributed as dist
@@ -364,7 +380,10 @@ def run_ours(args, world, rank_id, local):
         "config": {"workload": desc, "dims": dims, "nnz": nnz, "rank": R, "modes": N,
                    "tensor_seed": TENSOR_SEED, "factor_seed": FACTOR_SEED, "strategy": args.strategy,
                    "l2": "flushed between steps (512 MiB write, outside the timed events)",
-                   "parallelism": f"span partition x{world}" + (" + NCCL all-reduce of M per mode, overlapped with the next mode's kernel" if world > 1 else ""),
+                   "parallelism": f"span partition x{world}" + (
+                       (" + NCCL reduce-scatter of M per mode (row shards), overlapped with the next mode's kernel"
+                        if rs else " + NCCL all-reduce of M per mode, overlapped with the next mode's kernel")
+                       if world > 1 else ""),
                    "bytes_per_elem_per_mode": bpe},
         "per_mode_ms": [round(statistics.mean(x), 4) for x in mode_ms],
         "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
@@ -388,7 +407,12 @@ def run_ours(args, world, rank_id, local):
             ref = torch.zeros((dims[m], R), dtype=torch.float64, device=f"cuda:{dev}")
             full.mttkrp_device(fptr, R, m, ref.data_ptr(), strategy, cfg, stream=sptr)
             torch.cuda.synchronize()
-            errs.append(float(torch.linalg.norm(outs[m] - ref) / torch.linalg.norm(ref)))
+            got = outs[m]
+            if rs:  # gather the row shards back into the whole M_m
+                got = torch.empty_like(outs[m])
+                coll.all_gather(got, shards[m])
+                got = got[: dims[m]]
+            errs.append(float(torch.linalg.norm(got - ref) / torch.linalg.norm(ref)))
         result["check"] = {"rel_frobenius_vs_single_device": errs, "ranks": world}
     if not args.no_e2e:
         result["e2e"] = e2e_run(b, torch, dt, dims, R, N, nnz, args, dev, world)
@@ -522,49 +546,85 @@ ALS_CONFIGS = {
     "delicious_als": ([532924, 17262471, 2480308, 1443], 140_126_181, 16, 4,
                       "synthetic Delicious-shaped 532924x17262471x2480308x1443, 140,126,181 nnz, "
                       "power-law draws floor(I*u^4), R=16, CP-ALS 10 iterations (BASELINE configs[3])"),
+    # small 4-mode case for the multi-rank tests (not a BASELINE config)
+    "als_tiny": ([3000, 4000, 2500, 60], 400_000, 16, 2,
+                 "synthetic 4-mode 3000x4000x2500x60, 400,000 nnz, power-law draws floor(I*u^2), R=16, "
+                 "CP-ALS 10 iterations (test case)"),
     "enron_als": ([6066, 5699, 244268, 1176], 54_202_099, 16, 4,
                   "synthetic Enron-shaped 6066x5699x244268x1176, 54,202,099 nnz, power-law draws floor(I*u^4), "
                   "R=16, CP-ALS 10 iterations"),
 }
 
 
-def run_cpals(args):
-    """CP-ALS (proj/src/cpals.cpp:66-111) with every step on the device."""
+def run_cpals(args, world=1, rank_id=0, local=0):
+    """CP-ALS (proj/src/cpals.cpp:66-111) with every step on the device.  With
+    N > 1 ranks: the distributed driver (paper_2201_12523_b200.dist)
+    on contiguous span ranges -- reduce-scatter of M_n, local row-block solve,
+    all-reduce of the R x R Gram, all-gather of A_n."""
     import torch
 
     import paper_2201_12523_b200 as b
 
     dims, nnz, R, skew, desc = ALS_CONFIGS[args.config]
     N = len(dims)
-    torch.cuda.set_device(0)
+    dev = local
+    torch.cuda.set_device(dev)
+    if world > 1:
+        dist_init(torch, dev)
     bst = b.BuildStats()
     t0 = time.perf_counter()
-    dt = b.DeviceTensor.synthetic_draws(dims, nnz, TENSOR_SEED, skew, 64, 1 << 27, 0, bst)
+    full = b.DeviceTensor.synthetic_draws(dims, nnz, TENSOR_SEED, skew, 64, 1 << 27, dev, bst)
     build_s = time.perf_counter() - t0
-    cfg = b.ExecConfig(num_compute_units=torch.cuda.get_device_properties(0).multi_processor_count)
+    if world > 1:
+        lo, hi = b.partition(full.block_nnz(), 1024, world)[rank_id]
+        dt = full.slice(lo, hi, dev)
+        if not args.check:
+            del full
+    else:
+        dt = full
+    cfg = b.ExecConfig(num_compute_units=torch.cuda.get_device_properties(dev).multi_processor_count)
     iters = 10
-    b.cp_als(dt, b.CpAlsOptions(rank=R, max_iters=2, tol=-1e300, seed=FACTOR_SEED), cfg)  # warm-up
+    opts = lambda n: b.CpAlsOptions(rank=R, max_iters=n, tol=-1e300, seed=FACTOR_SEED)  # noqa: E731
+    if world > 1:
+        from paper_2201_12523_b200.dist import cp_als_distributed
+        als = lambda n, timing=False: cp_als_distributed(dt, dims, opts(n), cfg, timing=timing)  # noqa: E731
+    else:
+        als = lambda n, timing=False: b.cp_als(dt, opts(n), cfg)  # noqa: E731
+    als(2)  # warm-up
     torch.cuda.synchronize()
 
     def timed(n):
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        m = b.cp_als(dt, b.CpAlsOptions(rank=R, max_iters=n, tol=-1e300, seed=FACTOR_SEED), cfg)
+        m = als(n, True)
         e1.record()
         torch.cuda.synchronize()
         return m, e0.elapsed_time(e1)
 
     launches0 = b.kernel_launch_count()
-    with ClockSampler(0) as clk:
+    with ClockSampler(dev) as clk:
         model, ms_total = timed(iters)
         _, ms_two = timed(2)
-    # per-iteration device time of the ALS loop (CUDA events inside the C ABI
-    # around every iteration: N MTTKRPs + solve/normalise/Gram + fit); the
-    # call's fixed costs (allocation, init, final D2H of factors) excluded
+    # per-iteration device time of the ALS loop (CUDA events around every
+    # iteration: N MTTKRPs + solve/normalise/Gram + fit, and with N > 1 the
+    # collectives); the call's fixed costs (allocation, init, |X|^2, initial
+    # Grams, final copies) excluded.  Max over ranks.
     ms_iter = model.device_ms["iterations_ms"] / model.device_ms["iterations"]
+    ms_mt = model.device_ms["mttkrp_ms"] / iters
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms_iter, ms_mt], dtype=torch.float64, device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_iter, ms_mt = float(t[0]), float(t[1])
     # MTTKRP alone on the final factors: per-mode kernel time (roofline)
-    fac = [torch.from_numpy(a).cuda() for a in model.factors.factors]
-    outs = [torch.empty((d, R), dtype=torch.float64, device="cuda") for d in dims]
+    if world > 1:
+        fac = [a.contiguous() for a in model.factors]
+    else:
+        fac = [torch.from_numpy(a).cuda(dev) for a in model.factors.factors]
+    outs = [torch.empty((d, R), dtype=torch.float64, device=f"cuda:{dev}") for d in dims]
     sptr = torch.cuda.current_stream().cuda_stream
     for _ in range(3):
         for m in range(N):
@@ -579,32 +639,52 @@ def run_cpals(args):
         torch.cuda.synchronize()
         mode_ms.append(a0.elapsed_time(a1) / 5)
     bpe = bytes_per_elem(N, R)
-    mttkrp_gbps = nnz * N * bpe / (sum(mode_ms) * 1e-3) / 1e9
+    mttkrp_gbps = dt.nnz * N * bpe / (sum(mode_ms) * 1e-3) / 1e9
     peaks = {}
     try:
         peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
     except (OSError, ValueError):
         pass
     peak = peaks.get("hbm_gbs") or 6650.0
+    launches = b.kernel_launch_count() - launches0
+    check = None
+    if args.check and world > 1:
+        # the distributed run against single-device cp_als of the whole tensor
+        one = b.cp_als(full, opts(iters), cfg)
+        fdiff = max(abs(x - y) for x, y in zip(model.fit_history, one.fit_history))
+        ferr = [float(np.linalg.norm(a.cpu().numpy() - f) / np.linalg.norm(f))
+                for a, f in zip(model.factors, one.factors.factors)]
+        check = {"max_abs_fit_diff_vs_single_device": fdiff, "factor_rel_frobenius": ferr,
+                 "lambda_rel": float(np.linalg.norm(model.lambda_ - one.lambda_) / np.linalg.norm(one.lambda_)),
+                 "ranks": world}
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank_id != 0:
+        return
     print(json.dumps({
         "metric": "CP-ALS time per iteration (N MTTKRPs + device Gram/solve/normalise + fit)",
-        "value": round(ms_iter, 3), "unit": "ms", "n_gpus": 1, "steps": iters, "warmup": 2,
+        "value": round(ms_iter, 3), "unit": "ms", "n_gpus": world, "steps": iters, "warmup": 2,
         "ms_per_step": round(ms_iter, 3), "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic power-law draws (seeded)",
         "config": {"workload": desc, "dims": dims, "nnz": nnz, "rank": R, "skew": skew,
-                   "iterations": iters, "tol": "-inf (exactly 10 iterations, cpals.cpp:107)"},
+                   "iterations": iters, "tol": "-inf (exactly 10 iterations, cpals.cpp:107)",
+                   "parallelism": (f"span partition x{world}; per mode reduce-scatter of M_n, row-block solve, "
+                                   "all-reduce of the R x R Gram, all-gather of A_n") if world > 1 else "1 GPU"},
         "fit_history": model.fit_history,
         "cp_als_call_ms": {"iters_10": round(ms_total, 2), "iters_2": round(ms_two, 2),
-                           "note": "whole API call incl. allocation and D2H of the factors"},
+                           "note": "whole API call incl. allocation and the initial/final copies"},
         "device_ms": {"per_iteration": round(ms_iter, 3),
-                      "mttkrp_per_iteration": round(model.device_ms["mttkrp_ms"] / iters, 3),
-                      "dense_per_iteration": round(ms_iter - model.device_ms["mttkrp_ms"] / iters, 3)},
+                      "mttkrp_per_iteration": round(ms_mt, 3),
+                      "dense_per_iteration": round(ms_iter - ms_mt, 3)},
         "mttkrp_per_mode_ms": [round(x, 4) for x in mode_ms],
         "roofline": {"bound": "hbm", "achieved": round(mttkrp_gbps, 2), "peak": peak, "unit": "GB/s",
                      "frac": round(mttkrp_gbps / peak, 4), "traffic": None,
                      "kernel": "k_mttkrp_sorted (one launch per mode)"},
-        "clocks": clk.summary(), "gpu_launches": b.kernel_launch_count() - launches0,
+        "clocks": clk.summary(), "gpu_launches": launches,
         "build": {"seconds": round(build_s, 3), "nnz_per_s": round(nnz / build_s, 1)},
+        **({"check": check} if check else {}),
     }), flush=True)
 
 
@@ -842,6 +922,8 @@ def main():
                     default="nell2")
     ap.add_argument("--rank", type=int, default=0)
     ap.add_argument("--strategy", choices=["Auto", "Register", "Hierarchical"], default="Auto")
+    ap.add_argument("--reduce", choices=["reducescatter", "allreduce"], default="reducescatter",
+                    help="N > 1: how the per-rank partial M_n are combined (SURVEY 8e)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fp32", action="store_true", help="skip the fp32 variant line item")
@@ -864,8 +946,8 @@ def main():
         if args.impl == "reference":
             print(json.dumps({"impl": "reference", "unavailable": "CP-ALS reference timing not sampled "
                               "(140M-nnz reference build needs ~10 GB and hours of CPU)"}), flush=True)
-        elif rank_id == 0:
-            run_cpals(args)
+        else:
+            run_cpals(args, world, rank_id, local)
         return
     if args.impl == "reference":
         run_reference(args, world, rank_id)

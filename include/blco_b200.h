@@ -388,6 +388,39 @@ int blco_cp_als_timed(const blco_tensor* t, uint64_t rank, int max_iters, double
 int blco_fit(const blco_tensor* t, const double* const* factors, const double* lambda,
              uint64_t rank, const blco_exec_config* cfg, double* fit_out);
 
+/* ------------------------------------------------ distributed CP-ALS pieces
+ * The dense steps of one cp_als mode (proj/src/cpals.cpp:84-96) split where a
+ * multi-GPU run reduces across ranks: after a reduce-scatter
+ * of M_n, rank g holds `rows` rows of it; it solves them locally, the ranks
+ * all-reduce the R x R partial Gram (whose diagonal carries the column
+ * norms), normalise their rows and all-gather A_n.  The collectives are the
+ * caller's (torch.distributed / NCCL); paper_2201_12523_b200/dist.py is the
+ * driver.  Device pointers, enqueued on `stream`, never synchronised.
+ * Matrices are row-major R x R (full, symmetric) or rows x R.  Ranks up to
+ * 64.  The solve stages L in the device's constant bank (R = 16 / 32):
+ * one epilogue per device at a time. */
+/* *d_out = sum of squared values of t (tensor_norm_squared, cpals.cpp:15-20) */
+int blco_tensor_norm_sq(const blco_tensor* t, double* d_out, void* stream);
+/* d_gram = A^T A over `rows` rows of d_a (gram, dense_kernels.cpp:8-21) */
+int blco_als_gram(const double* d_a, uint64_t rows, uint64_t rank, double* d_gram, void* stream);
+/* V = hadamard_{m != mode} d_grams[m] (d_grams: order x R x R), its Cholesky
+ * factor with solve_normal's Tikhonov escalation (dense_kernels.cpp:68-92),
+ * d_a = d_m V^-1 over `rows` rows, d_gram = A^T A over those rows;
+ * d_status[0] = 1 when V stays singular after the maximal shift. */
+int blco_als_solve(const double* d_grams, int order, int mode, uint64_t rank, const double* d_m, uint64_t rows,
+                   double* d_a, double* d_gram, int* d_status, void* stream);
+/* normalize_columns (cpals.cpp:51-61) from the summed Gram G of every rank's
+ * rows: d_lambda = sqrt(diag G) (0 -> 1), d_gram_n = G / (l l^T) (the Gram of
+ * the normalised factor), d_a /= lambda over `rows` rows; with d_m != NULL
+ * also *d_inner = sum_{i,r} m[i,r] lambda[r] A[i,r] over those rows (the
+ * fit's <X, Xhat>, cpals.cpp:36-44). */
+int blco_als_normalize(const double* d_gram_sum, uint64_t rank, double* d_a, uint64_t rows, double* d_gram_n,
+                       double* d_lambda, const double* d_m, double* d_inner, void* stream);
+/* *d_fit = fit_value(xnormsq, *d_inner, |Xhat|^2 from d_grams and d_lambda)
+ * (cpals.cpp:23-49) */
+int blco_als_fit(const double* d_grams, int order, uint64_t rank, const double* d_lambda, const double* d_inner,
+                 double xnormsq, double* d_fit, void* stream);
+
 /* ----------------------------------------------------------- factories
  * FactorMatrices::random (proj/src/types.cpp:118-130), SplitMix64; host and
  * device (d_out[m] device pointers) produce identical bits. */

@@ -178,6 +178,11 @@ SIGNATURES = {
     "blco_cp_als_timed": (_I, [_P, _U64, _I, C.c_double, _U64, _I, C.POINTER(ExecCfg),
                                C.POINTER(_P), _PD, _PD, C.POINTER(_I), C.POINTER(CpAlsStats)]),
     "blco_fit": (_I, [_P, C.POINTER(_P), _PD, _U64, C.POINTER(ExecCfg), _PD]),
+    "blco_tensor_norm_sq": (_I, [_P, _P, _P]),
+    "blco_als_gram": (_I, [_P, _U64, _U64, _P, _P]),
+    "blco_als_solve": (_I, [_P, _I, _I, _U64, _P, _U64, _P, _P, _P, _P]),
+    "blco_als_normalize": (_I, [_P, _U64, _P, _U64, _P, _P, _P, _P, _P]),
+    "blco_als_fit": (_I, [_P, _I, _U64, _P, _P, C.c_double, _P, _P]),
     "blco_factors_random": (_I, [_PU64, _I, _U64, _U64, C.POINTER(_P)]),
     "blco_factors_random_device": (_I, [_PU64, _I, _U64, _U64, C.POINTER(_P), _P]),
     "blco_synth_uniform_host": (_I, [_I, _PU64, _U64, _U64, _PU64, _PD]),

@@ -18,6 +18,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 
 #include "internal.hpp"
 
@@ -365,6 +366,15 @@ __global__ void k_sumsq(const double* __restrict__ v, uint64_t n, double* __rest
   if (threadIdx.x == 0) out[blockIdx.x] = s;
 }
 
+// out (R x R, full) = the upper triangle of g mirrored (Gram partials keep
+// only i <= j, k_gram / k_solve_gram)
+__global__ void k_symmetrize(const double* __restrict__ g, int R, double* __restrict__ out) {
+  for (int p = threadIdx.x; p < R * R; p += blockDim.x) {
+    const int i = p / R, j = p % R;
+    out[p] = j >= i ? g[i * R + j] : g[j * R + i];
+  }
+}
+
 bool exact_rank(int R) { return R == 16 || R == 32; }
 
 unsigned grid_of(uint64_t n) {
@@ -376,6 +386,7 @@ unsigned grid_of(uint64_t n) {
 // bit-reproducible MTTKRPs (ExecConfig::deterministic).
 struct Dense {
   int R;
+  cudaStream_t s = nullptr;  // every launch and copy of the epilogue goes here
   DevBuf<double> L, small;  // small: R x R reduced Gram | R lambda | 1 scalar
   DevBuf<double> parts;     // partial slots (grown on demand)
 
@@ -383,8 +394,9 @@ struct Dense {
   // per-warp Gram slots at full occupancy), so no iteration reallocates --
   // a cudaFree/cudaMalloc inside the loop stalls the queued kernels.
   explicit Dense(int r) : R(r), L(static_cast<size_t>(r) * r), small(static_cast<size_t>(r) * r + r + 1) {
-    int nsm = 148;
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+    int nsm = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     slots(std::max<uint64_t>(uint64_t(nsm) * 32 * (kSolveThreads / 32) * r * r, uint64_t(148) * 16 * 4));
   }
 
@@ -394,126 +406,158 @@ struct Dense {
   }
   // sum nslots partials of `width` values in slot order into small[0..width)
   void reduce(uint64_t nslots, int width) {
-    k_reduce_ordered<<<width, 256>>>(parts.ptr, nslots, width, small.ptr);
+    k_reduce_ordered<<<width, 256, 0, s>>>(parts.ptr, nslots, width, small.ptr);
     count_launch();
     check_launch("k_reduce_ordered");
   }
   std::vector<double> fetch(int width) {
     std::vector<double> h(width);
-    B200_CUDA(cudaMemcpy(h.data(), small.ptr, width * 8, cudaMemcpyDeviceToHost));
+    B200_CUDA(cudaMemcpyAsync(h.data(), small.ptr, width * 8, cudaMemcpyDeviceToHost, s));
+    B200_CUDA(cudaStreamSynchronize(s));
     return h;
+  }
+
+  // upper triangle of Gram(A) over `rows` rows into small (dense_kernels.cpp:8-21)
+  void gram_upper(const double* a, uint64_t rows) {
+    const int RR = R * R;
+    if (!rows) {
+      B200_CUDA(cudaMemsetAsync(small.ptr, 0, RR * sizeof(double), s));
+      return;
+    }
+    const size_t smem = (static_cast<size_t>(RR) + kGramChunk * R) * sizeof(double);
+    if (smem > 48 * 1024)
+      ensure_dyn_smem(reinterpret_cast<const void*>(k_gram), smem);
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((rows + kGramChunk - 1) / kGramChunk, 148 * 8));
+    k_gram<<<grid, kT, smem, s>>>(a, rows, R, slots(uint64_t(grid) * RR));
+    count_launch();
+    check_launch("k_gram");
+    reduce(grid, RR);
   }
 
   std::vector<double> gram(const double* a, uint64_t rows) {
     const int RR = R * R;
     if (!rows) return std::vector<double>(RR, 0.0);
-    const size_t smem = (static_cast<size_t>(RR) + kGramChunk * R) * sizeof(double);
-    if (smem > 48 * 1024)
-      ensure_dyn_smem(reinterpret_cast<const void*>(k_gram), smem);
-    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((rows + kGramChunk - 1) / kGramChunk, 148 * 8));
-    k_gram<<<grid, kT, smem>>>(a, rows, R, slots(uint64_t(grid) * RR));
-    count_launch();
-    check_launch("k_gram");
-    reduce(grid, RR);
+    gram_upper(a, rows);
     std::vector<double> g = fetch(RR);
     for (int i = 0; i < R; ++i)
       for (int j = 0; j < i; ++j) g[i * R + j] = g[j * R + i];
     return g;
   }
 
-  // One ALS mode's dense steps, enqueued on the legacy stream without host
-  // round trips: V and its Cholesky factor (with Tikhonov escalation,
-  // dense_kernels.cpp:68-92) on the device, A = M V^-1 fused with Gram(A),
-  // then normalize_columns (cpals.cpp:51-61): lambda and the Gram of the
-  // normalised A_n stay on the device (dgrams[n], dlam).  For the last mode
-  // (m_inner set) also <X, Xhat> into *dinner.  status[0] is set when V stays
-  // singular after the maximal shift.
-  void solve_normalize(const double* m, double* a, uint64_t rows, double* dgrams, int N, int n, double* dlam,
-                       int* dstatus, const double* m_inner, double* dinner) {
+  // small's upper triangle -> out, full symmetric R x R
+  void symmetric_out(double* out) {
+    k_symmetrize<<<1, 256, 0, s>>>(small.ptr, R, out);
+    count_launch();
+    check_launch("k_symmetrize");
+  }
+
+  // Solve step of one ALS mode (cpals.cpp:84-91, solve_normal
+  // dense_kernels.cpp:68-92): V = hadamard_{m != n} grams[m] and its Cholesky
+  // factor (Tikhonov escalation) on the device, then A = M V^-1 over `rows`
+  // rows fused with Gram(A), whose upper triangle is left in small.
+  // status[0] is set when V stays singular after the maximal shift.
+  void solve(const double* m, double* a, uint64_t rows, const double* dgrams, int N, int n, int* dstatus) {
     const int RR = R * R;
-    // BLCO_B200_ALS_PROBE=1: device time of each step of this epilogue (stderr)
-    static const bool probe = std::getenv("BLCO_B200_ALS_PROBE") != nullptr;
-    cudaEvent_t pe[6] = {};
-    auto pmark = [&](int k) {
-      if (!probe) return;
-      cudaEventCreate(&pe[k]);
-      cudaEventRecord(pe[k], nullptr);
-    };
-    pmark(0);
-    k_small_prep<<<1, 256, 2 * RR * sizeof(double)>>>(dgrams, N, n, R, L.ptr, dstatus);
+    k_small_prep<<<1, 256, 2 * RR * sizeof(double), s>>>(dgrams, N, n, R, L.ptr, dstatus);
     count_launch();
     check_launch("k_small_prep");
-    pmark(1);
     if (exact_rank(R))
-      B200_CUDA(cudaMemcpyToSymbolAsync(c_L, L.ptr, RR * sizeof(double), 0, cudaMemcpyDeviceToDevice, nullptr));
-    pmark(2);
-    if (rows) {
-      auto launch = [&](auto kern, int rm, int rows_per) {
-        const size_t smem = (static_cast<size_t>(rm) * rm + 2 * static_cast<size_t>(rows_per) * (rm + 1)) * 8;
-        ensure_dyn_smem(reinterpret_cast<const void*>(kern), smem);
-        const int per_sm = blocks_per_sm(reinterpret_cast<const void*>(kern), kSolveThreads, smem);
-        const unsigned grid = static_cast<unsigned>(
-            std::min<uint64_t>((rows + rows_per - 1) / rows_per, 148ull * std::max(1, per_sm)));
-        const uint64_t nslots = uint64_t(grid) * (kSolveThreads / 32);
-        double* sl = slots(nslots * RR);
-        // R <= 32: every warp writes the whole upper triangle of its slot (the
-        // lower one is never read); R = 64: each warp owns one quadrant
-        if (rm > 32) B200_CUDA(cudaMemsetAsync(sl, 0, nslots * RR * 8, nullptr));
-        kern<<<grid, kSolveThreads, smem>>>(m, a, rows, R, L.ptr, sl);
-        count_launch();
-        check_launch("k_solve_gram");
-        reduce(nslots, RR);
-      };
-      if (R == 16) launch(k_solve_gram<16, true>, 16, solve_rows<16>());
-      else if (R == 32) launch(k_solve_gram<32, true>, 32, solve_rows<32>());
-      else if (R < 16) launch(k_solve_gram<16, false>, 16, solve_rows<16>());
-      else if (R < 32) launch(k_solve_gram<32, false>, 32, solve_rows<32>());
-      else if (R <= 64) launch(k_solve_gram<64, false>, 64, solve_rows<64>());
-      else throw_format("b200: cp_als supports rank <= 64 on the device");
-    } else {
-      B200_CUDA(cudaMemsetAsync(small.ptr, 0, RR * sizeof(double), nullptr));
+      B200_CUDA(cudaMemcpyToSymbolAsync(c_L, L.ptr, RR * sizeof(double), 0, cudaMemcpyDeviceToDevice, s));
+    if (!rows) {
+      B200_CUDA(cudaMemsetAsync(small.ptr, 0, RR * sizeof(double), s));
+      return;
     }
-    pmark(3);
-    k_small_norm<<<1, 256>>>(small.ptr, R, dgrams + static_cast<size_t>(n) * RR, dlam);
+    auto launch = [&](auto kern, int rm, int rows_per) {
+      const size_t smem = (static_cast<size_t>(rm) * rm + 2 * static_cast<size_t>(rows_per) * (rm + 1)) * 8;
+      ensure_dyn_smem(reinterpret_cast<const void*>(kern), smem);
+      const int per_sm = blocks_per_sm(reinterpret_cast<const void*>(kern), kSolveThreads, smem);
+      const unsigned grid = static_cast<unsigned>(
+          std::min<uint64_t>((rows + rows_per - 1) / rows_per, 148ull * std::max(1, per_sm)));
+      const uint64_t nslots = uint64_t(grid) * (kSolveThreads / 32);
+      double* sl = slots(nslots * RR);
+      // R <= 32: every warp writes the whole upper triangle of its slot (the
+      // lower one is never read); R = 64: each warp owns one quadrant
+      if (rm > 32) B200_CUDA(cudaMemsetAsync(sl, 0, nslots * RR * 8, s));
+      kern<<<grid, kSolveThreads, smem, s>>>(m, a, rows, R, L.ptr, sl);
+      count_launch();
+      check_launch("k_solve_gram");
+      reduce(nslots, RR);
+    };
+    if (R == 16) launch(k_solve_gram<16, true>, 16, solve_rows<16>());
+    else if (R == 32) launch(k_solve_gram<32, true>, 32, solve_rows<32>());
+    else if (R < 16) launch(k_solve_gram<16, false>, 16, solve_rows<16>());
+    else if (R < 32) launch(k_solve_gram<32, false>, 32, solve_rows<32>());
+    else if (R <= 64) launch(k_solve_gram<64, false>, 64, solve_rows<64>());
+    else throw_format("b200: cp_als supports rank <= 64 on the device");
+  }
+
+  // normalize_columns (cpals.cpp:51-61) given G = Gram(A) (upper triangle
+  // read): lambda = sqrt(diag G), gram_n = Gram(A / lambda) = G / (l l^T),
+  // A /= lambda over `rows` rows, and with m_inner the fit's
+  // <X, Xhat> = sum m lambda A over those rows into *dinner (cpals.cpp:36-44).
+  void normalize(const double* G, double* a, uint64_t rows, double* gram_n, double* dlam,
+                 const double* m_inner, double* dinner) {
+    k_small_norm<<<1, 256, 0, s>>>(G, R, gram_n, dlam);
     count_launch();
     check_launch("k_small_norm");
-    if (m_inner) B200_CUDA(cudaMemsetAsync(dinner, 0, sizeof(double), nullptr));
+    if (m_inner) B200_CUDA(cudaMemsetAsync(dinner, 0, sizeof(double), s));
     if (rows) {
       const unsigned grid = grid_of(rows * R);
       double* part = m_inner ? slots(grid) : nullptr;
-      k_scale_inner<<<grid, kT>>>(a, rows, R, dlam, m_inner, part);
+      k_scale_inner<<<grid, kT, 0, s>>>(a, rows, R, dlam, m_inner, part);
       count_launch();
       check_launch("k_scale_inner");
       if (m_inner) {
-        k_reduce_ordered<<<1, 256>>>(part, grid, 1, dinner);
+        k_reduce_ordered<<<1, 256, 0, s>>>(part, grid, 1, dinner);
         count_launch();
         check_launch("k_reduce_ordered");
       }
     }
-    pmark(4);
+  }
+
+  // One ALS mode's dense steps, enqueued without host round trips: solve,
+  // then normalize with the Gram of this device's rows.  lambda and the Gram
+  // of the normalised A_n stay on the device (dgrams[n], dlam); for the last
+  // mode (m_inner set) also <X, Xhat> into *dinner.
+  void solve_normalize(const double* m, double* a, uint64_t rows, double* dgrams, int N, int n, double* dlam,
+                       int* dstatus, const double* m_inner, double* dinner) {
+    // BLCO_B200_ALS_PROBE=1: device time of each step of this epilogue (stderr)
+    static const bool probe = std::getenv("BLCO_B200_ALS_PROBE") != nullptr;
+    cudaEvent_t pe[3] = {};
+    auto pmark = [&](int k) {
+      if (!probe) return;
+      cudaEventCreate(&pe[k]);
+      cudaEventRecord(pe[k], s);
+    };
+    pmark(0);
+    solve(m, a, rows, dgrams, N, n, dstatus);
+    pmark(1);
+    normalize(small.ptr, a, rows, dgrams + static_cast<size_t>(n) * R * R, dlam, m_inner, dinner);
+    pmark(2);
     if (probe) {
-      cudaEventSynchronize(pe[4]);
-      float t[4];
-      for (int k = 0; k < 4; ++k) cudaEventElapsedTime(&t[k], pe[k], pe[k + 1]);
-      std::fprintf(stderr, "[als probe] mode %d rows %llu: prep %.3f symbol %.3f solve+gram %.3f norm+scale %.3f ms\n",
-                   n, static_cast<unsigned long long>(rows), t[0], t[1], t[2], t[3]);
-      for (int k = 0; k < 5; ++k) cudaEventDestroy(pe[k]);
+      cudaEventSynchronize(pe[2]);
+      float t[2];
+      for (int k = 0; k < 2; ++k) cudaEventElapsedTime(&t[k], pe[k], pe[k + 1]);
+      std::fprintf(stderr, "[als probe] mode %d rows %llu: prep+solve+gram %.3f norm+scale %.3f ms\n",
+                   n, static_cast<unsigned long long>(rows), t[0], t[1]);
+      for (int k = 0; k < 3; ++k) cudaEventDestroy(pe[k]);
     }
   }
 
   double inner(const double* m, const double* a, uint64_t rows, const std::vector<double>& lambda) {
     if (!rows) return 0.0;
     double* lam = small.ptr + R * R;
-    B200_CUDA(cudaMemcpy(lam, lambda.data(), R * 8, cudaMemcpyHostToDevice));
+    B200_CUDA(cudaMemcpyAsync(lam, lambda.data(), R * 8, cudaMemcpyHostToDevice, s));
     const unsigned grid = grid_of(rows * R);
-    k_inner<<<grid, kT>>>(m, a, rows, R, lam, slots(grid));
+    k_inner<<<grid, kT, 0, s>>>(m, a, rows, R, lam, slots(grid));
     count_launch();
     check_launch("k_inner");
-    k_reduce_ordered<<<1, 256>>>(parts.ptr, grid, 1, lam + R);
+    k_reduce_ordered<<<1, 256, 0, s>>>(parts.ptr, grid, 1, lam + R);
     count_launch();
     check_launch("k_reduce_ordered");
     double h = 0;
-    B200_CUDA(cudaMemcpy(&h, lam + R, 8, cudaMemcpyDeviceToHost));
+    B200_CUDA(cudaMemcpyAsync(&h, lam + R, 8, cudaMemcpyDeviceToHost, s));
+    B200_CUDA(cudaStreamSynchronize(s));
     return h;
   }
 };
@@ -531,6 +575,19 @@ double tensor_norm_sq(const blco_tensor& t) {
   double h = 0;
   B200_CUDA(cudaMemcpy(&h, out.ptr, 8, cudaMemcpyDeviceToHost));
   return h;
+}
+
+// Dense epilogue state per (device, rank) for the calling thread: the
+// distributed ALS pieces below are called once per mode, so their partial
+// buffers must not be reallocated per call.
+Dense& dense_cache(int R, cudaStream_t s) {
+  thread_local std::map<std::pair<int, int>, std::unique_ptr<Dense>> cache;
+  int dev = 0;
+  B200_CUDA(cudaGetDevice(&dev));
+  auto& d = cache[{dev, R}];
+  if (!d) d = std::make_unique<Dense>(R);
+  d->s = s;
+  return *d;
 }
 
 double recon_norm_sq(const std::vector<std::vector<double>>& grams, const std::vector<double>& lam,
@@ -744,6 +801,70 @@ int blco_fit(const blco_tensor* t, const double* const* factors, const double* l
     std::vector<double> lam(lambda, lambda + rank);
     *fit_out = fit_value(xn, dense.inner(ml.ptr, A[N - 1].ptr, l.dims[N - 1], lam),
                          recon_norm_sq(grams, lam, R));
+  });
+}
+
+// ------------------------------------------- distributed CP-ALS pieces
+// The dense steps of one ALS mode split where a multi-GPU run reduces across
+// ranks: see include/blco_b200.h.
+
+int blco_tensor_norm_sq(const blco_tensor* t, double* d_out, void* stream) {
+  return guarded([&] {
+    DeviceGuard dg(t->device);
+    auto s = static_cast<cudaStream_t>(stream);
+    Dense& d = dense_cache(1, s);
+    if (!t->nnz) {
+      B200_CUDA(cudaMemsetAsync(d_out, 0, sizeof(double), s));
+      return;
+    }
+    const unsigned grid = grid_of(t->nnz);
+    double* part = d.slots(grid);
+    k_sumsq<<<grid, kT, 0, s>>>(t->vals.ptr, t->nnz, part);
+    count_launch();
+    check_launch("k_sumsq");
+    k_reduce_ordered<<<1, 256, 0, s>>>(part, grid, 1, d_out);
+    count_launch();
+    check_launch("k_reduce_ordered");
+  });
+}
+
+int blco_als_gram(const double* d_a, uint64_t rows, uint64_t rank, double* d_gram, void* stream) {
+  return guarded([&] {
+    if (rank < 1 || rank > 64) throw_format("cp_als: rank must be in [1, 64] on the device");
+    Dense& d = dense_cache(static_cast<int>(rank), static_cast<cudaStream_t>(stream));
+    d.gram_upper(d_a, rows);
+    d.symmetric_out(d_gram);
+  });
+}
+
+int blco_als_solve(const double* d_grams, int order, int mode, uint64_t rank, const double* d_m, uint64_t rows,
+                   double* d_a, double* d_gram, int* d_status, void* stream) {
+  return guarded([&] {
+    if (rank < 1 || rank > 64) throw_format("cp_als: rank must be in [1, 64] on the device");
+    if (order < 1 || mode < 0 || mode >= order) throw_format("cp_als: mode out of range");
+    Dense& d = dense_cache(static_cast<int>(rank), static_cast<cudaStream_t>(stream));
+    d.solve(d_m, d_a, rows, d_grams, order, mode, d_status);
+    d.symmetric_out(d_gram);
+  });
+}
+
+int blco_als_normalize(const double* d_gram_sum, uint64_t rank, double* d_a, uint64_t rows, double* d_gram_n,
+                       double* d_lambda, const double* d_m, double* d_inner, void* stream) {
+  return guarded([&] {
+    if (rank < 1 || rank > 64) throw_format("cp_als: rank must be in [1, 64] on the device");
+    Dense& d = dense_cache(static_cast<int>(rank), static_cast<cudaStream_t>(stream));
+    d.normalize(d_gram_sum, d_a, rows, d_gram_n, d_lambda, d_m, d_inner);
+  });
+}
+
+int blco_als_fit(const double* d_grams, int order, uint64_t rank, const double* d_lambda, const double* d_inner,
+                 double xnormsq, double* d_fit, void* stream) {
+  return guarded([&] {
+    if (xnormsq == 0.0) throw_format("cp_als: zero-norm tensor");
+    k_small_fit<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(d_grams, order, static_cast<int>(rank), d_lambda,
+                                                                 d_inner, xnormsq, d_fit);
+    count_launch();
+    check_launch("k_small_fit");
   });
 }
 

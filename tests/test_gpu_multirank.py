@@ -55,3 +55,26 @@ def test_two_rank_all_mode_streaming(gpu):
     d = _torchrun(["--config", "reddit_stream_tiny", "--steps", "1"])
     assert d["n_gpus"] == 2 and d["value"] > 0
     assert d["config"]["nnz"] > 19_000_000 and "all-reduce" in d["config"]["step"]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_multi_rank_reduce_scatter_step(gpu, world):
+    """The default N > 1 combine: reduce-scatter of M_n into row shards
+    (SURVEY.md 8e); --check all-gathers the shards and compares them with a
+    single-device MTTKRP of the whole tensor."""
+    d = _torchrun(["--config", "cfg1", "--steps", "2", "--warmup", "3", "--no-cpu-baseline", "--no-e2e", "--check",
+                   "--reduce", "reducescatter"], world=world)
+    assert "reduce-scatter" in d["config"]["parallelism"]
+    assert max(d["check"]["rel_frobenius_vs_single_device"]) <= 1e-12
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_distributed_cp_als(gpu, world):
+    """cp_als_distributed (reduce-scatter of M_n, row-block solve, all-reduced
+    Gram, all-gathered A_n) against single-device cp_als on the whole tensor:
+    the fit history within 1e-10 and the factors within 1e-8."""
+    d = _torchrun(["--config", "als_tiny", "--check"], world=world)
+    c = d["check"]
+    assert d["n_gpus"] == world and len(d["fit_history"]) == 10
+    assert c["max_abs_fit_diff_vs_single_device"] <= 1e-10
+    assert max(c["factor_rel_frobenius"]) <= 1e-8 and c["lambda_rel"] <= 1e-8

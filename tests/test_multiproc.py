@@ -2,9 +2,10 @@
 
 Each rank takes its contiguous nnz-balanced span range (blco_partition, the
 product's partitioner), computes the partial M of that range, and the ranks
-sum the partials with an all-reduce -- the same plumbing bench.py runs over
-NCCL.  No GPU here, so the per-rank partial product comes from the oracle
-(test infrastructure); the GPU-side partial products are covered by
+sum the partials with an all-reduce, or reduce-scatter them into row shards
+and all-gather those (paper_2201_12523_b200.dist) -- the same plumbing
+bench.py and the distributed CP-ALS run over NCCL.  No GPU here, so the
+per-rank partial product comes from the oracle (test infrastructure); the GPU-side partial products are covered by
 tests/test_gpu_mttkrp.py::test_slices_sum_to_whole.
 """
 import os
@@ -27,7 +28,7 @@ def _free_port() -> int:
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, dims, nnz, rank_r, quota, out_q):
+def _worker(rank, world, port, dims, nnz, rank_r, quota, out_q, combine="allreduce"):
     sys.path.insert(0, str(ROOT))
     sys.path.insert(0, str(ROOT / "oracle"))
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -47,10 +48,25 @@ def _worker(rank, world, port, dims, nnz, rank_r, quota, out_q):
         coords[:, e - lo] = o.delinearize(layout, int(bidx[e]), int(keys[blk[e - lo]]))
     f = o.factors_random(dims, rank_r, 7)
     outs = []
+    from paper_2201_12523_b200.dist import Collectives, row_shard
+    coll = Collectives()
     for mode in range(len(dims)):
         part = torch.from_numpy(o.mttkrp_coo(dims, coords, bvals[lo:hi], f, mode))
-        dist.all_reduce(part)
-        outs.append(part.numpy())
+        if combine == "allreduce":
+            dist.all_reduce(part)
+            outs.append(part.numpy())
+            continue
+        # reduce-scatter into row shards of the padded partial,
+        # then all-gather them back (the distributed CP-ALS exchange)
+        r0, rows, per = row_shard(dims[mode], world, rank)
+        padded = torch.zeros((world * per, rank_r), dtype=torch.float64)
+        padded[: dims[mode]] = part
+        shard = torch.empty((per, rank_r), dtype=torch.float64)
+        coll.reduce_scatter(shard, padded)
+        assert r0 == rank * per and 0 <= rows <= per
+        whole = torch.empty_like(padded)
+        coll.all_gather(whole, shard)
+        outs.append(whole[: dims[mode]].numpy())
     sizes = torch.tensor([hi - lo], dtype=torch.int64)
     dist.all_reduce(sizes)
     if rank == 0:
@@ -60,13 +76,14 @@ def _worker(rank, world, port, dims, nnz, rank_r, quota, out_q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2])
-def test_partitioned_partials_allreduce_to_full(world):
+@pytest.mark.parametrize("world,combine", [(2, "allreduce"), (2, "reducescatter"), (3, "reducescatter")])
+def test_partitioned_partials_combine_to_full(world, combine):
     dims, nnz, rank_r = [37, 41, 29], 6000, 4
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, dims, nnz, rank_r, 512, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, dims, nnz, rank_r, 512, q, combine))
+             for r in range(world)]
     for p in procs:
         p.start()
     err, total = q.get(timeout=300)
