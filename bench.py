@@ -140,14 +140,23 @@ def cpu_model() -> str:
     return "unknown"
 
 
-def reference_sample_run(dims, nnz, rank, steps, warmup, target_step_s=4.0, threads=None, extra=False):
+def reference_sample_run(dims, nnz, rank, steps, warmup, target_step_s=4.0, threads=None, extra=False,
+                         sampler="alto_prefix", skew=None, op="mttkrp"):
     """Times the reference's blco::mttkrp (all modes) on the host.
 
-    The sample is the `S` elements of smallest ALTO index of the synthetic
-    tensor -- a contiguous prefix of the BLCO element order, i.e. exactly the
-    first S elements (first spans) the GPU processes -- built by the
-    reference's own build_blco from the COO subset.  S is calibrated so one
-    step takes ~target_step_s.  Returns (GB/s, dict).
+    sampler "alto_prefix": the `S` elements of smallest ALTO index of the
+    synthetic tensor -- a contiguous prefix of the BLCO element order, i.e.
+    exactly the first S elements (first spans) the GPU processes.
+    sampler "generator_prefix": the first S elements the seeded generator
+    emits (Feistel-uniform cells, or with `skew` set the first S distinct
+    draws floor(I u^skew)): the generator's key does not depend on nnz, so this is
+    a uniformly random subset of the same tensor's non-zeros over the same
+    dims (configs whose COO does not fit the host, or layouts > 64 bits).
+    Either sample is built by the reference's own build_blco; S is calibrated
+    so one step takes ~target_step_s, and the rate (bytes per second) is the
+    figure compared, i.e. linearly extrapolated by nnz.  op "stream" times
+    the reference stream_mttkrp (MemoryBlockSource, its DeviceBudget) per mode
+    instead.  Returns (GB/s, dict).
     """
     sys.path.insert(0, str(ROOT / "oracle"))
     from pyoracle import Oracle, RefLib, cfg_array
@@ -156,66 +165,110 @@ def reference_sample_run(dims, nnz, rank, steps, warmup, target_step_s=4.0, thre
     threads = threads or os.cpu_count() or 1
     order = len(dims)
     t0 = time.perf_counter()
-    # Generate the tensor lazily in ALTO-prefix order: full COO then select.
-    gen_n = nnz
-    if int(np.prod(np.array(dims, dtype=object))) >= 2**64 or make_wide(dims):
-        raise RuntimeError("reference sample: layouts wider than 64 bits not supported here")
-    idx, vals = oracle.synth_uniform(dims, gen_n, TENSOR_SEED)
-    alto = oracle.alto_lo(dims, idx)
-    order_idx = None
     factors = oracle.factors_random(dims, rank, FACTOR_SEED)
     cfg = cfg_array(num_threads=threads)
+    if sampler == "alto_prefix":
+        # Generate the tensor in full, then select ALTO prefixes.
+        gen_n = nnz
+        if int(np.prod(np.array(dims, dtype=object))) >= 2**64 or make_wide(dims):
+            raise RuntimeError("reference sample: ALTO-prefix sampling needs a layout of <= 64 bits")
+        idx, vals = oracle.synth_uniform(dims, gen_n, TENSOR_SEED)
+        alto = oracle.alto_lo(dims, idx)
+
+        def coo(S):
+            sel = np.argpartition(alto, S - 1)[:S] if S < gen_n else np.arange(gen_n)
+            return idx[:, sel], vals[sel]
+    else:
+        gen_n = nnz
+
+        def coo(S):
+            if skew:  # independent draws floor(I u^skew), first S distinct
+                return oracle.synth_draws(dims, S, TENSOR_SEED, skew)
+            return oracle.synth_uniform(dims, S, TENSOR_SEED)
     setup_s = time.perf_counter() - t0
 
     def sample(S):
-        nonlocal order_idx
         S = min(S, gen_n)
-        sel = np.argpartition(alto, S - 1)[:S] if S < gen_n else np.arange(gen_n)
-        return ref.build(dims, idx[:, sel], vals[sel], 64), S
+        sidx, svals = coo(S)
+        return ref.build(dims, sidx, svals, 64), S
 
-    def one_step(t):
+    def one_step(t, c=cfg):
         s = time.perf_counter()
         for mode in range(order):
-            t.mttkrp(factors, mode, cfg)
+            if op == "stream":
+                # DeviceBudget{capacity 24 GiB, 4 queues, 2 GiB} as the GPU arm
+                t.stream_mttkrp(factors, mode, 24 << 30, 4, (1 << 27) * 16, c)
+            else:
+                t.mttkrp(factors, mode, c)
         return time.perf_counter() - s
 
-    # calibrate
-    S = min(gen_n, 1 << 17)
+    # Step time t(S) = a + b S: a is the reference's per-call fixed cost
+    # (zero-initialised I_n x R outputs, factor copies, merge -- it scales
+    # with the dims, not nnz), b the per-element cost.  Fit both from two
+    # sample sizes and extrapolate to the full nnz: t_full = a + b nnz.
+    S_lo = min(gen_n, 1 << 16)
+    t_lo, S_lo = sample(S_lo)
+    one_step(t_lo)
+    d_lo = one_step(t_lo)
+    S = min(gen_n, max(4 * S_lo, 1 << 18))
     t, S = sample(S)
     dt = one_step(t)
-    while dt < target_step_s / 4 and S < gen_n:
-        S = min(gen_n, int(S * max(2.0, min(16.0, target_step_s / max(dt, 1e-3)))))
-        t, S = sample(S)
-        dt = one_step(t)
+    b_est = max((dt - d_lo) / max(S - S_lo, 1), 1e-12)
+    S2 = min(gen_n, max(S, int(target_step_s / b_est)), 1 << 25)
+    if S2 > S:
+        del t
+        t, S = sample(S2)
     for _ in range(warmup):
         one_step(t)
     times = [one_step(t) for _ in range(steps)]
     bpe = bytes_per_elem(order, rank)
     step_s = sum(times) / len(times)
-    gbps = S * order * bpe / step_s / 1e9
-    info = {"sample_nnz": S, "step_s": step_s, "threads": threads, "setup_s": setup_s,
-            "sample": f"first {S} elements in ALTO order of the {nnz}-nnz tensor "
-                      f"(reference build_blco on that COO subset), all {order} modes, R={rank}"}
+    per_elem = (step_s - d_lo) / (S - S_lo) if S > S_lo else step_s / S
+    fixed = max(0.0, d_lo - per_elem * S_lo)
+    if per_elem <= 0:
+        per_elem, fixed = step_s / S, 0.0
+    full_s = fixed + per_elem * nnz
+    gbps = nnz * order * bpe / full_s / 1e9
+    what = "blco::stream_mttkrp per mode (MemoryBlockSource, DeviceBudget{24 GiB, 4, 2 GiB})" if op == "stream" \
+        else "blco::mttkrp"
+    if sampler == "alto_prefix":
+        desc = f"first {S_lo} and {S} elements in ALTO order of the {nnz}-nnz tensor"
+    else:
+        desc = (f"first {S_lo} and {S} elements of the seeded generator (uniformly random subsets of the "
+                f"{nnz}-nnz tensor's non-zeros, same dims)")
+    desc += (f"; all-mode step time fitted as a + b*nnz (a = {fixed:.3f} s fixed per step, "
+             f"b = {per_elem * 1e9:.1f} ns per element) and extrapolated to the full {nnz} nnz "
+             f"= {full_s:.2f} s")
+    info = {"sample_nnz": S, "step_s": step_s, "full_step_s": full_s, "fixed_s": fixed, "per_elem_s": per_elem,
+            "threads": threads, "setup_s": setup_s,
+            "sample": f"{desc}; reference build_blco on that COO subset, {what}, all {order} modes, R={rank}"}
     if extra:
         # the reference anti-scales with threads, so also one
         # thread, and the oracle::mttkrp_coo loop (1 thread) on the same sample
-        cfg1 = cfg_array(num_threads=1)
-        s0 = time.perf_counter()
-        for mode in range(order):
-            t.mttkrp(factors, mode, cfg1)
-        one_s = time.perf_counter() - s0
-        sel = np.argpartition(alto, S - 1)[:S] if S < gen_n else np.arange(gen_n)
-        sidx, svals = idx[:, sel], vals[sel]
+        one_s = one_step(t, cfg_array(num_threads=1))
+        sidx, svals = coo(S)
         s0 = time.perf_counter()
         for mode in range(order):
             ref.mttkrp_coo(dims, sidx, svals, factors, mode)
         coo_s = time.perf_counter() - s0
-        info["reference_1_thread"] = {"value": round(S * order * bpe / one_s / 1e9, 4), "unit": "GB/s",
-                                      "step_s": round(one_s, 3)}
+        one_full = fixed * one_s / step_s + per_elem * (one_s / step_s) * nnz  # same a/b split, 1-thread scale
+        info["reference_1_thread"] = {"value": round(nnz * order * bpe / one_full / 1e9, 4), "unit": "GB/s",
+                                      "step_s": round(one_s, 3), "note": "sample step at 1 thread, scaled like "
+                                      "the fitted all-thread step"}
         info["oracle_mttkrp_coo_1_thread"] = {"value": round(S * order * bpe / coo_s / 1e9, 4), "unit": "GB/s",
                                               "step_s": round(coo_s, 3),
                                               "note": "reference oracle::mttkrp_coo (oracle.cpp:9-26)"}
     return gbps, info
+
+
+def cpu_baseline_entry(gbps, info) -> dict:
+    out = {"value": round(gbps, 4), "unit": "GB/s", "cores": info["threads"], "kind": "reference",
+           "sample": info["sample"], "sample_step_s": round(info["step_s"], 3),
+           "full_step_s_extrapolated": round(info["full_step_s"], 3), "cpu_model": cpu_model()}
+    for k in ("reference_1_thread", "oracle_mttkrp_coo_1_thread"):
+        if k in info:
+            out[k] = info[k]
+    return out
 
 
 def make_wide(dims) -> bool:
@@ -416,14 +469,13 @@ def run_ours(args, world, rank_id, local):
         result["check"] = {"rel_frobenius_vs_single_device": errs, "ranks": world}
     if not args.no_e2e:
         result["e2e"] = e2e_run(b, torch, dt, dims, R, N, nnz, args, dev, world)
-    if rank_id == 0 and world == 1 and not args.no_cpu_baseline and args.config in ("cfg1", "nell2"):
+    if rank_id == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            gbps, info = reference_sample_run(dims, nnz, R, steps=2, warmup=1, extra=True)
-            result["cpu_baseline"] = {"value": round(gbps, 4), "unit": "GB/s", "cores": info["threads"],
-                                      "kind": "reference", "sample": info["sample"],
-                                      "step_s": round(info["step_s"], 3), "cpu_model": cpu_model(),
-                                      "reference_1_thread": info["reference_1_thread"],
-                                      "oracle_mttkrp_coo_1_thread": info["oracle_mttkrp_coo_1_thread"]}
+            small = args.config in ("cfg1", "nell2")
+            gbps, info = reference_sample_run(dims, nnz, R, steps=2, warmup=1, extra=True,
+                                              sampler="alto_prefix" if small else "generator_prefix",
+                                              skew=None if int(np.prod(np.array(dims, dtype=object))) < 2**64 else 1)
+            result["cpu_baseline"] = cpu_baseline_entry(gbps, info)
         except Exception as e:  # noqa: BLE001
             result["cpu_baseline"] = {"value": None, "unit": "GB/s", "cores": None, "kind": "reference",
                                       "sample": f"failed: {e}"}
@@ -657,6 +709,12 @@ def run_cpals(args, world=1, rank_id=0, local=0):
         check = {"max_abs_fit_diff_vs_single_device": fdiff, "factor_rel_frobenius": ferr,
                  "lambda_rel": float(np.linalg.norm(model.lambda_ - one.lambda_) / np.linalg.norm(one.lambda_)),
                  "ranks": world}
+    cpu = None
+    if rank_id == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = als_reference_baseline(dims, nnz, R, skew, args.ref_step_s)
+        except Exception as e:  # noqa: BLE001
+            cpu = {"value": None, "unit": "ms", "cores": None, "kind": "reference", "sample": f"failed: {e}"}
     if world > 1:
         import torch.distributed as dist
         dist.barrier()
@@ -685,7 +743,25 @@ def run_cpals(args, world=1, rank_id=0, local=0):
         "clocks": clk.summary(), "gpu_launches": launches,
         "build": {"seconds": round(build_s, 3), "nnz_per_s": round(nnz / build_s, 1)},
         **({"check": check} if check else {}),
+        **({"cpu_baseline": cpu} if cpu else {}),
     }), flush=True)
+
+
+def als_reference_baseline(dims, nnz, R, skew, step_s=4.0) -> dict:
+    """The reference CPU MTTKRP part of one CP-ALS iteration (N blco::mttkrp
+    calls), timed on a generator-prefix sample of the same power-law tensor
+    and extrapolated linearly by nnz.  The reference iteration also runs the
+    dense Gram / solve / normalise steps on the host, so this is a lower bound
+    of its time per iteration."""
+    gbps, info = reference_sample_run(dims, nnz, R, steps=2, warmup=1, target_step_s=step_s,
+                                      sampler="generator_prefix", skew=skew)
+    N = len(dims)
+    ms = nnz * N * bytes_per_elem(N, R) / (gbps * 1e9) * 1e3
+    return {"value": round(ms, 1), "unit": "ms", "cores": info["threads"], "kind": "reference",
+            "sample": info["sample"], "mttkrp_gbps": round(gbps, 4), "sample_step_s": round(info["step_s"], 3),
+            "cpu_model": cpu_model(),
+            "note": "extrapolated: the reference's N-mode MTTKRP time per ALS iteration on the full tensor "
+                    "(its dense epilogue not included, so the reference iteration is slower still)"}
 
 
 STREAM_CONFIGS = {
@@ -867,6 +943,14 @@ def run_stream(args, world, rank_id, local):
             "total_s": round(sum(r.total_seconds for r in per_mode), 3),
             "overall_gbps_per_mode": [round(r.overall_gbps, 2) for r in per_mode],
             "note": "stream_mttkrp once per mode (the reference API): the tensor crosses the link N times"}
+    if rank_id == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            gbps, info = reference_sample_run(dims, nnz_target, R, steps=2, warmup=1, target_step_s=args.ref_step_s,
+                                              sampler="generator_prefix", op="stream")
+            result["cpu_baseline"] = cpu_baseline_entry(gbps, info)
+        except Exception as e:  # noqa: BLE001
+            result["cpu_baseline"] = {"value": None, "unit": "GB/s", "cores": None, "kind": "reference",
+                                      "sample": f"failed: {e}"}
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -875,27 +959,58 @@ def run_stream(args, world, rank_id, local):
 
 
 def run_reference(args, world, rank_id):
+    """--impl reference: the unmodified reference (oracle/_ref/libblco_ref.so)
+    on the host cores, same metric/unit as our arm for the config.  Rank 0
+    alone runs; bounded samples (reference_sample_run)."""
     if rank_id != 0:
         return
-    dims, nnz, R, desc = CONFIGS[args.config]
+    kind = "mttkrp"
+    if args.config in STREAM_CONFIGS:
+        dims, nnz, R, _, desc = STREAM_CONFIGS[args.config]
+        kind = "stream"
+    elif args.config in ALS_CONFIGS:
+        dims, nnz, R, skew, desc = ALS_CONFIGS[args.config]
+        kind = "als"
+    else:
+        dims, nnz, R, desc = CONFIGS[args.config]
     if args.rank:
         R = args.rank
     N = len(dims)
+    wide = int(np.prod(np.array(dims, dtype=object))) >= 2**64 or make_wide(dims)
     try:
+        if kind == "als":
+            cpu = als_reference_baseline(dims, nnz, R, skew, args.ref_step_s)
+            print(json.dumps({
+                "impl": "reference",
+                "metric": "CP-ALS time per iteration (N MTTKRPs + device Gram/solve/normalise + fit)",
+                "value": cpu["value"], "unit": "ms", "n_gpus": world, "steps": 2, "warmup": 1,
+                "ms_per_step": cpu["value"], "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic power-law draws (same generator and seeds as the ours arm)",
+                "config": {"workload": desc, "dims": dims, "nnz": nnz, "rank": R, "skew": skew},
+                "cpu_baseline": cpu,
+                "e2e": {"value": cpu["value"], "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+                "path": "unmodified reference blco::build_blco + blco::mttkrp x N (proj/src, oracle/_ref), "
+                        "extrapolated from a generator-prefix sample; dense epilogue not included"}), flush=True)
+            return
+        small = kind == "mttkrp" and not wide and nnz <= 200_000_000
         gbps, info = reference_sample_run(dims, nnz, R, steps=args.steps, warmup=args.warmup,
-                                          target_step_s=args.ref_step_s)
+                                          target_step_s=args.ref_step_s,
+                                          sampler="alto_prefix" if small else "generator_prefix",
+                                          skew=1 if kind == "mttkrp" and wide else None,
+                                          op="stream" if kind == "stream" else "mttkrp")
     except Exception as e:  # noqa: BLE001
         print(json.dumps({"impl": "reference", "unavailable": f"{type(e).__name__}: {e}"}), flush=True)
         return
     result = {
         "impl": "reference",
-        "metric": "MTTKRP all-mode throughput (algorithmic B_elem bytes / time)",
+        "metric": ("out-of-memory MTTKRP all-mode throughput (algorithmic B_elem bytes / time), host-link bound"
+                   if kind == "stream" else "MTTKRP all-mode throughput (algorithmic B_elem bytes / time)"),
         "value": round(gbps, 4),
         "unit": "GB/s",
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
-        "ms_per_step": round(info["step_s"] * 1e3, 3),
+        "ms_per_step": round(info["full_step_s"] * 1e3, 3),
         "higher_is_better": True,
         "scaling": "strong",
         "vs_baseline": None,
@@ -906,8 +1021,8 @@ def run_reference(args, world, rank_id):
         "cpu_baseline": {"value": round(gbps, 4), "unit": "GB/s", "cores": info["threads"], "kind": "reference",
                          "sample": info["sample"]},
         "e2e": {"value": round(gbps, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "path": "unmodified reference blco::build_blco + blco::mttkrp (proj/src, compiled into "
-                "oracle/_ref/libblco_ref.so), ExecConfig{num_threads = all host threads}",
+        "path": "unmodified reference blco::build_blco + blco::" + ("stream_mttkrp" if kind == "stream" else "mttkrp")
+                + " (proj/src, compiled into oracle/_ref/libblco_ref.so), ExecConfig{num_threads = all host threads}",
     }
     print(json.dumps(result), flush=True)
 
@@ -934,25 +1049,16 @@ def main():
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
     world, rank_id, local = dist_env()
-    if args.config in STREAM_CONFIGS:
-        if args.impl == "reference":
-            if rank_id == 0:
-                print(json.dumps({"impl": "reference", "unavailable": "reference stream_mttkrp over 4.69B nnz "
-                                  "needs ~330 GB host RAM to build"}), flush=True)
-        else:
-            run_stream(args, world, rank_id, local)
-        return
-    if args.config in ALS_CONFIGS:
-        if args.impl == "reference":
-            print(json.dumps({"impl": "reference", "unavailable": "CP-ALS reference timing not sampled "
-                              "(140M-nnz reference build needs ~10 GB and hours of CPU)"}), flush=True)
-        else:
-            run_cpals(args, world, rank_id, local)
-        return
     if args.impl == "reference":
         run_reference(args, world, rank_id)
-    else:
-        run_ours(args, world, rank_id, local)
+        return
+    if args.config in STREAM_CONFIGS:
+        run_stream(args, world, rank_id, local)
+        return
+    if args.config in ALS_CONFIGS:
+        run_cpals(args, world, rank_id, local)
+        return
+    run_ours(args, world, rank_id, local)
 
 
 if __name__ == "__main__":

@@ -32,6 +32,36 @@
 namespace b200 {
 namespace {
 
+// Factor-row gathers of the computing phases.  BLCO_GATHER (compile time)
+// selects the L1 policy: 0 = ld.global.nc (cached in L1), 1 = ld.global.cg
+// (L2 only), 2 = L1::evict_last, 3 = L1::no_allocate.
+#ifndef BLCO_GATHER
+#define BLCO_GATHER 0
+#endif
+template <class T>
+__device__ __forceinline__ T gather_ld(const T* p) {
+#if BLCO_GATHER == 1
+  return __ldcg(p);
+#elif BLCO_GATHER == 2 || BLCO_GATHER == 3
+  if constexpr (sizeof(T) == 8) {
+    unsigned long long x;
+#if BLCO_GATHER == 2
+    asm("ld.global.nc.L1::evict_last.u64 %0, [%1];" : "=l"(x) : "l"(p));
+#else
+    asm("ld.global.nc.L1::no_allocate.u64 %0, [%1];" : "=l"(x) : "l"(p));
+#endif
+    T r;
+    memcpy(&r, &x, 8);
+    return r;
+  } else {
+    return __ldg(p);
+  }
+#else
+  return __ldg(p);
+#endif
+}
+
+
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kWarps = 8;
 constexpr int kCtaThreads = 32 * kWarps;
@@ -235,7 +265,7 @@ __device__ __forceinline__ void compute_range(const Params<N>& p, const Stage<N>
           const double* rp = p.factors[k] + static_cast<uint64_t>(w[u][k]) * R;
 #pragma unroll
           for (int c = 0; c < CPL; ++c)
-            rows[u][k].v[c] = (FULL || c < ncol_ok) ? __ldg(rp + col + c * LPE) : 0.0;
+            rows[u][k].v[c] = (FULL || c < ncol_ok) ? gather_ld(rp + col + c * LPE) : 0.0;
         }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -362,7 +392,7 @@ __device__ __forceinline__ void compute_range_fast(const Params<N>& p, const Sta
       for (int k = 0; k < N - 1; ++k) {
         const double* rp = fb[k] + static_cast<uint64_t>(w[u][k]) * RF;
 #pragma unroll
-        for (int c = 0; c < CPL; ++c) rows[u][k].v[c] = __ldg(rp + c * LPE);
+        for (int c = 0; c < CPL; ++c) rows[u][k].v[c] = gather_ld(rp + c * LPE);
       }
     consume(v, w, rows, next_row, U);
   }
@@ -385,7 +415,7 @@ __device__ __forceinline__ void compute_range_fast(const Params<N>& p, const Sta
         if (u < rem) {
           const double* rp = fb[k] + static_cast<uint64_t>(w[u][k]) * RF;
 #pragma unroll
-          for (int c = 0; c < CPL; ++c) rows[u][k].v[c] = __ldg(rp + c * LPE);
+          for (int c = 0; c < CPL; ++c) rows[u][k].v[c] = gather_ld(rp + c * LPE);
         }
     consume(v, w, rows, 0xffffffffu, rem);
   }
@@ -672,7 +702,7 @@ __device__ __forceinline__ void compute_range_f32(const ParamsF32<N>& p, const S
 #pragma unroll
         for (int c = 0; c < CPL; ++c)
           if (ok[u] && cok[c])
-            rows[u][k][c] = __ldg(reinterpret_cast<const VT*>(p.factors[k] + static_cast<uint64_t>(w[u][k]) * R +
+            rows[u][k][c] = gather_ld(reinterpret_cast<const VT*>(p.factors[k] + static_cast<uint64_t>(w[u][k]) * R +
                                                               col0 + V * (q + LPE * c)));
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
@@ -781,7 +811,7 @@ __device__ __forceinline__ void compute_range_f32_fast(const ParamsF32<N>& p, co
     for (int u = 0; u < U; ++u)
 #pragma unroll
       for (int k = 0; k < N - 1; ++k)
-        rows[u][k] = __ldg(reinterpret_cast<const VT*>(fb[k] + static_cast<uint64_t>(w[u][k]) * RF));
+        rows[u][k] = gather_ld(reinterpret_cast<const VT*>(fb[k] + static_cast<uint64_t>(w[u][k]) * RF));
     consume(v, w, rows, next_row, U);
   }
   const int rem = n - nfull * U;
@@ -800,7 +830,7 @@ __device__ __forceinline__ void compute_range_f32_fast(const ParamsF32<N>& p, co
     for (int u = 0; u < U; ++u)
 #pragma unroll
       for (int k = 0; k < N - 1; ++k)
-        if (u < rem) rows[u][k] = __ldg(reinterpret_cast<const VT*>(fb[k] + static_cast<uint64_t>(w[u][k]) * RF));
+        if (u < rem) rows[u][k] = gather_ld(reinterpret_cast<const VT*>(fb[k] + static_cast<uint64_t>(w[u][k]) * RF));
     consume(v, w, rows, 0xffffffffu, rem);
   }
 }
