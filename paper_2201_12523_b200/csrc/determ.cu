@@ -284,16 +284,18 @@ const DetIndex& det_index(const blco_tensor& t, int mode, cudaStream_t s) {
   return t.det.emplace(mode, std::move(d)).first->second;
 }
 
-thread_local DevBuf<double> t_partial;
+// per stream: launches on different streams of one thread may overlap
+thread_local std::map<cudaStream_t, DevBuf<double>> t_partials;
 
 }  // namespace
 
-void release_det_cache() { t_partial.reset(); }
+void release_det_cache() { t_partials.clear(); }
 
 void det_mttkrp_enqueue(const blco_tensor& t, MttkrpLaunch& a) {
   const DetIndex& d = det_index(t, a.mode, a.stream);
   const uint64_t elems = t.layout.dims[a.mode] * a.rank;
   if (!a.accumulate && elems) B200_CUDA(cudaMemsetAsync(a.out, 0, elems * 8, a.stream));
+  DevBuf<double>& t_partial = t_partials[a.stream];
   if (t_partial.n < d.nparts * a.rank) t_partial.alloc(d.nparts * a.rank);
   a.workgroups = d.chunk_begin.n;
   switch (t.layout.order) {

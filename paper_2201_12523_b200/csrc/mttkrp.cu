@@ -945,7 +945,9 @@ void merge_copies_enqueue(const double* copies, uint64_t elems, int ncopies, dou
 namespace {
 
 struct Workspace {
-  DevBuf<double> copies;
+  // hierarchical factor copies, one buffer per stream: launches on
+  // different streams of one thread may run concurrently
+  std::map<cudaStream_t, DevBuf<double>> copies;
   DevBuf<unsigned long long> counters;
   int device = -1;
 };
@@ -954,7 +956,7 @@ thread_local Workspace t_ws;
 }  // namespace
 
 void release_mttkrp_workspace() {
-  t_ws.copies.reset();
+  t_ws.copies.clear();
   t_ws.counters.reset();
   t_ws.device = -1;
 }
@@ -966,7 +968,7 @@ Workspace& workspace() {
   int dev = 0;
   B200_CUDA(cudaGetDevice(&dev));
   if (t_ws.device != dev) {
-    t_ws.copies.reset();
+    t_ws.copies.clear();
     t_ws.counters.reset();
     t_ws.device = dev;
   }
@@ -1071,13 +1073,13 @@ void launch_cfg(MttkrpLaunch& a) {
   bool merge = false;
   if (a.hier_copies) {
     p.out = a.hier_copies;  // caller merges once at the end
-  } else if (C == 1 && !a.accumulate) {
-    p.out = a.out;
+  } else if (C == 1) {
+    p.out = a.out;  // flushes add into M (zeroed above unless accumulating)
   } else {
-    Workspace& ws = workspace();
-    if (ws.copies.n < elems * C) ws.copies.alloc(elems * C);
-    B200_CUDA(cudaMemsetAsync(ws.copies.ptr, 0, elems * C * sizeof(double), a.stream));
-    p.out = ws.copies.ptr;
+    DevBuf<double>& cb = workspace().copies[a.stream];
+    if (cb.n < elems * C) cb.alloc(elems * C);
+    B200_CUDA(cudaMemsetAsync(cb.ptr, 0, elems * C * sizeof(double), a.stream));
+    p.out = cb.ptr;
     merge = true;
   }
   kern<<<dim3(static_cast<unsigned>(grid), ychunks), kCtaThreads, dyn, a.stream>>>(p);

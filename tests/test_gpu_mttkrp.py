@@ -306,3 +306,58 @@ def test_release_thread_caches(gpu, oracle):
     for m in range(3):
         assert rel_frobenius(got[m], want[m]) <= TOL
     assert rel_frobenius(gpu.mttkrp(t, f, 1, gpu.ExecConfig(deterministic=True)), want[1]) <= TOL
+
+
+_STREAMS_SCRIPT = r"""
+import sys, json
+import numpy as np
+import torch
+sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[1] + "/oracle")
+import paper_2201_12523_b200 as b
+from pyoracle import Oracle
+o = Oracle()
+out = {}
+cfgs = {"auto": (b.Strategy.Auto, b.ExecConfig()),
+        "hier_c3": (b.Strategy.Hierarchical, b.ExecConfig(num_factor_copies=3)),
+        "det": (b.Strategy.Auto, b.ExecConfig(deterministic=1))}
+for dims, nnz, R in (([300, 200, 500], 400_000, 32), ([64, 3000, 40, 9], 300_000, 16), ([5000, 7], 30_000, 8)):
+    dt = b.DeviceTensor.synthetic(dims, nnz, 11)
+    idx, vals = o.synth_uniform(dims, nnz, 11)
+    f = b.FactorMatrices.random(dims, R, 5)
+    fac = [torch.from_numpy(a).cuda() for a in f.factors]
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    for name, (strat, cfg) in cfgs.items():
+        errs = []
+        for m in range(len(dims)):
+            want = o.mttkrp_coo(dims, idx, vals, f.factors, m)
+            # accumulate=True launches back to back on one stream and
+            # concurrently on two (per-stream scratch: hierarchical copies,
+            # deterministic partials)
+            outs = [torch.zeros((dims[m], R), dtype=torch.float64, device="cuda") for _ in range(4)]
+            for k, o_ in enumerate(outs):
+                st = (s1, s1, s2, s2)[k]
+                dt.mttkrp_device([a.data_ptr() for a in fac], R, m, o_.data_ptr(), strat, cfg, accumulate=True,
+                                 stream=st.cuda_stream)
+            torch.cuda.synchronize()
+            for o_ in outs:
+                got = o_.cpu().numpy()
+                errs.append(float(np.sqrt(((got - want) ** 2).sum() / (want ** 2).sum())))
+        out[f"{dims} {name}"] = max(errs)
+print(json.dumps(out))
+"""
+
+
+def test_concurrent_streams_accumulate(gpu):
+    """blco_mttkrp_device with accumulate on two streams of one thread at
+    once (register, hierarchical with 3 factor copies, deterministic): each
+    launch's scratch is per stream, so every result matches the oracle."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = str(Path(__file__).resolve().parents[1])
+    r = subprocess.run([sys.executable, "-c", _STREAMS_SCRIPT, root], capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-2000:]
+    res = json.loads(r.stdout.strip().splitlines()[-1])
+    assert max(res.values()) <= TOL, res
