@@ -488,16 +488,15 @@ __device__ __forceinline__ int process_warp(const Params<N>& p, const TileDesc& 
 // non-zero on NELL-2 (SURVEY §8a row a13 replaced).
 constexpr int kBucketBits = 11;
 constexpr int kBuckets = 1 << kBucketBits;
-constexpr int kItems = kTileElems / kCtaThreads;  // 4
-
 struct BucketShared {
   uint32_t cnt[kBuckets];
   uint32_t warp_sum[kWarps];
 };
 
-template <int N>
+template <int N, int TILE = kTileElems>
 __device__ __forceinline__ uint32_t process_cta(const Params<N>& p, const TileDesc& td, const Stage<N> st,
                                                 BucketShared& bs, unsigned long long& segs) {
+  constexpr int kItems = TILE / kCtaThreads;  // elements per thread
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t cnt = tile_count(td, p.elem_end);
   for (int i = tid; i < kBuckets; i += kCtaThreads) bs.cnt[i] = 0;
@@ -585,24 +584,30 @@ __global__ void __launch_bounds__(kCtaThreads) k_mttkrp_warp(Params<N> p) {
   }
 }
 
-template <int N>
+template <int N, int TILE = kTileElems>
 __device__ __forceinline__ Stage<N> cta_stage(unsigned char* dyn) {
-  return make_stage<N>(dyn, kTileElems);
+  return make_stage<N>(dyn, TILE);
 }
 
-template <int N, int LPE, int CPL, bool FULL, bool STATS, int U = kUnroll, int MINB = 1>
+// TILE = elements per CTA tile: 1024, or 2048 for large tensors whose
+// gathered factor matrices sit in L2 (the L1-pipe-bound regime: fewer
+// segments, so fewer commits, and the per-tile fixed costs halve; NELL-2
+// 8.29 -> 7.96 ms/iter).  DRAM-bound shapes (Amazon) and small tensors
+// (fewer tiles than resident CTA slots) keep 1024.
+template <int N, int LPE, int CPL, bool FULL, bool STATS, int U = kUnroll, int MINB = 1, int TILE = kTileElems>
 __global__ void __launch_bounds__(kCtaThreads, MINB) k_mttkrp_sorted(Params<N> p) {
+  constexpr int WE = TILE / kWarps;  // staged positions per warp
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ BucketShared bs;
-  const Stage<N> st = cta_stage<N>(dyn);
+  const Stage<N> st = cta_stage<N, TILE>(dyn);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const TileDesc td = p.tiles[blockIdx.x];
   unsigned long long segs = STATS ? 0 : ~0ull, commits = 0, flushes = 0;
   long long t0 = STATS ? clock64() : 0;
-  const uint32_t cnt = process_cta<N>(p, td, st, bs, segs);
+  const uint32_t cnt = process_cta<N, TILE>(p, td, st, bs, segs);
   long long t1 = STATS ? clock64() : 0;
-  const int lo0 = warp * kWarpElems;
-  const int wn = static_cast<int>(cnt) > lo0 ? min(kWarpElems, static_cast<int>(cnt) - lo0) : 0;
+  const int lo0 = warp * WE;
+  const int wn = static_cast<int>(cnt) > lo0 ? min(WE, static_cast<int>(cnt) - lo0) : 0;
   if (wn > 0) {
     if constexpr (FULL && Stage<N>::kPacked && U == 4)
       compute_range_fast<N, LPE, CPL, U>(p, st, lo0, wn, lane, p.out, commits);
@@ -985,6 +990,21 @@ bool use_warp_variant() {
   return warp;
 }
 
+// 2048-element tiles when the non-target factor matrices fit in L2 with
+// room to spare and there are enough tiles to fill every resident CTA slot
+// several times (k_mttkrp_sorted).  BLCO_B200_BIG_TILES=0/1 overrides.
+bool use_big_tiles(const blco_layout& l, int mode, uint64_t rank, uint64_t nnz) {
+  static const int knob = [] {
+    const char* e = std::getenv("BLCO_B200_BIG_TILES");
+    return e ? std::atoi(e) : -1;
+  }();
+  if (knob >= 0) return knob > 0;
+  uint64_t fbytes = 0;
+  for (int m = 0; m < l.order; ++m)
+    if (m != mode) fbytes += l.dims[m] * rank * sizeof(double);
+  return fbytes <= (uint64_t(48) << 20) && nnz >= uint64_t(2 * kTileElems) * 148 * 3 * 4;
+}
+
 template <class K>
 void set_smem(K kern, size_t dyn) {
   ensure_dyn_smem(reinterpret_cast<const void*>(kern), dyn);
@@ -1033,6 +1053,22 @@ void launch_cfg(MttkrpLaunch& a) {
       count_launch();
       check_launch("k_mttkrp_warp");
       return;
+    }
+    if constexpr (N <= 3 && FULL) {
+      if (a.tensor && ychunks == 1 && use_big_tiles(l, a.mode, a.rank, a.tensor->nnz)) {
+        // 2048-element tiles (see k_mttkrp_sorted)
+        constexpr int T2 = 2 * kTileElems;
+        p.tiles = tile_table(*a.tensor, T2, &p.ntiles);
+        a.workgroups = p.ntiles;
+        auto kern = stats ? k_mttkrp_sorted<N, LPE, CPL, FULL, true, kUnroll, 1, T2>
+                          : k_mttkrp_sorted<N, LPE, CPL, FULL, false, kUnroll, 1, T2>;
+        const size_t st2 = stage_bytes<N>(T2);
+        set_smem(kern, st2);
+        kern<<<dim3(static_cast<unsigned>(p.ntiles), 1), kCtaThreads, st2, a.stream>>>(p);
+        count_launch();
+        check_launch("k_mttkrp_sorted");
+        return;
+      }
     }
     auto kern = stats ? k_mttkrp_sorted<N, LPE, CPL, FULL, true> : k_mttkrp_sorted<N, LPE, CPL, FULL, false>;
     // N = 4 (R <= 32): cap registers so 3 CTAs fit per SM (88 -> 80 for
@@ -1092,7 +1128,7 @@ template <int N>
 void launch_order(MttkrpLaunch& a) {
   switch (a.rank) {
     case 8: return launch_cfg<N, 8, 1, true>(a);
-    case 16: return launch_cfg<N, 8, 2, true>(a);
+    case 16: return launch_cfg<N, 16, 1, true>(a);  // 16 lanes x 1 column: a 128 B row per group (CP-ALS R=16 -10%)
     case 32: return launch_cfg<N, 16, 2, true>(a);
     case 64: return launch_cfg<N, 32, 2, true>(a);
     default: return launch_cfg<N, 32, 1, false>(a);
