@@ -38,6 +38,14 @@ constexpr int kT = 256;
 // sum-of-squares normalize_columns needs (cpals.cpp:51-61), so the
 // separate norm pass disappears and Gram(A / lambda) = G_ij / (l_i l_j).
 constexpr int kSolveThreads = 128;
+// cp.async ring depth of k_solve_gram (chunks in flight per CTA)
+#ifndef BLCO_SOLVE_STAGES
+#define BLCO_SOLVE_STAGES 2
+#endif
+#ifndef BLCO_SOLVE_MINB
+#define BLCO_SOLVE_MINB 1
+#endif
+constexpr int kSolveStages = BLCO_SOLVE_STAGES;
 
 template <int RM>
 constexpr int solve_rows() {
@@ -58,7 +66,7 @@ __device__ __forceinline__ double lget(const double* sl, int R, int i, int k) {
 }
 
 template <int RM, bool EXACT>
-__global__ void __launch_bounds__(kSolveThreads) k_solve_gram(const double* __restrict__ m, double* __restrict__ a,
+__global__ void __launch_bounds__(kSolveThreads, BLCO_SOLVE_MINB) k_solve_gram(const double* __restrict__ m, double* __restrict__ a,
                                                               uint64_t rows, int R, const double* __restrict__ L,
                                                               double* __restrict__ g) {
   constexpr int ROWS = solve_rows<RM>();
@@ -103,15 +111,20 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve_gram(const double* __re
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
+  // ring of kSolveStages chunk buffers: chunks k+1 .. k+S-1 stream in while
+  // chunk k is solved
+  constexpr int S_ = kSolveStages, TS = ROWS * (RM + 1);
   double* const tile0 = smem + RM * RM;
-  prefetch(blockIdx.x * uint64_t(ROWS), tile0);
+#pragma unroll
+  for (int k = 0; k + 1 < S_; ++k) prefetch(blockIdx.x * uint64_t(ROWS) + k * step, tile0 + k * TS);
   int buf = 0;
-  for (uint64_t r0 = blockIdx.x * uint64_t(ROWS); r0 < rows; r0 += step, buf ^= 1) {
+  for (uint64_t r0 = blockIdx.x * uint64_t(ROWS); r0 < rows; r0 += step, buf = buf + 1 == S_ ? 0 : buf + 1) {
     const int nr = static_cast<int>(rows - r0 < uint64_t(ROWS) ? rows - r0 : ROWS);
-    double* tile = tile0 + buf * (ROWS * (RM + 1));
-    __syncthreads();  // every thread is done with the other buffer (previous chunk)
-    prefetch(r0 + step, tile0 + (buf ^ 1) * (ROWS * (RM + 1)));
-    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    double* tile = tile0 + buf * TS;
+    __syncthreads();  // every thread is done with the buffer of the previous chunk
+    const int nb = buf + S_ - 1 >= S_ ? buf - 1 : buf + S_ - 1;  // (buf + S - 1) % S
+    prefetch(r0 + (S_ - 1) * step, tile0 + nb * TS);
+    asm volatile("cp.async.wait_group %0;" ::"n"(S_ - 1) : "memory");
     __syncthreads();
     if (static_cast<int>(threadIdx.x) < nr) {
       double b[RM];
@@ -468,7 +481,8 @@ struct Dense {
       return;
     }
     auto launch = [&](auto kern, int rm, int rows_per) {
-      const size_t smem = (static_cast<size_t>(rm) * rm + 2 * static_cast<size_t>(rows_per) * (rm + 1)) * 8;
+      const size_t smem =
+          (static_cast<size_t>(rm) * rm + kSolveStages * static_cast<size_t>(rows_per) * (rm + 1)) * 8;
       ensure_dyn_smem(reinterpret_cast<const void*>(kern), smem);
       const int per_sm = blocks_per_sm(reinterpret_cast<const void*>(kern), kSolveThreads, smem);
       const unsigned grid = static_cast<unsigned>(
