@@ -1061,7 +1061,7 @@ void launch_cfg(MttkrpLaunch& a) {
         p.tiles = tile_table(*a.tensor, T2, &p.ntiles);
         a.workgroups = p.ntiles;
         auto kern = stats ? k_mttkrp_sorted<N, LPE, CPL, FULL, true, kUnroll, 1, T2>
-                          : k_mttkrp_sorted<N, LPE, CPL, FULL, false, kUnroll, 1, T2>;
+                          : k_mttkrp_sorted<N, LPE, CPL, FULL, false, kUnroll, 3, T2>;  // <= 80 regs: 3 CTAs/SM (91 -> 2)
         const size_t st2 = stage_bytes<N>(T2);
         set_smem(kern, st2);
         kern<<<dim3(static_cast<unsigned>(p.ntiles), 1), kCtaThreads, st2, a.stream>>>(p);
