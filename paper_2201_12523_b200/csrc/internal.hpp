@@ -161,6 +161,7 @@ namespace b200 {
 // What one MTTKRP launch reads: the payload, its tile table and block bases.
 struct KernelView {
   const blco_layout* layout;
+  const blco_tensor* tensor;  // device-resident tensor (null for the streamed / pipelined views)
   const TileDesc* tiles;
   uint64_t ntiles;
   uint64_t elem_end;

@@ -840,17 +840,18 @@ __device__ __forceinline__ void compute_range_f32_fast(const ParamsF32<N>& p, co
   }
 }
 
-template <int N, int LPE, int V, int CPL, bool FULL>
-__global__ void __launch_bounds__(kCtaThreads) k_mttkrp_sorted_f32(ParamsF32<N> p) {
+template <int N, int LPE, int V, int CPL, bool FULL, int TILE = kTileElems, int MINB = 1>
+__global__ void __launch_bounds__(kCtaThreads, MINB) k_mttkrp_sorted_f32(ParamsF32<N> p) {
+  constexpr int WE = TILE / kWarps;
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ BucketShared bs;
-  const Stage<N> st = cta_stage<N>(dyn);
+  const Stage<N> st = cta_stage<N, TILE>(dyn);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const TileDesc td = p.base.tiles[blockIdx.x];
   unsigned long long segs = ~0ull;
-  const uint32_t cnt = process_cta<N>(p.base, td, st, bs, segs);
-  const int lo0 = warp * kWarpElems;
-  const int wn = static_cast<int>(cnt) > lo0 ? min(kWarpElems, static_cast<int>(cnt) - lo0) : 0;
+  const uint32_t cnt = process_cta<N, TILE>(p.base, td, st, bs, segs);
+  const int lo0 = warp * WE;
+  const int wn = static_cast<int>(cnt) > lo0 ? min(WE, static_cast<int>(cnt) - lo0) : 0;
   if (wn > 0) {
     if constexpr (FULL && CPL == 1 && Stage<N>::kPacked)
       compute_range_f32_fast<N, LPE, V>(p, st, lo0, wn, lane);
@@ -930,6 +931,7 @@ uint32_t mttkrp_tile_elems() { return kTileElems; }
 KernelView view_of(const blco_tensor& t) {
   KernelView v{};
   v.layout = &t.layout;
+  v.tensor = &t;
   v.tiles = tile_table(t, kTileElems, &v.ntiles);
   v.elem_end = t.nnz;
   v.idx = t.idx.ptr;
@@ -993,7 +995,7 @@ bool use_warp_variant() {
 // 2048-element tiles when the non-target factor matrices fit in L2 with
 // room to spare and there are enough tiles to fill every resident CTA slot
 // several times (k_mttkrp_sorted).  BLCO_B200_BIG_TILES=0/1 overrides.
-bool use_big_tiles(const blco_layout& l, int mode, uint64_t rank, uint64_t nnz) {
+bool use_big_tiles(const blco_layout& l, int mode, uint64_t rank, uint64_t nnz, uint64_t elem_bytes = 8) {
   static const int knob = [] {
     const char* e = std::getenv("BLCO_B200_BIG_TILES");
     return e ? std::atoi(e) : -1;
@@ -1001,7 +1003,7 @@ bool use_big_tiles(const blco_layout& l, int mode, uint64_t rank, uint64_t nnz) 
   if (knob >= 0) return knob > 0;
   uint64_t fbytes = 0;
   for (int m = 0; m < l.order; ++m)
-    if (m != mode) fbytes += l.dims[m] * rank * sizeof(double);
+    if (m != mode) fbytes += l.dims[m] * rank * elem_bytes;
   return fbytes <= (uint64_t(48) << 20) && nnz >= uint64_t(2 * kTileElems) * 148 * 3 * 4;
 }
 
@@ -1156,6 +1158,19 @@ void launch_f32_cfg(const KernelView& v, const float* const* factors, uint64_t r
   p.out = out;
   if (v.ntiles == 0) return;
   const unsigned ychunks = static_cast<unsigned>((rank + LPE * V * CPL - 1) / (LPE * V * CPL));
+  if constexpr (N <= 3 && FULL) {
+    if (v.tensor && ychunks == 1 && use_big_tiles(l, mode, rank, v.tensor->nnz, sizeof(float))) {
+      constexpr int T2 = 2 * kTileElems;  // as the fp64 kernel (k_mttkrp_sorted)
+      p.base.tiles = tile_table(*v.tensor, T2, &p.base.ntiles);
+      const size_t st2 = stage_bytes<N>(T2);
+      auto kern = k_mttkrp_sorted_f32<N, LPE, V, CPL, FULL, T2, 3>;
+      set_smem(kern, st2);
+      kern<<<dim3(static_cast<unsigned>(p.base.ntiles), 1), kCtaThreads, st2, s>>>(p);
+      count_launch();
+      check_launch("k_mttkrp_sorted_f32");
+      return;
+    }
+  }
   const size_t stage = stage_bytes<N>(kTileElems);
   auto kern = k_mttkrp_sorted_f32<N, LPE, V, CPL, FULL>;
   set_smem(kern, stage);
