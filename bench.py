@@ -547,20 +547,38 @@ def e2e_run(b, torch, dt, dims, R, N, nnz, args, dev, world):
     cfg = b.ExecConfig(num_compute_units=torch.cuda.get_device_properties(dev).multi_processor_count)
     strategy = b.Strategy[args.strategy]
     rep = b.AllModesReport()
+    rs = world > 1 and args.reduce == "reducescatter"
+    d2h = sum(d * R * 8 for d in dims)
     if world > 1:
         import torch.distributed as dist
-        douts = [torch.empty((d, R), dtype=torch.float64, device=f"cuda:{dev}") for d in dims]
-        touts = [torch.from_numpy(o) for o in outs]
+        if rs:
+            # row-padded partials (the padding rows stay zero), each rank
+            # reads back its own row shard of every M_n
+            from paper_2201_12523_b200.dist import Collectives, row_shard
+            coll = Collectives()
+            pads = [row_shard(d, world, 0)[2] for d in dims]
+            douts = [torch.zeros((world * p, R), dtype=torch.float64, device=f"cuda:{dev}") for p in pads]
+            shards = [torch.empty((p, R), dtype=torch.float64, device=f"cuda:{dev}") for p in pads]
+            touts = [torch.from_numpy(b.api.pinned_empty(p * R, np.float64).reshape(p, R)) for p in pads]
+            d2h = sum(p * R * 8 for p in pads)
+        else:
+            douts = [torch.empty((d, R), dtype=torch.float64, device=f"cuda:{dev}") for d in dims]
+            touts = [torch.from_numpy(o) for o in outs]
 
     def step():
         if world == 1:
             b.mttkrp_all_modes(ht, f, cfg, strategy, outs=outs, device=dev, report=rep)
             return
         b.mttkrp_all_modes(ht, f, cfg, strategy, device=dev, report=rep, device_outs=[o.data_ptr() for o in douts])
-        works = [dist.all_reduce(o, async_op=True) for o in douts]
-        for w, o, t in zip(works, douts, touts):
-            w.wait()
-            t.copy_(o, non_blocking=True)
+        if rs:
+            for o, sh, t in zip(douts, shards, touts):
+                coll.reduce_scatter(sh, o)
+                t.copy_(sh, non_blocking=True)
+        else:
+            works = [dist.all_reduce(o, async_op=True) for o in douts]
+            for w, o, t in zip(works, douts, touts):
+                w.wait()
+                t.copy_(o, non_blocking=True)
         torch.cuda.current_stream().synchronize()
 
     for _ in range(max(1, min(args.warmup, 3))):
@@ -578,7 +596,6 @@ def e2e_run(b, torch, dt, dims, R, N, nnz, args, dev, world):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         wall_ms = float(t.item())
     bpe = bytes_per_elem(N, R)
-    d2h = sum(d * R * 8 for d in dims)
     return {"value": round(nnz * N * bpe / (wall_ms * 1e-3) / 1e9, 2), "unit": "GB/s",
             "ms_per_step": round(wall_ms, 3), "api_device_ms_per_call": round(rep.device_ms, 3), "steps": n,
             "h2d_bytes_per_step": int(rep.h2d_bytes), "d2h_bytes_per_step": int(d2h),
@@ -586,7 +603,9 @@ def e2e_run(b, torch, dt, dims, R, N, nnz, args, dev, world):
             "timing": "host wall clock per step (synchronous API), max over ranks",
             "path": "mttkrp_all_modes (blco_mttkrp_all_host): pinned host payload uploaded in chunks under "
                     "the all-mode kernels, host factors in, M_n out to pinned host memory"
-                    + ("" if world == 1 else " after an NCCL all-reduce of the ranks' device partials")}
+                    + ("" if world == 1 else
+                       " after an NCCL reduce-scatter of the ranks' device partials (each rank reads its row shard)"
+                       if rs else " after an NCCL all-reduce of the ranks' device partials")}
 
 
 # ------------------------------------------------------------ reference arm

@@ -36,13 +36,16 @@ def _torchrun(args, timeout=600, world=2):
     return json.loads(lines[0])
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_multi_rank_all_mode_step(gpu, world):
-    """G ranks vs G = 1 (SURVEY.md 4 "multi-node without a cluster")."""
-    d = _torchrun(["--config", "cfg1", "--steps", "2", "--warmup", "3", "--no-cpu-baseline", "--check"], world=world)
+@pytest.mark.parametrize("world,combine", [(2, "reducescatter"), (3, "allreduce")])
+def test_multi_rank_all_mode_step(gpu, world, combine):
+    """G ranks vs G = 1 (SURVEY.md 4 "multi-node without a cluster"), the
+    device step and the e2e step, with either combine of the partials."""
+    d = _torchrun(["--config", "cfg1", "--steps", "2", "--warmup", "3", "--no-cpu-baseline", "--check",
+                   "--reduce", combine], world=world)
     assert d["n_gpus"] == world and d["value"] > 0
     assert max(d["check"]["rel_frobenius_vs_single_device"]) <= 1e-12
-    assert d["e2e"]["value"] > 0 and "all-reduce" in d["e2e"]["path"]
+    word = "reduce-scatter" if combine == "reducescatter" else "all-reduce"
+    assert d["e2e"]["value"] > 0 and word in d["e2e"]["path"] and word in d["config"]["parallelism"]
 
 
 def test_two_rank_reference_arm_prints_once(gpu):
