@@ -361,3 +361,48 @@ def test_concurrent_streams_accumulate(gpu):
     assert r.returncode == 0, r.stderr[-2000:]
     res = json.loads(r.stdout.strip().splitlines()[-1])
     assert max(res.values()) <= TOL, res
+
+
+_BIG_TILES_SCRIPT = r"""
+import sys, json
+import numpy as np
+sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[1] + "/oracle")
+import paper_2201_12523_b200 as b
+from pyoracle import Oracle
+o = Oracle()
+out = {}
+rng = np.random.default_rng(5)
+for dims, nnz, cap in (([300, 200, 500], 200_000, 3000), ([5000, 7], 30_000, 2047), ([90, 80, 70], 100_000, 1 << 27),
+                       ([2000, 3000, 10], 150_000, 4097)):
+    coo = b.synth_uniform_host(dims, nnz, 3)
+    t = b.build_blco(coo, 64, cap)  # many blocks, ragged tile tails at every block end
+    for R in (8, 16, 32, 64):
+        f = b.FactorMatrices(R, [rng.uniform(-1, 1, (d, R)) for d in dims])
+        for m in range(len(dims)):
+            want = o.mttkrp_coo(dims, coo.indices, coo.values, f.factors, m)
+            got = b.mttkrp(t, f, m, strategy=b.Strategy.Register)
+            got32 = b.mttkrp_f32(t, b.FactorMatrices(R, [a.astype(np.float32) for a in f.factors]), m)
+            e = float(np.sqrt(((got - want) ** 2).sum() / (want ** 2).sum()))
+            e32 = float(np.sqrt(((got32 - want) ** 2).sum() / (want ** 2).sum()))
+            out[f"{dims} cap {cap} R {R} mode {m}"] = [e, e32]
+print(json.dumps(out))
+"""
+
+
+def test_big_tiles_forced_on_ragged_blocks(gpu):
+    """The 2048-element tile path (fp64 and fp32 kernels) forced on
+    (BLCO_B200_BIG_TILES=1) for tensors of many small blocks, where every
+    block ends in a ragged tile: fp64 within 1e-12, fp32 within 1e-5."""
+    import json
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = str(Path(__file__).resolve().parents[1])
+    r = subprocess.run([sys.executable, "-c", _BIG_TILES_SCRIPT, root], capture_output=True, text=True,
+                       env=dict(os.environ, BLCO_B200_BIG_TILES="1"), timeout=900)
+    assert r.returncode == 0, r.stderr[-2000:]
+    res = json.loads(r.stdout.strip().splitlines()[-1])
+    assert max(v[0] for v in res.values()) <= TOL, res
+    assert max(v[1] for v in res.values()) <= 1e-5, res
