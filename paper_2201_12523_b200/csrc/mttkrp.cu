@@ -38,8 +38,42 @@ namespace {
 #ifndef BLCO_GATHER
 #define BLCO_GATHER 0
 #endif
+// L2 eviction priorities (compile time, BLCO_L2HINT bits): 1 = segment
+// commits (RED) evict_last, 2 = factor-row gathers evict_first.  A missed
+// commit costs a DRAM read and a later write-back, a missed gather only the
+// read, so keeping output lines longer may pay on DRAM-bound shapes.
+#ifndef BLCO_L2HINT
+#define BLCO_L2HINT 0
+#endif
+__device__ __forceinline__ uint64_t l2_evict_last() {
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t l2_evict_first() {
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void commit_add(double* a, double v) {
+#if BLCO_L2HINT & 1
+  asm volatile("red.global.add.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a), "d"(v), "l"(l2_evict_last()) : "memory");
+#else
+  atomicAdd(a, v);
+#endif
+}
+
 template <class T>
 __device__ __forceinline__ T gather_ld(const T* p) {
+#if BLCO_L2HINT & 2
+  if constexpr (sizeof(T) == 8) {
+    unsigned long long x;
+    asm("ld.global.nc.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(x) : "l"(p), "l"(l2_evict_first()));
+    T r;
+    memcpy(&r, &x, 8);
+    return r;
+  }
+#endif
 #if BLCO_GATHER == 1
   return __ldcg(p);
 #elif BLCO_GATHER == 2 || BLCO_GATHER == 3
@@ -295,13 +329,13 @@ __device__ __forceinline__ void compute_range(const Params<N>& p, const Stage<N>
           } else {
 #pragma unroll
             for (int c = 0; c < CPL; ++c)
-              if (FULL || c < ncol_ok) atomicAdd(copy_out + static_cast<uint64_t>(row) * R + col + c * LPE, acc[c]);
+              if (FULL || c < ncol_ok) commit_add(copy_out + static_cast<uint64_t>(row) * R + col + c * LPE, acc[c]);
             if (q == 0) ++flushes;
           }
         } else {
 #pragma unroll
           for (int c = 0; c < CPL; ++c)
-            if (FULL || c < ncol_ok) atomicAdd(copy_out + static_cast<uint64_t>(row) * R + col + c * LPE, acc[c]);
+            if (FULL || c < ncol_ok) commit_add(copy_out + static_cast<uint64_t>(row) * R + col + c * LPE, acc[c]);
         }
         if (FULL || ncol_ok > 0) ++commits;
 #pragma unroll
@@ -361,7 +395,7 @@ __device__ __forceinline__ void compute_range_fast(const Params<N>& p, const Sta
         if (nrow != row) {
           double* o = ob + static_cast<uint64_t>(row) * RF;
 #pragma unroll
-          for (int c = 0; c < CPL; ++c) atomicAdd(o + c * LPE, acc[c]);
+          for (int c = 0; c < CPL; ++c) commit_add(o + c * LPE, acc[c]);
           ++commits;
 #pragma unroll
           for (int c = 0; c < CPL; ++c) acc[c] = 0.0;
