@@ -502,8 +502,12 @@ const TileDesc* tile_table(const blco_tensor& t, uint32_t tile_elems, uint64_t* 
         h.push_back(TileDesc{off, static_cast<uint32_t>(std::min<uint64_t>(tile_elems, t.offsets[b + 1] - off)),
                              static_cast<uint32_t>(b)});
     DevBuf<TileDesc> d(h.size());
-    if (!h.empty())
+    if (!h.empty()) {
       B200_CUDA(cudaMemcpy(d.ptr, h.data(), h.size() * sizeof(TileDesc), cudaMemcpyHostToDevice));
+      // the table is read by kernels on any stream, non-blocking ones
+      // included: wait until the staged pageable copy has landed
+      B200_CUDA(cudaDeviceSynchronize());
+    }
     it = t.tiles.emplace(tile_elems, std::move(d)).first;
   }
   *ntiles = it->second.n;

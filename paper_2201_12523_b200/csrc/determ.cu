@@ -280,6 +280,8 @@ const DetIndex& det_index(const blco_tensor& t, int mode, cudaStream_t s) {
   up(d.multi_nparts, mn);
   up(d.block_off, t.offsets);
   d.nparts = parts;
+  // staged pageable uploads above: land them before kernels on any stream
+  B200_CUDA(cudaDeviceSynchronize());
   std::lock_guard<std::mutex> g(t.mu);
   return t.det.emplace(mode, std::move(d)).first->second;
 }

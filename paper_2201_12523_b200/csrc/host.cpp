@@ -1,3 +1,4 @@
+#include <cstdlib>
 // host.cpp -- host-side pieces of the C ABI: errors, bit layout, batch table,
 // config, partitioning and the host restatements of the seeded generators.
 //
@@ -67,6 +68,11 @@ int blocks_per_sm(const void* kernel, int threads, size_t dyn_smem) {
   B200_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, threads, dyn_smem));
   g_occupancy[key] = n;
   return n;
+}
+
+bool poison_allocations() {
+  static const bool on = std::getenv("BLCO_B200_POISON") != nullptr;
+  return on;
 }
 
 int bits_for_extent(uint64_t extent) { return extent <= 1 ? 0 : 64 - __builtin_clzll(extent - 1); }

@@ -74,6 +74,10 @@ blco_layout make_layout(const uint64_t* dims, int order, int target_bits);
 uint64_t key_upper(const blco_layout& l, int mode, uint64_t key);
 
 // --------------------------------------------------------- device buffers
+// BLCO_B200_POISON=1 (debug): fill every new device buffer with 0xFF bytes
+// (NaN doubles, all-ones indices), so a read before the first write shows.
+bool poison_allocations();
+
 template <class T>
 struct DevBuf {
   T* ptr = nullptr;
@@ -94,7 +98,10 @@ struct DevBuf {
   ~DevBuf() { reset(); }
   void alloc(size_t count) {
     reset();
-    if (count) B200_CUDA(cudaMalloc(&ptr, count * sizeof(T)));
+    if (count) {
+      B200_CUDA(cudaMalloc(&ptr, count * sizeof(T)));
+      if (poison_allocations()) B200_CUDA(cudaMemset(ptr, 0xFF, count * sizeof(T)));
+    }
     n = count;
   }
   void reset() {

@@ -24,6 +24,7 @@
 //   shared-memory stash (hierarchical path, :139-155), whose rows flush to
 //   the CTA's factor copy at the end (:210-215).
 #include <algorithm>
+#include <type_traits>
 #include <cstdlib>
 #include <cstring>
 
@@ -142,6 +143,7 @@ struct Stage {
   static constexpr int NM = (N + 3) / 4;
   static constexpr bool kPacked = N <= 3;
   static constexpr int kRowPad = 8;  // row plane over-read by the 4-row loads
+  static constexpr bool kRowInRecord = false;
   double* val;     // [W] (general layout)
   uint4* meta;     // general: [NM][W]; packed: records [W]
   uint32_t* rows;  // packed: [W + kRowPad]
@@ -203,6 +205,30 @@ __device__ __forceinline__ Stage<N> make_stage(unsigned char* base, int W) {
     return Stage<N>{reinterpret_cast<double*>(base + Stage<N>::NM * sizeof(uint4) * W), reinterpret_cast<uint4*>(base),
                     nullptr, W};
 }
+
+// Compact staging for N = 3 when both non-target coordinates fit in 16
+// bits (NELL-2: 14-15 bits): one 16-byte record {value, w0 | w1 << 16, row}
+// per element and no row plane -- 20 -> 16 B of shared memory per element
+// (more L1 beside the staging) and one LDS.128 per element in the computing
+// phase instead of a record plus a share of the row plane.
+struct StageC {
+  static constexpr int NM = 1;
+  static constexpr bool kPacked = true;
+  static constexpr bool kRowInRecord = true;
+  uint4* meta;
+  __device__ __forceinline__ void put(int j, double v, const uint32_t (&w)[4]) const {
+    const uint64_t b = static_cast<uint64_t>(__double_as_longlong(v));
+    meta[j] = make_uint4(static_cast<uint32_t>(b), static_cast<uint32_t>(b >> 32), w[0] | (w[1] << 16), w[2]);
+  }
+  __device__ __forceinline__ void get(int j, double& v, uint32_t (&w)[4]) const {
+    const uint4 x = meta[j];
+    v = __longlong_as_double(static_cast<long long>((static_cast<uint64_t>(x.y) << 32) | x.x));
+    w[0] = x.z & 0xffffu;
+    w[1] = x.z >> 16;
+    w[2] = x.w;
+  }
+  __device__ __forceinline__ uint32_t row(int j) const { return reinterpret_cast<const uint32_t*>(meta)[4 * j + 3]; }
+};
 
 // Decodes one element into packed words (non-target modes ascending, row last).
 template <int N>
@@ -351,14 +377,14 @@ __device__ __forceinline__ void compute_range(const Params<N>& p, const Stage<N>
 // stripped: the row stride is a compile-time constant, the lane's column
 // offset is folded into per-mode base pointers once, and every batch but the
 // group's last runs without element masks.
-template <int N, int LPE, int CPL, int U>
-__device__ __forceinline__ void compute_range_fast(const Params<N>& p, const Stage<N> st, int lo0, int wn, int lane,
+template <int N, int LPE, int CPL, int U, class ST = Stage<N>>
+__device__ __forceinline__ void compute_range_fast(const Params<N>& p, const ST st, int lo0, int wn, int lane,
                                                    double* __restrict__ out, unsigned long long& commits) {
   constexpr int G = 32 / LPE;
   constexpr int NW = 4 * Stage<N>::NM;
   constexpr int NO = N > 1 ? N - 1 : 1;
   constexpr int RF = LPE * CPL;
-  constexpr bool kRows4 = G == 2 && U == 4;
+  constexpr bool kRows4 = G == 2 && U == 4 && !ST::kRowInRecord;
   const int g = lane / LPE, q = lane % LPE;
   int h = wn / G;
   if constexpr (kRows4) {
@@ -412,7 +438,9 @@ __device__ __forceinline__ void compute_range_fast(const Params<N>& p, const Sta
     Row<CPL> rows[U][NO];
 #pragma unroll
     for (int u = 0; u < U; ++u) st.get(j0 + u, v[u], w[u]);
-    if constexpr (kRows4) {
+    if constexpr (ST::kRowInRecord) {
+      // the row came with the record
+    } else if constexpr (kRows4) {
       const uint4 r4 = st.rows4(j0);
       w[0][N - 1] = r4.x, w[1][N - 1] = r4.y, w[2][N - 1] = r4.z, w[3][N - 1] = r4.w;
     } else {
@@ -440,7 +468,7 @@ __device__ __forceinline__ void compute_range_fast(const Params<N>& p, const Sta
     for (int u = 0; u < U; ++u) {
       const int j = u < rem ? j0 + u : j0;
       st.get(j, v[u], w[u]);
-      w[u][N - 1] = st.row(j);
+      if constexpr (!ST::kRowInRecord) w[u][N - 1] = st.row(j);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u)
@@ -527,8 +555,8 @@ struct BucketShared {
   uint32_t warp_sum[kWarps];
 };
 
-template <int N, int TILE = kTileElems>
-__device__ __forceinline__ uint32_t process_cta(const Params<N>& p, const TileDesc& td, const Stage<N> st,
+template <int N, int TILE = kTileElems, class ST = Stage<N>>
+__device__ __forceinline__ uint32_t process_cta(const Params<N>& p, const TileDesc& td, const ST st,
                                                 BucketShared& bs, unsigned long long& segs) {
   constexpr int kItems = TILE / kCtaThreads;  // elements per thread
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -628,24 +656,28 @@ __device__ __forceinline__ Stage<N> cta_stage(unsigned char* dyn) {
 // segments, so fewer commits, and the per-tile fixed costs halve; NELL-2
 // 8.29 -> 7.96 ms/iter).  DRAM-bound shapes (Amazon) and small tensors
 // (fewer tiles than resident CTA slots) keep 1024.
-template <int N, int LPE, int CPL, bool FULL, bool STATS, int U = kUnroll, int MINB = 1, int TILE = kTileElems>
+template <int N, int LPE, int CPL, bool FULL, bool STATS, int U = kUnroll, int MINB = 1, int TILE = kTileElems,
+          bool CMP = false>
 __global__ void __launch_bounds__(kCtaThreads, MINB) k_mttkrp_sorted(Params<N> p) {
   constexpr int WE = TILE / kWarps;  // staged positions per warp
+  using ST = std::conditional_t<CMP, StageC, Stage<N>>;
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ BucketShared bs;
-  const Stage<N> st = cta_stage<N, TILE>(dyn);
+  ST st;
+  if constexpr (CMP) st = StageC{reinterpret_cast<uint4*>(dyn)};
+  else st = cta_stage<N, TILE>(dyn);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const TileDesc td = p.tiles[blockIdx.x];
   unsigned long long segs = STATS ? 0 : ~0ull, commits = 0, flushes = 0;
   long long t0 = STATS ? clock64() : 0;
-  const uint32_t cnt = process_cta<N, TILE>(p, td, st, bs, segs);
+  const uint32_t cnt = process_cta<N, TILE, ST>(p, td, st, bs, segs);
   long long t1 = STATS ? clock64() : 0;
   const int lo0 = warp * WE;
   const int wn = static_cast<int>(cnt) > lo0 ? min(WE, static_cast<int>(cnt) - lo0) : 0;
   if (wn > 0) {
     if constexpr (FULL && Stage<N>::kPacked && U == 4)
-      compute_range_fast<N, LPE, CPL, U>(p, st, lo0, wn, lane, p.out, commits);
-    else
+      compute_range_fast<N, LPE, CPL, U, ST>(p, st, lo0, wn, lane, p.out, commits);
+    else if constexpr (!CMP)
       compute_range<N, LPE, CPL, FULL, false, U>(p, st, lo0, wn, lane, blockIdx.y * LPE * CPL, p.out, nullptr,
                                               nullptr, commits, flushes);
   }
@@ -1041,6 +1073,15 @@ bool use_big_tiles(const blco_layout& l, int mode, uint64_t rank, uint64_t nnz, 
   return fbytes <= (uint64_t(48) << 20) && nnz >= uint64_t(2 * kTileElems) * 148 * 3 * 4;
 }
 
+// BLCO_B200_COMPACT_STAGE=0 disables the compact N = 3 staging (StageC).
+bool compact_stage_knob() {
+  static const bool on = [] {
+    const char* e = std::getenv("BLCO_B200_COMPACT_STAGE");
+    return !(e && std::string(e) == "0");
+  }();
+  return on;
+}
+
 template <class K>
 void set_smem(K kern, size_t dyn) {
   ensure_dyn_smem(reinterpret_cast<const void*>(kern), dyn);
@@ -1098,7 +1139,17 @@ void launch_cfg(MttkrpLaunch& a) {
         a.workgroups = p.ntiles;
         auto kern = stats ? k_mttkrp_sorted<N, LPE, CPL, FULL, true, kUnroll, 1, T2>
                           : k_mttkrp_sorted<N, LPE, CPL, FULL, false, kUnroll, 3, T2>;  // <= 80 regs: 3 CTAs/SM (91 -> 2)
-        const size_t st2 = stage_bytes<N>(T2);
+        size_t st2 = stage_bytes<N>(T2);
+        if constexpr (N == 3) {
+          bool narrow = compact_stage_knob();
+          for (int m = 0; m < N; ++m)
+            if (m != a.mode && l.dims[m] > 65536) narrow = false;
+          if (narrow) {  // 16-byte records with the row inside (StageC)
+            kern = stats ? k_mttkrp_sorted<N, LPE, CPL, FULL, true, kUnroll, 1, T2, true>
+                         : k_mttkrp_sorted<N, LPE, CPL, FULL, false, kUnroll, 3, T2, true>;
+            st2 = static_cast<size_t>(T2) * sizeof(uint4);
+          }
+        }
         set_smem(kern, st2);
         kern<<<dim3(static_cast<unsigned>(p.ntiles), 1), kCtaThreads, st2, a.stream>>>(p);
         count_launch();

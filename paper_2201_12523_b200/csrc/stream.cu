@@ -12,6 +12,7 @@
 // intervals come from CUDA events.
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <fcntl.h>
 #include <unistd.h>
@@ -51,6 +52,7 @@ struct Queue {
   DevBuf<double> vals;
   DevBuf<uint32_t> base;
   DevBuf<TileDesc> tiles;
+  std::vector<TileDesc> htiles;  // host copy, alive while its upload is in flight
   uint64_t capacity = 0;  // elements
 };
 
@@ -218,11 +220,17 @@ void stream_impl(const blco_layout* layout, uint64_t max_nnz_per_block, BlockFee
           q.idx.alloc(cap);
           q.vals.alloc(cap);
           q.base.alloc(BLCO_MAX_DEV_ORDER);
-          std::vector<TileDesc> h;
+          std::vector<TileDesc>& h = q.htiles;
+          h.clear();
           for (uint64_t off = 0; off < cap; off += tile)
             h.push_back(TileDesc{off, static_cast<uint32_t>(std::min<uint64_t>(tile, cap - off)), 0u});
           q.tiles.alloc(h.size());
-          B200_CUDA(cudaMemcpy(q.tiles.ptr, h.data(), h.size() * sizeof(TileDesc), cudaMemcpyHostToDevice));
+          // ordered on the queue's stream: a plain cudaMemcpy from pageable
+          // memory returns once the data is staged, and the queue is a
+          // non-blocking stream -- its kernels could read the table before
+          // the DMA lands (seen as a wrong block every few calls with 3 queues)
+          B200_CUDA(cudaMemcpyAsync(q.tiles.ptr, h.data(), h.size() * sizeof(TileDesc), cudaMemcpyHostToDevice,
+                                    q.stream));
           q.capacity = cap;
         }
         NvtxRange nv("stream: block transfer + compute");
@@ -248,7 +256,12 @@ void stream_impl(const blco_layout* layout, uint64_t max_nnz_per_block, BlockFee
         feed.transferred(ordinal, tr.e);
         if (feed.validate()) enqueue_block_check(l, bv.key, q.idx.ptr, bv.nnz, dbad.ptr, q.stream);
         // a transient source buffer may be overwritten by the next pull
-        if (bv.nnz && !(bv.flags & BLCO_BLOCK_STABLE) && (!is_pinned(bv.idx) || !is_pinned(bv.vals)))
+        static const int dbg_sync = [] {
+          const char* e = std::getenv("BLCO_B200_STREAM_SYNC");
+          return e ? std::atoi(e) : 0;
+        }();
+        if ((dbg_sync & 1) ||
+            (bv.nnz && !(bv.flags & BLCO_BLOCK_STABLE) && (!is_pinned(bv.idx) || !is_pinned(bv.vals))))
           B200_CUDA(cudaEventSynchronize(tr.e));
 
         B200_CUDA(cudaEventRecord(cp.b, q.stream));
@@ -273,6 +286,7 @@ void stream_impl(const blco_layout* layout, uint64_t max_nnz_per_block, BlockFee
           mttkrp_enqueue(a);
         }
         B200_CUDA(cudaEventRecord(cp.e, q.stream));
+        if (dbg_sync & 2) B200_CUDA(cudaEventSynchronize(cp.e));
         bytes += bbytes;
         ++ordinal;
       }

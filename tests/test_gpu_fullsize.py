@@ -155,3 +155,23 @@ def test_delicious_full_size_rows(gpu, oracle):
     for mode in range(4):
         got = gpu.mttkrp(dt, f, mode)[rows[mode].astype(np.int64)]
         assert rel_frobenius(got, want[mode]) <= TOL, mode
+
+
+def test_repeated_streaming_three_queues(gpu):
+    """Regression: repeated stream_mttkrp_all_modes calls with 3 queues in one
+    process.  A queue's tile table used to be uploaded with a plain pageable
+    cudaMemcpy, which returns once the data is staged; the queue is a
+    non-blocking stream, so its kernels could read the table before the DMA
+    landed, and every third call or so one block came out wrong (rel. error
+    0.18-0.30).  scripts/stream_repro.py: one Reddit ALTO chunk (73M
+    elements), 2^24-element blocks, 4 calls against a device-resident MTTKRP."""
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    r = subprocess.run([sys.executable, str(root / "scripts" / "stream_repro.py"), "1", "24", "4", "3"],
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-2000:]
+    errs = [float(ln.split("err ")[1].split()[0]) for ln in r.stdout.splitlines() if ln.startswith("rep ")]
+    assert len(errs) == 4 and max(errs) <= 1e-12, r.stdout
