@@ -808,8 +808,8 @@ __device__ __forceinline__ void compute_range_f32(const ParamsF32<N>& p, const S
 }
 
 // Lean fp32 computing phase for an exact rank (R == LPE * V), packed stage.
-template <int N, int LPE, int V>
-__device__ __forceinline__ void compute_range_f32_fast(const ParamsF32<N>& p, const Stage<N> st, int lo0, int wn,
+template <int N, int LPE, int V, class ST = Stage<N>>
+__device__ __forceinline__ void compute_range_f32_fast(const ParamsF32<N>& p, const ST st, int lo0, int wn,
                                                        int lane) {
   using VT = typename VecF<V>::type;
   constexpr int G = 32 / LPE;
@@ -817,7 +817,7 @@ __device__ __forceinline__ void compute_range_f32_fast(const ParamsF32<N>& p, co
   constexpr int NO = N > 1 ? N - 1 : 1;
   constexpr int RF = LPE * V;
   constexpr int U = kUnroll;
-  constexpr bool kRows4 = G == 2 && U == 4;
+  constexpr bool kRows4 = G == 2 && U == 4 && !ST::kRowInRecord;
   const int g = lane / LPE, q = lane % LPE;
   int h = wn / G;
   if constexpr (kRows4) {
@@ -870,7 +870,9 @@ __device__ __forceinline__ void compute_range_f32_fast(const ParamsF32<N>& p, co
     VT rows[U][NO];
 #pragma unroll
     for (int u = 0; u < U; ++u) st.get(j0 + u, v[u], w[u]);
-    if constexpr (kRows4) {
+    if constexpr (ST::kRowInRecord) {
+      // the row came with the record
+    } else if constexpr (kRows4) {
       const uint4 r4 = st.rows4(j0);
       w[0][N - 1] = r4.x, w[1][N - 1] = r4.y, w[2][N - 1] = r4.z, w[3][N - 1] = r4.w;
     } else {
@@ -906,22 +908,25 @@ __device__ __forceinline__ void compute_range_f32_fast(const ParamsF32<N>& p, co
   }
 }
 
-template <int N, int LPE, int V, int CPL, bool FULL, int TILE = kTileElems, int MINB = 1>
+template <int N, int LPE, int V, int CPL, bool FULL, int TILE = kTileElems, int MINB = 1, bool CMP = false>
 __global__ void __launch_bounds__(kCtaThreads, MINB) k_mttkrp_sorted_f32(ParamsF32<N> p) {
   constexpr int WE = TILE / kWarps;
+  using ST = std::conditional_t<CMP, StageC, Stage<N>>;
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ BucketShared bs;
-  const Stage<N> st = cta_stage<N, TILE>(dyn);
+  ST st;
+  if constexpr (CMP) st = StageC{reinterpret_cast<uint4*>(dyn)};
+  else st = cta_stage<N, TILE>(dyn);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const TileDesc td = p.base.tiles[blockIdx.x];
   unsigned long long segs = ~0ull;
-  const uint32_t cnt = process_cta<N, TILE>(p.base, td, st, bs, segs);
+  const uint32_t cnt = process_cta<N, TILE, ST>(p.base, td, st, bs, segs);
   const int lo0 = warp * WE;
   const int wn = static_cast<int>(cnt) > lo0 ? min(WE, static_cast<int>(cnt) - lo0) : 0;
   if (wn > 0) {
     if constexpr (FULL && CPL == 1 && Stage<N>::kPacked)
-      compute_range_f32_fast<N, LPE, V>(p, st, lo0, wn, lane);
-    else
+      compute_range_f32_fast<N, LPE, V, ST>(p, st, lo0, wn, lane);
+    else if constexpr (!CMP)
       compute_range_f32<N, LPE, V, CPL, FULL>(p, st, lo0, wn, lane, blockIdx.y * LPE * V * CPL);
   }
 }
@@ -1247,8 +1252,17 @@ void launch_f32_cfg(const KernelView& v, const float* const* factors, uint64_t r
     if (v.tensor && ychunks == 1 && use_big_tiles(l, mode, rank, v.tensor->nnz, sizeof(float))) {
       constexpr int T2 = 2 * kTileElems;  // as the fp64 kernel (k_mttkrp_sorted)
       p.base.tiles = tile_table(*v.tensor, T2, &p.base.ntiles);
-      const size_t st2 = stage_bytes<N>(T2);
+      size_t st2 = stage_bytes<N>(T2);
       auto kern = k_mttkrp_sorted_f32<N, LPE, V, CPL, FULL, T2, 3>;
+      if constexpr (N == 3 && CPL == 1) {
+        bool narrow = compact_stage_knob();
+        for (int m = 0; m < N; ++m)
+          if (m != mode && l.dims[m] > 65536) narrow = false;
+        if (narrow) {  // 16-byte records with the row inside (StageC)
+          kern = k_mttkrp_sorted_f32<N, LPE, V, CPL, FULL, T2, 3, true>;
+          st2 = static_cast<size_t>(T2) * sizeof(uint4);
+        }
+      }
       set_smem(kern, st2);
       kern<<<dim3(static_cast<unsigned>(p.base.ntiles), 1), kCtaThreads, st2, s>>>(p);
       count_launch();
