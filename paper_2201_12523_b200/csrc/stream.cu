@@ -188,6 +188,10 @@ void stream_impl(const blco_layout* layout, uint64_t max_nnz_per_block, BlockFee
     cudaEvent_t start, stop;
     B200_CUDA(cudaEventCreate(&start));
     B200_CUDA(cudaEventCreate(&stop));
+    // zeroed before the device sync below: the queues are non-blocking
+    // streams, not ordered after the legacy-stream memset
+    DevBuf<unsigned> dbad(1);  // read_blco_block check bits of file-fed blocks
+    B200_CUDA(cudaMemset(dbad.ptr, 0, sizeof(unsigned)));
     B200_CUDA(cudaDeviceSynchronize());
     B200_CUDA(cudaEventRecord(start, qs[0].stream));
     for (int q = 1; q < Q; ++q) B200_CUDA(cudaStreamWaitEvent(qs[q].stream, start, 0));
@@ -195,8 +199,6 @@ void stream_impl(const blco_layout* layout, uint64_t max_nnz_per_block, BlockFee
     std::vector<Interval> timeline;
     std::vector<int32_t> block_queue;
     std::vector<double> sleep_arg(1, budget->injected_transfer_latency_s);
-    DevBuf<unsigned> dbad(1);  // read_blco_block check bits of file-fed blocks
-    B200_CUDA(cudaMemset(dbad.ptr, 0, sizeof(unsigned)));
     uint64_t ordinal = 0, bytes = 0;
     std::string err;
     int err_code = BLCO_OK;
