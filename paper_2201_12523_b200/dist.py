@@ -32,7 +32,8 @@ from typing import Sequence
 import numpy as np
 
 from . import _lib as L
-from .api import CpAlsError, CpAlsOptions, DeviceTensor, ExecConfig, FormatError, Strategy, _check, factors_random_device
+from .api import (CpAlsError, CpAlsOptions, DeviceTensor, Error, ExecConfig, FormatError, Strategy, _check,
+                  factors_random_device)
 
 lib = L.lib
 
@@ -209,7 +210,7 @@ def cp_als_distributed(t: DeviceTensor, dims: Sequence[int], opts: CpAlsOptions,
             ev[-1][1].record()
         f = float(scal[2].item())  # the iteration's one host round trip
         if int(status.item()):
-            raise FormatError("solve_normal: matrix singular after maximal diagonal shift")
+            raise Error("solve_normal: matrix singular after maximal diagonal shift")  # as blco_cp_als
         hist.append(f)
         if not np.isfinite(f):
             raise CpAlsError(f"cp_als: non-finite fit at iteration {it + 1}", hist)
