@@ -377,7 +377,13 @@ __device__ __forceinline__ void compute_range(const Params<N>& p, const Stage<N>
 // stripped: the row stride is a compile-time constant, the lane's column
 // offset is folded into per-mode base pointers once, and every batch but the
 // group's last runs without element masks.
-template <int N, int LPE, int CPL, int U, class ST = Stage<N>>
+// PRIV: `out` is a CTA-private M_n in shared memory (k_mttkrp_priv).  Rows
+// are then < kBuckets, so the bucket grouping makes every row's run in a
+// tile contiguous and collision-free: a lane group owns the rows of its
+// interior segments outright (plain shared-memory add) and only its first
+// and last segment, which may continue in the neighbouring group, need an
+// atomic (fp64 shared atomics are CAS loops).
+template <int N, int LPE, int CPL, int U, class ST = Stage<N>, bool PRIV = false>
 __device__ __forceinline__ void compute_range_fast(const Params<N>& p, const ST st, int lo0, int wn, int lane,
                                                    double* __restrict__ out, unsigned long long& commits) {
   constexpr int G = 32 / LPE;
@@ -403,6 +409,7 @@ __device__ __forceinline__ void compute_range_fast(const Params<N>& p, const ST 
   double acc[CPL];
 #pragma unroll
   for (int c = 0; c < CPL; ++c) acc[c] = 0.0;
+  bool first_seg = true;
 
   auto consume = [&](const double (&v)[U], const uint32_t (&w)[U][NW], const Row<CPL> (&rows)[U][NO],
                      uint32_t next_row, int valid) {
@@ -420,8 +427,19 @@ __device__ __forceinline__ void compute_range_fast(const Params<N>& p, const ST 
         const uint32_t nrow = u + 1 < valid ? w[u + 1][N - 1] : next_row;
         if (nrow != row) {
           double* o = ob + static_cast<uint64_t>(row) * RF;
+          if constexpr (PRIV) {
+            if (first_seg || (u + 1 >= valid && next_row == 0xffffffffu)) {
 #pragma unroll
-          for (int c = 0; c < CPL; ++c) commit_add(o + c * LPE, acc[c]);
+              for (int c = 0; c < CPL; ++c) atomicAdd(o + c * LPE, acc[c]);
+            } else {
+#pragma unroll
+              for (int c = 0; c < CPL; ++c) o[c * LPE] += acc[c];
+            }
+            first_seg = false;
+          } else {
+#pragma unroll
+            for (int c = 0; c < CPL; ++c) commit_add(o + c * LPE, acc[c]);
+          }
           ++commits;
 #pragma unroll
           for (int c = 0; c < CPL; ++c) acc[c] = 0.0;
@@ -933,6 +951,39 @@ __global__ void __launch_bounds__(kCtaThreads, MINB) k_mttkrp_sorted_f32(ParamsF
 
 // Persistent CTAs; dynamic shared memory = tile stage + stash (slots x R
 // doubles + tags).
+// Hierarchical strategy, privatised form (exact ranks, N <= 3): when the
+// whole target mode fits in shared memory beside the staging, each
+// persistent CTA accumulates its segment sums into a private copy of M_n in
+// shared memory -- the reference's work-group stash with one slot per row,
+// so nothing is ever evicted (mttkrp.cpp:139-155, 83-89) -- and flushes it
+// once at the end, one RED per non-zero element.  The computing phase is
+// K4's lean one with the commit target in shared memory, so a short,
+// high-conflict mode costs no global atomics per tile.
+template <int N, int LPE, int CPL>
+__global__ void __launch_bounds__(kCtaThreads) k_mttkrp_priv(Params<N> p) {
+  constexpr int WE = kTileElems / kWarps;
+  extern __shared__ __align__(16) unsigned char dyn[];
+  __shared__ BucketShared bs;
+  const Stage<N> st = cta_stage<N>(dyn);
+  double* const priv = reinterpret_cast<double*>(dyn + stage_bytes<N>(kTileElems));
+  const uint64_t elems = p.copy_elems;  // I_n * R
+  for (uint64_t i = threadIdx.x; i < elems; i += blockDim.x) priv[i] = 0.0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned long long segs = ~0ull, commits = 0;
+  for (uint64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
+    const TileDesc td = p.tiles[tile];
+    const uint32_t cnt = process_cta<N>(p, td, st, bs, segs);  // its barriers also order the zeroing
+    const int lo0 = warp * WE;
+    const int wn = static_cast<int>(cnt) > lo0 ? min(WE, static_cast<int>(cnt) - lo0) : 0;
+    if (wn > 0) compute_range_fast<N, LPE, CPL, kUnroll, Stage<N>, true>(p, st, lo0, wn, lane, priv, commits);
+    __syncthreads();  // stage reused by the next tile
+  }
+  for (uint64_t i = threadIdx.x; i < elems; i += blockDim.x) {
+    const double v = priv[i];
+    if (v != 0.0) atomicAdd(p.out + i, v);
+  }
+}
+
 template <int N, int LPE, int CPL, bool FULL, bool STATS>
 __global__ void __launch_bounds__(kCtaThreads) k_mttkrp_hier(Params<N> p) {
   extern __shared__ __align__(16) unsigned char dyn[];
@@ -1181,6 +1232,29 @@ void launch_cfg(MttkrpLaunch& a) {
   B200_CUDA(cudaGetDevice(&dev));
   B200_CUDA(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   B200_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  if constexpr (FULL && Stage<N>::kPacked) {
+    // privatised form (k_mttkrp_priv) when M_n fits beside the staging and
+    // one copy is asked for; ~half the shared memory at most, so at least
+    // two CTAs stay resident per SM
+    const size_t privb = elems * sizeof(double);
+    const int C1 = std::max(1, a.cfg.num_factor_copies);
+    if (C1 == 1 && !stats && !a.hier_copies && ychunks == 1 && l.dims[a.mode] <= uint64_t(kBuckets) &&
+        tile_stage + privb + sizeof(BucketShared) + 1024 <= static_cast<size_t>(smem_optin) / 2) {
+      const size_t dyn = tile_stage + privb;
+      auto kern = k_mttkrp_priv<N, LPE, CPL>;
+      set_smem(kern, dyn);
+      const int per_sm = std::max(blocks_per_sm(reinterpret_cast<const void*>(kern), kCtaThreads, dyn), 1);
+      const uint64_t grid = std::min<uint64_t>(p.ntiles, static_cast<uint64_t>(nsm) * per_sm);
+      p.out = a.out;
+      p.ncopies = 1;
+      a.workgroups = grid;
+      a.stash_slots = static_cast<int>(l.dims[a.mode]);
+      kern<<<dim3(static_cast<unsigned>(grid), 1), kCtaThreads, dyn, a.stream>>>(p);
+      count_launch();
+      check_launch("k_mttkrp_priv");
+      return;
+    }
+  }
   const size_t budget = static_cast<size_t>(smem_optin) - sizeof(BucketShared) - tile_stage - 1024;
   const size_t per_slot = a.rank * sizeof(double) + sizeof(uint32_t);
   const uint64_t fit = budget / per_slot;
