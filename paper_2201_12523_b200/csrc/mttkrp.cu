@@ -1213,14 +1213,25 @@ void launch_cfg(MttkrpLaunch& a) {
         return;
       }
     }
+    size_t stage1 = tile_stage;
     auto kern = stats ? k_mttkrp_sorted<N, LPE, CPL, FULL, true> : k_mttkrp_sorted<N, LPE, CPL, FULL, false>;
+    if constexpr (N == 3 && FULL) {
+      bool narrow = compact_stage_knob();
+      for (int m = 0; m < N; ++m)
+        if (m != a.mode && l.dims[m] > 65536) narrow = false;
+      if (narrow) {  // 16-byte records with the row inside (StageC)
+        kern = stats ? k_mttkrp_sorted<N, LPE, CPL, FULL, true, kUnroll, 1, kTileElems, true>
+                     : k_mttkrp_sorted<N, LPE, CPL, FULL, false, kUnroll, 1, kTileElems, true>;
+        stage1 = static_cast<size_t>(kTileElems) * sizeof(uint4);
+      }
+    }
     // N = 4 (R <= 32): cap registers so 3 CTAs fit per SM (88 -> 80 for
     // R=16; the DRAM-bound Delicious modes run 6% faster with the extra warps
     // in flight).  N <= 3 already fits 3; higher orders would spill.
     if constexpr (N == 4 && LPE * CPL <= 32)
       if (!stats) kern = k_mttkrp_sorted<N, LPE, CPL, FULL, false, kUnroll, 3>;
-    set_smem(kern, tile_stage);
-    kern<<<grid, kCtaThreads, tile_stage, a.stream>>>(p);
+    set_smem(kern, stage1);
+    kern<<<grid, kCtaThreads, stage1, a.stream>>>(p);
     count_launch();
     check_launch("k_mttkrp_sorted");
     return;
