@@ -390,7 +390,7 @@ __device__ __forceinline__ void compute_range_fast(const Params<N>& p, const ST 
   constexpr int NW = 4 * Stage<N>::NM;
   constexpr int NO = N > 1 ? N - 1 : 1;
   constexpr int RF = LPE * CPL;
-  constexpr bool kRows4 = G == 2 && U == 4 && !ST::kRowInRecord;
+  constexpr bool kRows4 = G == 2 && U == 4 && !ST::kRowInRecord && ST::kPacked;
   const int g = lane / LPE, q = lane % LPE;
   int h = wn / G;
   if constexpr (kRows4) {
@@ -693,7 +693,7 @@ __global__ void __launch_bounds__(kCtaThreads, MINB) k_mttkrp_sorted(Params<N> p
   const int lo0 = warp * WE;
   const int wn = static_cast<int>(cnt) > lo0 ? min(WE, static_cast<int>(cnt) - lo0) : 0;
   if (wn > 0) {
-    if constexpr (FULL && Stage<N>::kPacked && U == 4)
+    if constexpr (FULL && U == 4)  // lean phase for every order (N >= 4: general stage, no 4-row loads)
       compute_range_fast<N, LPE, CPL, U, ST>(p, st, lo0, wn, lane, p.out, commits);
     else if constexpr (!CMP)
       compute_range<N, LPE, CPL, FULL, false, U>(p, st, lo0, wn, lane, blockIdx.y * LPE * CPL, p.out, nullptr,
@@ -835,7 +835,7 @@ __device__ __forceinline__ void compute_range_f32_fast(const ParamsF32<N>& p, co
   constexpr int NO = N > 1 ? N - 1 : 1;
   constexpr int RF = LPE * V;
   constexpr int U = kUnroll;
-  constexpr bool kRows4 = G == 2 && U == 4 && !ST::kRowInRecord;
+  constexpr bool kRows4 = G == 2 && U == 4 && !ST::kRowInRecord && ST::kPacked;
   const int g = lane / LPE, q = lane % LPE;
   int h = wn / G;
   if constexpr (kRows4) {
