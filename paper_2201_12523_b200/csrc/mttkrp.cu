@@ -942,7 +942,7 @@ __global__ void __launch_bounds__(kCtaThreads, MINB) k_mttkrp_sorted_f32(ParamsF
   const int lo0 = warp * WE;
   const int wn = static_cast<int>(cnt) > lo0 ? min(WE, static_cast<int>(cnt) - lo0) : 0;
   if (wn > 0) {
-    if constexpr (FULL && CPL == 1 && Stage<N>::kPacked)
+    if constexpr (FULL && CPL == 1)  // lean phase for every order
       compute_range_f32_fast<N, LPE, V, ST>(p, st, lo0, wn, lane);
     else if constexpr (!CMP)
       compute_range_f32<N, LPE, V, CPL, FULL>(p, st, lo0, wn, lane, blockIdx.y * LPE * V * CPL);
