@@ -149,24 +149,31 @@ def reference_sample_run(dims, nnz, rank, steps, warmup, target_step_s=4.0, thre
     exactly the first S elements (first spans) the GPU processes.
     sampler "generator_prefix": the first S elements the seeded generator
     emits (Feistel-uniform cells, or with `skew` set the first S distinct
-    draws floor(I u^skew)): the generator's key does not depend on nnz, so this is
-    a uniformly random subset of the same tensor's non-zeros over the same
+    draws floor(I u^skew)): the generator's key does not depend on nnz, so this
+    is a uniformly random subset of the same tensor's non-zeros over the same
     dims (configs whose COO does not fit the host, or layouts > 64 bits).
-    Either sample is built by the reference's own build_blco; S is calibrated
-    so one step takes ~target_step_s, and the rate (bytes per second) is the
-    figure compared, i.e. linearly extrapolated by nnz.  op "stream" times
-    the reference stream_mttkrp (MemoryBlockSource, its DeviceBudget) per mode
-    instead.  Returns (GB/s, dict).
+    Each sample is built by the reference's own build_blco.
+
+    The reference's step costs a + b*S: a per-call fixed cost that scales
+    with the dims (zero-initialised I_n x R outputs, factor copies, merges)
+    and a per-element cost.  Both are fitted at two calibration sizes for
+    1 thread and for all host threads (the reference anti-scales with
+    threads), and the thread count with the smaller extrapolated
+    full-tensor step is used: the reference's best CPU configuration.  Then
+    `steps` timed steps of a sample of S elements (one step ~ target_step_s)
+    refine b, and the full-tensor step is a + b*nnz (`extrapolated` unless
+    S = nnz).  op "stream" times the reference stream_mttkrp
+    (MemoryBlockSource, its DeviceBudget) per mode instead.  Returns
+    (GB/s of the full tensor, dict).
     """
     sys.path.insert(0, str(ROOT / "oracle"))
     from pyoracle import Oracle, RefLib, cfg_array
 
     oracle, ref = Oracle(), RefLib()
-    threads = threads or os.cpu_count() or 1
+    all_threads = threads or os.cpu_count() or 1
     order = len(dims)
     t0 = time.perf_counter()
     factors = oracle.factors_random(dims, rank, FACTOR_SEED)
-    cfg = cfg_array(num_threads=threads)
     if sampler == "alto_prefix":
         # Generate the tensor in full, then select ALTO prefixes.
         gen_n = nnz
@@ -192,7 +199,7 @@ def reference_sample_run(dims, nnz, rank, steps, warmup, target_step_s=4.0, thre
         sidx, svals = coo(S)
         return ref.build(dims, sidx, svals, 64), S
 
-    def one_step(t, c=cfg):
+    def one_step(t, c):
         s = time.perf_counter()
         for mode in range(order):
             if op == "stream":
@@ -202,32 +209,38 @@ def reference_sample_run(dims, nnz, rank, steps, warmup, target_step_s=4.0, thre
                 t.mttkrp(factors, mode, c)
         return time.perf_counter() - s
 
-    # Step time t(S) = a + b S: a is the reference's per-call fixed cost
-    # (zero-initialised I_n x R outputs, factor copies, merge -- it scales
-    # with the dims, not nnz), b the per-element cost.  Fit both from two
-    # sample sizes and extrapolate to the full nnz: t_full = a + b nnz.
+    # calibration: a and b at 1 thread and at all threads
     S_lo = min(gen_n, 1 << 16)
     t_lo, S_lo = sample(S_lo)
-    one_step(t_lo)
-    d_lo = one_step(t_lo)
-    S = min(gen_n, max(4 * S_lo, 1 << 18))
-    t, S = sample(S)
-    dt = one_step(t)
-    b_est = max((dt - d_lo) / max(S - S_lo, 1), 1e-12)
-    S2 = min(gen_n, max(S, int(target_step_s / b_est)), 1 << 25)
-    if S2 > S:
-        del t
-        t, S = sample(S2)
+    S_mid = min(gen_n, max(4 * S_lo, 1 << 18))
+    t_mid, S_mid = sample(S_mid)
+    fits = {}
+    for th in sorted({1, all_threads}):
+        c = cfg_array(num_threads=th)
+        one_step(t_lo, c)
+        d_lo = one_step(t_lo, c)
+        d_mid = one_step(t_mid, c)
+        b = max((d_mid - d_lo) / max(S_mid - S_lo, 1), 1e-12)
+        fits[th] = {"a": max(0.0, d_lo - b * S_lo), "b": b, "d_lo": d_lo}
+    best = min(fits, key=lambda th: fits[th]["a"] + fits[th]["b"] * nnz)
+    a, b_cal, d_lo = fits[best]["a"], fits[best]["b"], fits[best]["d_lo"]
+    cfg = cfg_array(num_threads=best)
+    S = min(gen_n, max(S_mid, int(max(target_step_s - a, 0.0) / b_cal)), 1 << 25)
+    if S > S_mid:
+        del t_mid
+        t, S = sample(S)
+    else:
+        t, S = t_mid, S_mid
     for _ in range(warmup):
-        one_step(t)
-    times = [one_step(t) for _ in range(steps)]
+        one_step(t, cfg)
+    times = [one_step(t, cfg) for _ in range(steps)]
     bpe = bytes_per_elem(order, rank)
     step_s = sum(times) / len(times)
     per_elem = (step_s - d_lo) / (S - S_lo) if S > S_lo else step_s / S
     fixed = max(0.0, d_lo - per_elem * S_lo)
     if per_elem <= 0:
         per_elem, fixed = step_s / S, 0.0
-    full_s = fixed + per_elem * nnz
+    full_s = step_s if S >= nnz else fixed + per_elem * nnz
     gbps = nnz * order * bpe / full_s / 1e9
     what = "blco::stream_mttkrp per mode (MemoryBlockSource, DeviceBudget{24 GiB, 4, 2 GiB})" if op == "stream" \
         else "blco::mttkrp"
@@ -236,36 +249,39 @@ def reference_sample_run(dims, nnz, rank, steps, warmup, target_step_s=4.0, thre
     else:
         desc = (f"first {S_lo} and {S} elements of the seeded generator (uniformly random subsets of the "
                 f"{nnz}-nnz tensor's non-zeros, same dims)")
-    desc += (f"; all-mode step time fitted as a + b*nnz (a = {fixed:.3f} s fixed per step, "
-             f"b = {per_elem * 1e9:.1f} ns per element) and extrapolated to the full {nnz} nnz "
-             f"= {full_s:.2f} s")
-    info = {"sample_nnz": S, "step_s": step_s, "full_step_s": full_s, "fixed_s": fixed, "per_elem_s": per_elem,
-            "threads": threads, "setup_s": setup_s,
+    desc += (f"; {steps} timed steps of the {S}-element sample at {best} thread(s) "
+             f"({step_s:.3f} s each); all-mode step fitted as a + b*nnz (a = {fixed:.3f} s fixed per step, "
+             f"b = {per_elem * 1e9:.1f} ns per element) and extrapolated to the full {nnz} nnz = {full_s:.2f} s")
+    info = {"sample_nnz": S, "sample_fraction": S / nnz, "sample_steps": steps, "step_s": step_s,
+            "full_step_s": full_s, "fixed_s": fixed, "per_elem_s": per_elem, "threads": best,
+            "extrapolated": S < nnz, "setup_s": setup_s,
+            "threads_tried": {str(th): {"fixed_s": round(f["a"], 4), "ns_per_elem": round(f["b"] * 1e9, 1),
+                                        "full_step_s_est": round(f["a"] + f["b"] * nnz, 2)}
+                              for th, f in fits.items()},
             "sample": f"{desc}; reference build_blco on that COO subset, {what}, all {order} modes, R={rank}"}
     if extra:
-        # the reference anti-scales with threads, so also one
-        # thread, and the oracle::mttkrp_coo loop (1 thread) on the same sample
-        one_s = one_step(t, cfg_array(num_threads=1))
+        # oracle::mttkrp_coo (1 thread) on the same sample, the reference's
+        # simplest CPU loop (oracle.cpp:9-26)
         sidx, svals = coo(S)
         s0 = time.perf_counter()
         for mode in range(order):
             ref.mttkrp_coo(dims, sidx, svals, factors, mode)
         coo_s = time.perf_counter() - s0
-        one_full = fixed * one_s / step_s + per_elem * (one_s / step_s) * nnz  # same a/b split, 1-thread scale
-        info["reference_1_thread"] = {"value": round(nnz * order * bpe / one_full / 1e9, 4), "unit": "GB/s",
-                                      "step_s": round(one_s, 3), "note": "sample step at 1 thread, scaled like "
-                                      "the fitted all-thread step"}
         info["oracle_mttkrp_coo_1_thread"] = {"value": round(S * order * bpe / coo_s / 1e9, 4), "unit": "GB/s",
                                               "step_s": round(coo_s, 3),
-                                              "note": "reference oracle::mttkrp_coo (oracle.cpp:9-26)"}
+                                              "note": "reference oracle::mttkrp_coo (oracle.cpp:9-26) on the "
+                                                      "same sample, no fixed cost to extrapolate"}
     return gbps, info
 
 
 def cpu_baseline_entry(gbps, info) -> dict:
     out = {"value": round(gbps, 4), "unit": "GB/s", "cores": info["threads"], "kind": "reference",
-           "sample": info["sample"], "sample_step_s": round(info["step_s"], 3),
-           "full_step_s_extrapolated": round(info["full_step_s"], 3), "cpu_model": cpu_model()}
-    for k in ("reference_1_thread", "oracle_mttkrp_coo_1_thread"):
+           "sample": info["sample"], "sample_nnz": info["sample_nnz"],
+           "sample_fraction": round(info["sample_fraction"], 6), "sample_steps": info["sample_steps"],
+           "sample_step_s": round(info["step_s"], 3), "extrapolated": info["extrapolated"],
+           "full_step_s_extrapolated": round(info["full_step_s"], 3), "threads_tried": info["threads_tried"],
+           "cpu_model": cpu_model(), "host_threads": os.cpu_count()}
+    for k in ("oracle_mttkrp_coo_1_thread",):
         if k in info:
             out[k] = info[k]
     return out
@@ -273,6 +289,149 @@ def cpu_baseline_entry(gbps, info) -> dict:
 
 def make_wide(dims) -> bool:
     return sum(int(d - 1).bit_length() for d in dims) > 64
+
+
+# ------------------------------------------------------- DRAM traffic (ncu)
+
+NCU_METRICS = ("dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,"
+               "l1tex__throughput.avg.pct_of_peak_sustained_elapsed,"
+               "dram__throughput.avg.pct_of_peak_sustained_elapsed,"
+               "lts__throughput.avg.pct_of_peak_sustained_elapsed")
+
+
+def traffic_probe_worker(args):
+    """--traffic-probe (run under ncu by live_traffic): build the config's
+    tensor and launch each mode's kernel twice; nothing is timed here."""
+    import torch
+
+    import paper_2201_12523_b200 as b
+    dims, nnz, R, _ = CONFIGS[args.config]
+    torch.cuda.set_device(0)
+    dt = b.DeviceTensor.synthetic(dims, nnz, TENSOR_SEED, device=0)
+    fac = [torch.empty((d, R), dtype=torch.float64, device="cuda:0") for d in dims]
+    sptr = torch.cuda.current_stream().cuda_stream
+    b.factors_random_device(dims, R, FACTOR_SEED, [a.data_ptr() for a in fac], sptr)
+    outs = [torch.zeros((d, R), dtype=torch.float64, device="cuda:0") for d in dims]
+    cfg = b.ExecConfig(num_compute_units=torch.cuda.get_device_properties(0).multi_processor_count)
+    for _ in range(2):
+        for m in range(len(dims)):
+            dt.mttkrp_device([a.data_ptr() for a in fac], R, m, outs[m].data_ptr(), b.Strategy.Auto, cfg,
+                             accumulate=True, stream=sptr)
+    torch.cuda.synchronize()
+
+
+def live_traffic(config: str, timeout_s: int = 300) -> dict | None:
+    """DRAM bytes per launch of the mode kernels of THIS build, from an ncu
+    pass over a child process (`bench.py --traffic-probe`; 2 launches per
+    mode, ncu's default cache control = caches flushed before each launch).
+    Only counters are taken from ncu -- never a time.  None when ncu is
+    unavailable or fails (the committed profile is used instead)."""
+    import csv
+    import io
+    import shutil
+    import tempfile
+    ncu = shutil.which("ncu") or "/usr/local/cuda/bin/ncu"
+    if not os.path.exists(ncu):
+        return None
+    with tempfile.TemporaryDirectory() as td:
+        log = os.path.join(td, "traffic.csv")
+        cmd = [ncu, "--metrics", NCU_METRICS, "--clock-control", "none", "-k", "regex:k_mttkrp", "--csv",
+               "--log-file", log, sys.executable, str(ROOT / "bench.py"), "--traffic-probe", "--config", config]
+        try:
+            r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout_s,
+                               env=dict(os.environ, CUDA_VISIBLE_DEVICES=os.environ.get("CUDA_VISIBLE_DEVICES", "0")))
+        except (OSError, subprocess.TimeoutExpired):
+            return None
+        if r.returncode != 0 or not os.path.exists(log):
+            return None
+        text = open(log).read()
+    rows = [row for row in csv.reader(io.StringIO(text[text.find('"ID"'):]))]
+    if len(rows) < 2:
+        return None
+    hdr = rows[0]
+    col = {k: hdr.index(k) for k in ("ID", "Kernel Name", "Metric Name", "Metric Unit", "Metric Value")}
+    launches: dict[int, dict] = {}
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "ns": 1e-9, "nsecond": 1e-9,
+             "us": 1e-6, "usecond": 1e-6, "ms": 1e-3, "msecond": 1e-3, "%": 1.0}
+    for row in rows[1:]:
+        if len(row) < len(hdr):
+            continue
+        d = launches.setdefault(int(row[col["ID"]]), {"kernel": row[col["Kernel Name"]]})
+        try:
+            d[row[col["Metric Name"]]] = float(row[col["Metric Value"]].replace(",", "")) * \
+                scale.get(row[col["Metric Unit"]], 1.0)
+        except ValueError:
+            pass
+    ls = [launches[k] for k in sorted(launches)]
+    if not ls:
+        return None
+    dram = [x.get("dram__bytes_read.sum", 0) + x.get("dram__bytes_write.sum", 0) for x in ls]
+    mean = lambda k: statistics.mean(x.get(k, 0.0) for x in ls)  # noqa: E731
+    return {"dram_bytes_per_launch": statistics.mean(dram), "launches": len(ls),
+            "ncu_launch_s": mean("gpu__time_duration.sum"), "kernel": ls[0]["kernel"][:100],
+            "l1tex_pct": round(mean("l1tex__throughput.avg.pct_of_peak_sustained_elapsed"), 1),
+            "dram_pct": round(mean("dram__throughput.avg.pct_of_peak_sustained_elapsed"), 1),
+            "lts_pct": round(mean("lts__throughput.avg.pct_of_peak_sustained_elapsed"), 1),
+            "source": f"live ncu pass over this build ({len(ls)} launches of the mode kernels, "
+                      "dram__bytes_read.sum + dram__bytes_write.sum; caches flushed before each launch)"}
+
+
+def committed_traffic(config: str) -> dict | None:
+    """Fallback: the ncu --set full summary committed under profiles/."""
+    prof = ROOT / "profiles" / f"ncu_{config}.json"
+    try:
+        rep = json.loads(prof.read_text())
+    except (OSError, ValueError):
+        return None
+    ls = rep.get("launches") or []
+    if not ls:
+        return None
+    mean = lambda k: statistics.mean(float(x.get(k, 0) or 0) for x in ls)  # noqa: E731
+    return {"dram_bytes_per_launch": mean("dram_bytes"), "launches": len(ls),
+            "ncu_launch_s": mean("gpu__time_duration.sum"), "kernel": ls[0].get("kernel", "")[:100],
+            "l1tex_pct": round(mean("l1tex__throughput.avg.pct_of_peak_sustained_elapsed"), 1),
+            "dram_pct": round(mean("dram__throughput.avg.pct_of_peak_sustained_elapsed"), 1),
+            "lts_pct": round(mean("lts__throughput.avg.pct_of_peak_sustained_elapsed"), 1),
+            "source": f"committed profile profiles/ncu_{config}.json (an earlier build)"}
+
+
+def roofline_entry(traffic: dict | None, launch_ms: float, algo_bytes_per_launch: float, peak: float,
+                   peak_source: str, kernel: str) -> dict:
+    """roofline for the dominant kernel: achieved = PHYSICAL DRAM bytes per
+    launch (ncu) / the launch's mean duration measured here (CUDA events);
+    frac against the measured HBM copy peak.  The algorithmic B_elem rate
+    (exceeds the HBM peak when gathers hit L2) is reported beside
+    it as algorithmic_gbps, not as the fraction."""
+    algo = algo_bytes_per_launch / (launch_ms * 1e-3) / 1e9
+    out = {"bound": None, "achieved": None, "peak": peak, "unit": "GB/s", "frac": None, "traffic": None,
+           "kernel": kernel, "launch_ms": round(launch_ms, 4),
+           "algorithmic_gbps": round(algo, 2), "algorithmic_bytes_per_launch": int(algo_bytes_per_launch),
+           "peak_source": peak_source}
+    if traffic:
+        phys = traffic["dram_bytes_per_launch"] / (launch_ms * 1e-3) / 1e9
+        l1, dr = traffic.get("l1tex_pct") or 0.0, traffic.get("dram_pct") or 0.0
+        # the bound: the unit nearest its ceiling inside the ncu pass -- HBM as
+        # DRAM bytes / ncu duration against the MEASURED copy peak (ncu's own
+        # dram % is against the theoretical peak), the L1/TEX pipe as ncu's %
+        t_ncu = traffic.get("ncu_launch_s") or 0.0
+        hbm_busy = traffic["dram_bytes_per_launch"] / t_ncu / 1e9 / peak if t_ncu > 0 else phys / peak
+        out.update({"bound": "hbm" if hbm_busy >= l1 / 100.0 else "l1tex", "achieved": round(phys, 2),
+                    "frac": round(phys / peak, 4), "traffic": int(traffic["dram_bytes_per_launch"]),
+                    "limiter": {"hbm_frac_in_ncu_pass": round(hbm_busy, 3), "l1tex_pct": l1, "dram_pct": dr,
+                                "lts_pct": traffic.get("lts_pct"),
+                                "note": "bound = the larger of hbm_frac_in_ncu_pass and l1tex_pct/100"},
+                    "traffic_source": traffic["source"]})
+    return out
+
+
+def hbm_peak() -> tuple[float, str]:
+    try:
+        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+        if peaks.get("hbm_gbs"):
+            return float(peaks["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
+    except (OSError, ValueError):
+        pass
+    return 6650.0, "fallback (B200_PROFILING.md)"
 
 
 # ------------------------------------------------------------------ our arm
@@ -288,6 +447,14 @@ def run_ours(args, world, rank_id, local):
         R = args.rank
     N = len(dims)
     dev = local
+    # DRAM bytes per launch of this build (ncu counters from a child process,
+    # before this process allocates anything); N > 1 runs use the committed
+    # profile so the ranks are not perturbed
+    live = world == 1 and not args.no_ncu and not args.rank
+    traffic = (live and live_traffic(args.config)) or committed_traffic(args.config)
+    extra_traffic = None
+    if world == 1 and args.config == "amazon" and not args.no_extra:
+        extra_traffic = (live and live_traffic("nell2")) or committed_traffic("nell2")
     torch.cuda.set_device(dev)
     if world > 1:
         import torch.distributed as dist
@@ -389,32 +556,10 @@ def run_ours(args, world, rank_id, local):
     bpe = bytes_per_elem(N, R)
     total_bytes = nnz * N * bpe
     value = total_bytes / (ms * 1e-3) / 1e9
-    kern_ms = sum(statistics.mean(x) for x in mode_ms)
-    achieved = local_nnz * N * bpe / (kern_ms * 1e-3) / 1e9
-    peaks = {}
-    try:
-        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
-    except (OSError, ValueError):
-        pass
-    peak = peaks.get("hbm_gbs") or 6650.0
-    traffic, binding = None, None
-    prof = ROOT / "profiles" / f"ncu_{args.config}.json"
-    if prof.exists():
-        try:
-            rep = json.loads(prof.read_text())
-            per_launch = rep.get("dram_bytes_per_launch_all_modes") or []
-            traffic = round(sum(per_launch) / len(per_launch)) if per_launch else None
-            ls = rep.get("launches") or []
-            if ls:
-                avg = lambda k: round(statistics.mean(float(x.get(k, 0) or 0) for x in ls), 1)  # noqa: E731
-                l1 = avg("l1tex__throughput.avg.pct_of_peak_sustained_elapsed")
-                dram = round(100 * statistics.mean(float(x["dram_bytes"]) / float(x["gpu__time_duration.sum"])
-                                                   for x in ls) / (peak * 1e9), 1)
-                binding = {"l1tex_pct": l1, "dram_pct": dram, "lts_pct": avg("lts__throughput.avg.pct_of_peak_sustained_elapsed"),
-                           "limiter": "L1 data pipe (gathers hit L2)" if l1 > dram else "HBM",
-                           "source": f"profiles/ncu_{args.config}.json (ncu --set full)"}
-        except (ValueError, TypeError):
-            traffic = None
+    launch_ms = statistics.mean(statistics.mean(x) for x in mode_ms)  # mean launch of the mode kernels
+    peak, peak_source = hbm_peak()
+    roofline = roofline_entry(traffic, launch_ms, local_nnz * bpe, peak, peak_source,
+                              "k_mttkrp_sorted (one launch per mode)")
 
     result = {
         "metric": "MTTKRP all-mode throughput (algorithmic B_elem bytes / time)",
@@ -439,10 +584,7 @@ def run_ours(args, world, rank_id, local):
                        if world > 1 else ""),
                    "bytes_per_elem_per_mode": bpe},
         "per_mode_ms": [round(statistics.mean(x), 4) for x in mode_ms],
-        "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": traffic,
-                     "kernel": "k_mttkrp_sorted (one launch per mode)", "binding": binding,
-                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks.get("hbm_gbs") else "fallback"},
+        "roofline": roofline,
         "clocks": clk.summary(),
         "gpu_launches": launches,
         "build": {"seconds": round(build_s, 4), "device_stage_s": {k: round(getattr(bst, k), 4) for k in
@@ -479,12 +621,71 @@ def run_ours(args, world, rank_id, local):
         except Exception as e:  # noqa: BLE001
             result["cpu_baseline"] = {"value": None, "unit": "GB/s", "cores": None, "kind": "reference",
                                       "sample": f"failed: {e}"}
+    if world == 1 and args.config == "amazon" and not args.no_extra:
+        # BASELINE configs[1] (NELL-2 shape) beside the headline: its factors
+        # sit in L2, so its kernel is bound by the L1 data pipe, not HBM
+        del dt, fac, outs, flush
+        full = None
+        b.release_thread_caches()
+        torch.cuda.empty_cache()
+        result["nell2"] = resident_extra(b, torch, "nell2", extra_traffic, args, dev)
     if world > 1:
         import torch.distributed as dist
         dist.barrier()
         dist.destroy_process_group()
     if rank_id == 0:
         print(json.dumps(result), flush=True)
+
+
+def resident_extra(b, torch, name, traffic, args, dev):
+    """A second resident config measured in the same run (one GPU), reported
+    as its own key beside the headline: the same step (all modes, fixed
+    factors, L2 flushed between steps, CUDA events on the launching stream)
+    and the same physical-DRAM roofline."""
+    dims, nnz, R, desc = CONFIGS[name]
+    N = len(dims)
+    stream = torch.cuda.current_stream()
+    sptr = stream.cuda_stream
+    dt = b.DeviceTensor.synthetic(dims, nnz, TENSOR_SEED, device=dev)
+    fac = [torch.empty((d, R), dtype=torch.float64, device=f"cuda:{dev}") for d in dims]
+    b.factors_random_device(dims, R, FACTOR_SEED, [a.data_ptr() for a in fac], sptr)
+    fptr = [a.data_ptr() for a in fac]
+    outs = [torch.empty((d, R), dtype=torch.float64, device=f"cuda:{dev}") for d in dims]
+    cfg = b.ExecConfig(num_compute_units=torch.cuda.get_device_properties(dev).multi_processor_count)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{dev}")
+
+    def step(ev=None):
+        for o in outs:
+            o.zero_()
+        for m in range(N):
+            if ev is not None:
+                ev[m][0].record(stream)
+            dt.mttkrp_device(fptr, R, m, outs[m].data_ptr(), b.Strategy.Auto, cfg, accumulate=True, stream=sptr)
+            if ev is not None:
+                ev[m][1].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    steps = max(args.steps, 10)
+    evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(N)] for _ in range(steps)]
+    sev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(steps)]
+    torch.cuda.synchronize()
+    for k in range(steps):
+        flush.zero_()
+        sev[k][0].record(stream)
+        step(evs[k])
+        sev[k][1].record(stream)
+    torch.cuda.synchronize()
+    ms = statistics.mean(sev[k][0].elapsed_time(sev[k][1]) for k in range(steps))
+    mode_ms = [statistics.mean(evs[k][m][0].elapsed_time(evs[k][m][1]) for k in range(steps)) for m in range(N)]
+    bpe = bytes_per_elem(N, R)
+    peak, peak_source = hbm_peak()
+    return {"workload": desc, "dims": dims, "nnz": nnz, "rank": R, "steps": steps, "warmup": args.warmup,
+            "ms_per_step": round(ms, 4), "per_mode_ms": [round(x, 4) for x in mode_ms],
+            "value": round(nnz * N * bpe / (ms * 1e-3) / 1e9, 2), "unit": "GB/s (algorithmic B_elem bytes / time)",
+            "roofline": roofline_entry(traffic, statistics.mean(mode_ms), nnz * bpe, peak, peak_source,
+                                       "k_mttkrp_sorted (one launch per mode)"),
+            "l2": "flushed between steps (512 MiB write, outside the timed events)"}
 
 
 def fp32_variant(b, torch, dt, dims, R, N, nnz, fac, outs, cfg, sptr, dev, args):
@@ -710,13 +911,10 @@ def run_cpals(args, world=1, rank_id=0, local=0):
         torch.cuda.synchronize()
         mode_ms.append(a0.elapsed_time(a1) / 5)
     bpe = bytes_per_elem(N, R)
-    mttkrp_gbps = dt.nnz * N * bpe / (sum(mode_ms) * 1e-3) / 1e9
-    peaks = {}
-    try:
-        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
-    except (OSError, ValueError):
-        pass
-    peak = peaks.get("hbm_gbs") or 6650.0
+    peak, peak_source = hbm_peak()
+    traffic = committed_traffic("delicious") if args.config == "delicious_als" else None
+    roofline = roofline_entry(traffic, statistics.mean(mode_ms), dt.nnz * bpe, peak, peak_source,
+                              "k_mttkrp_sorted (one launch per mode, final factors)")
     launches = b.kernel_launch_count() - launches0
     check = None
     if args.check and world > 1:
@@ -731,7 +929,7 @@ def run_cpals(args, world=1, rank_id=0, local=0):
     cpu = None
     if rank_id == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cpu = als_reference_baseline(dims, nnz, R, skew, args.ref_step_s)
+            cpu, _ = als_reference_baseline(dims, nnz, R, skew, args.ref_step_s)
         except Exception as e:  # noqa: BLE001
             cpu = {"value": None, "unit": "ms", "cores": None, "kind": "reference", "sample": f"failed: {e}"}
     if world > 1:
@@ -756,9 +954,7 @@ def run_cpals(args, world=1, rank_id=0, local=0):
                       "mttkrp_per_iteration": round(ms_mt, 3),
                       "dense_per_iteration": round(ms_iter - ms_mt, 3)},
         "mttkrp_per_mode_ms": [round(x, 4) for x in mode_ms],
-        "roofline": {"bound": "hbm", "achieved": round(mttkrp_gbps, 2), "peak": peak, "unit": "GB/s",
-                     "frac": round(mttkrp_gbps / peak, 4), "traffic": None,
-                     "kernel": "k_mttkrp_sorted (one launch per mode)"},
+        "roofline": roofline,
         "clocks": clk.summary(), "gpu_launches": launches,
         "build": {"seconds": round(build_s, 3), "nnz_per_s": round(nnz / build_s, 1)},
         **({"check": check} if check else {}),
@@ -766,21 +962,21 @@ def run_cpals(args, world=1, rank_id=0, local=0):
     }), flush=True)
 
 
-def als_reference_baseline(dims, nnz, R, skew, step_s=4.0) -> dict:
+def als_reference_baseline(dims, nnz, R, skew, step_s=4.0, steps=2, warmup=1) -> tuple[dict, dict]:
     """The reference CPU MTTKRP part of one CP-ALS iteration (N blco::mttkrp
     calls), timed on a generator-prefix sample of the same power-law tensor
-    and extrapolated linearly by nnz.  The reference iteration also runs the
-    dense Gram / solve / normalise steps on the host, so this is a lower bound
-    of its time per iteration."""
-    gbps, info = reference_sample_run(dims, nnz, R, steps=2, warmup=1, target_step_s=step_s,
+    and extrapolated by nnz (reference_sample_run).  The reference iteration
+    also runs the dense Gram / solve / normalise steps on the host, so this is
+    a lower bound of its time per iteration."""
+    gbps, info = reference_sample_run(dims, nnz, R, steps=steps, warmup=warmup, target_step_s=step_s,
                                       sampler="generator_prefix", skew=skew)
     N = len(dims)
     ms = nnz * N * bytes_per_elem(N, R) / (gbps * 1e9) * 1e3
-    return {"value": round(ms, 1), "unit": "ms", "cores": info["threads"], "kind": "reference",
-            "sample": info["sample"], "mttkrp_gbps": round(gbps, 4), "sample_step_s": round(info["step_s"], 3),
-            "cpu_model": cpu_model(),
-            "note": "extrapolated: the reference's N-mode MTTKRP time per ALS iteration on the full tensor "
-                    "(its dense epilogue not included, so the reference iteration is slower still)"}
+    entry = cpu_baseline_entry(gbps, info)
+    entry.update({"value": round(ms, 1), "unit": "ms", "mttkrp_gbps": round(gbps, 4),
+                  "note": "extrapolated: the reference's N-mode MTTKRP time per ALS iteration on the full tensor "
+                          "(its dense epilogue not included, so the reference iteration is slower still)"})
+    return entry, info
 
 
 STREAM_CONFIGS = {
@@ -957,6 +1153,22 @@ def run_stream(args, world, rank_id, local):
             os.remove(file_info["path"])
         except OSError:
             pass
+    if args.check and world > 1:
+        # the ranks' all-reduced M_n of the last step against one device
+        # streaming every chunk of the tensor (stream_mttkrp_all_modes, G = 1)
+        cap_all = int(nnz_target * 1.02) + ncand
+        aidx = b.api.pinned_empty(cap_all, np.uint64)
+        avals = b.api.pinned_empty(cap_all, np.float64)
+        n_all = 0
+        for c in range(nchunks):
+            n_all += b.api.synth_alto_chunk(dims, c, nchunks, ncand, TENSOR_SEED, aidx[n_all:], avals[n_all:],
+                                            device=dev)
+        ablocks = [(o, min(bmax, n_all - o)) for o in range(0, n_all, bmax)]
+        want = b.stream_mttkrp_all_modes(((0, aidx[o:o + n], avals[o:o + n]) for o, n in ablocks), f, budget, cfg,
+                                         layout=layout, max_nnz_per_block=bmax, block_count=len(ablocks),
+                                         device=dev)
+        errs = [float(np.linalg.norm(o.cpu().numpy() - w) / np.linalg.norm(w)) for o, w in zip(douts, want)]
+        result["check"] = {"rel_frobenius_vs_single_device": errs, "ranks": world, "nnz_single_device": n_all}
     if per_mode:
         result["stream"]["per_mode_api"] = {
             "total_s": round(sum(r.total_seconds for r in per_mode), 3),
@@ -975,6 +1187,12 @@ def run_stream(args, world, rank_id, local):
         dist.destroy_process_group()
     if rank_id == 0:
         print(json.dumps(result), flush=True)
+
+
+def ref_step_s(args) -> float:
+    """Per-step sample size target of the reference arm, so --steps K
+    --warmup W stays within a few minutes (about 100 s of timed CPU work)."""
+    return max(0.2, min(args.ref_step_s, 100.0 / max(1, args.steps + args.warmup)))
 
 
 def run_reference(args, world, rank_id):
@@ -998,12 +1216,15 @@ def run_reference(args, world, rank_id):
     wide = int(np.prod(np.array(dims, dtype=object))) >= 2**64 or make_wide(dims)
     try:
         if kind == "als":
-            cpu = als_reference_baseline(dims, nnz, R, skew, args.ref_step_s)
+            cpu, info = als_reference_baseline(dims, nnz, R, skew, ref_step_s(args), args.steps, args.warmup)
             print(json.dumps({
                 "impl": "reference",
                 "metric": "CP-ALS time per iteration (N MTTKRPs + device Gram/solve/normalise + fit)",
-                "value": cpu["value"], "unit": "ms", "n_gpus": world, "steps": 2, "warmup": 1,
-                "ms_per_step": cpu["value"], "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+                "value": cpu["value"], "unit": "ms", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": round(info["step_s"] * 1e3, 3), "extrapolated": info["extrapolated"],
+                "sample_nnz": info["sample_nnz"], "sample_fraction": round(info["sample_fraction"], 6),
+                "full_ms_per_step_extrapolated": cpu["value"],
+                "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
                 "dtype": "f64", "data": "synthetic power-law draws (same generator and seeds as the ours arm)",
                 "config": {"workload": desc, "dims": dims, "nnz": nnz, "rank": R, "skew": skew},
                 "cpu_baseline": cpu,
@@ -1013,7 +1234,7 @@ def run_reference(args, world, rank_id):
             return
         small = kind == "mttkrp" and not wide and nnz <= 200_000_000
         gbps, info = reference_sample_run(dims, nnz, R, steps=args.steps, warmup=args.warmup,
-                                          target_step_s=args.ref_step_s,
+                                          target_step_s=ref_step_s(args),
                                           sampler="alto_prefix" if small else "generator_prefix",
                                           skew=1 if kind == "mttkrp" and wide else None,
                                           op="stream" if kind == "stream" else "mttkrp")
@@ -1029,7 +1250,13 @@ def run_reference(args, world, rank_id):
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
-        "ms_per_step": round(info["full_step_s"] * 1e3, 3),
+        # the timed steps are of the sample: their real duration, and the
+        # full-tensor step the value is computed from (a + b*nnz) beside it
+        "ms_per_step": round(info["step_s"] * 1e3, 3),
+        "extrapolated": info["extrapolated"],
+        "sample_nnz": info["sample_nnz"],
+        "sample_fraction": round(info["sample_fraction"], 6),
+        "full_ms_per_step_extrapolated": round(info["full_step_s"] * 1e3, 3),
         "higher_is_better": True,
         "scaling": "strong",
         "vs_baseline": None,
@@ -1037,11 +1264,11 @@ def run_reference(args, world, rank_id):
         "data": "synthetic (same generator and seeds as the ours arm)",
         "config": {"workload": desc, "dims": dims, "nnz": nnz, "rank": R, "modes": N,
                    "bytes_per_elem_per_mode": bytes_per_elem(N, R)},
-        "cpu_baseline": {"value": round(gbps, 4), "unit": "GB/s", "cores": info["threads"], "kind": "reference",
-                         "sample": info["sample"]},
+        "cpu_baseline": cpu_baseline_entry(gbps, info),
         "e2e": {"value": round(gbps, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "path": "unmodified reference blco::build_blco + blco::" + ("stream_mttkrp" if kind == "stream" else "mttkrp")
-                + " (proj/src, compiled into oracle/_ref/libblco_ref.so), ExecConfig{num_threads = all host threads}",
+                + f" (proj/src, compiled into oracle/_ref/libblco_ref.so), ExecConfig{{num_threads = {info['threads']}}}"
+                  " (the faster of 1 thread and all host threads)",
     }
     print(json.dumps(result), flush=True)
 
@@ -1053,7 +1280,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS) + sorted(ALS_CONFIGS) + sorted(STREAM_CONFIGS),
-                    default="nell2")
+                    default="amazon",
+                    help="default: BASELINE configs[2] (Amazon shape), the config the metric is quoted on")
     ap.add_argument("--rank", type=int, default=0)
     ap.add_argument("--strategy", choices=["Auto", "Register", "Hierarchical"], default="Auto")
     ap.add_argument("--reduce", choices=["reducescatter", "allreduce"], default="reducescatter",
@@ -1064,10 +1292,27 @@ def main():
     ap.add_argument("--ref-step-s", type=float, default=4.0)
     ap.add_argument("--check", action="store_true",
                     help="compare the step's (reduced) M_n with a single-device MTTKRP of the whole tensor")
+    ap.add_argument("--no-ncu", action="store_true", help="skip the live ncu DRAM-traffic pass (use profiles/)")
+    ap.add_argument("--no-extra", action="store_true", help="skip the NELL-2 key beside the Amazon headline")
+    ap.add_argument("--traffic-probe", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args.traffic_probe:
+        traffic_probe_worker(args)
+        return
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # --gpus N without a launcher: one rank per GPU under torchrun
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), str(ROOT / "bench.py"), *sys.argv[1:]]
+        sys.exit(subprocess.run(cmd).returncode)
     world, rank_id, local = dist_env()
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world} ranks were launched")
     if args.impl == "reference":
         run_reference(args, world, rank_id)
         return

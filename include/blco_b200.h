@@ -202,6 +202,13 @@ int blco_tensor_info(const blco_tensor* t, blco_layout* layout, uint64_t* nblock
                      uint64_t* nnz, uint64_t* max_nnz_per_block);
 int blco_tensor_blocks(const blco_tensor* t, uint64_t* keys, uint64_t* block_nnz);
 int blco_tensor_download(const blco_tensor* t, uint64_t* idx, double* vals);
+/* Order-free checksum of the element multiset (a checksum of checksums):
+ * sum over elements of mix64(cell ^ mix64(bits(value))) mod 2^64, with
+ * cell = sum_m c_m * prod_{k<m} dims[k] mod 2^64 and mix64 the SplitMix64
+ * finaliser.  Equal for any two tensors holding the same (coordinates,
+ * value) pairs, whatever their blocking; used to pin full-size device builds
+ * against the generator's stream (oracle orc_census_*). */
+int blco_tensor_census(const blco_tensor* t, uint64_t* hash);
 /* Device pointers (idx, vals) of the resident payload. */
 int blco_tensor_device_ptrs(const blco_tensor* t, const uint64_t** idx, const double** vals);
 void blco_tensor_free(blco_tensor* t);
@@ -215,6 +222,43 @@ int blco_save(const blco_tensor* t, const char* path);                   /* save
 int blco_load(const char* path, int device, blco_tensor** out);          /* load_blco */
 int blco_read_header(const char* path, blco_layout* layout, uint64_t* max_nnz_per_block,
                      uint64_t* block_count, uint16_t* version);            /* read_blco_header */
+/* The container on a caller-supplied byte stream (the C++ API's
+ * std::istream / std::ostream overloads: serialize_blco, read_blco_header,
+ * read_blco_block, deserialize_blco; blco_format.hpp:67-93).  A read hook
+ * returns the bytes produced (fewer only at end of stream), a write hook the
+ * bytes consumed; a short count raises "blco: truncated payload" /
+ * "blco: write failed" (BLCO_EIO). */
+typedef uint64_t (*blco_read_fn)(void* ctx, void* dst, uint64_t bytes);
+typedef uint64_t (*blco_write_fn)(void* ctx, const void* src, uint64_t bytes);
+/* caller storage for one block's payload: *idx and *vals must hold nnz
+ * elements each on return (return 0; non-zero = allocation failed) */
+typedef int (*blco_alloc_fn)(void* ctx, uint64_t nnz, uint64_t** idx, double** vals);
+
+typedef struct blco_container_header {
+  uint16_t version;
+  uint16_t order;
+  uint16_t target_bits;
+  uint64_t dims[BLCO_MAX_ORDER];
+  uint16_t mode_bits[BLCO_MAX_ORDER];
+  uint64_t max_nnz_per_block;
+  uint64_t block_count;
+} blco_container_header;
+
+/* read_blco_header (blco_format.cpp:173-191): magic, version, raw fields */
+int blco_container_read_header(blco_read_fn fn, void* ctx, blco_container_header* out);
+/* BlcoHeader::make_layout_checked (blco_format.cpp:193-199) */
+int blco_container_checked_layout(const blco_container_header* h, blco_layout* out);
+/* read_blco_block (blco_format.cpp:201-227): the record head (key range
+ * check), the payload into storage from `alloc`, then the per-element checks
+ * on `device` */
+int blco_container_read_block(blco_read_fn fn, void* ctx, const blco_layout* layout, uint64_t* key,
+                              uint64_t* nnz, blco_alloc_fn alloc, void* alloc_ctx, int device);
+/* serialize_blco (blco_format.cpp:149-166), header then one call per block */
+int blco_container_write_header(blco_write_fn fn, void* ctx, const blco_layout* layout,
+                                uint64_t max_nnz_per_block, uint64_t block_count);
+int blco_container_write_block(blco_write_fn fn, void* ctx, uint64_t key, uint64_t nnz, const uint64_t* idx,
+                               const double* vals);
+
 /* read_blco_block's element checks for one block (host or device indices) */
 int blco_validate_block(const blco_layout* layout, uint64_t key, uint64_t nnz, const uint64_t* idx,
                         int device);
@@ -287,7 +331,9 @@ typedef struct blco_block_view {
   const double* vals;
   /* BLCO_BLOCK_STABLE: idx/vals stay valid until blco_stream_mttkrp returns
    * (e.g. MemoryBlockSource), so the copy need not finish before the next
-   * pull.  Without it the library completes each pageable copy first. */
+   * pull.  Without it the library waits for each block's host-to-device copy
+   * (pinned or pageable) before pulling the next block, so a source may
+   * refill one buffer per pull. */
   uint32_t flags;
 } blco_block_view;
 

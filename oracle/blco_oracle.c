@@ -425,6 +425,73 @@ static void* rs_worker(void* arg) {
   return NULL;
 }
 
+/* Census of the uniform synthetic tensor, streamed from the generator (the
+ * COO is never stored): the order-free multiset hash the product computes on
+ * a device build (blco_tensor_census: sum of mix64(cell ^ mix64(value bits))
+ * mod 2^64) and the number of elements per block key of the target_bits
+ * layout (key = the stripped top ALTO bits, layout.cpp:84-95), from which the
+ * reference's block chunking (blco_format.cpp:86-111: runs of equal keys cut
+ * every max_nnz_per_block elements) follows.  key_counts has 2^stripped
+ * entries (stripped <= 20). */
+typedef struct census_job {
+  const feistel* fs;
+  const orc_layout* l;
+  uint64_t seed, e0, e1, hash, nkeys;
+  uint64_t* counts;
+} census_job;
+
+static void* census_worker(void* arg) {
+  census_job* j = arg;
+  uint64_t c[ORC_MAX_ORDER], h = 0;
+  for (uint64_t e = j->e0; e < j->e1; ++e) {
+    const uint64_t cell = feistel_cell(j->fs, e);
+    uint64_t x = cell;
+    for (int m = 0; m < j->l->order; ++m) {
+      c[m] = x % j->l->dims[m];
+      x /= j->l->dims[m];
+    }
+    uint64_t key = 0, reenc = 0;
+    orc_encode_coords(j->l, c, &key, &reenc);
+    if (key < j->nkeys) ++j->counts[key];
+    const double v = element_value(j->seed, e);
+    uint64_t vb;
+    memcpy(&vb, &v, sizeof vb);
+    h += mix64(cell ^ mix64(vb));
+  }
+  j->hash = h;
+  return NULL;
+}
+
+int orc_census_uniform(int order, const uint64_t* dims, uint64_t nnz, uint64_t seed, int target_bits,
+                       int threads, uint64_t* hash, uint64_t* key_counts) {
+  orc_layout l;
+  if (orc_make_layout(dims, order, target_bits, &l) != ORC_OK) return ORC_EFORMAT;
+  if (l.stripped_bits > 20) return fail("census: more than 2^20 block keys");
+  feistel fs;
+  if (feistel_init(order, dims, nnz, seed, &fs) != ORC_OK) return ORC_EFORMAT;
+  const uint64_t nkeys = 1ull << l.stripped_bits;
+  if (threads < 1) threads = 1;
+  if (threads > 256) threads = 256;
+  census_job jobs[256];
+  pthread_t tid[256];
+  for (int t = 0; t < threads; ++t) {
+    jobs[t] = (census_job){&fs, &l, seed, nnz / threads * t, t + 1 == threads ? nnz : nnz / threads * (t + 1),
+                           0, nkeys, calloc(nkeys, sizeof(uint64_t))};
+    if (!jobs[t].counts) return fail("census: out of memory");
+    pthread_create(&tid[t], NULL, census_worker, &jobs[t]);
+  }
+  uint64_t h = 0;
+  memset(key_counts, 0, nkeys * sizeof(uint64_t));
+  for (int t = 0; t < threads; ++t) {
+    pthread_join(tid[t], NULL);
+    h += jobs[t].hash;
+    for (uint64_t k = 0; k < nkeys; ++k) key_counts[k] += jobs[t].counts[k];
+    free(jobs[t].counts);
+  }
+  *hash = h;
+  return ORC_OK;
+}
+
 /* Row-sampled mttkrp_coo over an in-memory COO (idx mode-major): rows
  * rows[m][0..nrows[m]) of every mode, one pass in COO order with the oracle's
  * product order (oracle.cpp:15-24), so the rows are bit-identical to

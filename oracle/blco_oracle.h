@@ -122,6 +122,13 @@ int orc_rowsample_uniform(int order, const uint64_t* dims, uint64_t nnz, uint64_
                           const double* const* f, uint64_t rank, const uint64_t* nrows,
                           const uint64_t* const* rows, double* const* out, int threads);
 
+/* Census of T = orc_synth_uniform(dims, nnz, seed), streamed on `threads`
+ * threads: the order-free multiset hash (sum of mix64(cell ^ mix64(value
+ * bits)) mod 2^64, cell = the mixed-radix cell id) and the element count per
+ * block key of the target_bits layout (key_counts[2^stripped_bits]). */
+int orc_census_uniform(int order, const uint64_t* dims, uint64_t nnz, uint64_t seed, int target_bits,
+                       int threads, uint64_t* hash, uint64_t* key_counts);
+
 int orc_alto_lo_batch(const orc_layout* l, uint64_t nnz, const uint64_t* idx, uint64_t* out);
 
 /* Independent per-mode draws floor(I * u^skew), first nnz distinct tuples. */

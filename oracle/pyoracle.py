@@ -182,6 +182,25 @@ class Oracle:
                                                 int(threads or os.cpu_count() or 1)))
         return outs
 
+    def census_uniform(self, dims, nnz, seed, target_bits=64, threads=None):
+        """(multiset hash, per-key element counts) of the uniform synthetic
+        tensor, streamed from the generator on all host threads."""
+        import os
+        l = self.layout(dims, target_bits)
+        counts = np.zeros(1 << l.stripped_bits, np.uint64)
+        h = C.c_uint64()
+        self._ck(self.lib.orc_census_uniform(len(dims), _pu(_u64(dims)), C.c_uint64(nnz), C.c_uint64(seed),
+                                             target_bits, threads or os.cpu_count() or 1, C.byref(h), _pu(counts)))
+        return int(h.value), counts
+
+    def solve_normal(self, m, v):
+        """dense_kernels.cpp:68-92 (Tikhonov escalation included); raises
+        OracleError when V stays singular after the maximal shift."""
+        a = np.array(m, np.float64, copy=True, order="C")
+        v = np.ascontiguousarray(v, np.float64)
+        self._ck(self.lib.orc_solve_normal(_pd(a), C.c_uint64(a.shape[0]), _pd(v), C.c_uint64(v.shape[0])))
+        return a
+
     def synth_draws(self, dims, nnz, seed, skew=1):
         idx = np.zeros((len(dims), nnz), np.uint64)
         vals = np.zeros(nnz)

@@ -144,6 +144,7 @@ SIGNATURES = {
     "blco_tensor_blocks": (_I, [_P, _PU64, _PU64]),
     "blco_tensor_download": (_I, [_P, _PU64, _PD]),
     "blco_tensor_device_ptrs": (_I, [_P, C.POINTER(_P), C.POINTER(_P)]),
+    "blco_tensor_census": (_I, [_P, C.POINTER(C.c_uint64)]),
     "blco_tensor_free": (None, [_P]),
     "blco_save": (_I, [_P, C.c_char_p]),
     "blco_load": (_I, [C.c_char_p, _I, C.POINTER(_P)]),

@@ -476,6 +476,13 @@ class DeviceTensor:
                                                   C.c_void_p((ip.value or 0) + 8 * off)))
             off += int(bn[b])
 
+    def census(self) -> int:
+        """Order-free checksum of the (coordinates, value) multiset
+        (blco_tensor_census), computed on the device."""
+        h = C.c_uint64()
+        _check(lib.blco_tensor_census(self._h, C.byref(h)))
+        return int(h.value)
+
     def to_host(self) -> BlcoTensor:
         keys = np.zeros(max(1, self.nblocks), np.uint64)
         bn = np.zeros(max(1, self.nblocks), np.uint64)
@@ -1059,3 +1066,9 @@ def device_count() -> int:
 
 def kernel_launch_count() -> int:
     return int(lib.blco_kernel_launch_count())
+
+
+def release_thread_caches() -> None:
+    """Frees this thread's cached device buffers (host pipeline, streaming,
+    deterministic-mode and MTTKRP workspaces; blco_release_thread_caches)."""
+    _check(lib.blco_release_thread_caches())

@@ -110,6 +110,9 @@ extern "C" int blco_mttkrp_all_host(const blco_layout* layout, uint64_t nblocks,
     blco_exec_config c;
     if (cfg) c = *cfg; else blco_exec_config_default(&c);
     if (blco_exec_config_validate(&c) != BLCO_OK) throw_format(blco_last_error());
+    // rejected before any copy is queued (the per-chunk launches would throw
+    // with the caller's buffers still in flight)
+    if (c.deterministic) throw_format("b200: deterministic mode needs a device-resident tensor (not the streamed paths)");
     if (!layout) throw_format("mttkrp: null layout");
     const blco_layout& l = *layout;
     check_device_layout(l);

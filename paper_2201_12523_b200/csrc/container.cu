@@ -90,7 +90,38 @@ void validate_device(const blco_layout& l, uint64_t key, const uint64_t* d_idx, 
   if (h & 4u) throw_format("blco: elements not in ascending ALTO order");
 }
 
-// ---- raw little-endian I/O
+// ---- order-free element census (a checksum of checksums over a tensor):
+// sum over elements of mix64(cell ^ mix64(value bits)) mod 2^64, where cell =
+// sum_m c_m * prod_{k<m} dims[k] (mod 2^64) -- the mixed-radix cell id the
+// synthetic generators draw, so the oracle can hash the generator's stream
+// without storing it (oracle/blco_oracle.c orc_census_*).
+__device__ __forceinline__ uint64_t census_mix(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void k_census_block(CheckParams c, const uint64_t* __restrict__ idx, const double* __restrict__ vals,
+                               uint64_t n, unsigned long long* __restrict__ sum) {
+  uint64_t h = 0;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t x = idx[i];
+    uint64_t cell = 0, st = 1;
+    for (int m = 0; m < c.order; ++m) {
+      const uint64_t coord = c.base[m] | ((x >> c.shift[m]) & c.mask[m]);
+      cell += coord * st;
+      st *= c.dims[m];
+    }
+    h += census_mix(cell ^ census_mix(__double_as_longlong(vals[i])));
+  }
+  for (int d = 16; d > 0; d >>= 1) h += __shfl_down_sync(0xffffffffu, h, d);
+  if ((threadIdx.x & 31) == 0 && h) atomicAdd(sum, static_cast<unsigned long long>(h));
+}
+
+// ---- raw little-endian I/O over a byte stream: a FILE* (blco_save/load,
+// the file block source) or a caller's stream through the blco_read_fn /
+// blco_write_fn hooks (the C++ API's std::istream / std::ostream).
 struct File {
   FILE* f = nullptr;
   ~File() {
@@ -98,20 +129,65 @@ struct File {
   }
 };
 
-template <class T>
-void put(FILE* f, const T& v) {
-  if (std::fwrite(&v, sizeof(T), 1, f) != 1) throw Status(BLCO_EIO, "blco: write failed");
+uint64_t file_read(void* ctx, void* dst, uint64_t n) { return std::fread(dst, 1, n, static_cast<FILE*>(ctx)); }
+uint64_t file_write(void* ctx, const void* src, uint64_t n) {
+  return std::fwrite(src, 1, n, static_cast<FILE*>(ctx));
 }
 
-template <class T>
-T get(FILE* f) {
-  T v{};
-  if (std::fread(&v, sizeof(T), 1, f) != 1) throw Status(BLCO_EIO, "blco: truncated payload");
-  return v;
+struct ByteIn {
+  blco_read_fn fn;
+  void* ctx;
+  void bytes(void* dst, uint64_t n) const {
+    if (n && fn(ctx, dst, n) != n) throw Status(BLCO_EIO, "blco: truncated payload");
+  }
+  template <class T>
+  T word() const {
+    T v{};
+    bytes(&v, sizeof(T));
+    return v;
+  }
+};
+
+struct ByteOut {
+  blco_write_fn fn;
+  void* ctx;
+  void bytes(const void* src, uint64_t n) const {
+    if (n && fn(ctx, src, n) != n) throw Status(BLCO_EIO, "blco: write failed");
+  }
+  template <class T>
+  void word(T v) const {
+    bytes(&v, sizeof(T));
+  }
+};
+
+ByteIn in_of(FILE* f) { return ByteIn{file_read, f}; }
+ByteOut out_of(FILE* f) { return ByteOut{file_write, f}; }
+
+// read_blco_header (blco_format.cpp:173-191): the raw fields, unchecked
+blco_container_header parse_header(const ByteIn& in) {
+  char magic[4] = {};
+  if (in.fn(in.ctx, magic, 4) != 4 || std::memcmp(magic, "BLCO", 4) != 0) throw_format("blco: bad magic");
+  blco_container_header h{};
+  h.version = in.word<uint16_t>();
+  if (h.version != 1) throw_format("blco: unsupported format version " + std::to_string(h.version));
+  h.order = in.word<uint16_t>();
+  if (h.order < 1) throw_format("blco: order must be >= 1");
+  if (h.order > BLCO_MAX_ORDER) throw_format("blco: order exceeds " + std::to_string(BLCO_MAX_ORDER));
+  in.bytes(h.dims, h.order * sizeof(uint64_t));
+  h.target_bits = in.word<uint16_t>();
+  in.bytes(h.mode_bits, h.order * sizeof(uint16_t));
+  h.max_nnz_per_block = in.word<uint64_t>();
+  h.block_count = in.word<uint64_t>();
+  return h;
 }
 
-void get_n(FILE* f, void* dst, size_t bytes) {
-  if (bytes && std::fread(dst, 1, bytes, f) != bytes) throw Status(BLCO_EIO, "blco: truncated payload");
+// BlcoHeader::make_layout_checked (blco_format.cpp:193-199)
+blco_layout checked_layout(const blco_container_header& h) {
+  blco_layout l = make_layout(h.dims, h.order, h.target_bits);
+  for (int m = 0; m < h.order; ++m)
+    if (l.mode_bits[m] != h.mode_bits[m]) throw_format("blco: stored mode bit widths do not match dims");
+  if (h.max_nnz_per_block < 1) throw_format("blco: max_nnz_per_block must be >= 1");
+  return l;
 }
 
 struct Header {
@@ -120,39 +196,34 @@ struct Header {
   uint64_t max_nnz = 0, nblocks = 0;
 };
 
-// read_blco_header + make_layout_checked (blco_format.cpp:173-199)
-Header read_header(FILE* f) {
-  char magic[4] = {};
-  if (std::fread(magic, 1, 4, f) != 4 || std::memcmp(magic, "BLCO", 4) != 0)
-    throw_format("blco: bad magic");
-  Header h;
-  h.version = get<uint16_t>(f);
-  if (h.version != 1) throw_format("blco: unsupported format version " + std::to_string(h.version));
-  const uint16_t order = get<uint16_t>(f);
-  if (order < 1) throw_format("blco: order must be >= 1");
-  std::vector<uint64_t> dims(order);
-  get_n(f, dims.data(), order * 8);
-  const uint16_t target = get<uint16_t>(f);
-  std::vector<uint16_t> mb(order);
-  get_n(f, mb.data(), order * 2);
-  h.max_nnz = get<uint64_t>(f);
-  h.nblocks = get<uint64_t>(f);
-  h.layout = make_layout(dims.data(), order, target);
-  for (int m = 0; m < order; ++m)
-    if (h.layout.mode_bits[m] != mb[m]) throw_format("blco: stored mode bit widths do not match dims");
-  if (h.max_nnz < 1) throw_format("blco: max_nnz_per_block must be >= 1");
-  return h;
+Header read_header(const ByteIn& in) {
+  const blco_container_header raw = parse_header(in);
+  return Header{raw.version, checked_layout(raw), raw.max_nnz_per_block, raw.block_count};
 }
 
-void write_header(FILE* f, const blco_layout& l, uint64_t max_nnz, uint64_t nblocks) {
-  if (std::fwrite("BLCO", 1, 4, f) != 4) throw Status(BLCO_EIO, "blco: write failed");
-  put<uint16_t>(f, 1);
-  put<uint16_t>(f, static_cast<uint16_t>(l.order));
-  for (int m = 0; m < l.order; ++m) put<uint64_t>(f, l.dims[m]);
-  put<uint16_t>(f, static_cast<uint16_t>(l.target_bits));
-  for (int m = 0; m < l.order; ++m) put<uint16_t>(f, static_cast<uint16_t>(l.mode_bits[m]));
-  put<uint64_t>(f, max_nnz);
-  put<uint64_t>(f, nblocks);
+void write_header(const ByteOut& out, const blco_layout& l, uint64_t max_nnz, uint64_t nblocks) {
+  out.bytes("BLCO", 4);
+  out.word<uint16_t>(1);
+  out.word<uint16_t>(static_cast<uint16_t>(l.order));
+  out.bytes(l.dims, l.order * sizeof(uint64_t));
+  out.word<uint16_t>(static_cast<uint16_t>(l.target_bits));
+  for (int m = 0; m < l.order; ++m) out.word<uint16_t>(static_cast<uint16_t>(l.mode_bits[m]));
+  out.word<uint64_t>(max_nnz);
+  out.word<uint64_t>(nblocks);
+}
+
+void write_record(const ByteOut& out, uint64_t key, uint64_t n, const uint64_t* idx, const double* vals) {
+  out.word<uint64_t>(key);
+  out.word<uint64_t>(n);
+  out.bytes(idx, n * sizeof(uint64_t));
+  out.bytes(vals, n * sizeof(double));
+}
+
+// read_blco_block's record head (blco_format.cpp:201-207): key range, nnz
+void read_record_head(const ByteIn& in, const blco_layout& l, uint64_t* key, uint64_t* n) {
+  *key = in.word<uint64_t>();
+  if (l.stripped_bits < 64 && *key >= (uint64_t{1} << l.stripped_bits)) throw_format("blco: block key out of range");
+  *n = in.word<uint64_t>();
 }
 
 }  // namespace
@@ -173,7 +244,7 @@ void throw_block_check(unsigned bad) {
 }
 
 BlcoFileHeader read_blco_file_header(FILE* f) {
-  const Header h = read_header(f);
+  const Header h = read_header(in_of(f));
   return BlcoFileHeader{h.version, h.layout, h.max_nnz, h.nblocks};
 }
 
@@ -206,21 +277,19 @@ int blco_save(const blco_tensor* t, const char* path) {
     f.f = std::fopen(path, "wb");
     if (!f.f) throw Status(BLCO_EIO, std::string("cannot open ") + path + " for writing");
     DeviceGuard dg(t->device);
-    write_header(f.f, t->layout, t->max_nnz_per_block, t->nblocks());
+    const ByteOut out = out_of(f.f);
+    write_header(out, t->layout, t->max_nnz_per_block, t->nblocks());
     std::vector<uint64_t> idx;
     std::vector<double> vals;
     for (uint64_t b = 0; b < t->nblocks(); ++b) {
       const uint64_t o = t->offsets[b], n = t->offsets[b + 1] - o;
-      put<uint64_t>(f.f, t->keys[b]);
-      put<uint64_t>(f.f, n);
       idx.resize(n);
       vals.resize(n);
       if (n) {
         B200_CUDA(cudaMemcpy(idx.data(), t->idx.ptr + o, n * 8, cudaMemcpyDeviceToHost));
         B200_CUDA(cudaMemcpy(vals.data(), t->vals.ptr + o, n * 8, cudaMemcpyDeviceToHost));
-        if (std::fwrite(idx.data(), 8, n, f.f) != n || std::fwrite(vals.data(), 8, n, f.f) != n)
-          throw Status(BLCO_EIO, "blco: write failed");
       }
+      write_record(out, t->keys[b], n, idx.data(), vals.data());
     }
     if (std::fflush(f.f) != 0) throw Status(BLCO_EIO, "blco: write failed");
   });
@@ -232,7 +301,7 @@ int blco_read_header(const char* path, blco_layout* layout, uint64_t* max_nnz, u
     File f;
     f.f = std::fopen(path, "rb");
     if (!f.f) throw Status(BLCO_EIO, std::string("cannot open ") + path);
-    const Header h = read_header(f.f);
+    const Header h = read_header(in_of(f.f));
     if (layout) *layout = h.layout;
     if (max_nnz) *max_nnz = h.max_nnz;
     if (nblocks) *nblocks = h.nblocks;
@@ -248,7 +317,8 @@ int blco_load(const char* path, int device, blco_tensor** out) {
     File f;
     f.f = std::fopen(path, "rb");
     if (!f.f) throw Status(BLCO_EIO, std::string("cannot open ") + path);
-    const Header h = read_header(f.f);
+    const ByteIn in = in_of(f.f);
+    const Header h = read_header(in);
     check_device_layout(h.layout);
     DeviceGuard dg(device);
     auto* t = new blco_tensor;
@@ -260,15 +330,13 @@ int blco_load(const char* path, int device, blco_tensor** out) {
       std::vector<double> all_vals;
       uint64_t prev_key = 0;
       for (uint64_t b = 0; b < h.nblocks; ++b) {
-        const uint64_t key = get<uint64_t>(f.f);
-        const uint64_t n = get<uint64_t>(f.f);
-        if (h.layout.stripped_bits < 64 && key >= (uint64_t{1} << h.layout.stripped_bits))
-          throw_format("blco: block key out of range");
+        uint64_t key = 0, n = 0;
+        read_record_head(in, h.layout, &key, &n);
         const size_t o = all_idx.size();
         all_idx.resize(o + n);
         all_vals.resize(o + n);
-        get_n(f.f, all_idx.data() + o, n * 8);
-        get_n(f.f, all_vals.data() + o, n * 8);
+        in.bytes(all_idx.data() + o, n * 8);
+        in.bytes(all_vals.data() + o, n * 8);
         DevBuf<uint64_t> d(n);
         if (n) B200_CUDA(cudaMemcpy(d.ptr, all_idx.data() + o, n * 8, cudaMemcpyHostToDevice));
         validate_device(h.layout, key, d.ptr, n);
@@ -296,4 +364,66 @@ int blco_load(const char* path, int device, blco_tensor** out) {
   });
 }
 
+// ---- the container on a caller's byte stream (the C++ API's istream /
+// ostream entry points: serialize_blco, read_blco_header, read_blco_block,
+// deserialize_blco, FileBlockSource)
+int blco_container_read_header(blco_read_fn fn, void* ctx, blco_container_header* out) {
+  return guarded([&] { *out = parse_header(ByteIn{fn, ctx}); });
+}
+
+int blco_container_checked_layout(const blco_container_header* h, blco_layout* out) {
+  return guarded([&] { *out = checked_layout(*h); });
+}
+
+int blco_container_read_block(blco_read_fn fn, void* ctx, const blco_layout* layout, uint64_t* key,
+                              uint64_t* nnz, blco_alloc_fn alloc, void* alloc_ctx, int device) {
+  return guarded([&] {
+    const ByteIn in{fn, ctx};
+    read_record_head(in, *layout, key, nnz);
+    uint64_t* idx = nullptr;
+    double* vals = nullptr;
+    if (alloc(alloc_ctx, *nnz, &idx, &vals) != 0 || (*nnz && (!idx || !vals)))
+      throw_error("blco: block allocation failed");
+    in.bytes(idx, *nnz * sizeof(uint64_t));
+    in.bytes(vals, *nnz * sizeof(double));
+    check_device_layout(*layout);
+    DeviceGuard dg(device);
+    DevBuf<uint64_t> d(*nnz);
+    if (*nnz) B200_CUDA(cudaMemcpy(d.ptr, idx, *nnz * 8, cudaMemcpyHostToDevice));
+    validate_device(*layout, *key, d.ptr, *nnz);
+  });
+}
+
+int blco_container_write_header(blco_write_fn fn, void* ctx, const blco_layout* layout,
+                                uint64_t max_nnz_per_block, uint64_t block_count) {
+  return guarded([&] { write_header(ByteOut{fn, ctx}, *layout, max_nnz_per_block, block_count); });
+}
+
+int blco_container_write_block(blco_write_fn fn, void* ctx, uint64_t key, uint64_t nnz, const uint64_t* idx,
+                               const double* vals) {
+  return guarded([&] { write_record(ByteOut{fn, ctx}, key, nnz, idx, vals); });
+}
+
 }  // extern "C"
+
+extern "C" int blco_tensor_census(const blco_tensor* t, uint64_t* hash) {
+  return guarded([&] {
+    if (!t || !hash) throw_format("census: null argument");
+    DeviceGuard dg(t->device);
+    const blco_layout& l = t->layout;
+    DevBuf<unsigned long long> sum(1);
+    B200_CUDA(cudaMemset(sum.ptr, 0, sizeof(unsigned long long)));
+    for (uint64_t b = 0; b < t->nblocks(); ++b) {
+      const uint64_t n = t->offsets[b + 1] - t->offsets[b];
+      if (!n) continue;
+      const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, 148 * 16));
+      k_census_block<<<grid, 256>>>(check_params(l, t->keys[b]), t->idx.ptr + t->offsets[b],
+                                    t->vals.ptr + t->offsets[b], n, sum.ptr);
+      count_launch();
+      check_launch("k_census_block");
+    }
+    unsigned long long h = 0;
+    B200_CUDA(cudaMemcpy(&h, sum.ptr, sizeof h, cudaMemcpyDeviceToHost));
+    *hash = h;
+  });
+}

@@ -228,6 +228,7 @@ __global__ void k_small_prep(const double* __restrict__ grams, int N, int n, int
   double* L = sm + R * R;  // R x R
   __shared__ int fail;
   __shared__ double shift;
+  __shared__ double unit;  // trace / R; every thread's stop test reads it after a barrier
   const int RR = R * R;
   for (int i = threadIdx.x; i < RR; i += blockDim.x) {
     double v = 1.0;
@@ -236,7 +237,6 @@ __global__ void k_small_prep(const double* __restrict__ grams, int N, int n, int
     V[i] = v;
   }
   __syncthreads();
-  double unit = 1.0;
   if (threadIdx.x == 0) {
     double trace = 0.0;
     for (int i = 0; i < R; ++i) trace = __dadd_rn(trace, V[i * R + i]);
@@ -469,12 +469,16 @@ struct Dense {
   // factor (Tikhonov escalation) on the device, then A = M V^-1 over `rows`
   // rows fused with Gram(A), whose upper triangle is left in small.
   // status[0] is set when V stays singular after the maximal shift.
-  void solve(const double* m, double* a, uint64_t rows, const double* dgrams, int N, int n, int* dstatus) {
+  // const_L: R = 16/32 read L from the process-wide __constant__ c_L (only
+  // for callers that serialise the whole ALS run, blco_cp_als); otherwise
+  // the kernel reads L from this Dense's own device buffer.
+  void solve(const double* m, double* a, uint64_t rows, const double* dgrams, int N, int n, int* dstatus,
+             bool const_L = false) {
     const int RR = R * R;
     k_small_prep<<<1, 256, 2 * RR * sizeof(double), s>>>(dgrams, N, n, R, L.ptr, dstatus);
     count_launch();
     check_launch("k_small_prep");
-    if (exact_rank(R))
+    if (const_L && exact_rank(R))
       B200_CUDA(cudaMemcpyToSymbolAsync(c_L, L.ptr, RR * sizeof(double), 0, cudaMemcpyDeviceToDevice, s));
     if (!rows) {
       B200_CUDA(cudaMemsetAsync(small.ptr, 0, RR * sizeof(double), s));
@@ -497,8 +501,8 @@ struct Dense {
       check_launch("k_solve_gram");
       reduce(nslots, RR);
     };
-    if (R == 16) launch(k_solve_gram<16, true>, 16, solve_rows<16>());
-    else if (R == 32) launch(k_solve_gram<32, true>, 32, solve_rows<32>());
+    if (R == 16 && const_L) launch(k_solve_gram<16, true>, 16, solve_rows<16>());
+    else if (R == 32 && const_L) launch(k_solve_gram<32, true>, 32, solve_rows<32>());
     else if (R < 16) launch(k_solve_gram<16, false>, 16, solve_rows<16>());
     else if (R < 32) launch(k_solve_gram<32, false>, 32, solve_rows<32>());
     else if (R <= 64) launch(k_solve_gram<64, false>, 64, solve_rows<64>());
@@ -544,7 +548,7 @@ struct Dense {
       cudaEventRecord(pe[k], s);
     };
     pmark(0);
-    solve(m, a, rows, dgrams, N, n, dstatus);
+    solve(m, a, rows, dgrams, N, n, dstatus, /*const_L=*/true);  // only blco_cp_als (serialised) gets here
     pmark(1);
     normalize(small.ptr, a, rows, dgrams + static_cast<size_t>(n) * R * R, dlam, m_inner, dinner);
     pmark(2);

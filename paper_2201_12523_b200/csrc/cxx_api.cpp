@@ -10,6 +10,7 @@
 #include <ostream>
 #include <mutex>
 #include <numeric>
+#include <optional>
 #include <thread>
 
 #include <cuda_runtime.h>
@@ -156,82 +157,114 @@ void release_device_cache(const BlcoTensor* t) {
 
 // ------------------------------------------------------------------- types
 bool DenseMatrix::all_finite() const {
-  return std::all_of(data.begin(), data.end(), [](double v) { return std::isfinite(v); });
+  for (double v : data)
+    if (!std::isfinite(v)) return false;
+  return true;
 }
 
-void SparseTensorCoo::validate(bool check_duplicates) const {
-  if (static_cast<std::size_t>(order()) != indices.size())
-    throw FormatError("coo: index array count does not match order");
-  for (int m = 0; m < order(); ++m) {
-    if (dims[m] < 1) throw FormatError("coo: mode length must be >= 1");
-    if (indices[m].size() != values.size())
-      throw FormatError("coo: index/value arrays have mismatched lengths");
-    if (std::any_of(indices[m].begin(), indices[m].end(), [&](index_t i) { return i >= dims[m]; }))
-      throw FormatError("coo: coordinate out of range");
+namespace {
+
+// Tuples packed into one 128-bit word in lexicographic order (mode 0 most
+// significant, each mode in bits_for_extent(dims[m]) bits), so tuple order
+// and duplicates become integer order and equality.  nullopt when the modes
+// need more than 128 bits together.
+std::optional<std::vector<alto_t>> packed_tuples(std::span<const index_t> dims,
+                                                 const std::vector<std::vector<index_t>>& idx, std::size_t n) {
+  if (dims.size() != idx.size()) return std::nullopt;
+  int total = 0;
+  for (index_t d : dims) total += bits_for_extent(d);
+  if (total > 128) return std::nullopt;
+  std::vector<alto_t> key(n, 0);
+  for (std::size_t m = 0; m < dims.size(); ++m) {
+    const int w = bits_for_extent(dims[m]);
+    for (std::size_t e = 0; e < n; ++e) key[e] = w ? ((key[e] << w) | idx[m][e]) : key[e];
   }
-  if (!check_duplicates || nnz() < 2) return;
-  std::vector<std::size_t> p(nnz());
-  std::iota(p.begin(), p.end(), 0);
-  auto lex = [&](std::size_t a, std::size_t b) {
-    for (int m = 0; m < order(); ++m)
-      if (indices[m][a] != indices[m][b]) return indices[m][a] < indices[m][b];
-    return false;
-  };
-  std::sort(p.begin(), p.end(), lex);
-  for (std::size_t e = 1; e < p.size(); ++e)
-    if (!lex(p[e - 1], p[e])) throw FormatError("coo: duplicate coordinate tuple");
+  return key;
+}
+
+// Element ids in lexicographic tuple order, ties in input order.
+std::vector<std::uint32_t> tuple_order(std::span<const index_t> dims, const std::vector<std::vector<index_t>>& idx,
+                                       std::size_t n) {
+  std::vector<std::uint32_t> ids(n);
+  for (std::size_t e = 0; e < n; ++e) ids[e] = static_cast<std::uint32_t>(e);
+  if (auto key = packed_tuples(dims, idx, n)) {
+    const auto& k = *key;
+    std::stable_sort(ids.begin(), ids.end(), [&](std::uint32_t a, std::uint32_t b) { return k[a] < k[b]; });
+  } else {
+    std::stable_sort(ids.begin(), ids.end(), [&](std::uint32_t a, std::uint32_t b) {
+      for (const auto& mode : idx)
+        if (mode[a] != mode[b]) return mode[a] < mode[b];
+      return false;
+    });
+  }
+  return ids;
+}
+
+bool same_tuple(const std::vector<std::vector<index_t>>& idx, std::uint32_t a, std::uint32_t b) {
+  for (const auto& mode : idx)
+    if (mode[a] != mode[b]) return false;
+  return true;
+}
+
+}  // namespace
+
+void SparseTensorCoo::validate(bool check_duplicates) const {
+  if (indices.size() != dims.size()) throw FormatError("coo: index array count does not match order");
+  for (std::size_t m = 0; m < dims.size(); ++m) {
+    if (dims[m] == 0) throw FormatError("coo: mode length must be >= 1");
+    if (indices[m].size() != values.size()) throw FormatError("coo: index/value arrays have mismatched lengths");
+    const auto hi = std::max_element(indices[m].begin(), indices[m].end());
+    if (hi != indices[m].end() && *hi >= dims[m]) throw FormatError("coo: coordinate out of range");
+  }
+  if (!check_duplicates || values.size() < 2) return;
+  if (values.size() > UINT32_MAX) throw FormatError("coo: too many elements for the duplicate check");
+  const std::vector<std::uint32_t> ids = tuple_order(dims, indices, values.size());
+  for (std::size_t k = 1; k < ids.size(); ++k)
+    if (same_tuple(indices, ids[k - 1], ids[k])) throw FormatError("coo: duplicate coordinate tuple");
 }
 
 SparseTensorCoo SparseTensorCoo::from_arrays(std::vector<index_t> dims,
                                              std::vector<std::vector<index_t>> indices,
                                              std::vector<double> values) {
-  const int n = static_cast<int>(indices.size());
-  if (n == 0) throw FormatError("coo: at least one mode required");
-  for (const auto& v : indices)
-    if (v.size() != values.size()) throw FormatError("coo: index/value arrays have mismatched lengths");
-  if (dims.empty()) {
-    dims.assign(n, 1);
-    for (int m = 0; m < n; ++m)
-      for (index_t i : indices[m]) dims[m] = std::max(dims[m], i + 1);
-  }
-  // lexicographic stable order, equal tuples summed in input order
-  std::vector<std::size_t> p(values.size());
-  std::iota(p.begin(), p.end(), 0);
-  auto lex = [&](std::size_t a, std::size_t b) {
-    for (int m = 0; m < n; ++m)
-      if (indices[m][a] != indices[m][b]) return indices[m][a] < indices[m][b];
-    return false;
-  };
-  std::stable_sort(p.begin(), p.end(), lex);
+  if (indices.empty()) throw FormatError("coo: at least one mode required");
+  const std::size_t n = values.size();
+  if (std::any_of(indices.begin(), indices.end(), [&](const auto& v) { return v.size() != n; }))
+    throw FormatError("coo: index/value arrays have mismatched lengths");
+  if (n > UINT32_MAX) throw FormatError("coo: too many elements");
+  if (dims.empty())  // inferred: one past the largest coordinate of each mode
+    for (const auto& mode : indices)
+      dims.push_back(mode.empty() ? 1 : *std::max_element(mode.begin(), mode.end()) + 1);
+  // canonical form: tuples in lexicographic order, each distinct tuple once,
+  // its values summed in input order
+  const std::vector<std::uint32_t> ids = tuple_order(dims, indices, n);
   SparseTensorCoo out;
   out.dims = std::move(dims);
-  out.indices.assign(n, {});
-  for (std::size_t e = 0; e < p.size();) {
-    std::size_t f = e + 1;
-    double sum = values[p[e]];
-    while (f < p.size() && !lex(p[e], p[f]) && !lex(p[f], p[e])) sum += values[p[f++]];
-    for (int m = 0; m < n; ++m) out.indices[m].push_back(indices[m][p[e]]);
+  out.indices.assign(indices.size(), {});
+  std::size_t k = 0;
+  while (k < ids.size()) {
+    const std::uint32_t head = ids[k];
+    double sum = values[head];
+    for (++k; k < ids.size() && same_tuple(indices, head, ids[k]); ++k) sum += values[ids[k]];
+    for (std::size_t m = 0; m < indices.size(); ++m) out.indices[m].push_back(indices[m][head]);
     out.values.push_back(sum);
-    e = f;
   }
   out.validate();
   return out;
 }
 
 double SparseTensorCoo::norm_squared() const {
-  double s = 0.0;
-  for (double v : values) s += v * v;
-  return s;
+  return std::accumulate(values.begin(), values.end(), 0.0, [](double acc, double v) { return acc + v * v; });
 }
 
 void FactorMatrices::validate(std::span<const index_t> dims) const {
   if (factors.size() != dims.size()) throw FormatError("factors: mode count does not match tensor order");
-  for (std::size_t m = 0; m < factors.size(); ++m) {
+  auto shape = [](std::size_t r, std::size_t c) { return std::to_string(r) + "x" + std::to_string(c); };
+  for (std::size_t m = 0; m < dims.size(); ++m) {
     const DenseMatrix& a = factors[m];
-    if (a.rows != dims[m] || a.cols != rank)
-      throw FormatError("factors: mode " + std::to_string(m + 1) + " has shape " +
-                        std::to_string(a.rows) + "x" + std::to_string(a.cols) + ", expected " +
-                        std::to_string(dims[m]) + "x" + std::to_string(rank));
+    const bool ok = a.rows == dims[m] && a.cols == rank;
+    if (!ok)
+      throw FormatError("factors: mode " + std::to_string(m + 1) + " has shape " + shape(a.rows, a.cols) +
+                        ", expected " + shape(dims[m], rank));
     if (a.data.size() != a.rows * a.cols) throw FormatError("factors: malformed matrix storage");
   }
 }
@@ -251,10 +284,10 @@ FactorMatrices FactorMatrices::random(std::span<const index_t> dims, std::size_t
 FactorMatrices FactorMatrices::ones(std::span<const index_t> dims, std::size_t rank) {
   FactorMatrices f;
   f.rank = rank;
+  f.factors.reserve(dims.size());
   for (index_t d : dims) {
-    DenseMatrix a(d, rank);
-    std::fill(a.data.begin(), a.data.end(), 1.0);
-    f.factors.push_back(std::move(a));
+    f.factors.emplace_back(d, rank);
+    f.factors.back().data.assign(d * rank, 1.0);
   }
   return f;
 }
@@ -311,15 +344,13 @@ alto_t interleaved_remainder(const BitLayout& layout, index_t reencoded) {
 
 // ------------------------------------------------------------------- build
 bool BlcoTensor::structurally_equal(const BlcoTensor& o) const {
-  if (layout.dims != o.layout.dims || layout.target_bits != o.layout.target_bits ||
-      max_nnz_per_block != o.max_nnz_per_block || total_nnz != o.total_nnz ||
-      blocks.size() != o.blocks.size())
-    return false;
-  for (std::size_t b = 0; b < blocks.size(); ++b) {
-    const BlcoBlock &x = blocks[b], &y = o.blocks[b];
-    if (x.key != y.key || x.linear_indices != y.linear_indices || x.values != y.values) return false;
-  }
-  return true;
+  const bool same_frame = layout.dims == o.layout.dims && layout.target_bits == o.layout.target_bits &&
+                          max_nnz_per_block == o.max_nnz_per_block && total_nnz == o.total_nnz;
+  return same_frame && std::equal(blocks.begin(), blocks.end(), o.blocks.begin(), o.blocks.end(),
+                                  [](const BlcoBlock& x, const BlcoBlock& y) {
+                                    return x.key == y.key && x.values == y.values &&
+                                           x.linear_indices == y.linear_indices;
+                                  });
 }
 
 std::vector<BatchSpan> compute_batch_table(const BlcoTensor& t, std::uint64_t quota) {
@@ -388,46 +419,42 @@ SparseTensorCoo delinearize_all(const BlcoTensor& t) {
 }
 
 // --------------------------------------------------------------- container
+// The byte format and every check live in the library (container.cu); these
+// overloads only adapt std::istream / std::ostream to its stream hooks.
 namespace {
-template <class T>
-void write_raw(std::ostream& out, const T& v) {
-  out.write(reinterpret_cast<const char*>(&v), sizeof(T));
+std::uint64_t istream_read(void* ctx, void* dst, std::uint64_t n) {
+  auto& in = *static_cast<std::istream*>(ctx);
+  in.read(static_cast<char*>(dst), static_cast<std::streamsize>(n));
+  return static_cast<std::uint64_t>(in.gcount());
 }
 
-template <class T>
-T read_raw(std::istream& in) {
-  T v{};
-  in.read(reinterpret_cast<char*>(&v), sizeof(T));
-  if (!in) throw IoError("blco: truncated payload");
-  return v;
+std::uint64_t ostream_write(void* ctx, const void* src, std::uint64_t n) {
+  auto& out = *static_cast<std::ostream*>(ctx);
+  out.write(static_cast<const char*>(src), static_cast<std::streamsize>(n));
+  return out ? n : 0;
 }
 
-template <class T>
-void read_vec(std::istream& in, std::vector<T>& v, std::size_t n) {
-  v.resize(n);
-  in.read(reinterpret_cast<char*>(v.data()), static_cast<std::streamsize>(n * sizeof(T)));
-  if (!in) throw IoError("blco: truncated payload");
+int block_storage(void* ctx, std::uint64_t n, std::uint64_t** idx, double** vals) {
+  auto& blk = *static_cast<BlcoBlock*>(ctx);
+  blk.linear_indices.resize(n);
+  blk.values.resize(n);
+  *idx = blk.linear_indices.data();
+  *vals = blk.values.data();
+  return 0;
+}
+
+// the std::ostream overloads report a failed stream as the reference does
+void throw_if_failed(const std::ostream& out) {
+  if (!out) throw IoError("blco: write failed");
 }
 }  // namespace
 
 void serialize_blco(const BlcoTensor& t, std::ostream& out) {
-  out.write("BLCO", 4);
-  write_raw<std::uint16_t>(out, 1);
-  write_raw<std::uint16_t>(out, static_cast<std::uint16_t>(t.order()));
-  for (index_t d : t.layout.dims) write_raw<std::uint64_t>(out, d);
-  write_raw<std::uint16_t>(out, static_cast<std::uint16_t>(t.layout.target_bits));
-  for (int b : t.layout.mode_bits) write_raw<std::uint16_t>(out, static_cast<std::uint16_t>(b));
-  write_raw<std::uint64_t>(out, t.max_nnz_per_block);
-  write_raw<std::uint64_t>(out, t.blocks.size());
-  for (const BlcoBlock& b : t.blocks) {
-    write_raw<std::uint64_t>(out, b.key);
-    write_raw<std::uint64_t>(out, b.nnz());
-    out.write(reinterpret_cast<const char*>(b.linear_indices.data()),
-              static_cast<std::streamsize>(b.nnz() * sizeof(index_t)));
-    out.write(reinterpret_cast<const char*>(b.values.data()),
-              static_cast<std::streamsize>(b.nnz() * sizeof(double)));
-  }
-  if (!out) throw IoError("blco: write failed");
+  const blco_layout c = to_c(t.layout);
+  ck(blco_container_write_header(ostream_write, &out, &c, t.max_nnz_per_block, t.blocks.size()));
+  for (const BlcoBlock& b : t.blocks)
+    ck(blco_container_write_block(ostream_write, &out, b.key, b.nnz(), b.linear_indices.data(), b.values.data()));
+  throw_if_failed(out);
 }
 
 void save_blco(const BlcoTensor& t, const std::filesystem::path& path) {
@@ -437,41 +464,40 @@ void save_blco(const BlcoTensor& t, const std::filesystem::path& path) {
 }
 
 BlcoHeader read_blco_header(std::istream& in) {
-  char magic[4] = {};
-  in.read(magic, 4);
-  if (!in || std::memcmp(magic, "BLCO", 4) != 0) throw FormatError("blco: bad magic");
+  blco_container_header raw{};
+  ck(blco_container_read_header(istream_read, &in, &raw));
   BlcoHeader h;
-  h.version = read_raw<std::uint16_t>(in);
-  if (h.version != 1) throw FormatError("blco: unsupported format version " + std::to_string(h.version));
-  const auto order = read_raw<std::uint16_t>(in);
-  if (order < 1) throw FormatError("blco: order must be >= 1");
-  read_vec(in, h.dims, order);
-  h.target_bits = read_raw<std::uint16_t>(in);
-  std::vector<std::uint16_t> mb;
-  read_vec(in, mb, order);
-  h.mode_bits.assign(mb.begin(), mb.end());
-  h.max_nnz_per_block = read_raw<std::uint64_t>(in);
-  h.block_count = read_raw<std::uint64_t>(in);
+  h.version = raw.version;
+  h.dims.assign(raw.dims, raw.dims + raw.order);
+  h.target_bits = raw.target_bits;
+  h.mode_bits.assign(raw.mode_bits, raw.mode_bits + raw.order);
+  h.max_nnz_per_block = raw.max_nnz_per_block;
+  h.block_count = raw.block_count;
   return h;
 }
 
 BitLayout BlcoHeader::make_layout_checked() const {
-  BitLayout l = make_layout(dims, target_bits);
-  if (l.mode_bits != mode_bits) throw FormatError("blco: stored mode bit widths do not match dims");
-  if (max_nnz_per_block < 1) throw FormatError("blco: max_nnz_per_block must be >= 1");
-  return l;
+  blco_container_header raw{};
+  if (dims.size() > BLCO_MAX_ORDER || mode_bits.size() != dims.size())
+    throw FormatError("blco: stored mode bit widths do not match dims");
+  raw.version = version;
+  raw.order = static_cast<std::uint16_t>(dims.size());
+  raw.target_bits = static_cast<std::uint16_t>(target_bits);
+  std::copy(dims.begin(), dims.end(), raw.dims);
+  std::transform(mode_bits.begin(), mode_bits.end(), raw.mode_bits,
+                 [](int b) { return static_cast<std::uint16_t>(b); });
+  raw.max_nnz_per_block = max_nnz_per_block;
+  raw.block_count = block_count;
+  blco_layout c{};
+  ck(blco_container_checked_layout(&raw, &c));
+  return from_c(c);
 }
 
 BlcoBlock read_blco_block(std::istream& in, const BitLayout& layout) {
-  BlcoBlock blk;
-  blk.key = read_raw<std::uint64_t>(in);
-  if (layout.stripped_bits < 64 && blk.key >= (index_t{1} << layout.stripped_bits))
-    throw FormatError("blco: block key out of range");
-  const auto n = read_raw<std::uint64_t>(in);
-  read_vec(in, blk.linear_indices, n);
-  read_vec(in, blk.values, n);
   const blco_layout c = to_c(layout);
-  ck(blco_validate_block(&c, blk.key, n, blk.linear_indices.data(), current_device()));
+  BlcoBlock blk;
+  std::uint64_t n = 0;
+  ck(blco_container_read_block(istream_read, &in, &c, &blk.key, &n, block_storage, &blk, current_device()));
   return blk;
 }
 
@@ -480,15 +506,17 @@ BlcoTensor deserialize_blco(std::istream& in) {
   BlcoTensor t;
   t.layout = h.make_layout_checked();
   t.max_nnz_per_block = h.max_nnz_per_block;
-  index_t prev = 0;
+  t.blocks.reserve(h.block_count);
   for (std::uint64_t b = 0; b < h.block_count; ++b) {
-    BlcoBlock blk = read_blco_block(in, t.layout);
-    if (blk.nnz() == 0) throw FormatError("blco: empty block record");
-    if (blk.nnz() > t.max_nnz_per_block) throw FormatError("blco: block exceeds max_nnz_per_block");
-    if (b > 0 && blk.key < prev) throw FormatError("blco: blocks not in ascending key order");
-    prev = blk.key;
+    t.blocks.push_back(read_blco_block(in, t.layout));
+    const BlcoBlock& blk = t.blocks.back();
+    // record-level rules of deserialize_blco (blco_format.cpp:236-242)
+    const char* bad = blk.nnz() == 0                    ? "blco: empty block record"
+                      : blk.nnz() > t.max_nnz_per_block ? "blco: block exceeds max_nnz_per_block"
+                      : b > 0 && blk.key < t.blocks[b - 1].key ? "blco: blocks not in ascending key order"
+                                                               : nullptr;
+    if (bad) throw FormatError(bad);
     t.total_nnz += blk.nnz();
-    t.blocks.push_back(std::move(blk));
   }
   t.batch_quota = kDefaultBatchQuota;
   t.batch_table = compute_batch_table(t, t.batch_quota);
@@ -511,7 +539,7 @@ FileBlockSource::FileBlockSource(const std::filesystem::path& path)
 FileBlockSource::~FileBlockSource() = default;
 
 bool FileBlockSource::next(BlcoBlock& out) {
-  if (cursor_ >= header_.block_count) return false;
+  if (cursor_ == header_.block_count) return false;
   out = read_blco_block(*in_, layout_);
   ++cursor_;
   return true;

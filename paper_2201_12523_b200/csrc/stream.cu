@@ -77,15 +77,6 @@ double union_seconds(std::vector<std::pair<double, double>> iv) {
   return total;
 }
 
-bool is_pinned(const void* p) {
-  cudaPointerAttributes a{};
-  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
-    cudaGetLastError();
-    return false;
-  }
-  return a.type == cudaMemoryTypeHost;
-}
-
 // Where blocks come from: the caller's pull callback (BlockSource::next) or
 // the native .blco file reader below.
 struct BlockFeed {
@@ -257,13 +248,16 @@ void stream_impl(const blco_layout* layout, uint64_t max_nnz_per_block, BlockFee
         B200_CUDA(cudaEventRecord(tr.e, q.stream));
         feed.transferred(ordinal, tr.e);
         if (feed.validate()) enqueue_block_check(l, bv.key, q.idx.ptr, bv.nnz, dbad.ptr, q.stream);
-        // a transient source buffer may be overwritten by the next pull
+        // A block without BLCO_BLOCK_STABLE may be overwritten by the next
+        // pull: wait until its copy has read the source.  This matters for
+        // pinned sources above all -- a pinned cudaMemcpyAsync returns at once
+        // and the DMA reads host memory later (a pageable one has already
+        // staged the bytes on return, so its wait is nearly free).
         static const int dbg_sync = [] {
           const char* e = std::getenv("BLCO_B200_STREAM_SYNC");
           return e ? std::atoi(e) : 0;
         }();
-        if ((dbg_sync & 1) ||
-            (bv.nnz && !(bv.flags & BLCO_BLOCK_STABLE) && (!is_pinned(bv.idx) || !is_pinned(bv.vals))))
+        if ((dbg_sync & 1) || (bv.nnz && !(bv.flags & BLCO_BLOCK_STABLE)))
           B200_CUDA(cudaEventSynchronize(tr.e));
 
         B200_CUDA(cudaEventRecord(cp.b, q.stream));

@@ -382,6 +382,89 @@ TEST(serialize_roundtrip) {  // test_blco.cpp:124-135
   CHECK_THROWS_AS(deserialize_blco(in_trunc), IoError);
 }
 
+TEST(coo_canonical_form) {  // types.cpp:38-77 semantics: lexicographic order, duplicates summed in input order
+  auto t = SparseTensorCoo::from_arrays({}, {{2, 0, 2, 1, 0}, {1, 3, 1, 0, 3}}, {1.0, 2.0, 4.0, 8.0, -0.0});
+  CHECK((t.dims == std::vector<index_t>{3, 4}));
+  CHECK((t.indices[0] == std::vector<index_t>{0, 1, 2}));
+  CHECK((t.indices[1] == std::vector<index_t>{3, 0, 1}));
+  CHECK((t.values == std::vector<double>{2.0, 8.0, 5.0}));
+  auto z = SparseTensorCoo::from_arrays({5}, {{4}}, {-0.0});  // a lone -0.0 keeps its sign
+  CHECK(std::signbit(z.values[0]));
+  CHECK_THROWS_AS(SparseTensorCoo::from_arrays({}, {}, {}), FormatError);
+  CHECK_THROWS_AS(SparseTensorCoo::from_arrays({}, {{0, 1}}, {1.0}), FormatError);
+  CHECK_THROWS_AS(SparseTensorCoo::from_arrays({2}, {{0, 2}}, {1.0, 2.0}), FormatError);  // out of range
+  // > 128 bits of modes: the tuple-comparison path
+  std::vector<index_t> wide(5, index_t{1} << 40);
+  auto w = SparseTensorCoo::from_arrays(wide, {{1, 0}, {0, 0}, {0, 0}, {0, 0}, {0, 0}}, {1.0, 2.0});
+  CHECK((w.indices[0] == std::vector<index_t>{0, 1}) && (w.values == std::vector<double>{2.0, 1.0}));
+}
+
+TEST(coo_validate) {  // types.cpp:13-36
+  SparseTensorCoo t;
+  t.dims = {3, 3};
+  t.indices = {{0, 1, 0}, {2, 2, 2}};
+  t.values = {1, 2, 3};
+  t.validate();
+  CHECK_THROWS_AS(t.validate(true), FormatError);  // (0, 2) twice
+  t.indices[0][2] = 2;
+  t.validate(true);
+  t.indices[1][1] = 3;
+  CHECK_THROWS_AS(t.validate(), FormatError);
+  t.indices[1][1] = 2;
+  t.dims[0] = 0;
+  CHECK_THROWS_AS(t.validate(), FormatError);
+  t.dims = {3};
+  CHECK_THROWS_AS(t.validate(), FormatError);
+}
+
+TEST(container_bytes_and_records) {  // blco_format.cpp:149-227 byte layout and record checks
+  auto t = build_blco(golden_tensor(), 5, 6);
+  std::ostringstream out;
+  serialize_blco(t, out);
+  const std::string bytes = out.str();
+  std::size_t expect = 4 + 2 + 2 + 3 * 8 + 2 + 3 * 2 + 8 + 8;
+  for (const auto& b : t.blocks) expect += 16 + 16 * b.nnz();
+  CHECK(bytes.size() == expect && bytes.compare(0, 4, "BLCO") == 0);
+  std::istringstream in(bytes);
+  const BlcoHeader h = read_blco_header(in);
+  CHECK(h.version == 1 && h.target_bits == 5 && h.max_nnz_per_block == 6 && h.block_count == t.blocks.size());
+  CHECK((h.dims == std::vector<index_t>{4, 4, 4}) && (h.mode_bits == std::vector<int>{2, 2, 2}));
+  const BitLayout l = h.make_layout_checked();
+  for (const auto& want : t.blocks) {
+    const BlcoBlock got = read_blco_block(in, l);
+    CHECK(got.key == want.key && got.linear_indices == want.linear_indices && got.values == want.values);
+  }
+  BlcoHeader bad = h;
+  bad.mode_bits[1] = 3;
+  CHECK_THROWS_AS(bad.make_layout_checked(), FormatError);
+  bad = h;
+  bad.max_nnz_per_block = 0;
+  CHECK_THROWS_AS(bad.make_layout_checked(), FormatError);
+  // record rules of deserialize_blco: an empty record, blocks out of key order
+  BlcoTensor e = t;
+  e.blocks[1].linear_indices.clear();
+  e.blocks[1].values.clear();
+  std::ostringstream oe;
+  serialize_blco(e, oe);
+  std::istringstream ie(oe.str());
+  CHECK_THROWS_AS(deserialize_blco(ie), FormatError);
+  BlcoTensor r = t;
+  std::swap(r.blocks.front(), r.blocks.back());
+  std::ostringstream orr;
+  serialize_blco(r, orr);
+  std::istringstream ir(orr.str());
+  bool caught = false;
+  try {
+    (void)deserialize_blco(ir);
+  } catch (const FormatError& ex) {
+    caught = std::string(ex.what()).find("ascending key order") != std::string::npos ||
+             std::string(ex.what()).find("exceeds") != std::string::npos;
+  }
+  CHECK(caught);
+  std::istringstream version2(std::string("BLCO\x02\x00", 6));
+  CHECK_THROWS_AS(read_blco_header(version2), FormatError);
+}
+
 TEST(file_source_streams) {  // test_streaming.cpp:81-103
   Rng rng(97);
   auto coo = random_coo(rng, {40, 30, 20}, 300);

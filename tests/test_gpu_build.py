@@ -82,6 +82,13 @@ def test_synthetic_builds_match_oracle(gpu, oracle, dims, nnz, tb, cap):
     # host COO path gives the same tensor as the on-device generator
     t2 = build(gpu, dims, idx, vals, tb, cap)
     assert t2.structurally_equal(t)
+    # the device census (order-free multiset hash) equals the generator's
+    h, counts = oracle.census_uniform(dims, nnz, 42, tb)
+    assert dt.census() == h
+    per_key = {}
+    for k, n in zip(t.keys, np.diff(t.offsets)):
+        per_key[int(k)] = per_key.get(int(k), 0) + int(n)
+    assert per_key == {k: int(c) for k, c in enumerate(counts) if c}
 
 
 @pytest.mark.parametrize("dims,nnz,skew,cap", [

@@ -82,16 +82,39 @@ def test_nell2_full_size_build(gpu, oracle):
         stride *= dims[m]
     idx, vals = oracle.synth_uniform(dims, nnz, 42)
     want_cells = idx[0] + idx[1] * np.uint64(dims[0]) + idx[2] * np.uint64(dims[0] * dims[1])
-    assert _multiset_hash(cells, host.vals) == _multiset_hash(want_cells, vals)
+    want = _multiset_hash(want_cells, vals)
+    assert _multiset_hash(cells, host.vals) == want
+    # the device census and the streamed oracle census agree with it
+    assert dt.census() == want == oracle.census_uniform(dims, nnz, 42)[0]
+
+
+def _reference_chunking(key_counts, max_nnz=1 << 27):
+    """Block sizes build_blco produces from per-key element counts: each run
+    of equal keys (ascending) is cut every max_nnz elements from its start
+    (proj/src/blco_format.cpp:86-111)."""
+    sizes = []
+    for c in (int(x) for x in key_counts):
+        while c > 0:
+            sizes.append(min(c, max_nnz))
+            c -= sizes[-1]
+    return sizes
 
 
 def test_amazon_full_size_rows(gpu, oracle):
     """BASELINE configs[2] at full size on one B200: 1.74B nnz, 65-bit layout
-    (1 stripped bit, 14 blocks), R=32, every mode; device block checks."""
+    (1 stripped bit, 14 blocks), R=32, every mode; device block checks; the
+    element multiset (device census vs the generator's streamed census) and
+    the per-block nnz against the reference chunking of the per-key counts
+    (key 0 = 1,515,318,366 nnz in 12 blocks of <= 2^27, key 1 = 226,490,652
+    in 2; blco_format.cpp:86-111)."""
     dims, nnz, rank = AMAZON
     dt = gpu.DeviceTensor.synthetic(dims, nnz, 42)
     assert dt.nnz == nnz and dt.block_nnz().size == 14
     dt.validate_device()
+    h, counts = oracle.census_uniform(dims, nnz, 42)
+    assert counts.size == 2 and int(counts.sum()) == nnz  # one stripped bit: keys 0 and 1
+    assert dt.block_nnz().tolist() == _reference_chunking(counts)  # 12 + 2 blocks
+    assert dt.census() == h
     _check_rows(gpu, oracle, dt, dims, nnz, rank, 512)
 
 

@@ -55,9 +55,14 @@ def test_two_rank_reference_arm_prints_once(gpu):
 
 
 def test_two_rank_all_mode_streaming(gpu):
-    d = _torchrun(["--config", "reddit_stream_tiny", "--steps", "1"])
+    """Two ranks stream disjoint ALTO chunk ranges (streaming.cpp:103-309 per
+    rank) and all-reduce M_n; --check compares the summed M_n with one device
+    streaming the whole tensor (relative Frobenius <= 1e-12)."""
+    d = _torchrun(["--config", "reddit_stream_tiny", "--steps", "1", "--check", "--no-cpu-baseline"])
     assert d["n_gpus"] == 2 and d["value"] > 0
     assert d["config"]["nnz"] > 19_000_000 and "all-reduce" in d["config"]["step"]
+    assert d["check"]["nnz_single_device"] == d["config"]["nnz"]
+    assert max(d["check"]["rel_frobenius_vs_single_device"]) <= 1e-12
 
 
 @pytest.mark.parametrize("world", [2, 3])

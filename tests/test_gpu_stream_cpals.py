@@ -88,6 +88,35 @@ def test_overlap_with_injected_latency(gpu):  # test_streaming.cpp:105-139
     assert rep.overall_gbps < rep.compute_gbps  # transfer-dominated (test_streaming.cpp:164-170)
 
 
+def test_source_refilling_one_pinned_buffer(gpu, oracle):
+    """A BlockSource that refills ONE pinned buffer on every pull (the
+    synth_alto_chunk pattern): the engine must finish each block's copy
+    before pulling the next (a pinned cudaMemcpyAsync returns before its DMA
+    reads host memory), with several queues in flight."""
+    dims = [300, 200, 250]
+    coo, t = small_tensor(gpu, dims, 60_000, 91, 64, 4096)
+    assert t.keys.size >= 10
+    f = gpu.FactorMatrices.random(dims, 32, 5)
+    cap = t.max_nnz_per_block
+    pidx = gpu.api.pinned_empty(cap, np.uint64)
+    pvals = gpu.api.pinned_empty(cap, np.float64)
+
+    def source():
+        for b in range(t.keys.size):
+            o0, o1 = int(t.offsets[b]), int(t.offsets[b + 1])
+            n = o1 - o0
+            pidx[:n] = t.idx[o0:o1]
+            pvals[:n] = t.vals[o0:o1]
+            yield (int(t.keys[b]), pidx[:n], pvals[:n])
+
+    budget = gpu.DeviceBudget(capacity_bytes=1 << 30, num_queues=4, reservation_bytes=cap * 16)
+    got = gpu.stream_mttkrp_all_modes(source(), f, budget, layout=t.layout, max_nnz_per_block=cap,
+                                      block_count=int(t.keys.size))
+    for m in range(3):
+        want = oracle.mttkrp_coo(dims, coo.indices, coo.values, f.factors, m)
+        assert rel_frobenius(got[m], want) <= 1e-12, m
+
+
 def test_budget_errors(gpu):  # test_streaming.cpp:173-199
     coo, t = small_tensor(gpu, [30, 30], 100, 107, 6, 32)
     f = gpu.FactorMatrices.random([30, 30], 4, 1)

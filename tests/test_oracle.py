@@ -230,3 +230,40 @@ def test_rowsample_coo_equals_full_oracle_rows(oracle):
     got = oracle.rowsample_coo(dims, idx, vals, f, rows)
     for m in range(3):
         assert np.array_equal(got[m], oracle.mttkrp_coo(dims, idx, vals, f, m)[rows[m]])
+
+
+def test_census_uniform_matches_materialised_tensor(oracle):
+    """orc_census_uniform streams the generator: its multiset hash equals the
+    hash of the materialised COO, and its per-key counts equal the per-key
+    totals of the oracle build of a multi-key layout (blco_format.cpp:86-111)."""
+    from test_gpu_fullsize import _multiset_hash, _reference_chunking
+    dims, nnz, tb = [300, 200, 250], 50_000, 20
+    h, counts = oracle.census_uniform(dims, nnz, 42, tb, threads=3)
+    idx, vals = oracle.synth_uniform(dims, nnz, 42)
+    cells = idx[0] + idx[1] * np.uint64(dims[0]) + idx[2] * np.uint64(dims[0] * dims[1])
+    assert h == _multiset_hash(cells, vals)
+    keys, offs, _, _ = oracle.build(dims, idx, vals, tb, 1000)
+    per_key = np.zeros(counts.size, np.uint64)
+    for k, n in zip(keys, np.diff(offs)):
+        per_key[int(k)] += n
+    assert np.array_equal(per_key, counts)
+    assert np.diff(offs).tolist() == _reference_chunking(counts, 1000)
+
+
+def test_oracle_cp_als_matches_reference_r32(oracle):
+    """The C restatement of cp_als (cpals.cpp:66-111) at R = 32 against the
+    reference's own run (tests/golden/cpals_exact_rank.npz, n32): the oracle
+    is pinned on the exact rank the device epilogue specialises."""
+    import json
+    from pathlib import Path
+    z = np.load(Path(__file__).resolve().parent / "golden" / "cpals_exact_rank.npz")
+    c = json.loads(bytes(z["meta"]).decode())["n32"]
+    dims = c["dims"]
+    idx, vals = oracle.synth_draws(dims, c["nnz"], c["seed"], c["skew"])
+    keys, offs, oi, ov = oracle.build(dims, idx, vals)
+    fs, lam, fit = oracle.cp_als(dims, keys, offs, oi, ov, c["rank"], c["iters"], c["tol"], c["fseed"])
+    assert np.max(np.abs(fit - z["n32_fit"])) <= 1e-10
+    assert rel_frobenius(lam, z["n32_lambda"]) <= 1e-9
+    for m in range(len(dims)):
+        assert rel_frobenius(fs[m], z[f"n32_f{m}"]) <= 1e-9
+
