@@ -497,8 +497,27 @@ def run_ours(args, world, rank_id, local):
     strategy = b.Strategy[args.strategy]
     cfg = b.ExecConfig(num_compute_units=torch.cuda.get_device_properties(dev).multi_processor_count)
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{dev}")
+    # N > 1 over NCCL: the library's own communicator drives the per-mode
+    # reduction (blco_dist_mttkrp_all; torch only moves the NCCL unique id).
+    # The gloo plumbing runs (ranks sharing one GPU) keep torch's collectives.
+    lib_coll = (world > 1 and os.environ.get("BLCO_B200_DIST_BACKEND", "nccl") == "nccl"
+                and os.environ.get("BLCO_B200_COLLECTIVES", "library") == "library")
+    if lib_coll:
+        import torch.distributed as dist
+        uid = [b.Communicator.unique_id() if rank_id == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = b.Communicator(uid[0], world, rank_id, dev)
+        if not rs:
+            shards = outs
+
+
+    def lib_step(ev=None):
+        comm.mttkrp_all(dt, fptr, R, [o.data_ptr() for o in outs], [x.data_ptr() for x in shards],
+                        reduce=args.reduce, strategy=strategy, config=cfg, stream=sptr)
 
     def step(ev=None):
+        if lib_coll:
+            return lib_step(ev)
         for o in outs:
             o.zero_()
         works = []
@@ -546,7 +565,21 @@ def run_ours(args, world, rank_id, local):
     if world > 1:
         dist.barrier()
     step_ms = [sev[k][0].elapsed_time(sev[k][1]) for k in range(args.steps)]
-    mode_ms = [[evs[k][m][0].elapsed_time(evs[k][m][1]) for k in range(args.steps)] for m in range(N)]
+    if lib_coll:
+        # one library call per step: the mode kernels alone, timed after the
+        # step loop on the same slice (the roofline's launch duration)
+        mode_ms = []
+        for m in range(N):
+            o = torch.zeros((dims[m], R), dtype=torch.float64, device=f"cuda:{dev}")
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(3):
+                dt.mttkrp_device(fptr, R, m, o.data_ptr(), strategy, cfg, accumulate=True, stream=sptr)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            mode_ms.append([e0.elapsed_time(e1) / 3])
+    else:
+        mode_ms = [[evs[k][m][0].elapsed_time(evs[k][m][1]) for k in range(args.steps)] for m in range(N)]
     ms = sum(step_ms) / len(step_ms)
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{dev}")
@@ -581,6 +614,8 @@ def run_ours(args, world, rank_id, local):
                    "parallelism": f"span partition x{world}" + (
                        (" + NCCL reduce-scatter of M per mode (row shards), overlapped with the next mode's kernel"
                         if rs else " + NCCL all-reduce of M per mode, overlapped with the next mode's kernel")
+                       + (" (libblco_b200 communicator, blco_dist_mttkrp_all)" if lib_coll else
+                          " (torch.distributed)")
                        if world > 1 else ""),
                    "bytes_per_elem_per_mode": bpe},
         "per_mode_ms": [round(statistics.mean(x), 4) for x in mode_ms],

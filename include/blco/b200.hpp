@@ -24,6 +24,8 @@
 #include <utility>
 #include <vector>
 
+struct blco_multi;  // include/blco_b200.h (the multi-GPU handle)
+
 namespace blco {
 
 // ---------------------------------------------------------------- common.hpp
@@ -231,6 +233,42 @@ DenseMatrix mttkrp(const BlcoTensor& t, const FactorMatrices& f, int mode,
 std::vector<DenseMatrix> mttkrp_all_modes(const BlcoTensor& t, const FactorMatrices& f,
                                           const ExecConfig& config = {},
                                           Strategy strategy = Strategy::Auto);
+
+// B200 extension, multi-GPU (the reference has no multi-device
+// path): one host thread drives G GPUs.  The tensor's element
+// spans are cut into G contiguous nnz-balanced ranges, device g holds range g
+// and a replica of the factors, every device runs each mode's kernel on its
+// range, and the partial M_n are summed by NCCL over NVLink/NVSwitch (an
+// all-reduce, or a reduce-scatter into row shards), the reduction of mode n
+// overlapping the kernel of mode n+1.  Results equal mttkrp(t, f, n) within
+// the fp64 summation-order tolerance.
+enum class Reduction { AllReduce, ReduceScatter };
+
+struct MultiReport {
+  int devices = 0;
+  double device_ms = 0.0;  // kernels + collectives, max over devices
+  std::uint64_t h2d_bytes = 0, d2h_bytes = 0;
+};
+
+class MultiDeviceTensor {
+ public:
+  MultiDeviceTensor(const BlcoTensor& t, std::vector<int> devices);
+  ~MultiDeviceTensor();
+  MultiDeviceTensor(const MultiDeviceTensor&) = delete;
+  MultiDeviceTensor& operator=(const MultiDeviceTensor&) = delete;
+
+  std::vector<DenseMatrix> mttkrp_all_modes(const FactorMatrices& f, Reduction how = Reduction::AllReduce,
+                                            const ExecConfig& config = {}, Strategy strategy = Strategy::Auto,
+                                            MultiReport* report = nullptr);
+  const std::vector<int>& devices() const { return devices_; }
+  // element range [first, second) of the ALTO-ordered tensor held by each device
+  std::vector<std::pair<std::uint64_t, std::uint64_t>> ranges() const;
+
+ private:
+  std::vector<int> devices_;
+  std::vector<index_t> dims_;
+  ::blco_multi* handle_ = nullptr;
+};
 
 // ------------------------------------------------------------- streaming.hpp
 struct DeviceBudget {

@@ -434,6 +434,69 @@ int blco_cp_als_timed(const blco_tensor* t, uint64_t rank, int max_iters, double
 int blco_fit(const blco_tensor* t, const double* const* factors, const double* lambda,
              uint64_t rank, const blco_exec_config* cfg, double* fit_out);
 
+/* ------------------------------------------------------------ multi-GPU
+ * The partition of SURVEY.md 8e inside the library: the tensor's element
+ * spans are cut into G contiguous nnz-balanced ranges (blco_partition), the
+ * factor matrices are replicated, every device runs each mode's kernel on its
+ * range into a full partial M_n, and the partials are summed by NCCL over
+ * NVLink/NVSwitch -- per mode an all-reduce (BLCO_REDUCE_ALL: every device
+ * holds M_n) or a reduce-scatter (BLCO_REDUCE_SCATTER: device g holds rows
+ * [g*P, (g+1)*P) of M_n, P = ceil(I_n / G), from partials padded to G*P rows).
+ * The collective of mode n runs on the communicator's stream, ordered after
+ * that mode's kernel by an event, so it overlaps the kernel of mode n+1.
+ * NCCL is loaded at run time (libnccl.so.2, reusing a copy already in the
+ * process; BLCO_B200_NCCL overrides the path); G = 1 needs no NCCL.  Errors
+ * from NCCL return BLCO_ENCCL.  The reference has no multi-device path
+ * (SPEC.md:489): this is the north_star's multi-GPU subsystem. */
+#define BLCO_REDUCE_ALL 0
+#define BLCO_REDUCE_SCATTER 1
+#define BLCO_COMM_ID_BYTES 128
+
+/* NCCL's version code (e.g. 22809), or BLCO_ENCCL when NCCL is absent */
+int blco_nccl_version(int* version);
+
+/* One member of a G-rank communicator: its device, NCCL communicator and
+ * collective stream.  Multi-process use (one process per GPU): rank 0 calls
+ * blco_comm_unique_id, the caller moves the BLCO_COMM_ID_BYTES bytes to every
+ * rank (any channel), each rank calls blco_comm_init_rank on its device. */
+typedef struct blco_comm blco_comm;
+int blco_comm_unique_id(uint8_t* id);
+int blco_comm_init_rank(const uint8_t* id, int nranks, int rank, int device, blco_comm** out);
+/* single-process: comms_out[g] for devices[g], g < ndev (ncclCommInitAll) */
+int blco_comm_init_all(const int* devices, int ndev, blco_comm** comms_out);
+void blco_comm_free(blco_comm* comm);
+
+/* One rank's all-mode step: d_outs[n] (device, I_n x R rows; G*P rows for
+ * BLCO_REDUCE_SCATTER) are zeroed, receive this rank's partial M_n from the
+ * kernel of mode n on `stream`, and are reduced across the communicator on
+ * its stream; BLCO_REDUCE_SCATTER leaves this rank's P x R shard in
+ * d_shards[n].  `local` must live on the communicator's device (e.g. a
+ * blco_tensor_slice of the rank's blco_partition range).  Enqueued only:
+ * `stream` is made to wait for the collectives before the call returns. */
+int blco_dist_mttkrp_all(const blco_tensor* local, const double* const* d_factors, uint64_t rank,
+                         blco_comm* comm, int reduce, int strategy, const blco_exec_config* cfg,
+                         double* const* d_outs, double* const* d_shards, void* stream);
+
+/* One host thread driving G devices of this process (SURVEY.md 8b
+ * "Threading"): blco_multi_create partitions `t` (any device) into G span
+ * ranges copied peer-to-peer onto devices[g]; blco_multi_mttkrp_all uploads
+ * the host factors to every device, runs the all-mode step with the chosen
+ * reduction (group calls around each mode's G collectives) and writes every
+ * M_n to the host outs[n] (I_n x R): from device 0 after an all-reduce, or
+ * each device's row shard after a reduce-scatter. */
+typedef struct blco_multi blco_multi;
+typedef struct blco_multi_report {
+  int devices;
+  double device_ms;   /* kernels + collectives, max over devices (CUDA events) */
+  uint64_t h2d_bytes; /* factor replicas uploaded */
+  uint64_t d2h_bytes; /* M_n read back */
+} blco_multi_report;
+int blco_multi_create(const blco_tensor* t, const int* devices, int ndev, blco_multi** out);
+int blco_multi_info(const blco_multi* m, int* ndev, uint64_t* elem_begin, uint64_t* elem_end);
+int blco_multi_mttkrp_all(blco_multi* m, const double* const* factors, uint64_t rank, int reduce, int strategy,
+                          const blco_exec_config* cfg, double* const* outs, blco_multi_report* report);
+void blco_multi_free(blco_multi* m);
+
 /* ------------------------------------------------ distributed CP-ALS pieces
  * The dense steps of one cp_als mode (proj/src/cpals.cpp:84-96) split where a
  * multi-GPU run reduces across ranks: after a reduce-scatter
@@ -443,8 +506,9 @@ int blco_fit(const blco_tensor* t, const double* const* factors, const double* l
  * caller's (torch.distributed / NCCL); paper_2201_12523_b200/dist.py is the
  * driver.  Device pointers, enqueued on `stream`, never synchronised.
  * Matrices are row-major R x R (full, symmetric) or rows x R.  Ranks up to
- * 64.  The solve stages L in the device's constant bank (R = 16 / 32):
- * one epilogue per device at a time. */
+ * 64.  The solve reads L from its own device buffer (the constant-bank
+ * variant is reserved to blco_cp_als, which serialises its runs), so
+ * concurrent calls on different streams are safe. */
 /* *d_out = sum of squared values of t (tensor_norm_squared, cpals.cpp:15-20) */
 int blco_tensor_norm_sq(const blco_tensor* t, double* d_out, void* stream);
 /* d_gram = A^T A over `rows` rows of d_a (gram, dense_kernels.cpp:8-21) */

@@ -115,6 +115,26 @@ _PU64 = C.POINTER(C.c_uint64)
 _PD = C.POINTER(C.c_double)
 
 # name -> (restype, argtypes); every symbol declared in include/blco_b200.h
+
+class MultiReport(C.Structure):
+    _fields_ = [("devices", C.c_int), ("device_ms", C.c_double), ("h2d_bytes", C.c_uint64),
+                ("d2h_bytes", C.c_uint64)]
+
+
+REDUCE_ALL, REDUCE_SCATTER, COMM_ID_BYTES = 0, 1, 128
+
+
+class ContainerHeader(C.Structure):
+    _fields_ = [("version", C.c_uint16), ("order", C.c_uint16), ("target_bits", C.c_uint16),
+                ("dims", C.c_uint64 * MAX_ORDER), ("mode_bits", C.c_uint16 * MAX_ORDER),
+                ("max_nnz_per_block", C.c_uint64), ("block_count", C.c_uint64)]
+
+# container stream hooks (blco_read_fn / blco_write_fn / blco_alloc_fn)
+READ_FN = C.CFUNCTYPE(C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64)
+WRITE_FN = C.CFUNCTYPE(C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64)
+ALLOC_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_uint64, C.POINTER(C.POINTER(C.c_uint64)),
+                       C.POINTER(C.POINTER(C.c_double)))
+
 SIGNATURES = {
     "blco_last_error": (C.c_char_p, []),
     "blco_abi_version": (_I, []),
@@ -188,6 +208,24 @@ SIGNATURES = {
     "blco_factors_random_device": (_I, [_PU64, _I, _U64, _U64, C.POINTER(_P), _P]),
     "blco_synth_uniform_host": (_I, [_I, _PU64, _U64, _U64, _PU64, _PD]),
     "blco_partition": (_I, [_PU64, _U64, _U64, _I, _PU64, _PU64]),
+    "blco_nccl_version": (_I, [C.POINTER(_I)]),
+    "blco_comm_unique_id": (_I, [_P]),
+    "blco_comm_init_rank": (_I, [_P, _I, _I, _I, C.POINTER(_P)]),
+    "blco_comm_init_all": (_I, [C.POINTER(_I), _I, C.POINTER(_P)]),
+    "blco_comm_free": (None, [_P]),
+    "blco_dist_mttkrp_all": (_I, [_P, C.POINTER(_P), _U64, _P, _I, _I, C.POINTER(ExecCfg), C.POINTER(_P),
+                                  C.POINTER(_P), _P]),
+    "blco_multi_create": (_I, [_P, C.POINTER(_I), _I, C.POINTER(_P)]),
+    "blco_multi_info": (_I, [_P, C.POINTER(_I), _PU64, _PU64]),
+    "blco_multi_mttkrp_all": (_I, [_P, C.POINTER(_P), _U64, _I, _I, C.POINTER(ExecCfg), C.POINTER(_P),
+                                   C.POINTER(MultiReport)]),
+    "blco_multi_free": (None, [_P]),
+    "blco_container_read_header": (_I, [READ_FN, _P, _P]),
+    "blco_container_checked_layout": (_I, [_P, C.POINTER(Layout)]),
+    "blco_container_read_block": (_I, [READ_FN, _P, C.POINTER(Layout), C.POINTER(_U64), C.POINTER(_U64), ALLOC_FN,
+                                       _P, _I]),
+    "blco_container_write_header": (_I, [WRITE_FN, _P, C.POINTER(Layout), _U64, _U64]),
+    "blco_container_write_block": (_I, [WRITE_FN, _P, _U64, _U64, _P, _P]),
     "blco_device_count": (_I, []),
     "blco_kernel_launch_count": (_U64, []),
     "blco_release_thread_caches": (_I, []),

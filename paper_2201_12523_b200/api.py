@@ -1032,6 +1032,108 @@ def partition(block_nnz: Sequence[int], quota: int, nparts: int) -> list[tuple[i
     return [(int(x), int(y)) for x, y in zip(b, e)]
 
 
+# ------------------------------------------------------------- multi-GPU
+# The library's own multi-GPU partition (include/blco_b200.h "multi-GPU"):
+# NCCL is driven inside libblco_b200.so, torch only moves the unique id.
+
+REDUCE = {"allreduce": L.REDUCE_ALL, "reducescatter": L.REDUCE_SCATTER}
+
+
+def nccl_version() -> int:
+    """NCCL's version code as the library resolved it (raises when absent)."""
+    v = C.c_int()
+    _check(lib.blco_nccl_version(C.byref(v)))
+    return int(v.value)
+
+
+class Communicator:
+    """One rank of a G-rank communicator (blco_comm): one process per GPU.
+    Rank 0 calls `unique_id()`, the caller moves the bytes to every rank
+    (e.g. torch.distributed.broadcast_object_list), each rank constructs
+    Communicator(uid, nranks, rank, device)."""
+
+    def __init__(self, uid: bytes | None, nranks: int, rank: int, device: int):
+        self._h = C.c_void_p()
+        buf = (C.c_uint8 * L.COMM_ID_BYTES).from_buffer_copy(uid or bytes(L.COMM_ID_BYTES))
+        _check(lib.blco_comm_init_rank(buf, nranks, rank, device, C.byref(self._h)))
+        self.nranks, self.rank, self.device = nranks, rank, device
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_uint8 * L.COMM_ID_BYTES)()
+        _check(lib.blco_comm_unique_id(buf))
+        return bytes(buf)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            lib.blco_comm_free(h)
+            self._h = C.c_void_p(0)
+
+    def mttkrp_all(self, local: "DeviceTensor", d_factors: Sequence[int], rank: int, d_outs: Sequence[int],
+                   d_shards: Sequence[int] | None = None, reduce: str = "allreduce",
+                   strategy: "Strategy" = None, config: "ExecConfig | None" = None, stream: int = 0) -> None:
+        """blco_dist_mttkrp_all: this rank's partial M_n of every mode, reduced
+        across the communicator per mode (enqueued on `stream`)."""
+        c = (config or ExecConfig())._c()
+        fp = (C.c_void_p * len(d_factors))(*d_factors)
+        op = (C.c_void_p * len(d_outs))(*d_outs)
+        sp = (C.c_void_p * len(d_outs))(*(d_shards or [0] * len(d_outs)))
+        st = int(strategy if strategy is not None else Strategy.Auto)
+        _check(lib.blco_dist_mttkrp_all(local.handle, fp, rank, self._h, REDUCE[reduce], st, C.byref(c), op, sp,
+                                        C.c_void_p(stream)))
+
+
+@dataclass
+class MultiReport:
+    devices: int = 0
+    device_ms: float = 0.0
+    h2d_bytes: int = 0
+    d2h_bytes: int = 0
+
+
+class MultiDeviceTensor:
+    """A tensor partitioned over several GPUs of this process, driven by one
+    host thread (blco_multi): contiguous nnz-balanced span ranges, replicated
+    factors, per-mode NCCL all-reduce or reduce-scatter of the partial M_n."""
+
+    def __init__(self, t: "DeviceTensor", devices: Sequence[int]):
+        self._h = C.c_void_p()
+        devs = (C.c_int * len(devices))(*devices)
+        _check(lib.blco_multi_create(t.handle, devs, len(devices), C.byref(self._h)))
+        self.devices = list(devices)
+        self.dims = list(t.layout.dims)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            lib.blco_multi_free(h)
+            self._h = C.c_void_p(0)
+
+    def ranges(self) -> list[tuple[int, int]]:
+        n = C.c_int()
+        b = np.zeros(len(self.devices), np.uint64)
+        e = np.zeros(len(self.devices), np.uint64)
+        _check(lib.blco_multi_info(self._h, C.byref(n), _pu64(b), _pu64(e)))
+        return [(int(x), int(y)) for x, y in zip(b, e)]
+
+    def mttkrp_all_modes(self, f: "FactorMatrices", reduce: str = "allreduce", strategy: "Strategy" = None,
+                         config: "ExecConfig | None" = None, report: MultiReport | None = None) -> list[np.ndarray]:
+        f.validate(self.dims)
+        fs = [_f64(a) for a in f.factors]
+        outs = [np.zeros((d, f.rank)) for d in self.dims]
+        c = (config or ExecConfig())._c()
+        r = L.MultiReport()
+        st = int(strategy if strategy is not None else Strategy.Auto)
+        _check(lib.blco_multi_mttkrp_all(self._h, (C.c_void_p * len(fs))(*[a.ctypes.data for a in fs]), f.rank,
+                                         REDUCE[reduce], st, C.byref(c),
+                                         (C.c_void_p * len(outs))(*[o.ctypes.data for o in outs]), C.byref(r)))
+        if report is not None:
+            report.devices, report.device_ms = r.devices, r.device_ms
+            report.h2d_bytes, report.d2h_bytes = r.h2d_bytes, r.d2h_bytes
+        return outs
+
+
 def factors_random_device(dims: Sequence[int], rank: int, seed: int, d_ptrs: Sequence[int],
                           stream: int = 0) -> None:
     ptrs = (C.c_void_p * len(d_ptrs))(*d_ptrs)

@@ -637,6 +637,60 @@ std::vector<DenseMatrix> mttkrp_all_modes(const BlcoTensor& t, const FactorMatri
   return out;
 }
 
+// --------------------------------------------------------------- multi-GPU
+MultiDeviceTensor::MultiDeviceTensor(const BlcoTensor& t, std::vector<int> devices)
+    : devices_(std::move(devices)), dims_(t.dims()) {
+  if (devices_.empty()) throw FormatError("multi: need at least one device");
+  // staged on the first device, then cut into span ranges copied peer to peer
+  const blco_layout l = to_c(t.layout);
+  std::vector<std::uint64_t> keys, nnz;
+  std::vector<const std::uint64_t*> idx;
+  std::vector<const double*> vals;
+  for (const auto& b : t.blocks) {
+    if (b.linear_indices.size() != b.values.size())
+      throw FormatError("blco: block index/value arrays have mismatched lengths");
+    keys.push_back(b.key);
+    nnz.push_back(b.nnz());
+    idx.push_back(b.linear_indices.data());
+    vals.push_back(b.values.data());
+  }
+  blco_tensor* staged = nullptr;
+  ck(blco_tensor_upload(&l, t.max_nnz_per_block, keys.size(), keys.data(), nnz.data(), idx.data(), vals.data(),
+                        devices_[0], &staged));
+  std::unique_ptr<blco_tensor, void (*)(blco_tensor*)> guard(staged, blco_tensor_free);
+  ck(blco_multi_create(staged, devices_.data(), static_cast<int>(devices_.size()), &handle_));
+}
+
+MultiDeviceTensor::~MultiDeviceTensor() { blco_multi_free(handle_); }
+
+std::vector<std::pair<std::uint64_t, std::uint64_t>> MultiDeviceTensor::ranges() const {
+  int n = 0;
+  std::vector<std::uint64_t> b(devices_.size()), e(devices_.size());
+  ck(blco_multi_info(handle_, &n, b.data(), e.data()));
+  std::vector<std::pair<std::uint64_t, std::uint64_t>> r;
+  for (int g = 0; g < n; ++g) r.emplace_back(b[g], e[g]);
+  return r;
+}
+
+std::vector<DenseMatrix> MultiDeviceTensor::mttkrp_all_modes(const FactorMatrices& f, Reduction how,
+                                                             const ExecConfig& config, Strategy strategy,
+                                                             MultiReport* report) {
+  config.validate();
+  f.validate(dims_);
+  std::vector<DenseMatrix> out;
+  std::vector<double*> optr;
+  for (index_t d : dims_) out.emplace_back(d, f.rank);
+  for (auto& o : out) optr.push_back(o.data.data());
+  const auto ptrs = factor_ptrs(f);
+  const blco_exec_config c = to_c(config);
+  blco_multi_report r{};
+  ck(blco_multi_mttkrp_all(handle_, ptrs.data(), f.rank,
+                           how == Reduction::ReduceScatter ? BLCO_REDUCE_SCATTER : BLCO_REDUCE_ALL,
+                           static_cast<int>(strategy), &c, optr.data(), &r));
+  if (report) *report = MultiReport{r.devices, r.device_ms, r.h2d_bytes, r.d2h_bytes};
+  return out;
+}
+
 // --------------------------------------------------------------- streaming
 bool MemoryBlockSource::next(BlcoBlock& out) {
   if (cursor_ >= t_->blocks.size()) return false;

@@ -12,6 +12,8 @@
 #include <string>
 #include <vector>
 
+#include <cuda_runtime.h>
+
 #include "blco/blco_format.hpp"
 #include "blco/cpals.hpp"
 #include "blco/layout.hpp"
@@ -463,6 +465,25 @@ TEST(container_bytes_and_records) {  // blco_format.cpp:149-227 byte layout and 
   CHECK(caught);
   std::istringstream version2(std::string("BLCO\x02\x00", 6));
   CHECK_THROWS_AS(read_blco_header(version2), FormatError);
+}
+
+TEST(multi_device_all_modes) {  // B200 multi-GPU extension: G = every visible device (1 here)
+  Rng rng(211);
+  auto coo = random_coo(rng, {60, 50, 40}, 4000);
+  auto t = build_blco(coo, 12, 500);
+  auto f = random_factors(rng, coo.dims, 8);
+  int n = 0;
+  cudaGetDeviceCount(&n);
+  std::vector<int> devs;
+  for (int g = 0; g < n; ++g) devs.push_back(g);
+  MultiDeviceTensor mt(t, devs);
+  CHECK(mt.ranges().size() == devs.size() && mt.ranges().back().second == t.total_nnz);
+  for (Reduction how : {Reduction::AllReduce, Reduction::ReduceScatter}) {
+    MultiReport rep;
+    auto got = mt.mttkrp_all_modes(f, how, {}, Strategy::Auto, &rep);
+    CHECK(rep.devices == n && rep.device_ms > 0);
+    for (int m = 0; m < 3; ++m) CHECK(rel_frobenius(got[m], mttkrp_coo(coo, f, m)) <= 1e-12);
+  }
 }
 
 TEST(file_source_streams) {  // test_streaming.cpp:81-103

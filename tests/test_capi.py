@@ -153,3 +153,58 @@ def test_merge_copies(blco):  # proj/tests/test_mttkrp.cpp:246-265
     assert np.array_equal(blco.merge_copies([a]), a)
     with pytest.raises(blco.FormatError):
         blco.merge_copies([a, np.zeros((2, 2))])
+
+
+def test_container_stream_hooks_match_reference_bytes(blco, reflib):
+    """blco_container_write_header/_block (the C++ serialize_blco path) write
+    the reference's serialize_blco bytes (blco_format.cpp:149-166), and
+    blco_container_read_header / _checked_layout parse them back
+    (:173-199); header-level errors keep the reference's messages.  No GPU:
+    the per-element block checks are not reached."""
+    import ctypes as C
+    from paper_2201_12523_b200 import _lib as L
+    dims = [40, 35, 30, 12]
+    rng = np.random.default_rng(3)
+    cells = rng.choice(40 * 35 * 30 * 12, size=500, replace=False)
+    idx = np.array(np.unravel_index(cells, dims[::-1])[::-1], np.uint64)
+    vals = rng.uniform(-1, 1, 500)
+    rt = reflib.build(dims, idx, vals, 14, 64)
+    want = rt.serialize()
+    out = bytearray()
+    wfn = L.WRITE_FN(lambda ctx, src, n: (out.extend(C.string_at(src, n)), n)[1])
+    lay = blco.make_layout(dims, 14)
+    keys, offs, bi, bv = rt.blocks()
+    blocks = list(zip(keys, offs[:-1], offs[1:]))
+    assert L.lib.blco_container_write_header(wfn, None, C.byref(lay._c), 64, len(blocks)) == 0
+    for key, lo, hi in blocks:
+        bidx, bvals = np.ascontiguousarray(bi[lo:hi]), np.ascontiguousarray(bv[lo:hi])
+        assert L.lib.blco_container_write_block(wfn, None, int(key), bidx.size, bidx.ctypes.data,
+                                                bvals.ctypes.data) == 0
+    assert bytes(out) == want
+    pos = [0]
+
+    def reader(data):
+        def fn(ctx, dst, n):
+            k = min(n, len(data) - pos[0])
+            C.memmove(dst, data[pos[0]:pos[0] + k], k)
+            pos[0] += k
+            return k
+        return L.READ_FN(fn)
+
+    h = L.ContainerHeader()
+    rfn = reader(want)
+    assert L.lib.blco_container_read_header(rfn, None, C.byref(h)) == 0
+    assert (h.version, h.order, h.target_bits, h.max_nnz_per_block, h.block_count) == (1, 4, 14, 64, len(blocks))
+    assert list(h.dims[:4]) == dims and list(h.mode_bits[:4]) == list(lay.mode_bits)
+    c = L.Layout()
+    assert L.lib.blco_container_checked_layout(C.byref(h), C.byref(c)) == 0
+    assert c.total_bits == lay.total_bits and c.stripped_bits == lay.stripped_bits
+    h.mode_bits[1] += 1
+    assert L.lib.blco_container_checked_layout(C.byref(h), C.byref(c)) == L.EFORMAT
+    assert b"mode bit widths" in L.lib.blco_last_error()
+    for bad, msg in ((b"XLCO" + want[4:], b"bad magic"), (want[:4] + b"\x02\x00" + want[6:], b"version 2"),
+                     (want[:9], b"truncated payload")):
+        pos[0] = 0
+        st = L.lib.blco_container_read_header(reader(bad), None, C.byref(h))
+        assert st != 0 and msg in L.lib.blco_last_error(), (msg, L.lib.blco_last_error())
+
