@@ -137,6 +137,11 @@ typedef struct blco_mttkrp_stats {
    * computing phase (gather, multiply, commit) */
   uint64_t processing_cycles;
   uint64_t computing_cycles;
+  /* the kernel family that ran (REGISTER / HIERARCHICAL).  Under AUTO,
+   * `strategy` is the reference's choose_strategy label (mttkrp.cpp:17-21)
+   * while the B200 runs the register kernel for every mode length (measured
+   * faster everywhere) */
+  int32_t kernel;
 } blco_mttkrp_stats;
 
 /* BuildStats (proj/include/blco/blco_format.hpp:49-54), device stage times */

@@ -52,6 +52,7 @@ class MttkrpStats(C.Structure):
         ("kernel_ms", C.c_float),
         ("processing_cycles", C.c_uint64),
         ("computing_cycles", C.c_uint64),
+        ("kernel", C.c_int32),
     ]
 
 

@@ -123,6 +123,7 @@ class MttkrpStats:
     kernel_ms: float = 0.0
     processing_cycles: int = 0  # sorted register kernel: SM cycles, summed over CTAs
     computing_cycles: int = 0   # ... and over warps
+    kernel: Strategy = Strategy.Register  # the kernel family that ran (Auto: register; `strategy` = reference label)
 
 
 @dataclass
@@ -548,6 +549,7 @@ def _fill_stats(stats: MttkrpStats, st: L.MttkrpStats) -> None:
     stats.kernel_ms = st.kernel_ms
     stats.processing_cycles = st.processing_cycles
     stats.computing_cycles = st.computing_cycles
+    stats.kernel = Strategy(st.kernel) if st.kernel else stats.strategy
 
 
 def build_blco(coo: SparseTensorCoo, target_bits: int = 64, max_nnz_per_block: int = 1 << 27,

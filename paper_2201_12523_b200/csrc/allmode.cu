@@ -227,7 +227,7 @@ extern "C" int blco_mttkrp_all_host(const blco_layout* layout, uint64_t nblocks,
     B200_CUDA(cudaStreamWaitEvent(x.comp, x.tables, 0));
     std::vector<int> strat(N);
     for (int m = 0; m < N; ++m)
-      strat[m] = strategy == BLCO_STRATEGY_AUTO ? blco_choose_strategy(l.dims[m], &c) : strategy;
+      strat[m] = strategy == BLCO_STRATEGY_AUTO ? auto_kernel(l.dims[m], c) : strategy;
     for (size_t k = 0; k < chunks.size(); ++k) {
       B200_CUDA(cudaStreamWaitEvent(x.comp, x.chunk_ev[k], 0));
       for (int m = 0; m < N; ++m) {

@@ -79,7 +79,7 @@ void validate_device(const blco_layout& l, uint64_t key, const uint64_t* d_idx, 
   if (!n) return;
   DevBuf<unsigned> bad(1);
   B200_CUDA(cudaMemset(bad.ptr, 0, sizeof(unsigned)));
-  const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, 148 * 16));
+  const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, sm_count() * 16));
   k_check_block<<<grid, 256>>>(check_params(l, key), d_idx, n, bad.ptr);
   count_launch();
   check_launch("k_check_block");
@@ -231,7 +231,7 @@ void read_record_head(const ByteIn& in, const blco_layout& l, uint64_t* key, uin
 void enqueue_block_check(const blco_layout& l, uint64_t key, const uint64_t* d_idx, uint64_t n, unsigned* d_bad,
                          cudaStream_t s) {
   if (!n) return;
-  const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, 148 * 16));
+  const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, sm_count() * 16));
   k_check_block<<<grid, 256, 0, s>>>(check_params(l, key), d_idx, n, d_bad);
   count_launch();
   check_launch("k_check_block");
@@ -416,7 +416,7 @@ extern "C" int blco_tensor_census(const blco_tensor* t, uint64_t* hash) {
     for (uint64_t b = 0; b < t->nblocks(); ++b) {
       const uint64_t n = t->offsets[b + 1] - t->offsets[b];
       if (!n) continue;
-      const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, 148 * 16));
+      const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, sm_count() * 16));
       k_census_block<<<grid, 256>>>(check_params(l, t->keys[b]), t->idx.ptr + t->offsets[b],
                                     t->vals.ptr + t->offsets[b], n, sum.ptr);
       count_launch();

@@ -391,7 +391,7 @@ __global__ void k_symmetrize(const double* __restrict__ g, int R, double* __rest
 bool exact_rank(int R) { return R == 16 || R == 32; }
 
 unsigned grid_of(uint64_t n) {
-  return static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>((n + kT - 1) / kT, 148 * 16)));
+  return static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>((n + kT - 1) / kT, sm_count() * 16)));
 }
 
 // Every reduction of the epilogue writes per-CTA (or per-warp) partials that
@@ -407,10 +407,8 @@ struct Dense {
   // per-warp Gram slots at full occupancy), so no iteration reallocates --
   // a cudaFree/cudaMalloc inside the loop stalls the queued kernels.
   explicit Dense(int r) : R(r), L(static_cast<size_t>(r) * r), small(static_cast<size_t>(r) * r + r + 1) {
-    int nsm = 148, dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    slots(std::max<uint64_t>(uint64_t(nsm) * 32 * (kSolveThreads / 32) * r * r, uint64_t(148) * 16 * 4));
+    const int nsm = sm_count();
+    slots(std::max<uint64_t>(uint64_t(nsm) * 32 * (kSolveThreads / 32) * r * r, uint64_t(nsm) * 16 * 4));
   }
 
   double* slots(uint64_t n) {
@@ -440,7 +438,7 @@ struct Dense {
     const size_t smem = (static_cast<size_t>(RR) + kGramChunk * R) * sizeof(double);
     if (smem > 48 * 1024)
       ensure_dyn_smem(reinterpret_cast<const void*>(k_gram), smem);
-    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((rows + kGramChunk - 1) / kGramChunk, 148 * 8));
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((rows + kGramChunk - 1) / kGramChunk, sm_count() * 8));
     k_gram<<<grid, kT, smem, s>>>(a, rows, R, slots(uint64_t(grid) * RR));
     count_launch();
     check_launch("k_gram");
@@ -490,7 +488,7 @@ struct Dense {
       ensure_dyn_smem(reinterpret_cast<const void*>(kern), smem);
       const int per_sm = blocks_per_sm(reinterpret_cast<const void*>(kern), kSolveThreads, smem);
       const unsigned grid = static_cast<unsigned>(
-          std::min<uint64_t>((rows + rows_per - 1) / rows_per, 148ull * std::max(1, per_sm)));
+          std::min<uint64_t>((rows + rows_per - 1) / rows_per, uint64_t(sm_count()) * std::max(1, per_sm)));
       const uint64_t nslots = uint64_t(grid) * (kSolveThreads / 32);
       double* sl = slots(nslots * RR);
       // R <= 32: every warp writes the whole upper triangle of its slot (the
@@ -632,8 +630,7 @@ void mttkrp_into(const blco_tensor& t, const std::vector<const double*>& f, uint
   a.factors = f.data();
   a.rank = R;
   a.mode = mode;
-  a.strategy = strategy == BLCO_STRATEGY_AUTO ? blco_choose_strategy(t.layout.dims[mode], &cfg)
-                                              : strategy;
+  a.strategy = strategy == BLCO_STRATEGY_AUTO ? auto_kernel(t.layout.dims[mode], cfg) : strategy;
   a.cfg = cfg;
   a.out = out;
   a.stream = nullptr;

@@ -232,7 +232,7 @@ const DetIndex& det_index(const blco_tensor& t, int mode, cudaStream_t s) {
                                                             l.field_mask[mode], rows.ptr, counts.ptr);
     count_launch();
     check_launch("k_det_rows");
-    k_det_iota<<<static_cast<unsigned>(std::min<uint64_t>((t.nnz + 255) / 256, 148 * 16)), 256, 0, s>>>(
+    k_det_iota<<<static_cast<unsigned>(std::min<uint64_t>((t.nnz + 255) / 256, sm_count() * 16)), 256, 0, s>>>(
         perm_alt.ptr, t.nnz);
     count_launch();
     check_launch("k_det_iota");

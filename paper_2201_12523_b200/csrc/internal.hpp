@@ -63,6 +63,10 @@ int guarded(F&& f) {
 // hot enqueue paths make no attribute calls in steady state.
 void ensure_dyn_smem(const void* kernel, size_t bytes);
 int blocks_per_sm(const void* kernel, int threads, size_t dyn_smem);
+// SMs of the current device (queried once per device; 148 on B200)
+int sm_count();
+// the kernel family Strategy::Auto runs for a mode of `len` rows (host.cpp)
+int auto_kernel(uint64_t len, const blco_exec_config& c);
 
 extern std::atomic<uint64_t> g_launches;
 inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }

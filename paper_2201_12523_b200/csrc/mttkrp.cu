@@ -1126,7 +1126,7 @@ bool use_big_tiles(const blco_layout& l, int mode, uint64_t rank, uint64_t nnz, 
   uint64_t fbytes = 0;
   for (int m = 0; m < l.order; ++m)
     if (m != mode) fbytes += l.dims[m] * rank * elem_bytes;
-  return fbytes <= (uint64_t(48) << 20) && nnz >= uint64_t(2 * kTileElems) * 148 * 3 * 4;
+  return fbytes <= (uint64_t(48) << 20) && nnz >= uint64_t(2 * kTileElems) * sm_count() * 3 * 4;
 }
 
 // BLCO_B200_COMPACT_STAGE=0 disables the compact N = 3 staging (StageC).
@@ -1401,8 +1401,11 @@ void validate_call(const blco_tensor* t, uint64_t rank, int mode, const blco_exe
 
 // Enqueue with optional stats (stats forces a stream synchronisation).
 void run(MttkrpLaunch& a, blco_mttkrp_stats* stats) {
-  if (a.strategy == BLCO_STRATEGY_AUTO)
-    a.strategy = blco_choose_strategy(a.view.layout->dims[a.mode], &a.cfg);
+  int label = a.strategy;  // what MttkrpStats::strategy reports (the reference's choice under Auto)
+  if (a.strategy == BLCO_STRATEGY_AUTO) {
+    label = blco_choose_strategy(a.view.layout->dims[a.mode], &a.cfg);
+    a.strategy = auto_kernel(a.view.layout->dims[a.mode], a.cfg);
+  }
   Workspace& ws = workspace();
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (stats) {
@@ -1423,7 +1426,8 @@ void run(MttkrpLaunch& a, blco_mttkrp_stats* stats) {
   B200_CUDA(cudaEventElapsedTime(&ms, e0, e1));
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
-  stats->strategy = a.strategy;
+  stats->strategy = label;
+  stats->kernel = a.strategy;
   stats->workgroups = a.workgroups;
   stats->segments = h[0];
   stats->stash_flushes = h[1];

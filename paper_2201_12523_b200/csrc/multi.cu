@@ -209,9 +209,13 @@ void validate_step(const RankStep& s) {
   if (!s.local || !s.comm || !s.factors || !s.outs) throw_format("dist: null argument");
   if (s.local->device != s.comm->device) throw_format("dist: tensor and communicator are on different devices");
   if (s.reduce != BLCO_REDUCE_ALL && s.reduce != BLCO_REDUCE_SCATTER) throw_format("dist: unknown reduction");
-  if (s.reduce == BLCO_REDUCE_SCATTER && !s.shards) throw_format("dist: reduce-scatter needs shard buffers");
   if (s.rank < 1) throw_format("factors: rank must be >= 1");
   if (s.cfg && s.cfg->deterministic) throw_format("b200: deterministic mode is single-device");
+  for (int n = 0; n < s.local->layout.order; ++n) {
+    if (!s.factors[n] || !s.outs[n]) throw_format("dist: null factor or output pointer");
+    if (s.reduce == BLCO_REDUCE_SCATTER && (!s.shards || !s.shards[n]))
+      throw_format("dist: reduce-scatter needs shard buffers");
+  }
 }
 
 }  // namespace

@@ -260,9 +260,7 @@ void radix_sort_pairs(K* keys, K* keys_alt, uint32_t* vals, uint32_t* vals_alt, 
   if (n <= 1 || end_bit <= begin_bit) return;
   const uint64_t ntiles = (n + kSortTile - 1) / kSortTile;
   DevBuf<uint64_t> hist(ntiles * kDigits);
-  int dev = 0, nsm = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const int nsm = sm_count();
   const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(ntiles, static_cast<uint64_t>(nsm) * 8));
   K *kin = keys, *kout = keys_alt;
   uint32_t *vin = vals, *vout = vals_alt;

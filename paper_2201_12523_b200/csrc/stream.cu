@@ -131,10 +131,15 @@ void stream_impl(const blco_layout* layout, uint64_t max_nnz_per_block, BlockFee
     uint64_t pinned = 0;
     for (int m = 0; m < l.order; ++m) pinned += l.dims[m] * rank * sizeof(double);
     for (int k = 0; k < NM; ++k) {
-      strat[k] = strategy_in == BLCO_STRATEGY_AUTO ? blco_choose_strategy(l.dims[modes[k]], &c) : strategy_in;
+      // the budget counts what the reference would keep resident (its
+      // choose_strategy label: C output copies for a hierarchical mode), so
+      // capacity errors match; Auto then runs the B200 kernel of choice
+      const int label =
+          strategy_in == BLCO_STRATEGY_AUTO ? blco_choose_strategy(l.dims[modes[k]], &c) : strategy_in;
+      strat[k] = strategy_in == BLCO_STRATEGY_AUTO ? auto_kernel(l.dims[modes[k]], c) : strategy_in;
       hier[k] = strat[k] == BLCO_STRATEGY_HIERARCHICAL;
       out_elems[k] = l.dims[modes[k]] * rank;
-      pinned += out_elems[k] * sizeof(double) * (hier[k] ? C : 1);
+      pinned += out_elems[k] * sizeof(double) * (label == BLCO_STRATEGY_HIERARCHICAL ? C : 1);
     }
     if (pinned > budget->capacity_bytes)
       throw_format("stream: factor matrices and output (" + std::to_string(pinned) +

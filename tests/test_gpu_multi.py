@@ -75,9 +75,11 @@ def test_dist_rejects_bad_arguments(gpu, case):
     dt, f, _ = case
     comm = gpu.Communicator(None, 1, 0, 0)
     with pytest.raises(gpu.FormatError, match="shard"):
-        comm.mttkrp_all(dt, [0, 0, 0], RANK, [1, 1, 1], None, reduce="reducescatter")
+        comm.mttkrp_all(dt, [1, 1, 1], RANK, [1, 1, 1], None, reduce="reducescatter")
+    with pytest.raises(gpu.FormatError, match="null factor"):
+        comm.mttkrp_all(dt, [0, 0, 0], RANK, [1, 1, 1])
     with pytest.raises(gpu.FormatError, match="deterministic"):
-        comm.mttkrp_all(dt, [0, 0, 0], RANK, [1, 1, 1], config=gpu.ExecConfig(deterministic=True))
+        comm.mttkrp_all(dt, [1, 1, 1], RANK, [1, 1, 1], config=gpu.ExecConfig(deterministic=True))
 
 
 def test_library_reuses_the_process_nccl(gpu):
