@@ -60,6 +60,10 @@ struct EncodeParams {
   uint64_t mask[BLCO_MAX_DEV_ORDER];
   uint8_t imap_mode[BLCO_MAX_BITS];
   uint8_t imap_bit[BLCO_MAX_BITS];
+  // per-mode scatter table: bit k of coordinate m lands at
+  // interleaved position pos[m][k] (k < mode_bits[m], layout.cpp:34-36)
+  uint8_t mode_bits[BLCO_MAX_DEV_ORDER];
+  uint8_t pos[BLCO_MAX_DEV_ORDER][32];
 };
 
 EncodeParams encode_params(const blco_layout& l) {
@@ -74,6 +78,12 @@ EncodeParams encode_params(const blco_layout& l) {
   }
   std::memcpy(p.imap_mode, l.imap_mode, sizeof p.imap_mode);
   std::memcpy(p.imap_bit, l.imap_bit, sizeof p.imap_bit);
+  for (int q = 0; q < l.total_bits && q < BLCO_MAX_BITS; ++q) {
+    const int m = l.imap_mode[q], k = l.imap_bit[q];
+    if (m < BLCO_MAX_DEV_ORDER && k < 32) p.pos[m][k] = static_cast<uint8_t>(q);
+  }
+  for (int m = 0; m < l.order && m < BLCO_MAX_DEV_ORDER; ++m)
+    p.mode_bits[m] = static_cast<uint8_t>(std::min(32, l.mode_bits[m]));
   return p;
 }
 
@@ -111,27 +121,50 @@ __global__ void k_synth(synth::Feistel f, uint64_t seed, int order, uint64_t nnz
   }
 }
 
-// K1: ALTO words + re-encoded index; perm = element id.
+// K1: ALTO words + re-encoded index; perm = element id.  Templated on the
+// order so every coordinate stays in a register: mode m's bits are scattered
+// to their interleaved positions through the per-mode table (linearize,
+// layout.cpp:71-82, one shift/or per bit, no dynamically indexed arrays);
+// the re-encoded index is sum_m (c_m & mask_m) << shift_m (encode_coords,
+// layout.cpp:97-107).
+template <int N>
 __global__ void k_encode(EncodeParams p, uint64_t nnz, const uint32_t* __restrict__ coords,
                          uint64_t* __restrict__ alto_lo, uint64_t* __restrict__ alto_hi,
                          uint64_t* __restrict__ reenc, uint32_t* __restrict__ perm) {
   for (uint64_t e = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; e < nnz;
        e += uint64_t(gridDim.x) * blockDim.x) {
-    uint32_t c[BLCO_MAX_DEV_ORDER];
-    uint64_t r = 0;
-    for (int m = 0; m < p.order; ++m) {
-      c[m] = coords[m * nnz + e];
-      r |= (static_cast<uint64_t>(c[m]) & p.mask[m]) << p.shift[m];
+    uint64_t r = 0, lo = 0, hi = 0;
+#pragma unroll
+    for (int m = 0; m < N; ++m) {
+      const uint32_t c = __ldcs(coords + m * nnz + e);
+      r |= (static_cast<uint64_t>(c) & p.mask[m]) << p.shift[m];
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        if (k >= p.mode_bits[m]) break;
+        const uint64_t bit = (c >> k) & 1u;
+        const int q = p.pos[m][k];
+        if (q < 64) lo |= bit << q;
+        else hi |= bit << (q - 64);
+      }
     }
-    uint64_t lo = 0, hi = 0;
-    const int n_lo = p.total_bits < 64 ? p.total_bits : 64;
-    for (int q = 0; q < n_lo; ++q) lo |= static_cast<uint64_t>((c[p.imap_mode[q]] >> p.imap_bit[q]) & 1u) << q;
-    for (int q = 64; q < p.total_bits; ++q)
-      hi |= static_cast<uint64_t>((c[p.imap_mode[q]] >> p.imap_bit[q]) & 1u) << (q - 64);
     alto_lo[e] = lo;
     if (alto_hi) alto_hi[e] = hi;
     reenc[e] = r;
     perm[e] = static_cast<uint32_t>(e);
+  }
+}
+
+using EncodeKernel = void (*)(EncodeParams, uint64_t, const uint32_t*, uint64_t*, uint64_t*, uint64_t*, uint32_t*);
+EncodeKernel encode_kernel(int order) {
+  switch (order) {
+    case 1: return k_encode<1>;
+    case 2: return k_encode<2>;
+    case 3: return k_encode<3>;
+    case 4: return k_encode<4>;
+    case 5: return k_encode<5>;
+    case 6: return k_encode<6>;
+    case 7: return k_encode<7>;
+    default: return k_encode<8>;
   }
 }
 
@@ -304,8 +337,8 @@ void build_from_device_coo(blco_tensor& t, DevBuf<uint32_t>& coords, DevBuf<doub
   DevBuf<uint64_t> lo(nnz), hi(wide ? nnz : 0), reenc(nnz);
   DevBuf<uint32_t> perm(nnz);
   const EncodeParams ep = encode_params(l);
-  k_encode<<<grid_for(nnz, 4), kThreads, 0, s>>>(ep, nnz, coords.ptr, lo.ptr, hi.ptr, reenc.ptr,
-                                                  perm.ptr);
+  encode_kernel(l.order)<<<grid_for(nnz, 4), kThreads, 0, s>>>(ep, nnz, coords.ptr, lo.ptr, hi.ptr, reenc.ptr,
+                                                                 perm.ptr);
   count_launch();
   check_launch("k_encode");
   coords.reset();
@@ -436,8 +469,11 @@ void build_from_device_coo(blco_tensor& t, DevBuf<uint32_t>& coords, DevBuf<doub
   flags.reset();
   keys_out.reset();
   sorted_hi.reset();
-  t.idx.alloc(nnz);
-  t.vals.alloc(nnz);
+  {
+    ScratchScope keep(false);  // the payload outlives the build
+    t.idx.alloc(nnz);
+    t.vals.alloc(nnz);
+  }
   k_gather<uint64_t><<<grid_for(nnz, 4), kThreads, 0, s>>>(reenc.ptr, perm_out.ptr, t.idx.ptr, nnz);
   k_gather<double><<<grid_for(nnz, 4), kThreads, 0, s>>>(vals.ptr, perm_out.ptr, t.vals.ptr, nnz);
   count_launch(2);
@@ -471,7 +507,10 @@ blco_tensor* new_tensor(const uint64_t* dims, int order, int target_bits, uint64
 void finalize_tensor(blco_tensor& t) {
   const blco_layout& l = t.layout;
   const uint64_t nb = t.nblocks();
-  t.block_base.alloc(std::max<uint64_t>(1, nb * l.order));
+  {
+    ScratchScope keep(false);  // lives with the tensor
+    t.block_base.alloc(std::max<uint64_t>(1, nb * l.order));
+  }
   if (nb) {
     DevBuf<uint64_t> dkeys(nb);
     DevBuf<uint8_t> dmode(BLCO_MAX_BITS), dbit(BLCO_MAX_BITS);
@@ -501,6 +540,7 @@ const TileDesc* tile_table(const blco_tensor& t, uint32_t tile_elems, uint64_t* 
       for (uint64_t off = t.offsets[b]; off < t.offsets[b + 1]; off += tile_elems)
         h.push_back(TileDesc{off, static_cast<uint32_t>(std::min<uint64_t>(tile_elems, t.offsets[b + 1] - off)),
                              static_cast<uint32_t>(b)});
+    ScratchScope keep(false);  // cached with the tensor
     DevBuf<TileDesc> d(h.size());
     if (!h.empty()) {
       B200_CUDA(cudaMemcpy(d.ptr, h.data(), h.size() * sizeof(TileDesc), cudaMemcpyHostToDevice));
@@ -526,6 +566,7 @@ int blco_build(const uint64_t* dims, int order, uint64_t nnz, const uint64_t* id
   *out = nullptr;
   return guarded([&] {
     DeviceGuard dg(device);
+    ScratchScope scratch;  // build temporaries: stream-ordered pool
     blco_tensor* t = new_tensor(dims, order, target_bits, max_nnz, device);
     try {
       DevBuf<uint32_t> coords(static_cast<size_t>(nnz) * order);
@@ -563,6 +604,7 @@ int blco_build_synthetic(const uint64_t* dims, int order, uint64_t nnz, uint64_t
   *out = nullptr;
   return guarded([&] {
     DeviceGuard dg(device);
+    ScratchScope scratch;  // build temporaries: stream-ordered pool
     blco_tensor* t = new_tensor(dims, order, target_bits, max_nnz, device);
     try {
       const synth::Feistel f = synth::make_feistel(dims, order, nnz, seed);
@@ -591,6 +633,7 @@ int blco_build_synthetic_draws(const uint64_t* dims, int order, uint64_t nnz, ui
   return guarded([&] {
     if (skew < 1 || skew > 64) throw_format("synth: skew exponent must lie in [1, 64]");
     DeviceGuard dg(device);
+    ScratchScope scratch;  // build temporaries: stream-ordered pool
     DevBuf<uint64_t> ddims(order);
     B200_CUDA(cudaMemcpy(ddims.ptr, dims, order * 8, cudaMemcpyHostToDevice));
     uint64_t ncand = nnz + nnz / 8 + 1024;
@@ -634,6 +677,7 @@ int blco_synth_alto_chunk(const uint64_t* dims, int order, uint64_t chunk, uint6
     const uint64_t width = static_cast<uint64_t>((space + nchunks - 1) / nchunks);
     const uint64_t lo = static_cast<uint64_t>(space * chunk / nchunks);
     DeviceGuard dg(device);
+    ScratchScope scratch;  // build temporaries: stream-ordered pool
     cudaStream_t s = 0;
     DevBuf<uint64_t> alto(ncand), alto_s(ncand), out_idx(ncand);
     DevBuf<uint32_t> ids(ncand), ids_s(ncand), ids_sel(ncand);

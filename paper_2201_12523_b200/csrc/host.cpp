@@ -70,6 +70,44 @@ int blocks_per_sm(const void* kernel, int threads, size_t dyn_smem) {
   return n;
 }
 
+namespace {
+thread_local bool t_scratch = false;
+}
+
+ScratchScope::ScratchScope(bool on) : prev(t_scratch) { t_scratch = on; }
+ScratchScope::~ScratchScope() { t_scratch = prev; }
+bool scratch_active() { return t_scratch; }
+
+void* scratch_alloc(size_t bytes) {
+  int dev = 0;
+  B200_CUDA(cudaGetDevice(&dev));
+  static std::mutex mu;
+  static std::map<int, bool> configured;
+  {
+    std::lock_guard<std::mutex> g(mu);
+    if (!configured[dev]) {
+      cudaMemPool_t pool;
+      B200_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+      uint64_t keep = uint64_t(4) << 30;  // cached between builds; the rest is released at syncs
+      B200_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+      configured[dev] = true;
+    }
+  }
+  void* p = nullptr;
+  B200_CUDA(cudaMallocAsync(&p, bytes, nullptr));
+  return p;
+}
+
+void scratch_trim() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    cudaDeviceSynchronize();
+    cudaMemPoolTrimTo(pool, 0);
+  }
+}
+
 int sm_count() {
   int dev = 0;
   B200_CUDA(cudaGetDevice(&dev));
@@ -175,6 +213,7 @@ int blco_release_thread_caches(void) {
     release_allmode_cache();
     release_det_cache();
     release_mttkrp_workspace();
+    scratch_trim();
   });
 }
 

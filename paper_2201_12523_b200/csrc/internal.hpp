@@ -82,19 +82,38 @@ uint64_t key_upper(const blco_layout& l, int mode, uint64_t key);
 // (NaN doubles, all-ones indices), so a read before the first write shows.
 bool poison_allocations();
 
+// Build-scoped scratch: while a ScratchScope is live on this thread, DevBuf
+// allocations are stream-ordered (cudaMallocAsync / cudaFreeAsync on the
+// legacy stream, the device's default pool keeping up to 4 GiB cached), so
+// the temporaries of a BLCO build no longer pay a device-synchronising
+// cudaMalloc / cudaFree per stage, and a repeated build reuses the pool.
+// Buffers that outlive the build (the tensor's payload) are allocated under
+// ScratchScope(false).  All users of scratch buffers run on the legacy stream.
+struct ScratchScope {
+  bool prev;
+  explicit ScratchScope(bool on = true);
+  ~ScratchScope();
+  ScratchScope(const ScratchScope&) = delete;
+  ScratchScope& operator=(const ScratchScope&) = delete;
+};
+bool scratch_active();
+void* scratch_alloc(size_t bytes);
+void scratch_trim();  // blco_release_thread_caches: return the pool's cached memory
+
 template <class T>
 struct DevBuf {
   T* ptr = nullptr;
   size_t n = 0;
+  bool scratch = false;  // stream-ordered (ScratchScope) allocation
   DevBuf() = default;
   explicit DevBuf(size_t count) { alloc(count); }
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  DevBuf(DevBuf&& o) noexcept : ptr(o.ptr), n(o.n) { o.ptr = nullptr, o.n = 0; }
+  DevBuf(DevBuf&& o) noexcept : ptr(o.ptr), n(o.n), scratch(o.scratch) { o.ptr = nullptr, o.n = 0; }
   DevBuf& operator=(DevBuf&& o) noexcept {
     if (this != &o) {
       reset();
-      ptr = o.ptr, n = o.n;
+      ptr = o.ptr, n = o.n, scratch = o.scratch;
       o.ptr = nullptr, o.n = 0;
     }
     return *this;
@@ -103,13 +122,18 @@ struct DevBuf {
   void alloc(size_t count) {
     reset();
     if (count) {
-      B200_CUDA(cudaMalloc(&ptr, count * sizeof(T)));
+      scratch = scratch_active();
+      if (scratch) ptr = static_cast<T*>(scratch_alloc(count * sizeof(T)));
+      else B200_CUDA(cudaMalloc(&ptr, count * sizeof(T)));
       if (poison_allocations()) B200_CUDA(cudaMemset(ptr, 0xFF, count * sizeof(T)));
     }
     n = count;
   }
   void reset() {
-    if (ptr) cudaFree(ptr);
+    if (ptr) {
+      if (scratch) cudaFreeAsync(ptr, nullptr);
+      else cudaFree(ptr);
+    }
     ptr = nullptr, n = 0;
   }
   size_t bytes() const { return n * sizeof(T); }

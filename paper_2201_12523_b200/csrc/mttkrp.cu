@@ -24,6 +24,8 @@
 //   shared-memory stash (hierarchical path, :139-155), whose rows flush to
 //   the CTA's factor copy at the end (:210-215).
 #include <algorithm>
+#include <map>
+#include <mutex>
 #include <type_traits>
 #include <cstdlib>
 #include <cstring>
@@ -1143,6 +1145,63 @@ void set_smem(K kern, size_t dyn) {
   ensure_dyn_smem(reinterpret_cast<const void*>(kern), dyn);
 }
 
+// BLCO_B200_L2WINDOW=f (0 < f <= 1; off by default): the launch gives the
+// smallest gathered factor matrix an L2 access-policy window -- persisting
+// hits, streaming misses, hit ratio = f * (max persisting L2) / window.  The
+// probe of SURVEY 7's "L2 residency control" lever for DRAM-bound shapes
+// (Amazon); measured in DESIGN.md 3.
+double l2_window_knob() {
+  static const double f = [] {
+    const char* e = std::getenv("BLCO_B200_L2WINDOW");
+    return e ? std::atof(e) : 0.0;
+  }();
+  return f;
+}
+
+template <int N, class K>
+void launch_tiles(K kern, dim3 grid, size_t smem, const Params<N>& p, const MttkrpLaunch& a) {
+  const double f = l2_window_knob();
+  if (f <= 0.0 || N < 2) {
+    kern<<<grid, kCtaThreads, smem, a.stream>>>(p);
+    return;
+  }
+  const blco_layout& l = *a.view.layout;
+  int best = -1;
+  uint64_t bytes = ~0ull;
+  for (int m = 0; m < N; ++m)
+    if (m != a.mode && l.dims[m] * a.rank * 8 < bytes) bytes = l.dims[m] * a.rank * 8, best = m;
+  int dev = 0, max_persist = 0, max_window = 0;
+  B200_CUDA(cudaGetDevice(&dev));
+  B200_CUDA(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev));
+  B200_CUDA(cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, dev));
+  const size_t persist = static_cast<size_t>(std::min(1.0, f) * max_persist);
+  static std::mutex mu;
+  static std::map<int, size_t> limit_set;
+  {
+    std::lock_guard<std::mutex> g(mu);
+    if (limit_set[dev] != persist) {
+      B200_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist));
+      limit_set[dev] = persist;
+    }
+  }
+  cudaLaunchAttribute attr{};
+  attr.id = cudaLaunchAttributeAccessPolicyWindow;
+  auto& w = attr.val.accessPolicyWindow;
+  w.base_ptr = const_cast<double*>(a.factors[best]);
+  w.num_bytes = std::min<size_t>(bytes, static_cast<size_t>(max_window));
+  w.hitRatio = w.num_bytes ? static_cast<float>(std::min(1.0, double(persist) / double(w.num_bytes))) : 0.0f;
+  w.hitProp = cudaAccessPropertyPersisting;
+  w.missProp = cudaAccessPropertyStreaming;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(kCtaThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = a.stream;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  B200_CUDA(cudaLaunchKernelEx(&cfg, kern, p));
+}
+
 template <int N, int LPE, int CPL, bool FULL>
 void launch_cfg(MttkrpLaunch& a) {
   const KernelView& v = a.view;
@@ -1231,7 +1290,7 @@ void launch_cfg(MttkrpLaunch& a) {
     if constexpr (N == 4 && LPE * CPL <= 32)
       if (!stats) kern = k_mttkrp_sorted<N, LPE, CPL, FULL, false, kUnroll, 3>;
     set_smem(kern, stage1);
-    kern<<<grid, kCtaThreads, stage1, a.stream>>>(p);
+    launch_tiles<N>(kern, grid, stage1, p, a);
     count_launch();
     check_launch("k_mttkrp_sorted");
     return;
