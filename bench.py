@@ -313,9 +313,8 @@ def traffic_probe_worker(args):
     b.factors_random_device(dims, R, FACTOR_SEED, [a.data_ptr() for a in fac], sptr)
     outs = [torch.zeros((d, R), dtype=torch.float64, device="cuda:0") for d in dims]
     cfg = b.ExecConfig(num_compute_units=torch.cuda.get_device_properties(0).multi_processor_count)
-    for _ in range(2):
-        for m in range(len(dims)):
-            dt.mttkrp_device([a.data_ptr() for a in fac], R, m, outs[m].data_ptr(), b.Strategy.Auto, cfg,
+    for _ in range(2):  # the step's kernels: the fused all-mode kernel where eligible, else one per mode
+        dt.mttkrp_all_device([a.data_ptr() for a in fac], R, [o.data_ptr() for o in outs], b.Strategy.Auto, cfg,
                              accumulate=True, stream=sptr)
     torch.cuda.synchronize()
 
@@ -676,7 +675,10 @@ def resident_extra(b, torch, name, traffic, args, dev):
     """A second resident config measured in the same run (one GPU), reported
     as its own key beside the headline: the same step (all modes, fixed
     factors, L2 flushed between steps, CUDA events on the launching stream)
-    and the same physical-DRAM roofline."""
+    through the library's all-mode device entry (blco_mttkrp_all_device: the
+    fused all-mode kernel when the factors sit in L2, else one kernel per
+    mode), the per-mode kernels timed beside it, and the same physical-DRAM
+    roofline for the kernel(s) the step launches."""
     dims, nnz, R, desc = CONFIGS[name]
     N = len(dims)
     stream = torch.cuda.current_stream()
@@ -686,41 +688,68 @@ def resident_extra(b, torch, name, traffic, args, dev):
     b.factors_random_device(dims, R, FACTOR_SEED, [a.data_ptr() for a in fac], sptr)
     fptr = [a.data_ptr() for a in fac]
     outs = [torch.empty((d, R), dtype=torch.float64, device=f"cuda:{dev}") for d in dims]
+    optr = [o.data_ptr() for o in outs]
     cfg = b.ExecConfig(num_compute_units=torch.cuda.get_device_properties(dev).multi_processor_count)
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{dev}")
 
-    def step(ev=None):
+    def step_all():
+        for o in outs:
+            o.zero_()
+        return dt.mttkrp_all_device(fptr, R, optr, b.Strategy.Auto, cfg, accumulate=True, stream=sptr)
+
+    def step_modes(ev=None):
         for o in outs:
             o.zero_()
         for m in range(N):
             if ev is not None:
                 ev[m][0].record(stream)
-            dt.mttkrp_device(fptr, R, m, outs[m].data_ptr(), b.Strategy.Auto, cfg, accumulate=True, stream=sptr)
+            dt.mttkrp_device(fptr, R, m, optr[m], b.Strategy.Auto, cfg, accumulate=True, stream=sptr)
             if ev is not None:
                 ev[m][1].record(stream)
 
-    for _ in range(args.warmup):
-        step()
     steps = max(args.steps, 10)
-    evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(N)] for _ in range(steps)]
-    sev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(steps)]
+
+    def timed(fn, per_mode=False):
+        for _ in range(args.warmup):
+            fn()
+        evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(N)] for _ in range(steps)]
+        sev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(steps)]
+        torch.cuda.synchronize()
+        for k in range(steps):
+            flush.zero_()
+            sev[k][0].record(stream)
+            fn(evs[k]) if per_mode else fn()
+            sev[k][1].record(stream)
+        torch.cuda.synchronize()
+        ms = statistics.mean(sev[k][0].elapsed_time(sev[k][1]) for k in range(steps))
+        mode_ms = ([statistics.mean(evs[k][m][0].elapsed_time(evs[k][m][1]) for k in range(steps)) for m in range(N)]
+                   if per_mode else None)
+        return ms, mode_ms
+
+    fused = step_all()
+    ms, _ = timed(step_all)
+    ms_modes, mode_ms = timed(step_modes, per_mode=True)
+    # the M_n of the two paths agree (same per-element terms, summation order aside)
+    step_all()
     torch.cuda.synchronize()
-    for k in range(steps):
-        flush.zero_()
-        sev[k][0].record(stream)
-        step(evs[k])
-        sev[k][1].record(stream)
+    ref = [o.clone() for o in outs]
+    step_modes()
     torch.cuda.synchronize()
-    ms = statistics.mean(sev[k][0].elapsed_time(sev[k][1]) for k in range(steps))
-    mode_ms = [statistics.mean(evs[k][m][0].elapsed_time(evs[k][m][1]) for k in range(steps)) for m in range(N)]
+    agree = max(float(torch.linalg.norm(a - o) / torch.linalg.norm(o)) for a, o in zip(ref, outs))
     bpe = bytes_per_elem(N, R)
     peak, peak_source = hbm_peak()
+    if fused:  # one launch per step
+        roof = roofline_entry(traffic, ms, nnz * N * bpe, peak, peak_source, "k_mttkrp_all3 (one launch per step)")
+    else:
+        roof = roofline_entry(traffic, statistics.mean(mode_ms), nnz * bpe, peak, peak_source,
+                              "k_mttkrp_sorted (one launch per mode)")
     return {"workload": desc, "dims": dims, "nnz": nnz, "rank": R, "steps": steps, "warmup": args.warmup,
-            "ms_per_step": round(ms, 4), "per_mode_ms": [round(x, 4) for x in mode_ms],
-            "value": round(nnz * N * bpe / (ms * 1e-3) / 1e9, 2), "unit": "GB/s (algorithmic B_elem bytes / time)",
-            "roofline": roofline_entry(traffic, statistics.mean(mode_ms), nnz * bpe, peak, peak_source,
-                                       "k_mttkrp_sorted (one launch per mode)"),
-            "l2": "flushed between steps (512 MiB write, outside the timed events)"}
+            "ms_per_step": round(ms, 4), "value": round(nnz * N * bpe / (ms * 1e-3) / 1e9, 2),
+            "unit": "GB/s (algorithmic B_elem bytes / time)",
+            "step_path": "fused all-mode kernel (blco_mttkrp_all_device)" if fused else "per-mode kernels",
+            "per_mode_kernels": {"ms_per_step": round(ms_modes, 4), "per_mode_ms": [round(x, 4) for x in mode_ms],
+                                 "rel_frobenius_vs_step": agree},
+            "roofline": roof, "l2": "flushed between steps (512 MiB write, outside the timed events)"}
 
 
 def fp32_variant(b, torch, dt, dims, R, N, nnz, fac, outs, cfg, sptr, dev, args):

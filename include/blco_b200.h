@@ -289,6 +289,17 @@ int blco_mttkrp_device(const blco_tensor* t, const double* const* d_factors, uin
  * register strategy only, no deterministic mode.  Tolerance 1e-5 relative
  * Frobenius against the fp64 oracle.  Device (d_*, stream, accumulate as in
  * blco_mttkrp_device) and host (factors in, out overwritten) entries. */
+/* Every mode of a device-resident tensor in one call (B200 extension: the
+ * all-mode step with fixed factors, BASELINE's "MTTKRP time/iter (all
+ * modes)").  d_outs[n] (I_n x R, device) receive M_n.  For order 3, R = 16 /
+ * 32, with factors + outputs within 64 MB (they stay in L2) one fused kernel
+ * stages each element once and gathers its three rows once for all three
+ * modes (k_mttkrp_all3; per-element terms in the oracle's order); otherwise
+ * the per-mode kernels run back to back on `stream`.  *fused (optional) says
+ * which.  BLCO_B200_FUSED=0 forces the per-mode kernels. */
+int blco_mttkrp_all_device(const blco_tensor* t, const double* const* d_factors, uint64_t rank, int strategy,
+                           const blco_exec_config* cfg, double* const* d_outs, int accumulate, void* stream,
+                           int* fused);
 int blco_mttkrp_device_f32(const blco_tensor* t, const float* const* d_factors, uint64_t rank, int mode,
                            const blco_exec_config* cfg, float* d_out, int accumulate, void* stream);
 int blco_mttkrp_f32(const blco_tensor* t, const float* const* factors, uint64_t rank, int mode,

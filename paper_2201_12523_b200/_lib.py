@@ -227,6 +227,8 @@ SIGNATURES = {
                                        _P, _I]),
     "blco_container_write_header": (_I, [WRITE_FN, _P, C.POINTER(Layout), _U64, _U64]),
     "blco_container_write_block": (_I, [WRITE_FN, _P, _U64, _U64, _P, _P]),
+    "blco_mttkrp_all_device": (_I, [_P, C.POINTER(_P), _U64, _I, C.POINTER(ExecCfg), C.POINTER(_P), _I, _P,
+                                    C.POINTER(_I)]),
     "blco_device_count": (_I, []),
     "blco_kernel_launch_count": (_U64, []),
     "blco_release_thread_caches": (_I, []),

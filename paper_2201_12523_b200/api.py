@@ -518,6 +518,19 @@ class DeviceTensor:
         if stats is not None:
             _fill_stats(stats, st)
 
+    def mttkrp_all_device(self, d_factors: Sequence[int], rank: int, d_outs: Sequence[int],
+                          strategy: Strategy = Strategy.Auto, config: ExecConfig | None = None,
+                          accumulate: bool = False, stream: int = 0) -> bool:
+        """Every mode in one call on device pointers (blco_mttkrp_all_device);
+        returns True when the fused all-mode kernel ran."""
+        c = (config or ExecConfig())._c()
+        fp = (C.c_void_p * len(d_factors))(*d_factors)
+        op = (C.c_void_p * len(d_outs))(*d_outs)
+        fused = C.c_int()
+        _check(lib.blco_mttkrp_all_device(self._h, fp, rank, int(strategy), C.byref(c), op, int(accumulate),
+                                          C.c_void_p(stream), C.byref(fused)))
+        return bool(fused.value)
+
 
 def mttkrp_f32(t, f, mode: int, config: ExecConfig | None = None) -> np.ndarray:
     """fp32 variant (blco_mttkrp_f32): factors as float32 (a FactorMatrices is

@@ -718,6 +718,144 @@ __global__ void __launch_bounds__(kCtaThreads, MINB) k_mttkrp_sorted(Params<N> p
   }
 }
 
+// ----------------------------------------- all-mode fused kernel (N = 3)
+// B200 extension for the all-mode step with fixed factors (BASELINE's
+// "MTTKRP time/iter (all modes)"; also the gradient of all-at-once CP
+// methods): every element is staged once, its three factor rows are gathered
+// once, and its three per-mode terms are formed in the oracle's product
+// order (oracle.cpp:15-24: value first, the other modes ascending):
+//   M0 += (v A1) A2,   M1 += (v A0) A2,   M2 += (v A0) A1,
+// so every term is bit-identical to the per-mode kernels' and only the
+// summation order differs.  The tile is grouped by the row of mode GM
+// (process_cta with p.mode = GM), so GM's terms accumulate along runs and
+// commit once per run; the other two modes commit per element (merged while
+// consecutive elements share a row).  Used when all three factors and
+// outputs sit in L2 (NELL-2: 26 MB), where the per-mode kernels are bound by
+// the L1 data pipe: 3 row gathers per element per step instead of 6, and one
+// staging pass instead of three.
+struct FusedOut {
+  const double* f[3];
+  double* out[3];
+};
+
+template <int GM, int LPE, int CPL, int U, class ST>
+__device__ __forceinline__ void compute_fused(const ST st, int lo0, int wn, int lane, const FusedOut& fo) {
+  constexpr int G = 32 / LPE;
+  constexpr int RF = LPE * CPL;
+  constexpr int MA = GM == 0 ? 1 : 0, MB = GM == 2 ? 1 : 2;  // the other modes, ascending
+  const int g = lane / LPE, q = lane % LPE;
+  int h = wn / G;
+  if (G > 1 && h > 1) {
+    h = (h & ~3) | 1;  // groups' staged records in disjoint banks
+    if ((G - 1) * h > wn) h = wn / G;
+  }
+  const int lo = lo0 + g * h;
+  const int n = (g == G - 1 ? wn - (G - 1) * h : h);
+  const double* fb[3] = {fo.f[0] + q, fo.f[1] + q, fo.f[2] + q};
+  double* ob[3] = {fo.out[0] + q, fo.out[1] + q, fo.out[2] + q};
+  double acc[CPL], pa[CPL], pb[CPL];
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) acc[c] = pa[c] = pb[c] = 0.0;
+  uint32_t ra = 0xffffffffu, rb = 0xffffffffu;
+  auto flush = [&](double (&x)[CPL], uint32_t row, int m) {
+    if (row == 0xffffffffu) return;
+    double* o = ob[m] + static_cast<uint64_t>(row) * RF;
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) commit_add(o + c * LPE, x[c]);
+  };
+  for (int b0 = 0; b0 < n; b0 += U) {
+    const int valid = min(U, n - b0);
+    const int j0 = lo + b0;
+    double v[U];
+    uint32_t w[U][4];
+    double rows[U][3][CPL];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = u < valid ? j0 + u : j0;
+      st.get(j, v[u], w[u]);
+      if constexpr (!ST::kRowInRecord) w[u][2] = st.row(j);
+    }
+    const uint32_t next_row = b0 + U < n ? st.row(j0 + U) : 0xffffffffu;
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (u < valid) {
+        uint32_t c3[3];
+        c3[GM] = w[u][2], c3[MA] = w[u][0], c3[MB] = w[u][1];
+#pragma unroll
+        for (int m = 0; m < 3; ++m) {
+          const double* rp = fb[m] + static_cast<uint64_t>(c3[m]) * RF;
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) rows[u][m][c] = gather_ld(rp + c * LPE);
+        }
+      }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (u >= valid) continue;
+      double t[3][CPL];
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        const double v0 = __dmul_rn(v[u], rows[u][0][c]);  // shared by the mode-1 and mode-2 terms
+        t[0][c] = __dmul_rn(__dmul_rn(v[u], rows[u][1][c]), rows[u][2][c]);
+        t[1][c] = __dmul_rn(v0, rows[u][2][c]);
+        t[2][c] = __dmul_rn(v0, rows[u][1][c]);
+      }
+      // grouped mode: run accumulation, one commit per run
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) acc[c] = __dadd_rn(acc[c], t[GM][c]);
+      const uint32_t row = w[u][2];
+      const uint32_t nrow = u + 1 < valid ? w[u + 1][2] : (b0 + U < n ? next_row : 0xffffffffu);
+      if (nrow != row) {
+        double* o = ob[GM] + static_cast<uint64_t>(row) * RF;
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+          commit_add(o + c * LPE, acc[c]);
+          acc[c] = 0.0;
+        }
+      }
+      // the other two modes: per element, merged while the row repeats
+      const uint32_t a = w[u][0], b = w[u][1];
+      if (a != ra) {
+        flush(pa, ra, MA);
+        ra = a;
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) pa[c] = t[MA][c];
+      } else {
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) pa[c] = __dadd_rn(pa[c], t[MA][c]);
+      }
+      if (b != rb) {
+        flush(pb, rb, MB);
+        rb = b;
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) pb[c] = t[MB][c];
+      } else {
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) pb[c] = __dadd_rn(pb[c], t[MB][c]);
+      }
+    }
+  }
+  flush(pa, ra, MA);
+  flush(pb, rb, MB);
+}
+
+template <int GM, int LPE, int CPL, int TILE, bool CMP, int MINB, int U>
+__global__ void __launch_bounds__(kCtaThreads, MINB) k_mttkrp_all3(Params<3> p, FusedOut fo) {
+  constexpr int WE = TILE / kWarps;
+  using ST = std::conditional_t<CMP, StageC, Stage<3>>;
+  extern __shared__ __align__(16) unsigned char dyn[];
+  __shared__ BucketShared bs;
+  ST st;
+  if constexpr (CMP) st = StageC{reinterpret_cast<uint4*>(dyn)};
+  else st = cta_stage<3, TILE>(dyn);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const TileDesc td = p.tiles[blockIdx.x];
+  unsigned long long segs = ~0ull;
+  const uint32_t cnt = process_cta<3, TILE, ST>(p, td, st, bs, segs);
+  const int lo0 = warp * WE;
+  const int wn = static_cast<int>(cnt) > lo0 ? min(WE, static_cast<int>(cnt) - lo0) : 0;
+  if (wn > 0) compute_fused<GM, LPE, CPL, U, ST>(st, lo0, wn, lane, fo);
+}
+
 // ------------------------------------------------ fp32 variant (register)
 // The same processing phase (CTA bucket grouping, fp64 values staged), with
 // fp32 factors, products and output (SURVEY.md 8c/8d "fp32 variant": 1e-5
@@ -1360,6 +1498,86 @@ void launch_cfg(MttkrpLaunch& a) {
   if (merge) merge_copies_enqueue(p.out, elems, C, a.out, a.accumulate, a.stream);
 }
 
+// ---- the all-mode fused kernel (k_mttkrp_all3): eligibility and launch
+// BLCO_B200_FUSED=0 disables it (per-mode kernels for every step).
+bool fused_knob() {
+  static const bool on = [] {
+    const char* e = std::getenv("BLCO_B200_FUSED");
+    return !(e && std::string(e) == "0");
+  }();
+  return on;
+}
+
+// Order 3, R = 16 / 32, not deterministic, and the three factors plus the
+// three outputs within 64 MB, so the whole gathered / committed working set
+// stays in the 126 MB L2: the regime where the per-mode kernels are bound by
+// the L1 data pipe.  Larger factors (Amazon) keep the per-mode kernels: there
+// the working set of one window of concurrent tiles would double and fall
+// out of L2.
+bool fused_eligible(const blco_tensor& t, uint64_t rank, const blco_exec_config& c) {
+  if (!fused_knob() || t.layout.order != 3 || (rank != 16 && rank != 32) || c.deterministic) return false;
+  uint64_t bytes = 0;
+  for (int m = 0; m < 3; ++m) bytes += 2 * t.layout.dims[m] * rank * sizeof(double);
+  return bytes <= (uint64_t(64) << 20) && t.nnz > 0;
+}
+
+// BLCO_B200_FUSED_CFG: register / latency trade of the fused kernel --
+// "u4m2": 4 elements gathered ahead per lane group, up to 128 registers
+// (2 CTAs per SM); "u2m3" (default): 2 elements ahead, <= 80 registers
+// (3 CTAs per SM).
+bool fused_u4() {
+  static const bool v = [] {
+    const char* e = std::getenv("BLCO_B200_FUSED_CFG");
+    return e && std::string(e) == "u4m2";
+  }();
+  return v;
+}
+
+template <int GM, int LPE, int CPL>
+void launch_all3_gm(const Params<3>& p, const FusedOut& fo, bool narrow, cudaStream_t s) {
+  constexpr int T2 = 2 * kTileElems;
+  auto kern = narrow ? k_mttkrp_all3<GM, LPE, CPL, T2, true, 3, 2> : k_mttkrp_all3<GM, LPE, CPL, T2, false, 3, 2>;
+  if (fused_u4())
+    kern = narrow ? k_mttkrp_all3<GM, LPE, CPL, T2, true, 2, 4> : k_mttkrp_all3<GM, LPE, CPL, T2, false, 2, 4>;
+  const size_t dyn = narrow ? static_cast<size_t>(T2) * sizeof(uint4) : stage_bytes<3>(T2);
+  set_smem(kern, dyn);
+  kern<<<dim3(static_cast<unsigned>(p.ntiles), 1), kCtaThreads, dyn, s>>>(p, fo);
+  count_launch();
+  check_launch("k_mttkrp_all3");
+}
+
+template <int LPE, int CPL>
+void launch_all3(const blco_tensor& t, const double* const* f, uint64_t rank, double* const* outs,
+                 cudaStream_t s) {
+  const blco_layout& l = t.layout;
+  Params<3> p{};
+  p.tiles = tile_table(t, 2 * kTileElems, &p.ntiles);
+  p.elem_end = t.nnz;
+  p.idx = t.idx.ptr;
+  p.val = t.vals.ptr;
+  p.block_base = t.block_base.ptr;
+  for (int m = 0; m < 3; ++m) {
+    p.shift[m] = static_cast<uint32_t>(l.field_shift[m]);
+    p.mask[m] = l.field_mask[m];
+  }
+  // group the tile by the shortest mode: the most elements per distinct row,
+  // so the most commits saved by run accumulation
+  int gm = 0;
+  for (int m = 1; m < 3; ++m)
+    if (l.dims[m] < l.dims[gm]) gm = m;
+  p.mode = gm;
+  p.rank = static_cast<int>(rank);
+  FusedOut fo{};
+  for (int m = 0; m < 3; ++m) fo.f[m] = f[m], fo.out[m] = outs[m];
+  bool narrow = compact_stage_knob();
+  for (int m = 0; m < 3; ++m)
+    if (m != gm && l.dims[m] > 65536) narrow = false;
+  if (p.ntiles == 0) return;
+  if (gm == 0) launch_all3_gm<0, LPE, CPL>(p, fo, narrow, s);
+  else if (gm == 1) launch_all3_gm<1, LPE, CPL>(p, fo, narrow, s);
+  else launch_all3_gm<2, LPE, CPL>(p, fo, narrow, s);
+}
+
 template <int N>
 void launch_order(MttkrpLaunch& a) {
   switch (a.rank) {
@@ -1557,6 +1775,43 @@ int blco_mttkrp_device(const blco_tensor* t, const double* const* d_factors, uin
     a.accumulate = accumulate;
     a.stream = static_cast<cudaStream_t>(stream);
     run(a, stats);
+  });
+}
+
+int blco_mttkrp_all_device(const blco_tensor* t, const double* const* d_factors, uint64_t rank, int strategy,
+                           const blco_exec_config* cfg, double* const* d_outs, int accumulate, void* stream,
+                           int* fused) {
+  return guarded([&] {
+    blco_exec_config c;
+    if (cfg) c = *cfg; else blco_exec_config_default(&c);
+    for (int m = 0; m < t->layout.order; ++m) validate_call(t, rank, m, &c);
+    DeviceGuard dg(t->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const bool use = strategy != BLCO_STRATEGY_HIERARCHICAL && fused_eligible(*t, rank, c);
+    if (fused) *fused = use ? 1 : 0;
+    if (use) {
+      NvtxRange nv("mttkrp all modes (fused)");
+      if (!accumulate)
+        for (int m = 0; m < 3; ++m)
+          B200_CUDA(cudaMemsetAsync(d_outs[m], 0, t->layout.dims[m] * rank * sizeof(double), s));
+      if (rank == 32) launch_all3<16, 2>(*t, d_factors, rank, d_outs, s);
+      else launch_all3<16, 1>(*t, d_factors, rank, d_outs, s);
+      return;
+    }
+    for (int m = 0; m < t->layout.order; ++m) {
+      MttkrpLaunch a{};
+      a.view = view_of(*t);
+      a.tensor = t;
+      a.factors = d_factors;
+      a.rank = rank;
+      a.mode = m;
+      a.strategy = strategy;
+      a.cfg = c;
+      a.out = d_outs[m];
+      a.accumulate = accumulate;
+      a.stream = s;
+      run(a, nullptr);
+    }
   });
 }
 

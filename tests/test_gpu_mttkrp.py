@@ -413,3 +413,79 @@ def test_big_tiles_forced_on_ragged_blocks(gpu):
     res = json.loads(r.stdout.strip().splitlines()[-1])
     assert max(v[0] for v in res.values()) <= TOL, res
     assert max(v[1] for v in res.values()) <= 1e-5, res
+
+
+FUSED_CASES = [
+    # (dims, nnz, rank, target_bits, cap): narrow staging (non-grouped modes <= 65536 rows), several
+    # keyed blocks, R = 16 / 32; a wide case (non-grouped modes > 65536 rows: the general stage)
+    ([3000, 2500, 4000], 300_000, 32, 64, 1 << 27),
+    ([3000, 2500, 4000], 300_000, 16, 20, 40_000),
+    ([70000, 100, 90000], 200_000, 16, 64, 1 << 27),
+    ([12092, 9184, 28818], 500_000, 32, 64, 1 << 27),  # NELL-2 dims
+]
+
+
+def _fused_worst(gpu, oracle, dims, nnz, rank, tb, cap):
+    import torch
+    dt = gpu.DeviceTensor.synthetic(dims, nnz, 5, tb, cap)
+    idx, vals = oracle.synth_uniform(dims, nnz, 5)
+    f = gpu.FactorMatrices.random(dims, rank, 9)
+    fac = [torch.from_numpy(a).cuda() for a in f.factors]
+    outs = [torch.full((d, rank), 3.0, dtype=torch.float64, device="cuda") for d in dims]
+    fused = dt.mttkrp_all_device([a.data_ptr() for a in fac], rank, [o.data_ptr() for o in outs])
+    torch.cuda.synchronize()
+    worst = 0.0
+    for m in range(3):
+        want = oracle.mttkrp_coo(dims, idx, vals, f.factors, m)
+        worst = max(worst, rel_frobenius(outs[m].cpu().numpy(), want))
+    return fused, worst
+
+
+@pytest.mark.parametrize("dims,nnz,rank,tb,cap", FUSED_CASES)
+def test_all_modes_fused_kernel(gpu, oracle, dims, nnz, rank, tb, cap):
+    """blco_mttkrp_all_device: the fused all-mode kernel (k_mttkrp_all3: one
+    staging pass, three rows gathered once per element, per-element terms in
+    the oracle's product order) against oracle::mttkrp_coo for every mode."""
+    fused, worst = _fused_worst(gpu, oracle, dims, nnz, rank, tb, cap)
+    assert fused
+    assert worst <= TOL
+
+
+def test_all_modes_device_falls_back_per_mode(gpu, oracle):
+    """Ineligible shapes (order 4, rank 33, or factors beyond the L2 budget)
+    run the per-mode kernels through the same entry."""
+    import torch
+    for dims, rank in (([40, 50, 30, 20], 16), ([300, 200, 100], 33), ([300000, 200000, 100], 32)):
+        dt = gpu.DeviceTensor.synthetic(dims, 30_000, 4)
+        idx, vals = oracle.synth_uniform(dims, 30_000, 4)
+        f = gpu.FactorMatrices.random(dims, rank, 9)
+        fac = [torch.from_numpy(a).cuda() for a in f.factors]
+        outs = [torch.empty((d, rank), dtype=torch.float64, device="cuda") for d in dims]
+        assert not dt.mttkrp_all_device([a.data_ptr() for a in fac], rank, [o.data_ptr() for o in outs])
+        torch.cuda.synchronize()
+        for m in range(len(dims)):
+            want = oracle.mttkrp_coo(dims, idx, vals, f.factors, m)
+            assert rel_frobenius(outs[m].cpu().numpy(), want) <= TOL
+
+
+def test_all_modes_fused_u4_subprocess(gpu):
+    """The other register/latency configuration of the fused kernel
+    (BLCO_B200_FUSED_CFG=u4m2, read once per process)."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    code = """
+import sys
+sys.path.insert(0, '.'); sys.path.insert(0, 'oracle'); sys.path.insert(0, 'tests')
+import paper_2201_12523_b200 as b
+from pyoracle import Oracle
+from test_gpu_mttkrp import FUSED_CASES, _fused_worst
+o = Oracle()
+print(max(_fused_worst(b, o, *c)[1] for c in FUSED_CASES))
+"""
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=600,
+                       env=dict(os.environ, BLCO_B200_FUSED_CFG="u4m2"))
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert float(r.stdout.strip().splitlines()[-1]) <= TOL
