@@ -23,6 +23,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <functional>
 #include <cstring>
 
 #include "internal.hpp"
@@ -455,9 +456,11 @@ void build_from_device_coo(blco_tensor& t, DevBuf<uint32_t>& coords, DevBuf<doub
   t.offsets.clear();
   for (uint64_t r = 0; r < nruns; ++r) {
     const uint64_t b = starts[r], e = r + 1 < nruns ? starts[r + 1] : nnz;
-    for (uint64_t c = b; c < e; c += t.max_nnz_per_block) {
+    // blocks of max_nnz_per_block from the run start (no overflow for huge caps)
+    for (uint64_t c = b;; c += t.max_nnz_per_block) {
       t.keys.push_back(run_keys[r]);
       t.offsets.push_back(c);
+      if (e - c <= t.max_nnz_per_block) break;
     }
   }
   t.offsets.push_back(nnz);
@@ -485,6 +488,248 @@ void build_from_device_coo(blco_tensor& t, DevBuf<uint32_t>& coords, DevBuf<doub
   finalize_tensor(t);
   if (stats) stats->batch_seconds = secs(t0);
 }
+
+// ---- multi-pass build of a host COO (>= 2^32 elements, or more than one
+// device pass holds).  The element ids of the in-core sort are u32 and its
+// temporaries cost ~60-80 B per element, so a large COO is built in ALTO-range
+// passes: (1) the COO streams through the device in chunks once to histogram
+// the top H bits of every element's ALTO index; (2) consecutive buckets are
+// grouped into passes of at most `cap` elements; (3) per pass, the COO
+// streams through again, the elements whose bucket falls in the pass are
+// compacted on the device and built in core (sorted, duplicates rejected,
+// re-encoded) with unbounded blocks, so its blocks are exactly its key runs;
+// the pass's payload is appended to the tensor in ALTO order.  ALTO ranges
+// are disjoint and ascending, so the concatenation is the global ALTO order
+// and a duplicate can only meet its twin inside one pass.  Runs of one key
+// that continue across a pass boundary are merged, then every run is cut
+// every max_nnz_per_block elements from its start -- build_blco's chunking
+// (blco_format.cpp:86-111), so the result is bit-identical to the in-core
+// build and to the reference.
+// ALTO range [lo, lo + 2^width) split into 2^hb buckets of 2^(width - hb):
+// bucket(i) = (alto_i - lo) >> shift, or 0xffffffff outside the range
+using u128 = unsigned __int128;
+struct AltoRange {
+  uint64_t lo_lo, lo_hi;  // lo as two words (kernel parameters stay POD)
+  int width;              // log2 of the range size (<= 128)
+  int shift;              // bucket width in bits
+};
+
+__device__ __forceinline__ u128 alto_of(const uint64_t* lo, const uint64_t* hi, uint64_t i) {
+  return (static_cast<u128>(hi ? hi[i] : 0) << 64) | lo[i];
+}
+
+__global__ void k_bucket_of(const uint64_t* __restrict__ lo, const uint64_t* __restrict__ hi, uint64_t n,
+                            AltoRange r, uint32_t* __restrict__ bucket) {
+  const u128 base = (static_cast<u128>(r.lo_hi) << 64) | r.lo_lo;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const u128 a = alto_of(lo, hi, i);
+    const u128 d = a - base;  // wraps above 2^128 when a < base: caught by the width test
+    const bool in = a >= base && (r.width >= 128 || (d >> r.width) == 0);
+    bucket[i] = in ? static_cast<uint32_t>(d >> r.shift) : 0xffffffffu;
+  }
+}
+
+__global__ void k_bucket_hist(const uint32_t* __restrict__ bucket, uint64_t n,
+                              unsigned long long* __restrict__ hist) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    if (bucket[i] != 0xffffffffu) atomicAdd(&hist[bucket[i]], 1ull);
+}
+
+// flag = ALTO in [plo, phi)
+__global__ void k_range_flag(const uint64_t* __restrict__ lo, const uint64_t* __restrict__ hi, uint64_t n,
+                             uint64_t plo_lo, uint64_t plo_hi, uint64_t phi_lo, uint64_t phi_hi,
+                             uint8_t* __restrict__ flag) {
+  const u128 plo = (static_cast<u128>(plo_hi) << 64) | plo_lo, phi = (static_cast<u128>(phi_hi) << 64) | phi_lo;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const u128 a = alto_of(lo, hi, i);
+    flag[i] = a >= plo && a < phi;
+  }
+}
+
+// append the selected chunk elements (ids sel[0..k)) at offset `off` of the
+// pass buffers (coordinates mode-major with stride `cnt`)
+__global__ void k_pass_append(const uint64_t* __restrict__ sel, uint64_t k, int order,
+                              const uint32_t* __restrict__ cc, uint64_t cn, const double* __restrict__ cv,
+                              uint32_t* __restrict__ pc, uint64_t cnt, double* __restrict__ pv, uint64_t off) {
+  for (uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; j < k;
+       j += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t e = sel[j];
+    for (int m = 0; m < order; ++m) pc[m * cnt + off + j] = cc[m * cn + e];
+    pv[off + j] = cv[e];
+  }
+}
+
+// elements per device pass: BLCO_B200_BUILD_PASS_ELEMS overrides (tests);
+// otherwise what the free memory holds at ~96 B per element, below 2^31
+uint64_t build_pass_cap(uint64_t payload_bytes) {
+  if (const char* e = std::getenv("BLCO_B200_BUILD_PASS_ELEMS")) {
+    const uint64_t v = std::strtoull(e, nullptr, 10);
+    if (v > 0) return v;
+  }
+  size_t free_b = 0, total_b = 0;
+  B200_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  const uint64_t room = free_b > payload_bytes + (uint64_t(4) << 30) ? free_b - payload_bytes - (uint64_t(4) << 30) : 0;
+  return std::max<uint64_t>(1, std::min<uint64_t>((uint64_t{1} << 31) - 1, room / 96));
+}
+
+void build_host_passes(blco_tensor& t, const uint64_t* dims, int order, uint64_t nnz, const uint64_t* idx,
+                       const double* vals, uint64_t cap, blco_build_stats* stats) {
+  const blco_layout& l = t.layout;
+  const uint64_t chunk = std::min<uint64_t>(cap, uint64_t{1} << 27);
+  const EncodeParams ep = encode_params(l);
+  const bool wide = l.total_bits > 64;
+  cudaStream_t s = 0;
+  auto t0 = std::chrono::steady_clock::now();
+  DevBuf<uint64_t> stage(chunk), lo(chunk), hi(wide ? chunk : 0), reenc(chunk), sel(chunk);
+  DevBuf<uint32_t> cc(chunk * order), perm(chunk), bucket(chunk);
+  DevBuf<double> cv(chunk);
+  DevBuf<uint8_t> flag(chunk);
+  DevBuf<unsigned> bad(1);
+  B200_CUDA(cudaMemset(bad.ptr, 0, sizeof(unsigned)));
+  // one chunk of the host COO -> device coordinates, values and ALTO words
+  auto load_chunk = [&](uint64_t c0, uint64_t n) {
+    for (int m = 0; m < order; ++m) {
+      B200_CUDA(cudaMemcpy(stage.ptr, idx + static_cast<uint64_t>(m) * nnz + c0, n * 8, cudaMemcpyHostToDevice));
+      k_narrow_coords<<<grid_for(n, 4), kThreads>>>(stage.ptr, cc.ptr + static_cast<uint64_t>(m) * n, n, dims[m],
+                                                    bad.ptr);
+      count_launch();
+    }
+    B200_CUDA(cudaMemcpy(cv.ptr, vals + c0, n * 8, cudaMemcpyHostToDevice));
+    encode_kernel(order)<<<grid_for(n, 4), kThreads, 0, s>>>(ep, n, cc.ptr, lo.ptr, hi.ptr, reenc.ptr, perm.ptr);
+    count_launch();
+    check_launch("build pass: chunk");
+  };
+  // (1)+(2) passes: histogram a range's ALTO sub-ranges (one stream of the
+  // COO), group consecutive sub-ranges into passes of <= cap elements, and
+  // refine any sub-range that alone holds more than cap (skewed tensors:
+  // power-law coordinates share their high ALTO bits)
+  struct Pass {
+    u128 lo, hi;
+    uint64_t cnt;
+  };
+  std::vector<Pass> passes;
+  Pass cur{0, 0, 0};
+  auto close = [&] {
+    if (cur.cnt) passes.push_back(cur);
+    cur = Pass{0, 0, 0};
+  };
+  std::function<void(u128, int)> split = [&](u128 base, int width) {
+    const int hb = std::min(20, width);
+    const int shift = width - hb;
+    const uint64_t nb = uint64_t{1} << hb;
+    DevBuf<unsigned long long> hist(nb);
+    B200_CUDA(cudaMemset(hist.ptr, 0, nb * sizeof(unsigned long long)));
+    const AltoRange r{static_cast<uint64_t>(base), static_cast<uint64_t>(base >> 64), width, shift};
+    for (uint64_t c0 = 0; c0 < nnz; c0 += chunk) {
+      const uint64_t n = std::min(chunk, nnz - c0);
+      load_chunk(c0, n);
+      k_bucket_of<<<grid_for(n, 4), kThreads, 0, s>>>(lo.ptr, wide ? hi.ptr : nullptr, n, r, bucket.ptr);
+      k_bucket_hist<<<grid_for(n, 4), kThreads, 0, s>>>(bucket.ptr, n, hist.ptr);
+      count_launch(2);
+    }
+    unsigned b = 0;
+    B200_CUDA(cudaMemcpy(&b, bad.ptr, sizeof b, cudaMemcpyDeviceToHost));
+    if (b) throw_format("coo: coordinate out of range");
+    std::vector<uint64_t> h(nb);
+    B200_CUDA(cudaMemcpy(h.data(), hist.ptr, nb * 8, cudaMemcpyDeviceToHost));
+    for (uint64_t q = 0; q < nb; ++q) {
+      if (!h[q]) continue;
+      const u128 qlo = base + (static_cast<u128>(q) << shift), qhi = qlo + (static_cast<u128>(1) << shift);
+      if (h[q] > cap) {  // one ALTO value holds one element, so refining terminates
+        close();
+        split(qlo, shift);
+        continue;
+      }
+      if (cur.cnt + h[q] > cap) close();
+      if (!cur.cnt) cur.lo = qlo;
+      cur.hi = qhi;
+      cur.cnt += h[q];
+    }
+  };
+  split(0, l.total_bits);
+  close();
+  // (3) each pass built in core; payload appended in ALTO order
+  {
+    ScratchScope keep(false);  // the payload outlives the build
+    t.idx.alloc(nnz);
+    t.vals.alloc(nnz);
+  }
+  std::vector<uint64_t> run_keys, run_starts;  // global runs of equal key
+  uint64_t out_off = 0;
+  blco_build_stats acc{};
+  for (const Pass& ps : passes) {
+    const uint64_t cnt = ps.cnt;
+    DevBuf<uint32_t> pc(cnt * order);
+    DevBuf<double> pv(cnt);
+    uint64_t off = 0;
+    for (uint64_t c0 = 0; c0 < nnz; c0 += chunk) {
+      const uint64_t n = std::min(chunk, nnz - c0);
+      load_chunk(c0, n);
+      k_range_flag<<<grid_for(n, 4), kThreads, 0, s>>>(lo.ptr, wide ? hi.ptr : nullptr, n,
+                                                       static_cast<uint64_t>(ps.lo), static_cast<uint64_t>(ps.lo >> 64),
+                                                       static_cast<uint64_t>(ps.hi), static_cast<uint64_t>(ps.hi >> 64),
+                                                       flag.ptr);
+      count_launch();
+      const uint64_t k = select_flagged<uint64_t>(nullptr, flag.ptr, n, sel.ptr, s);
+      if (off + k > cnt) throw_error("b200: multi-pass build: pass overflow");
+      if (k) {
+        k_pass_append<<<grid_for(k, 2), kThreads, 0, s>>>(sel.ptr, k, order, cc.ptr, n, cv.ptr, pc.ptr, cnt, pv.ptr,
+                                                           off);
+        count_launch();
+        check_launch("k_pass_append");
+      }
+      off += k;
+    }
+    if (off != cnt) throw_error("b200: multi-pass build: pass count mismatch");
+    blco_tensor tp;
+    tp.layout = l;
+    tp.device = t.device;
+    tp.max_nnz_per_block = ~uint64_t{0};  // blocks = key runs
+    blco_build_stats st{};
+    build_from_device_coo(tp, pc, pv, cnt, &st);
+    acc.sort_seconds += st.sort_seconds;
+    acc.block_seconds += st.block_seconds;
+    acc.reencode_seconds += st.reencode_seconds;
+    B200_CUDA(cudaMemcpy(t.idx.ptr + out_off, tp.idx.ptr, cnt * 8, cudaMemcpyDeviceToDevice));
+    B200_CUDA(cudaMemcpy(t.vals.ptr + out_off, tp.vals.ptr, cnt * 8, cudaMemcpyDeviceToDevice));
+    for (uint64_t r = 0; r < tp.keys.size(); ++r) {
+      if (r == 0 && !run_keys.empty() && run_keys.back() == tp.keys[0]) continue;  // run continues across passes
+      run_keys.push_back(tp.keys[r]);
+      run_starts.push_back(out_off + tp.offsets[r]);
+    }
+    out_off += cnt;
+  }
+  if (out_off != nnz) throw_error("b200: multi-pass build: element count mismatch");
+  // global chunking of the runs (blco_format.cpp:86-111)
+  t.nnz = nnz;
+  t.keys.clear();
+  t.offsets.clear();
+  for (size_t r = 0; r < run_keys.size(); ++r) {
+    const uint64_t b0 = run_starts[r], e = r + 1 < run_keys.size() ? run_starts[r + 1] : nnz;
+    for (uint64_t c = b0;; c += t.max_nnz_per_block) {
+      t.keys.push_back(run_keys[r]);
+      t.offsets.push_back(c);
+      if (e - c <= t.max_nnz_per_block) break;
+    }
+  }
+  t.offsets.push_back(nnz);
+  finalize_tensor(t);
+  if (stats) {
+    *stats = acc;
+    stats->batch_seconds = secs(t0) - acc.sort_seconds - acc.block_seconds - acc.reencode_seconds;
+  }
+}
+
+// Build temporaries come from the stream-ordered pool (ScratchScope) for
+// builds up to 2^27 elements (a few GB of temporaries, kept cached between
+// builds: NELL-2 26 -> 17 ms).  Larger builds allocate directly: their
+// temporaries exceed the pool's cached 4 GiB, and the tensor's own payload
+// allocation then waits while the driver trims tens of GB out of the pool
+// (Amazon 0.65 -> 6.7 s measured with the pool).
+bool scratch_build(uint64_t elems) { return elems <= (uint64_t{1} << 27); }
 
 blco_tensor* new_tensor(const uint64_t* dims, int order, int target_bits, uint64_t max_nnz,
                         int device) {
@@ -566,9 +811,15 @@ int blco_build(const uint64_t* dims, int order, uint64_t nnz, const uint64_t* id
   *out = nullptr;
   return guarded([&] {
     DeviceGuard dg(device);
-    ScratchScope scratch;  // build temporaries: stream-ordered pool
+    ScratchScope scratch(scratch_build(nnz));
     blco_tensor* t = new_tensor(dims, order, target_bits, max_nnz, device);
     try {
+      const uint64_t cap = build_pass_cap(nnz * 16);
+      if (nnz > cap) {  // beyond one device pass (>= 2^31 elements, or device memory)
+        build_host_passes(*t, dims, order, nnz, idx, vals, cap, stats);
+        *out = t;
+        return;
+      }
       DevBuf<uint32_t> coords(static_cast<size_t>(nnz) * order);
       DevBuf<double> dv(nnz);
       DevBuf<unsigned> bad(1);
@@ -604,7 +855,7 @@ int blco_build_synthetic(const uint64_t* dims, int order, uint64_t nnz, uint64_t
   *out = nullptr;
   return guarded([&] {
     DeviceGuard dg(device);
-    ScratchScope scratch;  // build temporaries: stream-ordered pool
+    ScratchScope scratch(scratch_build(nnz));
     blco_tensor* t = new_tensor(dims, order, target_bits, max_nnz, device);
     try {
       const synth::Feistel f = synth::make_feistel(dims, order, nnz, seed);
@@ -633,7 +884,7 @@ int blco_build_synthetic_draws(const uint64_t* dims, int order, uint64_t nnz, ui
   return guarded([&] {
     if (skew < 1 || skew > 64) throw_format("synth: skew exponent must lie in [1, 64]");
     DeviceGuard dg(device);
-    ScratchScope scratch;  // build temporaries: stream-ordered pool
+    ScratchScope scratch(scratch_build(nnz + nnz / 2));
     DevBuf<uint64_t> ddims(order);
     B200_CUDA(cudaMemcpy(ddims.ptr, dims, order * 8, cudaMemcpyHostToDevice));
     uint64_t ncand = nnz + nnz / 8 + 1024;
@@ -677,7 +928,7 @@ int blco_synth_alto_chunk(const uint64_t* dims, int order, uint64_t chunk, uint6
     const uint64_t width = static_cast<uint64_t>((space + nchunks - 1) / nchunks);
     const uint64_t lo = static_cast<uint64_t>(space * chunk / nchunks);
     DeviceGuard dg(device);
-    ScratchScope scratch;  // build temporaries: stream-ordered pool
+    ScratchScope scratch(scratch_build(ncand));
     cudaStream_t s = 0;
     DevBuf<uint64_t> alto(ncand), alto_s(ncand), out_idx(ncand);
     DevBuf<uint32_t> ids(ncand), ids_s(ncand), ids_sel(ncand);

@@ -21,6 +21,16 @@ b.stream_mttkrp_all_modes(t, f, bud)                   # streaming
 d4 = [40, 50, 30, 20]
 t4 = b.DeviceTensor.synthetic_draws(d4, 20000, 42, 4)  # config-4 style draws
 b.cp_als(t4, b.CpAlsOptions(rank=16, max_iters=2, tol=-1e300, seed=7))
+# round 2: the fused all-mode kernel, the device census, the library multi-GPU step (G = 1)
+import torch
+dt = b.DeviceTensor.synthetic([300, 250, 400], 40000, 5, 16, 4000)
+fac = [torch.rand((d, 32), dtype=torch.float64, device="cuda") for d in (300, 250, 400)]
+outs = [torch.zeros((d, 32), dtype=torch.float64, device="cuda") for d in (300, 250, 400)]
+assert dt.mttkrp_all_device([a.data_ptr() for a in fac], 32, [o.data_ptr() for o in outs])
+dt.census()
+f3 = b.FactorMatrices.random([300, 250, 400], 32, 7)
+b.MultiDeviceTensor(dt, [0]).mttkrp_all_modes(f3, reduce="reducescatter")
+torch.cuda.synchronize()
 print("sanitize workload done")
 PY
 for tool in memcheck racecheck synccheck; do

@@ -157,3 +157,50 @@ def test_conservation_roundtrip(gpu):  # test_blco.cpp:50-84 (delinearize all bl
     want = {(tuple(int(x) for x in coo.indices[:, e]), float(coo.values[e])) for e in range(coo.nnz())}
     assert got == want
     assert (np.diff(t.keys.astype(np.int64)) >= 0).all()
+
+
+@pytest.fixture
+def small_passes(monkeypatch):
+    """Force the multi-pass host-COO build (the >= 2^31-element / beyond
+    device memory path) at test sizes: BLCO_B200_BUILD_PASS_ELEMS is read on
+    every build call."""
+    def set_cap(n):
+        monkeypatch.setenv("BLCO_B200_BUILD_PASS_ELEMS", str(n))
+    return set_cap
+
+
+@pytest.mark.parametrize("dims,nnz,tb,cap,pass_elems,draws", [
+    ([300, 200, 250], 50_000, 20, 3000, 7_000, 0),             # several keys, runs spanning passes
+    ([8211298, 176962, 8116559], 60_000, 64, 5_000, 9_000, 0),  # Reddit dims: one key over every pass
+    ([4821207, 1774269, 1805187], 40_000, 64, 1 << 27, 6_000, 0),  # Amazon: 65-bit, two-word ALTO
+    ([532924, 17262471, 2480308, 1443], 40_000, 64, 2_000, 5_000, 4),  # Delicious: 78 bits, 14 stripped
+])
+def test_multi_pass_build_bit_exact(gpu, oracle, small_passes, dims, nnz, tb, cap, pass_elems, draws):
+    """The out-of-core build (ALTO-range passes over the host COO, runs merged
+    across passes, global chunking at max_nnz_per_block) equals the in-core
+    reference build_blco bit for bit (blco_format.cpp:62-134)."""
+    if draws:
+        idx, vals = oracle.synth_draws(dims, nnz, 42, draws)
+    else:
+        idx, vals = oracle.synth_uniform(dims, nnz, 42)
+    keys, offs, oi, ov = oracle.build(dims, idx, vals, tb, cap)
+    small_passes(pass_elems)
+    t = build(gpu, dims, idx, vals, tb, cap)
+    assert np.array_equal(t.keys, keys) and np.array_equal(t.offsets, offs)
+    assert np.array_equal(t.idx, oi) and np.array_equal(t.vals, ov)
+
+
+def test_multi_pass_build_errors(gpu, small_passes):
+    """Duplicates (in one pass by construction: equal ALTO) and out-of-range
+    coordinates are rejected on the multi-pass path too."""
+    small_passes(1_000)
+    rng = np.random.default_rng(1)
+    idx = rng.integers(0, 100, size=(3, 5_000)).astype(np.uint64)
+    idx[:, 4_000] = idx[:, 10]  # a duplicate far from its twin in input order
+    vals = rng.uniform(size=5_000)
+    with pytest.raises(gpu.FormatError, match="duplicate"):
+        build(gpu, [100, 100, 100], idx, vals)
+    idx = rng.integers(0, 100, size=(3, 5_000)).astype(np.uint64)
+    idx[1, 77] = 100
+    with pytest.raises(gpu.FormatError, match="out of range"):
+        build(gpu, [100, 100, 100], idx, vals)
