@@ -186,6 +186,9 @@ struct blco_tensor {
   // tile tables keyed by tile size, built lazily
   mutable std::mutex mu;
   mutable std::map<uint32_t, b200::DevBuf<b200::TileDesc>> tiles;
+  // panel-ordered tile tables (mttkrp.cu panel_tile_table), keyed by
+  // tile size, mode and panel widths
+  mutable std::map<uint64_t, b200::DevBuf<b200::TileDesc>> panel_tiles;
   // deterministic-mode indices keyed by mode, built lazily
   mutable std::map<int, b200::DetIndex> det;
 

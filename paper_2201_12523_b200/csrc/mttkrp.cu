@@ -1278,6 +1278,119 @@ bool compact_stage_knob() {
   return on;
 }
 
+// ---- panel-ordered tile tables (order 3, factors beyond L2)
+// The tile table fixes only the order CTAs are dispatched in; any order gives
+// the same terms (the commits are atomic, mttkrp.cpp:95-137 sums a segment
+// in element order inside one tile, which is kept).  ALTO order is a
+// Z-curve: a window of concurrent tiles is a box about equally wide in
+// every mode, so when the factors exceed L2 (Amazon: 1.2 + 2 x 0.45 GB at
+// R = 32) every target row misses (RED read-modify-write) and the gathered
+// rows are reused ~1.7x per mode (ncu: 433 DRAM bytes per element per mode).
+// A panel order is the loop nest
+//   for X-panel (target mode, 2^bx rows)  for Y-panel (2^by rows of the
+//   shorter non-target mode)  for tiles of the panel in ALTO order,
+// so the panel's output rows and Y rows stay in L2 while the longest
+// non-target mode Z streams through it: per element ~1/(rho 2^(bx+by)) Z-row
+// misses plus amortised X / Y misses.  Y panels are walked boustrophedon so
+// consecutive panels share their Y rows.  Each tile is assigned to the panel
+// of its middle element.
+// BLCO_B200_PANEL: "0" off; "bx,by" fixed widths; default: auto from
+// BLCO_B200_PANEL_MB (default 64) of L2 for the panel's X + Y rows.
+struct PanelPlan {
+  int x = -1, y = -1;
+  int bx = 0, by = 0;
+};
+
+PanelPlan panel_plan(const blco_layout& l, int mode, uint64_t rank) {
+  PanelPlan p;
+  if (l.order != 3 || rank == 0) return p;
+  uint64_t bytes = 0;
+  for (int m = 0; m < 3; ++m) bytes += l.dims[m] * rank * sizeof(double);
+  if (bytes <= (uint64_t(96) << 20)) return p;  // L2-resident working set: ALTO order is already local
+  // read per call (only reached by launches over GBs of factors), so a probe
+  // can sweep the widths in one process
+  const char* ek = std::getenv("BLCO_B200_PANEL");
+  const std::string knob = ek ? ek : "";
+  const char* em = std::getenv("BLCO_B200_PANEL_MB");
+  const uint64_t budget_mb = em ? std::strtoull(em, nullptr, 10) : 64ull;
+  if (knob == "0") return p;
+  int z = -1;
+  for (int m = 0; m < 3; ++m)
+    if (m != mode && (z < 0 || l.dims[m] > l.dims[z])) z = m;
+  p.x = mode;
+  p.y = 3 - mode - z;
+  if (!knob.empty() && knob.find(',') != std::string::npos) {
+    p.bx = std::atoi(knob.c_str());
+    p.by = std::atoi(knob.c_str() + knob.find(',') + 1);
+  } else {
+    const uint64_t rows = (budget_mb << 20) / (rank * sizeof(double));
+    int b = 0;
+    while ((uint64_t(2) << (b + 1)) <= rows) ++b;  // 2 * 2^b <= rows
+    p.bx = p.by = b;
+  }
+  if (p.bx <= 0 || p.by <= 0 || p.bx > 31 || p.by > 31 ||
+      (l.dims[p.x] <= (uint64_t(1) << p.bx) && l.dims[p.y] <= (uint64_t(1) << p.by)))
+    return PanelPlan{};  // one panel: nothing to reorder
+  return p;
+}
+
+__global__ void k_tile_panel(const TileDesc* __restrict__ tiles, uint64_t ntiles, const uint64_t* __restrict__ idx,
+                             const uint32_t* __restrict__ block_base, int x, int y, uint32_t sx, uint64_t mx,
+                             uint32_t sy, uint64_t my, int bx, int by, uint32_t npy, uint32_t* __restrict__ panel) {
+  const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (i >= ntiles) return;
+  const TileDesc td = tiles[i];
+  const uint64_t ix = idx[td.start + td.count / 2];
+  const uint32_t cx = block_base[uint64_t(td.block) * 3 + x] | static_cast<uint32_t>((ix >> sx) & mx);
+  const uint32_t cy = block_base[uint64_t(td.block) * 3 + y] | static_cast<uint32_t>((ix >> sy) & my);
+  const uint32_t px = cx >> bx;
+  uint32_t py = cy >> by;
+  if (px & 1u) py = npy - 1 - py;  // boustrophedon
+  panel[i] = px * npy + py;
+}
+
+// The tile table of t at tile_elems reordered by panel (stable: ALTO order
+// inside a panel), or null when the plan is empty.  Cached with the tensor.
+const TileDesc* panel_tile_table(const blco_tensor& t, uint32_t tile_elems, int mode, uint64_t rank,
+                                 uint64_t* ntiles) {
+  const PanelPlan pp = panel_plan(t.layout, mode, rank);
+  if (pp.x < 0) return nullptr;
+  uint64_t n = 0;
+  const TileDesc* base = tile_table(t, tile_elems, &n);
+  const uint64_t key = (uint64_t(tile_elems) << 32) | (uint64_t(mode) << 24) | (uint64_t(pp.bx) << 8) | pp.by;
+  std::lock_guard<std::mutex> g(t.mu);
+  auto it = t.panel_tiles.find(key);
+  if (it == t.panel_tiles.end()) {
+    const blco_layout& l = t.layout;
+    const uint32_t npy = static_cast<uint32_t>(((l.dims[pp.y] - 1) >> pp.by) + 1);
+    const uint64_t npx = ((l.dims[pp.x] - 1) >> pp.bx) + 1;
+    ScratchScope keep(false);  // cached with the tensor
+    DevBuf<uint32_t> d_panel(std::max<uint64_t>(n, 1));
+    DevBuf<TileDesc> d(n);
+    if (n) {
+      k_tile_panel<<<static_cast<unsigned>((n + 255) / 256), 256>>>(
+          base, n, t.idx.ptr, t.block_base.ptr, pp.x, pp.y, static_cast<uint32_t>(l.field_shift[pp.x]),
+          l.field_mask[pp.x], static_cast<uint32_t>(l.field_shift[pp.y]), l.field_mask[pp.y], pp.bx, pp.by, npy,
+          d_panel.ptr);
+      count_launch();
+      check_launch("k_tile_panel");
+      std::vector<uint32_t> panel(n);
+      std::vector<TileDesc> src(n), dst(n);
+      B200_CUDA(cudaMemcpy(panel.data(), d_panel.ptr, n * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+      B200_CUDA(cudaMemcpy(src.data(), base, n * sizeof(TileDesc), cudaMemcpyDeviceToHost));
+      std::vector<uint64_t> start(npx * npy + 1, 0);  // stable counting sort by panel
+      for (uint64_t i = 0; i < n; ++i) ++start[panel[i] + 1];
+      for (size_t k = 1; k < start.size(); ++k) start[k] += start[k - 1];
+      for (uint64_t i = 0; i < n; ++i) dst[start[panel[i]]++] = src[i];
+      B200_CUDA(cudaMemcpy(d.ptr, dst.data(), n * sizeof(TileDesc), cudaMemcpyHostToDevice));
+      B200_CUDA(cudaDeviceSynchronize());  // read by kernels on any stream
+    }
+    it = t.panel_tiles.emplace(key, std::move(d)).first;
+  }
+  *ntiles = it->second.n;
+  return it->second.ptr;
+}
+
 template <class K>
 void set_smem(K kern, size_t dyn) {
   ensure_dyn_smem(reinterpret_cast<const void*>(kern), dyn);
@@ -1408,6 +1521,12 @@ void launch_cfg(MttkrpLaunch& a) {
         count_launch();
         check_launch("k_mttkrp_sorted");
         return;
+      }
+    }
+    if constexpr (N == 3) {
+      if (a.tensor) {  // factors beyond L2: panel-ordered dispatch (panel_plan)
+        uint64_t nt = 0;
+        if (const TileDesc* pt = panel_tile_table(*a.tensor, kTileElems, a.mode, a.rank, &nt)) p.tiles = pt;
       }
     }
     size_t stage1 = tile_stage;

@@ -489,3 +489,28 @@ print(max(_fused_worst(b, o, *c)[1] for c in FUSED_CASES))
                        env=dict(os.environ, BLCO_B200_FUSED_CFG="u4m2"))
     assert r.returncode == 0, r.stderr[-2000:]
     assert float(r.stdout.strip().splitlines()[-1]) <= TOL
+
+
+@pytest.mark.parametrize("panel", ["", "10,10", "3,18", "17,2"])
+def test_panel_ordered_dispatch(gpu, oracle, monkeypatch, panel):
+    """Factors beyond L2 (here 307 MB at R = 32): the register kernel runs its
+    tiles in panel order (mttkrp.cu panel_plan: target-mode x shorter
+    non-target-mode panels, ALTO order inside), across keyed blocks and with
+    tiles straddling panel edges, against oracle::mttkrp_coo for every mode.
+    The reordered table is built once per (mode, widths): one k_tile_panel
+    launch beside the MTTKRP on first use, none after."""
+    monkeypatch.setenv("BLCO_B200_PANEL", panel)
+    dims = [600_000, 300_000, 300_000]
+    nnz = 400_000
+    dt = gpu.DeviceTensor.synthetic(dims, nnz, 11, 48, 90_000)
+    idx, vals = oracle.synth_uniform(dims, nnz, 11)
+    f = gpu.FactorMatrices.random(dims, 32, 5)
+    for mode in range(3):
+        want = oracle.mttkrp_coo(dims, idx, vals, f.factors, mode)
+        n0 = gpu.kernel_launch_count()
+        got = gpu.mttkrp(dt, f, mode, strategy=gpu.Strategy.Register)
+        n1 = gpu.kernel_launch_count()
+        again = gpu.mttkrp(dt, f, mode, strategy=gpu.Strategy.Register)
+        n2 = gpu.kernel_launch_count()
+        assert rel_frobenius(got, want) <= TOL and rel_frobenius(again, want) <= TOL, mode
+        assert n2 - n1 == 1 and n1 - n0 == 2, (mode, n1 - n0, n2 - n1)
