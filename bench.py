@@ -160,7 +160,8 @@ def reference_sample_run(dims, nnz, rank, steps, warmup, target_step_s=4.0, thre
     1 thread and for all host threads (the reference anti-scales with
     threads), and the thread count with the smaller extrapolated
     full-tensor step is used: the reference's best CPU configuration.  Then
-    `steps` timed steps of a sample of S elements (one step ~ target_step_s)
+    `steps` timed steps of a sample of S elements (the per-element part of a
+    step ~ target_step_s)
     refine b, and the full-tensor step is a + b*nnz (`extrapolated` unless
     S = nnz).  op "stream" times the reference stream_mttkrp
     (MemoryBlockSource, its DeviceBudget) per mode instead.  Returns
@@ -225,7 +226,10 @@ def reference_sample_run(dims, nnz, rank, steps, warmup, target_step_s=4.0, thre
     best = min(fits, key=lambda th: fits[th]["a"] + fits[th]["b"] * nnz)
     a, b_cal, d_lo = fits[best]["a"], fits[best]["b"], fits[best]["d_lo"]
     cfg = cfg_array(num_threads=best)
-    S = min(gen_n, max(S_mid, int(max(target_step_s - a, 0.0) / b_cal)), 1 << 25)
+    # the per-element part of a sample step ~ target_step_s on top of the
+    # fixed part, so b is fitted over seconds of element work, not over the
+    # noise of the fixed cost
+    S = min(gen_n, max(S_mid, int(target_step_s / b_cal)), 1 << 25)
     if S > S_mid:
         del t_mid
         t, S = sample(S)
@@ -632,6 +636,7 @@ def run_ours(args, world, rank_id, local):
         "config": {"workload": desc, "dims": dims, "nnz": nnz, "rank": R, "modes": N,
                    "tensor_seed": TENSOR_SEED, "factor_seed": FACTOR_SEED, "strategy": args.strategy,
                    "l2": "flushed between steps (512 MiB write, outside the timed events)",
+                   "tile_order": tile_order(dims, R),
                    "parallelism": f"span partition x{world}" + (
                        (" + NCCL reduce-scatter of M per mode (row shards), overlapped with the next mode's kernel"
                         if rs else " + NCCL all-reduce of M per mode, overlapped with the next mode's kernel")
@@ -1276,9 +1281,22 @@ def run_stream(args, world, rank_id, local):
         print(json.dumps(result), flush=True)
 
 
+def tile_order(dims, R) -> str:
+    """The CTA dispatch order the library picks (mttkrp.cu panel_plan)."""
+    knob = os.environ.get("BLCO_B200_PANEL", "")
+    if len(dims) < 3 or sum(dims) * R * 8 <= (96 << 20) or knob == "0":
+        return "ALTO"
+    if "," in knob:
+        return f"panel-ordered (BLCO_B200_PANEL={knob})"
+    mb = int(os.environ.get("BLCO_B200_PANEL_MB", "32"))
+    b = max(0, ((mb << 20) // (R * 8) // 2).bit_length() - 1)
+    return f"panel-ordered: 2^{b}-row panels of the target x second-longest mode, ALTO order inside"
+
+
 def ref_step_s(args) -> float:
-    """Per-step sample size target of the reference arm, so --steps K
-    --warmup W stays within a few minutes (about 100 s of timed CPU work)."""
+    """Per-step sample size target of the reference arm (seconds of
+    per-element work on top of the fixed per-call cost), so --steps K
+    --warmup W stays within a few minutes (about 100 s of element work)."""
     return max(0.2, min(args.ref_step_s, 100.0 / max(1, args.steps + args.warmup)))
 
 

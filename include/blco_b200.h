@@ -291,12 +291,12 @@ int blco_mttkrp_device(const blco_tensor* t, const double* const* d_factors, uin
  * blco_mttkrp_device) and host (factors in, out overwritten) entries. */
 /* Every mode of a device-resident tensor in one call (B200 extension: the
  * all-mode step with fixed factors, BASELINE's "MTTKRP time/iter (all
- * modes)").  d_outs[n] (I_n x R, device) receive M_n.  For order 3, R = 16 /
- * 32, with factors + outputs within 64 MB (they stay in L2) one fused kernel
- * stages each element once and gathers its three rows once for all three
- * modes (k_mttkrp_all3; per-element terms in the oracle's order); otherwise
- * the per-mode kernels run back to back on `stream`.  *fused (optional) says
- * which.  BLCO_B200_FUSED=0 forces the per-mode kernels. */
+ * modes)").  d_outs[n] (I_n x R, device) receive M_n: the per-mode
+ * kernels run back to back on `stream`.  With BLCO_B200_FUSED=1 (opt-in,
+ * measured slower on B200: L2-atomic bound), order 3, R = 16 / 32 and
+ * factors + outputs within 64 MB, one fused kernel stages each element once
+ * and gathers its three rows once for all three modes (k_mttkrp_all3;
+ * per-element terms in the oracle's order).  *fused (optional) says which. */
 int blco_mttkrp_all_device(const blco_tensor* t, const double* const* d_factors, uint64_t rank, int strategy,
                            const blco_exec_config* cfg, double* const* d_outs, int accumulate, void* stream,
                            int* fused);

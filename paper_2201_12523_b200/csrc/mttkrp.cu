@@ -1278,7 +1278,7 @@ bool compact_stage_knob() {
   return on;
 }
 
-// ---- panel-ordered tile tables (order 3, factors beyond L2)
+// ---- panel-ordered tile tables (orders >= 3, factors beyond L2)
 // The tile table fixes only the order CTAs are dispatched in; any order gives
 // the same terms (the commits are atomic, mttkrp.cpp:95-137 sums a segment
 // in element order inside one tile, which is kept).  ALTO order is a
@@ -1288,14 +1288,19 @@ bool compact_stage_knob() {
 // rows are reused ~1.7x per mode (ncu: 433 DRAM bytes per element per mode).
 // A panel order is the loop nest
 //   for X-panel (target mode, 2^bx rows)  for Y-panel (2^by rows of the
-//   shorter non-target mode)  for tiles of the panel in ALTO order,
-// so the panel's output rows and Y rows stay in L2 while the longest
-// non-target mode Z streams through it: per element ~1/(rho 2^(bx+by)) Z-row
-// misses plus amortised X / Y misses.  Y panels are walked boustrophedon so
-// consecutive panels share their Y rows.  Each tile is assigned to the panel
-// of its middle element.
-// BLCO_B200_PANEL: "0" off; "bx,by" fixed widths; default: auto from
-// BLCO_B200_PANEL_MB (default 64) of L2 for the panel's X + Y rows.
+//   second-longest non-target mode)  for tiles of the panel in ALTO order,
+// so a window of concurrent tiles spans few output and Y rows (they stay in
+// L2 across the panel) while the longest non-target mode Z streams.  Y
+// panels are walked boustrophedon so consecutive panels share their Y rows.
+// Each tile is assigned to the panel of its middle element.  Measured on
+// the Amazon shape (scripts/panel_probe.py, B200): 16,16 panels at R = 32
+// cut the DRAM bytes of a mode launch from 760 to 506 GB (the output rows'
+// write-backs from 215 to 29 GB) and the all-mode step from 384 to 345 ms;
+// wider panels (17,17: 354 ms; 18,16: 371 ms) overflow L2 with the
+// streamed rows, narrower ones (14,14: 361 ms) lose the reuse.
+// BLCO_B200_PANEL: "0" off; "bx,by" fixed widths; default: both widths from
+// BLCO_B200_PANEL_MB (default 32) of L2 for the panel's X + Y rows
+// (R = 32: 2^16 rows each).
 struct PanelPlan {
   int x = -1, y = -1;
   int bx = 0, by = 0;
@@ -1303,22 +1308,27 @@ struct PanelPlan {
 
 PanelPlan panel_plan(const blco_layout& l, int mode, uint64_t rank) {
   PanelPlan p;
-  if (l.order != 3 || rank == 0) return p;
+  if (l.order < 3 || rank == 0) return p;
   uint64_t bytes = 0;
-  for (int m = 0; m < 3; ++m) bytes += l.dims[m] * rank * sizeof(double);
+  for (int m = 0; m < l.order; ++m) bytes += l.dims[m] * rank * sizeof(double);
   if (bytes <= (uint64_t(96) << 20)) return p;  // L2-resident working set: ALTO order is already local
   // read per call (only reached by launches over GBs of factors), so a probe
   // can sweep the widths in one process
   const char* ek = std::getenv("BLCO_B200_PANEL");
   const std::string knob = ek ? ek : "";
   const char* em = std::getenv("BLCO_B200_PANEL_MB");
-  const uint64_t budget_mb = em ? std::strtoull(em, nullptr, 10) : 64ull;
+  const uint64_t budget_mb = em ? std::strtoull(em, nullptr, 10) : 32ull;
   if (knob == "0") return p;
-  int z = -1;
-  for (int m = 0; m < 3; ++m)
+  // Z = the longest non-target mode (streamed), Y = the next longest; for
+  // orders > 3 the remaining modes are left to L2 (short modes: Delicious'
+  // 1443 rows)
+  int z = -1, y = -1;
+  for (int m = 0; m < l.order; ++m)
     if (m != mode && (z < 0 || l.dims[m] > l.dims[z])) z = m;
+  for (int m = 0; m < l.order; ++m)
+    if (m != mode && m != z && (y < 0 || l.dims[m] > l.dims[y])) y = m;
   p.x = mode;
-  p.y = 3 - mode - z;
+  p.y = y;
   if (!knob.empty() && knob.find(',') != std::string::npos) {
     p.bx = std::atoi(knob.c_str());
     p.by = std::atoi(knob.c_str() + knob.find(',') + 1);
@@ -1335,14 +1345,14 @@ PanelPlan panel_plan(const blco_layout& l, int mode, uint64_t rank) {
 }
 
 __global__ void k_tile_panel(const TileDesc* __restrict__ tiles, uint64_t ntiles, const uint64_t* __restrict__ idx,
-                             const uint32_t* __restrict__ block_base, int x, int y, uint32_t sx, uint64_t mx,
+                             const uint32_t* __restrict__ block_base, int order, int x, int y, uint32_t sx, uint64_t mx,
                              uint32_t sy, uint64_t my, int bx, int by, uint32_t npy, uint32_t* __restrict__ panel) {
   const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
   if (i >= ntiles) return;
   const TileDesc td = tiles[i];
   const uint64_t ix = idx[td.start + td.count / 2];
-  const uint32_t cx = block_base[uint64_t(td.block) * 3 + x] | static_cast<uint32_t>((ix >> sx) & mx);
-  const uint32_t cy = block_base[uint64_t(td.block) * 3 + y] | static_cast<uint32_t>((ix >> sy) & my);
+  const uint32_t cx = block_base[uint64_t(td.block) * order + x] | static_cast<uint32_t>((ix >> sx) & mx);
+  const uint32_t cy = block_base[uint64_t(td.block) * order + y] | static_cast<uint32_t>((ix >> sy) & my);
   const uint32_t px = cx >> bx;
   uint32_t py = cy >> by;
   if (px & 1u) py = npy - 1 - py;  // boustrophedon
@@ -1369,7 +1379,7 @@ const TileDesc* panel_tile_table(const blco_tensor& t, uint32_t tile_elems, int 
     DevBuf<TileDesc> d(n);
     if (n) {
       k_tile_panel<<<static_cast<unsigned>((n + 255) / 256), 256>>>(
-          base, n, t.idx.ptr, t.block_base.ptr, pp.x, pp.y, static_cast<uint32_t>(l.field_shift[pp.x]),
+          base, n, t.idx.ptr, t.block_base.ptr, l.order, pp.x, pp.y, static_cast<uint32_t>(l.field_shift[pp.x]),
           l.field_mask[pp.x], static_cast<uint32_t>(l.field_shift[pp.y]), l.field_mask[pp.y], pp.bx, pp.by, npy,
           d_panel.ptr);
       count_launch();
@@ -1523,7 +1533,7 @@ void launch_cfg(MttkrpLaunch& a) {
         return;
       }
     }
-    if constexpr (N == 3) {
+    if constexpr (N >= 3) {
       if (a.tensor) {  // factors beyond L2: panel-ordered dispatch (panel_plan)
         uint64_t nt = 0;
         if (const TileDesc* pt = panel_tile_table(*a.tensor, kTileElems, a.mode, a.rank, &nt)) p.tiles = pt;
@@ -1618,13 +1628,16 @@ void launch_cfg(MttkrpLaunch& a) {
 }
 
 // ---- the all-mode fused kernel (k_mttkrp_all3): eligibility and launch
-// BLCO_B200_FUSED=0 disables it (per-mode kernels for every step).
+// Opt-in (BLCO_B200_FUSED=1, read per call): measured slower than the three
+// per-mode launches on every eligible shape (B200, interleaved A/B,
+// scripts/fused_ab.py: NELL-2 R=32 8.78 vs 7.28 ms, R=16 4.92 vs 4.74 ms,
+// config 1 0.112 vs 0.091 ms).  Halving the gathers moves the bound to L2:
+// the two ungrouped modes commit one RED per element (~1.9 per element vs
+// 3 x 0.32 for the grouped per-mode kernels), and fp64 REDs are served at a
+// lower L2 rate than loads (ncu: lts 89%, L1 82%).
 bool fused_knob() {
-  static const bool on = [] {
-    const char* e = std::getenv("BLCO_B200_FUSED");
-    return !(e && std::string(e) == "0");
-  }();
-  return on;
+  const char* e = std::getenv("BLCO_B200_FUSED");
+  return e && std::string(e) == "1";
 }
 
 // Order 3, R = 16 / 32, not deterministic, and the three factors plus the

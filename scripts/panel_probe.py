@@ -21,16 +21,18 @@ b.factors_random_device(dims, R, 7, [a.data_ptr() for a in fac], 0)
 flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 s = torch.cuda.current_stream().cuda_stream
 cfg = b.ExecConfig(num_compute_units=148)
+modes = [int(x) for x in os.environ.get("PROBE_MODES", "0,1,2").split(",")]
+reps = int(os.environ.get("PROBE_REPS", "3"))
 ref = [None] * 3
 for st in settings:
     os.environ["BLCO_B200_PANEL"] = st
     tot = 0.0
     row = []
-    for m in range(3):
+    for m in modes:
         out = torch.zeros((dims[m], R), dtype=torch.float64, device="cuda")
         dt.mttkrp_device([a.data_ptr() for a in fac], R, m, out.data_ptr(), b.Strategy.Register, cfg, stream=s)
         ts = []
-        for _ in range(3):
+        for _ in range(reps):
             flush.zero_()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
@@ -41,7 +43,7 @@ for st in settings:
         if ref[m] is None:
             ref[m] = out.clone()
         err = float(torch.linalg.norm(out - ref[m]) / torch.linalg.norm(ref[m]))
-        t = min(ts)
+        t = min(ts) if ts else float('nan')
         tot += t
         row.append(f"m{m} {t:.1f} ms ({err:.0e})")
         del out

@@ -442,10 +442,16 @@ def _fused_worst(gpu, oracle, dims, nnz, rank, tb, cap):
 
 
 @pytest.mark.parametrize("dims,nnz,rank,tb,cap", FUSED_CASES)
-def test_all_modes_fused_kernel(gpu, oracle, dims, nnz, rank, tb, cap):
-    """blco_mttkrp_all_device: the fused all-mode kernel (k_mttkrp_all3: one
-    staging pass, three rows gathered once per element, per-element terms in
-    the oracle's product order) against oracle::mttkrp_coo for every mode."""
+def test_all_modes_fused_kernel(gpu, oracle, monkeypatch, dims, nnz, rank, tb, cap):
+    """blco_mttkrp_all_device with BLCO_B200_FUSED=1: the fused all-mode
+    kernel (k_mttkrp_all3: one staging pass, three rows gathered once per
+    element, per-element terms in the oracle's product order) against
+    oracle::mttkrp_coo for every mode; without the knob the same entry runs
+    the per-mode kernels."""
+    monkeypatch.setenv("BLCO_B200_FUSED", "0")
+    fused, worst = _fused_worst(gpu, oracle, dims, nnz, rank, tb, cap)
+    assert not fused and worst <= TOL
+    monkeypatch.setenv("BLCO_B200_FUSED", "1")
     fused, worst = _fused_worst(gpu, oracle, dims, nnz, rank, tb, cap)
     assert fused
     assert worst <= TOL
@@ -486,26 +492,29 @@ o = Oracle()
 print(max(_fused_worst(b, o, *c)[1] for c in FUSED_CASES))
 """
     r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=600,
-                       env=dict(os.environ, BLCO_B200_FUSED_CFG="u4m2"))
+                       env=dict(os.environ, BLCO_B200_FUSED_CFG="u4m2", BLCO_B200_FUSED="1"))
     assert r.returncode == 0, r.stderr[-2000:]
     assert float(r.stdout.strip().splitlines()[-1]) <= TOL
 
 
-@pytest.mark.parametrize("panel", ["", "10,10", "3,18", "17,2"])
-def test_panel_ordered_dispatch(gpu, oracle, monkeypatch, panel):
-    """Factors beyond L2 (here 307 MB at R = 32): the register kernel runs its
-    tiles in panel order (mttkrp.cu panel_plan: target-mode x shorter
-    non-target-mode panels, ALTO order inside), across keyed blocks and with
-    tiles straddling panel edges, against oracle::mttkrp_coo for every mode.
-    The reordered table is built once per (mode, widths): one k_tile_panel
-    launch beside the MTTKRP on first use, none after."""
+@pytest.mark.parametrize("dims,panel", [
+    ([600_000, 300_000, 300_000], ""), ([600_000, 300_000, 300_000], "10,10"),
+    ([600_000, 300_000, 300_000], "3,18"), ([600_000, 300_000, 300_000], "17,2"),
+    ([300_000, 200_000, 150_000, 50], ""), ([300_000, 200_000, 150_000, 50], "12,9")])
+def test_panel_ordered_dispatch(gpu, oracle, monkeypatch, dims, panel):
+    """Factors beyond L2 (here 166-307 MB at R = 32): the register kernel runs
+    its tiles in panel order (mttkrp.cu panel_plan: target-mode x
+    second-longest non-target-mode panels, ALTO order inside), across keyed
+    blocks and with tiles straddling panel edges, against
+    oracle::mttkrp_coo for every mode.  The reordered table is built once per
+    (mode, widths): one k_tile_panel launch beside the MTTKRP on first use,
+    none after."""
     monkeypatch.setenv("BLCO_B200_PANEL", panel)
-    dims = [600_000, 300_000, 300_000]
     nnz = 400_000
     dt = gpu.DeviceTensor.synthetic(dims, nnz, 11, 48, 90_000)
     idx, vals = oracle.synth_uniform(dims, nnz, 11)
     f = gpu.FactorMatrices.random(dims, 32, 5)
-    for mode in range(3):
+    for mode in range(len(dims)):
         want = oracle.mttkrp_coo(dims, idx, vals, f.factors, mode)
         n0 = gpu.kernel_launch_count()
         got = gpu.mttkrp(dt, f, mode, strategy=gpu.Strategy.Register)
