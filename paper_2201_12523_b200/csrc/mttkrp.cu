@@ -1306,11 +1306,11 @@ struct PanelPlan {
   int bx = 0, by = 0;
 };
 
-PanelPlan panel_plan(const blco_layout& l, int mode, uint64_t rank) {
+PanelPlan panel_plan(const blco_layout& l, int mode, uint64_t rank, uint64_t elem_bytes) {
   PanelPlan p;
   if (l.order < 3 || rank == 0) return p;
   uint64_t bytes = 0;
-  for (int m = 0; m < l.order; ++m) bytes += l.dims[m] * rank * sizeof(double);
+  for (int m = 0; m < l.order; ++m) bytes += l.dims[m] * rank * elem_bytes;
   if (bytes <= (uint64_t(96) << 20)) return p;  // L2-resident working set: ALTO order is already local
   // read per call (only reached by launches over GBs of factors), so a probe
   // can sweep the widths in one process
@@ -1333,7 +1333,7 @@ PanelPlan panel_plan(const blco_layout& l, int mode, uint64_t rank) {
     p.bx = std::atoi(knob.c_str());
     p.by = std::atoi(knob.c_str() + knob.find(',') + 1);
   } else {
-    const uint64_t rows = (budget_mb << 20) / (rank * sizeof(double));
+    const uint64_t rows = (budget_mb << 20) / (rank * elem_bytes);
     int b = 0;
     while ((uint64_t(2) << (b + 1)) <= rows) ++b;  // 2 * 2^b <= rows
     p.bx = p.by = b;
@@ -1362,8 +1362,8 @@ __global__ void k_tile_panel(const TileDesc* __restrict__ tiles, uint64_t ntiles
 // The tile table of t at tile_elems reordered by panel (stable: ALTO order
 // inside a panel), or null when the plan is empty.  Cached with the tensor.
 const TileDesc* panel_tile_table(const blco_tensor& t, uint32_t tile_elems, int mode, uint64_t rank,
-                                 uint64_t* ntiles) {
-  const PanelPlan pp = panel_plan(t.layout, mode, rank);
+                                 uint64_t* ntiles, uint64_t elem_bytes = sizeof(double)) {
+  const PanelPlan pp = panel_plan(t.layout, mode, rank, elem_bytes);
   if (pp.x < 0) return nullptr;
   uint64_t n = 0;
   const TileDesc* base = tile_table(t, tile_elems, &n);
@@ -1762,6 +1762,13 @@ void launch_f32_cfg(const KernelView& v, const float* const* factors, uint64_t r
       count_launch();
       check_launch("k_mttkrp_sorted_f32");
       return;
+    }
+  }
+  if constexpr (N >= 3) {
+    if (v.tensor) {  // factors beyond L2: panel-ordered dispatch (panel_plan)
+      uint64_t nt = 0;
+      if (const TileDesc* pt = panel_tile_table(*v.tensor, kTileElems, mode, rank, &nt, sizeof(float)))
+        p.base.tiles = pt;
     }
   }
   const size_t stage = stage_bytes<N>(kTileElems);

@@ -1,5 +1,5 @@
 """Probe: panel-ordered tile dispatch (mttkrp.cu panel_plan) on an Amazon-shaped
-tensor.  For each BLCO_B200_PANEL setting: per-mode kernel ms (CUDA events,
+(or Delicious-shaped, order 4) tensor.  For each BLCO_B200_PANEL setting: per-mode kernel ms (CUDA events,
 L2 flushed between launches) and the relative difference from the ALTO-order
 result.  Usage: panel_probe.py [amazon|amazon_small] [setting ...]"""
 import os
@@ -9,21 +9,22 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import torch
 import paper_2201_12523_b200 as b
 
-cfgs = {"amazon": ([4821207, 1774269, 1805187], 1_741_809_018, 32),
-        "amazon_small": ([4821207, 1774269, 1805187], 200_000_000, 32),
-        "reddit_dev": ([8211298, 176962, 8116559], 1_000_000_000, 32)}
+cfgs = {"amazon": ([4821207, 1774269, 1805187], 1_741_809_018, 32, 0),
+        "amazon_small": ([4821207, 1774269, 1805187], 200_000_000, 32, 0),
+        "reddit_dev": ([8211298, 176962, 8116559], 1_000_000_000, 32, 0),
+        "delicious": ([532924, 17262471, 2480308, 1443], 140_126_181, 16, 4)}
 name = sys.argv[1] if len(sys.argv) > 1 else "amazon"
 settings = sys.argv[2:] or ["0", "", "16,16", "17,17", "18,17", "17,18", "18,18", "16,18", "18,16"]
-dims, nnz, R = cfgs[name]
-dt = b.DeviceTensor.synthetic(dims, nnz, 42)
+dims, nnz, R, skew = cfgs[name]
+dt = b.DeviceTensor.synthetic_draws(dims, nnz, 42, skew) if skew else b.DeviceTensor.synthetic(dims, nnz, 42)
 fac = [torch.empty((d, R), dtype=torch.float64, device="cuda") for d in dims]
 b.factors_random_device(dims, R, 7, [a.data_ptr() for a in fac], 0)
 flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 s = torch.cuda.current_stream().cuda_stream
 cfg = b.ExecConfig(num_compute_units=148)
-modes = [int(x) for x in os.environ.get("PROBE_MODES", "0,1,2").split(",")]
+modes = [int(x) for x in os.environ.get("PROBE_MODES", ",".join(map(str, range(len(dims))))).split(",")]
 reps = int(os.environ.get("PROBE_REPS", "3"))
-ref = [None] * 3
+ref = [None] * len(dims)
 for st in settings:
     os.environ["BLCO_B200_PANEL"] = st
     tot = 0.0

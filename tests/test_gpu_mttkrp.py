@@ -506,9 +506,9 @@ def test_panel_ordered_dispatch(gpu, oracle, monkeypatch, dims, panel):
     its tiles in panel order (mttkrp.cu panel_plan: target-mode x
     second-longest non-target-mode panels, ALTO order inside), across keyed
     blocks and with tiles straddling panel edges, against
-    oracle::mttkrp_coo for every mode.  The reordered table is built once per
-    (mode, widths): one k_tile_panel launch beside the MTTKRP on first use,
-    none after."""
+    oracle::mttkrp_coo for every mode (fp64 within 1e-12, the fp32 variant
+    within 1e-5).  The reordered table is built once per (mode, widths): one
+    k_tile_panel launch beside the MTTKRP on first use, none after."""
     monkeypatch.setenv("BLCO_B200_PANEL", panel)
     nnz = 400_000
     dt = gpu.DeviceTensor.synthetic(dims, nnz, 11, 48, 90_000)
@@ -523,3 +523,5 @@ def test_panel_ordered_dispatch(gpu, oracle, monkeypatch, dims, panel):
         n2 = gpu.kernel_launch_count()
         assert rel_frobenius(got, want) <= TOL and rel_frobenius(again, want) <= TOL, mode
         assert n2 - n1 == 1 and n1 - n0 == 2, (mode, n1 - n0, n2 - n1)
+        # the fp32 variant takes the same panel order (rows of R * 4 bytes)
+        assert rel_frobenius(gpu.mttkrp_f32(dt, f, mode).astype(np.float64), want) <= 1e-5, mode
