@@ -145,7 +145,9 @@ struct Stage {
   static constexpr int NM = (N + 3) / 4;
   static constexpr bool kPacked = N <= 3;
   static constexpr int kRowPad = 8;  // row plane over-read by the 4-row loads
-  static constexpr bool kRowInRecord = false;
+  // N >= 4: the row word sits in the last uint4 plane, so get() returns it
+  // with the other words (no separate row read per element)
+  static constexpr bool kRowInRecord = !kPacked;
   double* val;     // [W] (general layout)
   uint4* meta;     // general: [NM][W]; packed: records [W]
   uint32_t* rows;  // packed: [W + kRowPad]

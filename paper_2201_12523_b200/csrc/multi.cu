@@ -106,11 +106,21 @@ void check_status(int st) {
   if (st != BLCO_OK) throw Status(st, blco_last_error());
 }
 
+// BLCO_B200_NCCL_SINGLE=1 (read per call): a one-rank communicator still
+// creates an NCCL communicator, so the per-mode collectives run through NCCL
+// (a reduction over one rank is a copy).  It exercises the NCCL path --
+// binding, communicator setup, enqueue on the collective stream, events --
+// on a one-GPU box.
+bool nccl_single() {
+  const char* e = std::getenv("BLCO_B200_NCCL_SINGLE");
+  return e && std::string(e) == "1";
+}
+
 }  // namespace
 }  // namespace b200
 
 // A communicator member: one device of a G-device group.  G = 1 has no NCCL
-// communicator (the reduction is the identity).
+// communicator (the reduction is the identity) unless BLCO_B200_NCCL_SINGLE.
 struct blco_comm {
   int device = 0;
   int nranks = 1;
@@ -183,7 +193,7 @@ void mode_kernel(const RankStep& s, int n) {
 void mode_collective(const RankStep& s, int n) {
   blco_comm& c = *s.comm;
   const uint64_t rows = s.local->layout.dims[n];
-  if (c.nranks == 1) {
+  if (!c.comm) {  // one rank, no NCCL communicator
     if (s.reduce == BLCO_REDUCE_SCATTER && rows && s.shards && s.shards[n] != s.outs[n])
       B200_CUDA(cudaMemcpyAsync(s.shards[n], s.outs[n], rows * s.rank * sizeof(double), cudaMemcpyDeviceToDevice,
                                 c.stream));
@@ -267,9 +277,10 @@ int blco_comm_init_rank(const uint8_t* id, int nranks, int rank, int device, blc
     auto c = std::make_unique<blco_comm>();
     c->device = device, c->nranks = nranks, c->rank = rank;
     c->init_stream();
-    if (nranks > 1) {
+    if (nranks > 1 || nccl_single()) {
       ncclUniqueId u;
-      std::memcpy(&u, id, sizeof u);
+      if (nranks > 1) std::memcpy(&u, id, sizeof u);
+      else nccl_check(nccl().GetUniqueId(&u), "ncclGetUniqueId");  // the lone rank is its own root
       DeviceGuard dg(device);
       nccl_check(nccl().CommInitRank(&c->comm, nranks, u, rank), "ncclCommInitRank");
     }
@@ -281,7 +292,7 @@ int blco_comm_init_all(const int* devices, int ndev, blco_comm** out) {
   return guarded([&] {
     if (ndev < 1) throw_format("comm: need at least one device");
     std::vector<ncclComm_t> raw(ndev, nullptr);
-    if (ndev > 1) nccl_check(nccl().CommInitAll(raw.data(), ndev, devices), "ncclCommInitAll");
+    if (ndev > 1 || nccl_single()) nccl_check(nccl().CommInitAll(raw.data(), ndev, devices), "ncclCommInitAll");
     for (int g = 0; g < ndev; ++g) {
       auto* c = new blco_comm;
       c->device = devices[g], c->nranks = ndev, c->rank = g, c->comm = raw[g];
@@ -430,7 +441,7 @@ int blco_multi_mttkrp_all(blco_multi* m, const double* const* factors, uint64_t 
         if (reduce == BLCO_REDUCE_SCATTER) {
           lo = std::min<uint64_t>(l.dims[n], g * per);
           rows = std::min<uint64_t>(l.dims[n], lo + per) - lo;
-          src = G > 1 ? d[g].shard[n].ptr : d[g].part[n].ptr;
+          src = m->comms[g]->comm ? d[g].shard[n].ptr : d[g].part[n].ptr;  // reduce-scattered, or one rank's partial
         } else if (g > 0) {
           continue;
         }

@@ -92,3 +92,32 @@ def test_library_reuses_the_process_nccl(gpu):
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300,
                        env=dict(os.environ))
     assert r.returncode == 0, r.stderr[-2000:] + r.stdout
+
+
+@pytest.mark.parametrize("reduce", ["allreduce", "reducescatter"])
+def test_nccl_collectives_on_one_rank(gpu, case, monkeypatch, reduce):
+    """BLCO_B200_NCCL_SINGLE=1: the one-rank communicator and the one-device
+    driver create real NCCL communicators (ncclGetUniqueId +
+    ncclCommInitRank, ncclCommInitAll), so each mode's ncclReduceScatter /
+    ncclAllReduce is enqueued on the collective stream behind the mode
+    kernel's event -- the multi-GPU code path run over NCCL on a one-GPU box
+    (a reduction over one rank is a copy)."""
+    import torch
+    monkeypatch.setenv("BLCO_B200_NCCL_SINGLE", "1")
+    dt, f, want = case
+    comm = gpu.Communicator(None, 1, 0, 0)
+    fac = [torch.from_numpy(a).cuda() for a in f.factors]
+    outs = [torch.full((d, RANK), 7.0, dtype=torch.float64, device="cuda") for d in DIMS]
+    shards = [torch.full((d, RANK), -1.0, dtype=torch.float64, device="cuda") for d in DIMS]
+    s = torch.cuda.Stream()
+    for _ in range(2):  # the communicator is reused across steps
+        comm.mttkrp_all(dt, [a.data_ptr() for a in fac], RANK, [o.data_ptr() for o in outs],
+                        [x.data_ptr() for x in shards], reduce=reduce, stream=s.cuda_stream)
+        s.synchronize()
+        res = shards if reduce == "reducescatter" else outs
+        for m in range(3):
+            assert rel_frobenius(res[m].cpu().numpy(), want[m]) <= 1e-12, (reduce, m)
+    mt = gpu.MultiDeviceTensor(dt, [0])
+    got = mt.mttkrp_all_modes(f, reduce=reduce)
+    for m in range(3):
+        assert rel_frobenius(got[m], want[m]) <= 1e-12, (reduce, m)
