@@ -312,16 +312,40 @@ __global__ void k_small_fit(const double* __restrict__ grams, int N, int R, cons
 // Fused epilogue pass 2: A /= lambda column-wise (cpals.cpp:59-60) and, for
 // the last mode, the fit's <X, Xhat> = sum m[i,r] lambda[r] A[i,r]
 // (cpals.cpp:36-44) on the normalised A.
+// V2: even R and 16-byte aligned rows, two columns per thread with 16-byte
+// loads and stores (the pass is HBM-bound: 2 or 3 x I_n x R x 8 bytes).
+template <bool V2>
 __global__ void k_scale_inner(double* __restrict__ a, uint64_t rows, int R, const double* __restrict__ lambda,
                               const double* __restrict__ m, double* __restrict__ inner) {
+  __shared__ double rl[64], il[64];  // lambda and 1 / lambda (R <= 64)
+  for (int r = threadIdx.x; r < R; r += blockDim.x) rl[r] = lambda[r], il[r] = 1.0 / lambda[r];
+  __syncthreads();
   const uint64_t n = rows * R;
   double s = 0.0;
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
-       i += uint64_t(gridDim.x) * blockDim.x) {
-    const double l = lambda[(R & (R - 1)) == 0 ? i & (R - 1) : i % R];
-    const double x = a[i] * (1.0 / l);
-    a[i] = x;
-    if (m) s += m[i] * l * x;
+  if constexpr (V2) {
+    double2* a2 = reinterpret_cast<double2*>(a);
+    const double2* m2 = reinterpret_cast<const double2*>(m);
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n / 2;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+      const int c = static_cast<int>((R & (R - 1)) == 0 ? (2 * i) & (R - 1) : (2 * i) % R);
+      double2 x = a2[i];
+      x.x = x.x * il[c];
+      x.y = x.y * il[c + 1];
+      a2[i] = x;
+      if (m) {
+        const double2 y = m2[i];
+        s += y.x * rl[c] * x.x;
+        s += y.y * rl[c + 1] * x.y;
+      }
+    }
+  } else {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+      const int c = static_cast<int>((R & (R - 1)) == 0 ? i & (R - 1) : i % R);
+      const double x = a[i] * il[c];
+      a[i] = x;
+      if (m) s += m[i] * rl[c] * x;
+    }
   }
   if (!m) return;
   s = block_sum(s);
@@ -518,9 +542,12 @@ struct Dense {
     check_launch("k_small_norm");
     if (m_inner) B200_CUDA(cudaMemsetAsync(dinner, 0, sizeof(double), s));
     if (rows) {
-      const unsigned grid = grid_of(rows * R);
+      const bool v2 = R % 2 == 0 && reinterpret_cast<uintptr_t>(a) % 16 == 0 &&
+                      reinterpret_cast<uintptr_t>(m_inner) % 16 == 0;
+      const unsigned grid = grid_of(v2 ? rows * R / 2 : rows * R);
       double* part = m_inner ? slots(grid) : nullptr;
-      k_scale_inner<<<grid, kT, 0, s>>>(a, rows, R, dlam, m_inner, part);
+      if (v2) k_scale_inner<true><<<grid, kT, 0, s>>>(a, rows, R, dlam, m_inner, part);
+      else k_scale_inner<false><<<grid, kT, 0, s>>>(a, rows, R, dlam, m_inner, part);
       count_launch();
       check_launch("k_scale_inner");
       if (m_inner) {

@@ -1343,6 +1343,8 @@ PanelPlan panel_plan(const blco_layout& l, int mode, uint64_t rank, uint64_t ele
   if (p.bx <= 0 || p.by <= 0 || p.bx > 31 || p.by > 31 ||
       (l.dims[p.x] <= (uint64_t(1) << p.bx) && l.dims[p.y] <= (uint64_t(1) << p.by)))
     return PanelPlan{};  // one panel: nothing to reorder
+  const uint64_t npanels = (((l.dims[p.x] - 1) >> p.bx) + 1) * (((l.dims[p.y] - 1) >> p.by) + 1);
+  if (npanels > (uint64_t(1) << 26)) return PanelPlan{};  // widths far too narrow: keep ALTO order
   return p;
 }
 
