@@ -309,9 +309,14 @@ def traffic_probe_worker(args):
     import torch
 
     import paper_2201_12523_b200 as b
-    dims, nnz, R, _ = CONFIGS[args.config]
-    torch.cuda.set_device(0)
-    dt = b.DeviceTensor.synthetic(dims, nnz, TENSOR_SEED, device=0)
+    if args.config in ALS_CONFIGS:  # the CP-ALS config's MTTKRP kernels (power-law draws)
+        dims, nnz, R, skew, _ = ALS_CONFIGS[args.config]
+        torch.cuda.set_device(0)
+        dt = b.DeviceTensor.synthetic_draws(dims, nnz, TENSOR_SEED, skew, 64, 1 << 27, 0)
+    else:
+        dims, nnz, R, _ = CONFIGS[args.config]
+        torch.cuda.set_device(0)
+        dt = b.DeviceTensor.synthetic(dims, nnz, TENSOR_SEED, device=0)
     fac = [torch.empty((d, R), dtype=torch.float64, device="cuda:0") for d in dims]
     sptr = torch.cuda.current_stream().cuda_stream
     b.factors_random_device(dims, R, FACTOR_SEED, [a.data_ptr() for a in fac], sptr)
@@ -932,6 +937,10 @@ def run_cpals(args, world=1, rank_id=0, local=0):
     dims, nnz, R, skew, desc = ALS_CONFIGS[args.config]
     N = len(dims)
     dev = local
+    # DRAM bytes per MTTKRP launch of this build (ncu child process, before
+    # this process allocates anything), as run_ours
+    traffic = (world == 1 and not args.no_ncu and live_traffic(args.config)) or (
+        committed_traffic("delicious") if args.config == "delicious_als" else None)
     torch.cuda.set_device(dev)
     if world > 1:
         dist_init(torch, dev)
@@ -1004,7 +1013,6 @@ def run_cpals(args, world=1, rank_id=0, local=0):
         mode_ms.append(a0.elapsed_time(a1) / 5)
     bpe = bytes_per_elem(N, R)
     peak, peak_source = hbm_peak()
-    traffic = committed_traffic("delicious") if args.config == "delicious_als" else None
     roofline = roofline_entry(traffic, statistics.mean(mode_ms), dt.nnz * bpe, peak, peak_source,
                               "k_mttkrp_sorted (one launch per mode, final factors)")
     launches = b.kernel_launch_count() - launches0

@@ -65,8 +65,19 @@ __device__ __forceinline__ double lget(const double* sl, int R, int i, int k) {
   else return sl[i * R + k];
 }
 
+// RM = 16: capped at 168 registers so three CTAs fit per SM (shared memory
+// allows three); uncapped, ptxas takes 254 and two fit (ncu on the 17.3M-row
+// Delicious mode: 12.5% occupancy, issue-latency bound on the DFMA chains).
+#ifndef BLCO_SOLVE16_MINB
+#define BLCO_SOLVE16_MINB 3
+#endif
+template <int RM>
+constexpr int solve_min_blocks() {
+  return RM == 16 ? BLCO_SOLVE16_MINB : BLCO_SOLVE_MINB;
+}
+
 template <int RM, bool EXACT>
-__global__ void __launch_bounds__(kSolveThreads, BLCO_SOLVE_MINB) k_solve_gram(const double* __restrict__ m, double* __restrict__ a,
+__global__ void __launch_bounds__(kSolveThreads, solve_min_blocks<RM>()) k_solve_gram(const double* __restrict__ m, double* __restrict__ a,
                                                               uint64_t rows, int R, const double* __restrict__ L,
                                                               double* __restrict__ g) {
   constexpr int ROWS = solve_rows<RM>();
