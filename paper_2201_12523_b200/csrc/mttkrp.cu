@@ -1516,6 +1516,8 @@ void launch_cfg(MttkrpLaunch& a) {
         // 2048-element tiles (see k_mttkrp_sorted)
         constexpr int T2 = 2 * kTileElems;
         p.tiles = tile_table(*a.tensor, T2, &p.ntiles);
+        uint64_t nt = 0;
+        if (const TileDesc* pt = panel_tile_table(*a.tensor, T2, a.mode, a.rank, &nt)) p.tiles = pt;
         a.workgroups = p.ntiles;
         auto kern = stats ? k_mttkrp_sorted<N, LPE, CPL, FULL, true, kUnroll, 1, T2>
                           : k_mttkrp_sorted<N, LPE, CPL, FULL, false, kUnroll, 3, T2>;  // <= 80 regs: 3 CTAs/SM (91 -> 2)
