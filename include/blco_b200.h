@@ -297,6 +297,13 @@ int blco_mttkrp_device(const blco_tensor* t, const double* const* d_factors, uin
  * factors + outputs within 64 MB, one fused kernel stages each element once
  * and gathers its three rows once for all three modes (k_mttkrp_all3;
  * per-element terms in the oracle's order).  *fused (optional) says which. */
+/* CTA dispatch order of the register kernel for `mode` (B200 extension,
+ * mttkrp.cu panel_plan): when the factors exceed L2 the tiles run in panels
+ * of 2^bx target rows x 2^by rows of mode *y_mode, ALTO order inside a panel;
+ * *y_mode = -1 when they run in plain ALTO order.  elem_bytes = 8 (fp64) or
+ * 4 (the fp32 variant).  Reads BLCO_B200_PANEL / BLCO_B200_PANEL_MB. */
+int blco_panel_plan(const blco_layout* layout, int mode, uint64_t rank, uint64_t elem_bytes, int* y_mode, int* bx,
+                    int* by);
 int blco_mttkrp_all_device(const blco_tensor* t, const double* const* d_factors, uint64_t rank, int strategy,
                            const blco_exec_config* cfg, double* const* d_outs, int accumulate, void* stream,
                            int* fused);

@@ -9,7 +9,8 @@ from .api import (  # noqa: F401
     AllModesReport, MttkrpStats, SparseTensorCoo, SplitIndex, Strategy, StreamReport, VerifyError, build_blco,
     choose_strategy, compute_batch_table, cp_als, delinearize, device_count, encode_coords,
     factors_random_device, fit, interleaved_remainder, kernel_launch_count, linearize, release_thread_caches,
-    load_blco, make_layout, merge_copies, mttkrp, mttkrp_all_modes, mttkrp_f32, partition, read_blco_header, save_blco,
+    load_blco, make_layout, merge_copies, mttkrp, mttkrp_all_modes, mttkrp_f32, panel_plan, partition, read_blco_header,
+    save_blco,
     split_block_key, stream_mttkrp, stream_mttkrp_all_modes,
     synth_draws_host, synth_uniform_host, throughput_report, Communicator, MultiDeviceTensor, MultiReport,
     nccl_version)

@@ -150,6 +150,7 @@ SIGNATURES = {
     "blco_exec_config_default": (None, [C.POINTER(ExecCfg)]),
     "blco_exec_config_validate": (_I, [C.POINTER(ExecCfg)]),
     "blco_choose_strategy": (_I, [_U64, C.POINTER(ExecCfg)]),
+    "blco_panel_plan": (_I, [C.POINTER(Layout), _I, _U64, _U64, C.POINTER(_I), C.POINTER(_I), C.POINTER(_I)]),
     "blco_build": (_I, [_PU64, _I, _U64, _PU64, _PD, _I, _U64, _I, C.POINTER(_P),
                         C.POINTER(BuildStats)]),
     "blco_build_synthetic": (_I, [_PU64, _I, _U64, _U64, _I, _U64, _I, C.POINTER(_P),

@@ -196,6 +196,15 @@ def make_layout(dims: Sequence[int], target_bits: int = 64) -> BitLayout:
     return BitLayout(c)
 
 
+def panel_plan(layout: BitLayout, mode: int, rank: int, elem_bytes: int = 8) -> tuple[int, int, int] | None:
+    """The register kernel's CTA dispatch order for `mode` (blco_panel_plan,
+    B200 extension): (y_mode, bx, by) -- panels of 2^bx target rows x 2^by
+    rows of y_mode, ALTO order inside -- or None for plain ALTO order."""
+    y, bx, by = C.c_int(), C.c_int(), C.c_int()
+    _check(lib.blco_panel_plan(C.byref(layout._c), mode, rank, elem_bytes, C.byref(y), C.byref(bx), C.byref(by)))
+    return None if y.value < 0 else (y.value, bx.value, by.value)
+
+
 def linearize(layout: BitLayout, coords: Sequence[int]) -> int:
     if len(coords) != layout.order():
         raise FormatError("linearize: coordinate count does not match order")

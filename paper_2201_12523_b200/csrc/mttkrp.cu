@@ -1900,6 +1900,19 @@ using namespace b200;
 
 extern "C" {
 
+int blco_panel_plan(const blco_layout* layout, int mode, uint64_t rank, uint64_t elem_bytes, int* y_mode, int* bx,
+                    int* by) {
+  return guarded([&] {
+    if (!layout || !y_mode || !bx || !by) throw_format("panel_plan: null argument");
+    if (mode < 0 || mode >= layout->order) throw_format("mttkrp: mode out of range");
+    if (elem_bytes != 4 && elem_bytes != 8) throw_format("panel_plan: elem_bytes must be 4 or 8");
+    const PanelPlan p = panel_plan(*layout, mode, rank, elem_bytes);
+    *y_mode = p.x < 0 ? -1 : p.y;
+    *bx = p.bx;
+    *by = p.by;
+  });
+}
+
 int blco_mttkrp_device(const blco_tensor* t, const double* const* d_factors, uint64_t rank,
                        int mode, int strategy, const blco_exec_config* cfg, double* d_out,
                        int accumulate, void* stream, blco_mttkrp_stats* stats) {

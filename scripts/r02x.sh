@@ -1,0 +1,15 @@
+# round 2: every other BASELINE configuration with the current build, their reference arms,
+# and ncu --set full captures of the mode kernels (Amazon with panels, NELL-2, Delicious)
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 900 python bench.py --config cfg1 > gpurun_out/r02x_cfg1.json 2> gpurun_out/r02x_cfg1.err
+timeout 900 python bench.py --config nell2 > gpurun_out/r02x_nell2.json 2> gpurun_out/r02x_nell2.err
+timeout 900 python bench.py --config delicious_als > gpurun_out/r02x_als.json 2> gpurun_out/r02x_als.err
+timeout 2400 python bench.py --config reddit_stream > gpurun_out/r02x_stream.json 2> gpurun_out/r02x_stream.err
+for c in nell2 delicious_als reddit_stream; do
+  timeout 900 python bench.py --impl reference --config $c --steps 2 --warmup 1 > gpurun_out/r02x_reference_$c.json 2> /dev/null
+done
+PROBE_MODES=0,1,2 PROBE_REPS=0 timeout 1200 ncu --set full --import-source on --clock-control none -k regex:k_mttkrp_sorted -o gpurun_out/r02x_prof_amazon python scripts/panel_probe.py amazon "" > /dev/null 2>&1
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_mttkrp_sorted -s 4 -c 3 -o gpurun_out/r02x_prof_nell2 python bench.py --config nell2 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-fp32 --no-ncu > /dev/null 2>&1
+PROBE_REPS=0 timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_mttkrp_sorted -o gpurun_out/r02x_prof_delicious python scripts/panel_probe.py delicious "" > /dev/null 2>&1
+ls -la gpurun_out/r02x*

@@ -208,3 +208,34 @@ def test_container_stream_hooks_match_reference_bytes(blco, reflib):
         st = L.lib.blco_container_read_header(reader(bad), None, C.byref(h))
         assert st != 0 and msg in L.lib.blco_last_error(), (msg, L.lib.blco_last_error())
 
+
+
+def test_panel_plan(blco, monkeypatch):
+    """The register kernel's dispatch order (mttkrp.cu panel_plan, host
+    logic): ALTO order while the factors fit in L2; beyond it, panels of the
+    target mode x the second-longest non-target mode (the longest streams),
+    2 * 2^b rows within BLCO_B200_PANEL_MB (32 MB) of L2; the knob's
+    overrides and the fallbacks."""
+    amazon = blco.make_layout([4821207, 1774269, 1805187])
+    monkeypatch.delenv("BLCO_B200_PANEL", raising=False)
+    monkeypatch.delenv("BLCO_B200_PANEL_MB", raising=False)
+    assert blco.panel_plan(amazon, 0, 32) == (1, 16, 16)  # Z = mode 2 (1805187 > 1774269)
+    assert blco.panel_plan(amazon, 2, 32) == (1, 16, 16)  # Z = mode 0
+    assert blco.panel_plan(amazon, 1, 32) == (2, 16, 16)
+    assert blco.panel_plan(amazon, 0, 16) == (1, 17, 17)  # 128-byte rows
+    assert blco.panel_plan(amazon, 0, 32, 4) == (1, 17, 17)  # fp32 rows
+    assert blco.panel_plan(blco.make_layout([12092, 9184, 28818]), 0, 32) is None  # NELL-2: L2-resident
+    delicious = blco.make_layout([532924, 17262471, 2480308, 1443])
+    assert blco.panel_plan(delicious, 1, 16) == (0, 17, 17)  # Z = mode 2, mode 3 stays in L2
+    assert blco.panel_plan(delicious, 3, 16) == (2, 17, 17)  # Z = mode 1, Y = mode 2
+    assert blco.panel_plan(blco.make_layout([5000, 6000]), 0, 32) is None  # order 2
+    monkeypatch.setenv("BLCO_B200_PANEL_MB", "64")
+    assert blco.panel_plan(amazon, 0, 32) == (1, 17, 17)
+    monkeypatch.setenv("BLCO_B200_PANEL", "12,9")
+    assert blco.panel_plan(amazon, 0, 32) == (1, 12, 9)
+    monkeypatch.setenv("BLCO_B200_PANEL", "2,2")  # 2^36 panels: keep ALTO order
+    assert blco.panel_plan(amazon, 0, 32) is None
+    monkeypatch.setenv("BLCO_B200_PANEL", "0")
+    assert blco.panel_plan(amazon, 0, 32) is None
+    with pytest.raises(blco.FormatError):
+        blco.panel_plan(amazon, 3, 32)
