@@ -391,7 +391,7 @@ def committed_traffic(config: str) -> dict | None:
         rep = json.loads(prof.read_text())
     except (OSError, ValueError):
         return None
-    ls = rep.get("launches") or []
+    ls = [x for x in rep.get("launches") or [] if x.get("dram_bytes") == x.get("dram_bytes")]  # drop NaN replays
     if not ls:
         return None
     mean = lambda k: statistics.mean(float(x.get(k, 0) or 0) for x in ls)  # noqa: E731
