@@ -774,6 +774,7 @@ void finalize_tensor(blco_tensor& t) {
   std::lock_guard<std::mutex> g(t.mu);
   t.tiles.clear();
   t.panel_tiles.clear();
+  t.span_bits.clear();
   t.det.clear();
 }
 

@@ -189,6 +189,9 @@ struct blco_tensor {
   // panel-ordered tile tables (mttkrp.cu panel_tile_table), keyed by
   // tile size, mode and panel widths
   mutable std::map<uint64_t, b200::DevBuf<b200::TileDesc>> panel_tiles;
+  // per tile size: the largest coordinate span (bits) of each mode over the
+  // tiles (mttkrp.cu tile_span_bits, sizes the StageR record fields)
+  mutable std::map<uint32_t, std::vector<uint32_t>> span_bits;
   // deterministic-mode indices keyed by mode, built lazily
   mutable std::map<int, b200::DetIndex> det;
 

@@ -128,6 +128,10 @@ struct Params {
   // [segments, stash flushes, commit lanes, processing-phase cycles (per
   // CTA), computing-phase cycles (per warp)] or null
   unsigned long long* counters;
+  // StageR: bit offset and mask of each word slot (non-target modes
+  // ascending, the row last) in the packed 64-bit record field
+  uint32_t pk_off[N];
+  uint32_t pk_mask[N];
 };
 
 // ------------------------------------------------------------ staging layout
@@ -233,6 +237,51 @@ struct StageC {
   }
   __device__ __forceinline__ uint32_t row(int j) const { return reinterpret_cast<const uint32_t*>(meta)[4 * j + 3]; }
 };
+
+// Tile-relative compact staging for any order: one 16-byte record {value,
+// packed} per element, packed = sum_k (w_k - cmin_k) << off_k over the word
+// slots (non-target modes ascending, the row last), where cmin is the tile's
+// minimum of each slot (reduced in process_cta) and off/mask come from the
+// launch (Params::pk_off / pk_mask: the largest span of every mode over the
+// tensor's tiles, tile_span_bits; used when they sum to <= 64 bits).
+// Replaces the 20-24 bytes of Stage<N> for wide N = 3 modes (Amazon) and
+// N >= 4 (Delicious: a value plane plus a uint4 plane) by one LDS.128 per
+// element with the row inside.  get()/row() return the slots RELATIVE to
+// cmin; the computing phase folds cmin into its lane base pointers.
+template <int N>
+struct StageR {
+  static constexpr bool kPacked = true;
+  static constexpr bool kRowInRecord = true;
+  uint4* meta;
+  const uint32_t* cmin;  // [N] in shared memory, valid after process_cta
+  uint32_t off[N], msk[N];
+  __device__ __forceinline__ void put_rel(int j, double v, const uint32_t* w, const uint32_t (&cm)[N]) const {
+    uint64_t pk = 0;
+#pragma unroll
+    for (int k = 0; k < N; ++k) pk |= static_cast<uint64_t>(w[k] - cm[k]) << off[k];
+    const uint64_t b = static_cast<uint64_t>(__double_as_longlong(v));
+    meta[j] = make_uint4(static_cast<uint32_t>(b), static_cast<uint32_t>(b >> 32), static_cast<uint32_t>(pk),
+                         static_cast<uint32_t>(pk >> 32));
+  }
+  template <int NW>
+  __device__ __forceinline__ void get(int j, double& v, uint32_t (&w)[NW]) const {
+    const uint4 x = meta[j];
+    v = __longlong_as_double(static_cast<long long>((static_cast<uint64_t>(x.y) << 32) | x.x));
+    const uint64_t pk = (static_cast<uint64_t>(x.w) << 32) | x.z;
+#pragma unroll
+    for (int k = 0; k < N; ++k) w[k] = static_cast<uint32_t>(pk >> off[k]) & msk[k];
+  }
+  __device__ __forceinline__ uint32_t row(int j) const {
+    const uint4 x = meta[j];
+    const uint64_t pk = (static_cast<uint64_t>(x.w) << 32) | x.z;
+    return static_cast<uint32_t>(pk >> off[N - 1]) & msk[N - 1];
+  }
+};
+
+template <class ST>
+struct is_relative : std::false_type {};
+template <int N>
+struct is_relative<StageR<N>> : std::true_type {};
 
 // Decodes one element into packed words (non-target modes ascending, row last).
 template <int N>
@@ -409,7 +458,12 @@ __device__ __forceinline__ void compute_range_fast(const Params<N>& p, const ST 
   const double* fb[NO];
 #pragma unroll
   for (int k = 0; k < N - 1; ++k) fb[k] = p.factors[k] + q;
-  double* const ob = out + q;
+  double* ob = out + q;
+  if constexpr (is_relative<ST>::value) {  // StageR slots are relative to the tile's minimum
+#pragma unroll
+    for (int k = 0; k < N - 1; ++k) fb[k] += static_cast<uint64_t>(st.cmin[k]) * RF;
+    ob += static_cast<uint64_t>(st.cmin[N - 1]) * RF;
+  }
   double acc[CPL];
 #pragma unroll
   for (int c = 0; c < CPL; ++c) acc[c] = 0.0;
@@ -575,15 +629,19 @@ constexpr int kBuckets = 1 << kBucketBits;
 struct BucketShared {
   uint32_t cnt[kBuckets];
   uint32_t warp_sum[kWarps];
+  uint32_t cmin[8];  // StageR: the tile's minimum of each word slot
 };
 
 template <int N, int TILE = kTileElems, class ST = Stage<N>>
 __device__ __forceinline__ uint32_t process_cta(const Params<N>& p, const TileDesc& td, const ST st,
                                                 BucketShared& bs, unsigned long long& segs) {
   constexpr int kItems = TILE / kCtaThreads;  // elements per thread
+  constexpr bool REL = is_relative<ST>::value;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t cnt = tile_count(td, p.elem_end);
   for (int i = tid; i < kBuckets; i += kCtaThreads) bs.cnt[i] = 0;
+  if constexpr (REL)
+    if (tid < N) bs.cmin[tid] = 0xffffffffu;
   uint32_t base[N];
 #pragma unroll
   for (int m = 0; m < N; ++m) base[m] = __ldg(p.block_base + static_cast<uint64_t>(td.block) * N + m);
@@ -603,6 +661,17 @@ __device__ __forceinline__ uint32_t process_cta(const Params<N>& p, const TileDe
     decode<N>(p, base, ix[i], w[i]);
     const uint32_t e = tid + i * kCtaThreads;
     rank[i] = e < cnt ? atomicAdd(&bs.cnt[w[i][N - 1] & (kBuckets - 1)], 1u) : 0;
+  }
+  if constexpr (REL) {  // the tile's minimum of each word slot (StageR)
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      uint32_t m = 0xffffffffu;
+#pragma unroll
+      for (int i = 0; i < kItems; ++i)
+        if (tid + i * kCtaThreads < cnt) m = min(m, w[i][k]);
+      m = __reduce_min_sync(kFull, m);
+      if (lane == 0) atomicMin(&bs.cmin[k], m);
+    }
   }
   __syncthreads();
   // exclusive scan of the histogram: thread t owns buckets [8t, 8t+8)
@@ -628,10 +697,21 @@ __device__ __forceinline__ uint32_t process_cta(const Params<N>& p, const TileDe
 #pragma unroll
   for (int i = 0; i < per; ++i) bs.cnt[tid * per + i] = toff + loc[i];
   __syncthreads();
+  if constexpr (REL) {
+    uint32_t cm[N];
 #pragma unroll
-  for (int i = 0; i < kItems; ++i) {
-    const uint32_t e = tid + i * kCtaThreads;
-    if (e < cnt) st.put(static_cast<int>(bs.cnt[w[i][N - 1] & (kBuckets - 1)] + rank[i]), vv[i], w[i]);
+    for (int k = 0; k < N; ++k) cm[k] = bs.cmin[k];
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) {
+      const uint32_t e = tid + i * kCtaThreads;
+      if (e < cnt) st.put_rel(static_cast<int>(bs.cnt[w[i][N - 1] & (kBuckets - 1)] + rank[i]), vv[i], w[i], cm);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) {
+      const uint32_t e = tid + i * kCtaThreads;
+      if (e < cnt) st.put(static_cast<int>(bs.cnt[w[i][N - 1] & (kBuckets - 1)] + rank[i]), vv[i], w[i]);
+    }
   }
   __syncthreads();
   if (segs != ~0ull) {  // count runs (stats only)
@@ -678,16 +758,26 @@ __device__ __forceinline__ Stage<N> cta_stage(unsigned char* dyn) {
 // segments, so fewer commits, and the per-tile fixed costs halve; NELL-2
 // 8.29 -> 7.96 ms/iter).  DRAM-bound shapes (Amazon) and small tensors
 // (fewer tiles than resident CTA slots) keep 1024.
+// CMP (stage kind): 0 = Stage<N>, 1 = StageC (N = 3, absolute 16-bit
+// coordinates), 2 = StageR<N> (tile-relative packed record)
 template <int N, int LPE, int CPL, bool FULL, bool STATS, int U = kUnroll, int MINB = 1, int TILE = kTileElems,
-          bool CMP = false>
+          int CMP = 0>
 __global__ void __launch_bounds__(kCtaThreads, MINB) k_mttkrp_sorted(Params<N> p) {
   constexpr int WE = TILE / kWarps;  // staged positions per warp
-  using ST = std::conditional_t<CMP, StageC, Stage<N>>;
+  using ST = std::conditional_t<CMP == 1, StageC, std::conditional_t<CMP == 2, StageR<N>, Stage<N>>>;
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ BucketShared bs;
   ST st;
-  if constexpr (CMP) st = StageC{reinterpret_cast<uint4*>(dyn)};
-  else st = cta_stage<N, TILE>(dyn);
+  if constexpr (CMP == 1) {
+    st = StageC{reinterpret_cast<uint4*>(dyn)};
+  } else if constexpr (CMP == 2) {
+    st.meta = reinterpret_cast<uint4*>(dyn);
+    st.cmin = bs.cmin;
+#pragma unroll
+    for (int k = 0; k < N; ++k) st.off[k] = p.pk_off[k], st.msk[k] = p.pk_mask[k];
+  } else {
+    st = cta_stage<N, TILE>(dyn);
+  }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const TileDesc td = p.tiles[blockIdx.x];
   unsigned long long segs = STATS ? 0 : ~0ull, commits = 0, flushes = 0;
@@ -699,7 +789,7 @@ __global__ void __launch_bounds__(kCtaThreads, MINB) k_mttkrp_sorted(Params<N> p
   if (wn > 0) {
     if constexpr (FULL && U == 4)  // lean phase for every order (N >= 4: general stage, no 4-row loads)
       compute_range_fast<N, LPE, CPL, U, ST>(p, st, lo0, wn, lane, p.out, commits);
-    else if constexpr (!CMP)
+    else if constexpr (CMP == 0)
       compute_range<N, LPE, CPL, FULL, false, U>(p, st, lo0, wn, lane, blockIdx.y * LPE * CPL, p.out, nullptr,
                                               nullptr, commits, flushes);
   }
@@ -1405,6 +1495,98 @@ const TileDesc* panel_tile_table(const blco_tensor& t, uint32_t tile_elems, int 
   return it->second.ptr;
 }
 
+// ---- StageR field widths: the largest per-mode span over the tiles
+struct SpanParams {
+  uint32_t shift[BLCO_MAX_DEV_ORDER];
+  uint64_t mask[BLCO_MAX_DEV_ORDER];
+};
+
+__global__ void __launch_bounds__(256) k_tile_spans(const TileDesc* __restrict__ tiles,
+                                                    const uint64_t* __restrict__ idx,
+                                                    const uint32_t* __restrict__ block_base, int order, SpanParams sp,
+                                                    uint32_t* __restrict__ bits_out) {
+  __shared__ uint32_t lo[BLCO_MAX_DEV_ORDER], hi[BLCO_MAX_DEV_ORDER];
+  const TileDesc td = tiles[blockIdx.x];
+  if (threadIdx.x < BLCO_MAX_DEV_ORDER) lo[threadIdx.x] = 0xffffffffu, hi[threadIdx.x] = 0;
+  __syncthreads();
+  for (int m = 0; m < order; ++m) {
+    const uint32_t base = block_base[uint64_t(td.block) * order + m];
+    uint32_t mn = 0xffffffffu, mx = 0;
+    for (uint32_t i = threadIdx.x; i < td.count; i += blockDim.x) {
+      const uint32_t c = base | static_cast<uint32_t>((idx[td.start + i] >> sp.shift[m]) & sp.mask[m]);
+      mn = min(mn, c);
+      mx = max(mx, c);
+    }
+    mn = __reduce_min_sync(kFull, mn);
+    mx = __reduce_max_sync(kFull, mx);
+    if ((threadIdx.x & 31) == 0) {
+      atomicMin(&lo[m], mn);
+      atomicMax(&hi[m], mx);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < order && td.count) {
+    const uint32_t span = hi[threadIdx.x] - lo[threadIdx.x];
+    atomicMax(&bits_out[threadIdx.x], span ? 32u - __clz(span) : 0u);
+  }
+}
+
+// Per mode, the bits of the largest coordinate span (max - min) inside one
+// tile of tile_elems elements; cached with the tensor.
+std::vector<uint32_t> tile_span_bits(const blco_tensor& t, uint32_t tile_elems) {
+  uint64_t n = 0;
+  const TileDesc* tiles = tile_table(t, tile_elems, &n);
+  std::lock_guard<std::mutex> g(t.mu);
+  auto it = t.span_bits.find(tile_elems);
+  if (it == t.span_bits.end()) {
+    const blco_layout& l = t.layout;
+    std::vector<uint32_t> bits(l.order, 0);
+    if (n) {
+      SpanParams sp{};
+      for (int m = 0; m < l.order; ++m) sp.shift[m] = static_cast<uint32_t>(l.field_shift[m]), sp.mask[m] = l.field_mask[m];
+      ScratchScope keep(false);
+      DevBuf<uint32_t> d(BLCO_MAX_DEV_ORDER);
+      B200_CUDA(cudaMemset(d.ptr, 0, BLCO_MAX_DEV_ORDER * sizeof(uint32_t)));
+      for (uint64_t b0 = 0; b0 < n; b0 += (uint64_t(1) << 30)) {
+        const unsigned g = static_cast<unsigned>(std::min<uint64_t>(n - b0, uint64_t(1) << 30));
+        k_tile_spans<<<g, 256>>>(tiles + b0, t.idx.ptr, t.block_base.ptr, l.order, sp, d.ptr);
+        count_launch();
+        check_launch("k_tile_spans");
+      }
+      B200_CUDA(cudaMemcpy(bits.data(), d.ptr, l.order * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    }
+    it = t.span_bits.emplace(tile_elems, std::move(bits)).first;
+  }
+  return it->second;
+}
+
+// BLCO_B200_REL_STAGE=1 (read per call) enables the StageR record.  Opt-in:
+// measured slower on B200 in interleaved A/B runs (scripts/panel_probe.py
+// with the knob; Amazon 374-376 vs 357-368 ms per all-mode step, Delicious
+// 22.3-23.3 vs 20.0-21.9 ms): the LDS wavefronts it saves (~0.3-0.7 per
+// element) cost more in the per-element unpacking, the tile-minimum
+// reduction and the register cap (80 / 64) than they return.
+bool rel_stage_knob() {
+  const char* e = std::getenv("BLCO_B200_REL_STAGE");
+  return e && std::string(e) == "1";
+}
+
+// StageR field layout of a launch: slot k = the k-th non-target mode
+// (p.others), the row last; false when the spans need more than 64 bits.
+template <int N>
+bool rel_stage_plan(const blco_tensor* t, uint32_t tile_elems, Params<N>& p) {
+  if (!t || !rel_stage_knob()) return false;
+  const std::vector<uint32_t> bits = tile_span_bits(*t, tile_elems);
+  uint32_t off = 0;
+  for (int k = 0; k < N; ++k) {
+    const uint32_t b = bits[k < N - 1 ? p.others[k] : p.mode];
+    p.pk_off[k] = std::min<uint32_t>(off, 63);  // a 0-bit slot reads 0 through its mask
+    p.pk_mask[k] = b >= 32 ? 0xffffffffu : ((1u << b) - 1u);
+    off += b;
+  }
+  return off <= 64;
+}
+
 template <class K>
 void set_smem(K kern, size_t dyn) {
   ensure_dyn_smem(reinterpret_cast<const void*>(kern), dyn);
@@ -1527,8 +1709,8 @@ void launch_cfg(MttkrpLaunch& a) {
           for (int m = 0; m < N; ++m)
             if (m != a.mode && l.dims[m] > 65536) narrow = false;
           if (narrow) {  // 16-byte records with the row inside (StageC)
-            kern = stats ? k_mttkrp_sorted<N, LPE, CPL, FULL, true, kUnroll, 1, T2, true>
-                         : k_mttkrp_sorted<N, LPE, CPL, FULL, false, kUnroll, 3, T2, true>;
+            kern = stats ? k_mttkrp_sorted<N, LPE, CPL, FULL, true, kUnroll, 1, T2, 1>
+                         : k_mttkrp_sorted<N, LPE, CPL, FULL, false, kUnroll, 3, T2, 1>;
             st2 = static_cast<size_t>(T2) * sizeof(uint4);
           }
         }
@@ -1547,13 +1729,29 @@ void launch_cfg(MttkrpLaunch& a) {
     }
     size_t stage1 = tile_stage;
     auto kern = stats ? k_mttkrp_sorted<N, LPE, CPL, FULL, true> : k_mttkrp_sorted<N, LPE, CPL, FULL, false>;
+    // N = 3 with wide non-target modes (Amazon) and N = 4 (Delicious): the
+    // 16-byte tile-relative record (StageR) when every tile's spans fit
+    bool rel = false;
+    if constexpr ((N == 3 || N == 4) && FULL && LPE * CPL <= 32) {
+      bool narrow = N == 3 && compact_stage_knob();
+      for (int m = 0; m < N; ++m)
+        if (m != a.mode && l.dims[m] > 65536) narrow = false;
+      if (!narrow && !use_warp_variant() && rel_stage_plan<N>(a.tensor, kTileElems, p)) {
+        rel = true;
+        // <= 80 registers for N = 3 (3 CTAs/SM); <= 64 for N = 4 (4 CTAs/SM, as
+        // the Stage<4> kernel reaches uncapped)
+        kern = stats ? k_mttkrp_sorted<N, LPE, CPL, FULL, true, kUnroll, 1, kTileElems, 2>
+                     : k_mttkrp_sorted<N, LPE, CPL, FULL, false, kUnroll, N == 4 && CPL == 1 ? 4 : 3, kTileElems, 2>;
+        stage1 = static_cast<size_t>(kTileElems) * sizeof(uint4);
+      }
+    }
     if constexpr (N == 3 && FULL) {
       bool narrow = compact_stage_knob();
       for (int m = 0; m < N; ++m)
         if (m != a.mode && l.dims[m] > 65536) narrow = false;
       if (narrow) {  // 16-byte records with the row inside (StageC)
-        kern = stats ? k_mttkrp_sorted<N, LPE, CPL, FULL, true, kUnroll, 1, kTileElems, true>
-                     : k_mttkrp_sorted<N, LPE, CPL, FULL, false, kUnroll, 1, kTileElems, true>;
+        kern = stats ? k_mttkrp_sorted<N, LPE, CPL, FULL, true, kUnroll, 1, kTileElems, 1>
+                     : k_mttkrp_sorted<N, LPE, CPL, FULL, false, kUnroll, 1, kTileElems, 1>;
         stage1 = static_cast<size_t>(kTileElems) * sizeof(uint4);
       }
     }
@@ -1561,7 +1759,7 @@ void launch_cfg(MttkrpLaunch& a) {
     // R=16; the DRAM-bound Delicious modes run 6% faster with the extra warps
     // in flight).  N <= 3 already fits 3; higher orders would spill.
     if constexpr (N == 4 && LPE * CPL <= 32)
-      if (!stats) kern = k_mttkrp_sorted<N, LPE, CPL, FULL, false, kUnroll, 3>;
+      if (!stats && !rel) kern = k_mttkrp_sorted<N, LPE, CPL, FULL, false, kUnroll, 3>;
     set_smem(kern, stage1);
     launch_tiles<N>(kern, grid, stage1, p, a);
     count_launch();

@@ -26,7 +26,13 @@ modes = [int(x) for x in os.environ.get("PROBE_MODES", ",".join(map(str, range(l
 reps = int(os.environ.get("PROBE_REPS", "3"))
 ref = [None] * len(dims)
 for st in settings:
-    os.environ["BLCO_B200_PANEL"] = st
+    # "VAR=value[,VAR=value]" sets library knobs (read per call); anything else is BLCO_B200_PANEL
+    if "=" in st:
+        for kv in st.split(";"):
+            k, v = kv.split("=", 1)
+            os.environ[k] = v
+    else:
+        os.environ["BLCO_B200_PANEL"] = st
     tot = 0.0
     row = []
     for m in modes:
@@ -48,4 +54,4 @@ for st in settings:
         tot += t
         row.append(f"m{m} {t:.1f} ms ({err:.0e})")
         del out
-    print(f"{name} PANEL={st or 'auto'}: all modes {tot:.1f} ms | " + " | ".join(row), flush=True)
+    print(f"{name} {st if '=' in st else 'PANEL=' + (st or 'auto')}: all modes {tot:.1f} ms | " + " | ".join(row), flush=True)

@@ -525,3 +525,20 @@ def test_panel_ordered_dispatch(gpu, oracle, monkeypatch, dims, panel):
         assert n2 - n1 == 1 and n1 - n0 == 2, (mode, n1 - n0, n2 - n1)
         # the fp32 variant takes the same panel order (rows of R * 4 bytes)
         assert rel_frobenius(gpu.mttkrp_f32(dt, f, mode).astype(np.float64), want) <= 1e-5, mode
+
+
+@pytest.mark.parametrize("dims,rank", [([600_000, 300_000, 300_000], 32), ([300_000, 200_000, 150_000, 50], 16),
+                                       ([5000, 4000, 3000, 90], 16)])
+def test_tile_relative_stage(gpu, oracle, monkeypatch, dims, rank):
+    """BLCO_B200_REL_STAGE=1: the opt-in tile-relative 16-byte staging record
+    (StageR: every coordinate minus the tile's minimum, packed in 64 bits,
+    field widths from the largest per-mode span over the tiles) for wide
+    order-3 modes and order 4, across keyed blocks, against the oracle."""
+    monkeypatch.setenv("BLCO_B200_REL_STAGE", "1")
+    nnz = 300_000
+    dt = gpu.DeviceTensor.synthetic(dims, nnz, 13, 48, 70_000)
+    idx, vals = oracle.synth_uniform(dims, nnz, 13)
+    f = gpu.FactorMatrices.random(dims, rank, 3)
+    for mode in range(len(dims)):
+        want = oracle.mttkrp_coo(dims, idx, vals, f.factors, mode)
+        assert rel_frobenius(gpu.mttkrp(dt, f, mode, strategy=gpu.Strategy.Register), want) <= TOL, mode
