@@ -8,8 +8,9 @@
 //                                              (factorisation on host, the
 //                                               I_n row solves on device,
 //                                               fused with Gram(A_n))
-//   lambda = sqrt(diag Gram), A_n /= lambda     (device, fused with the
-//                                               fit's inner product)
+//   lambda = sqrt(diag Gram), A_n /= lambda     (device; folded into the
+//                                               next solves, Dense::solve_fold,
+//                                               and applied once at the end)
 // then fit = 1 - sqrt(max(0, |X|^2 - 2<X,Xhat> + |Xhat|^2)) / |X|.
 // Summation orders differ from the sequential host loops, so parity is
 // tolerance-based.
@@ -58,6 +59,9 @@ constexpr int solve_rows() {
 // straight from the constant bank (no shared-memory traffic).  One ALS runs
 // per device at a time (cp_als is synchronous on the legacy stream).
 __constant__ double c_L[32 * 32];
+// Column scaling of M applied as the rows are loaded (cp_als with folded
+// normalisation: M comes from the unnormalised factors, s = 1 / prod lambda)
+__constant__ double c_S[32];
 
 template <int RM, bool EXACT>
 __device__ __forceinline__ double lget(const double* sl, int R, int i, int k) {
@@ -79,7 +83,7 @@ constexpr int solve_min_blocks() {
 template <int RM, bool EXACT>
 __global__ void __launch_bounds__(kSolveThreads, solve_min_blocks<RM>()) k_solve_gram(const double* __restrict__ m, double* __restrict__ a,
                                                               uint64_t rows, int R, const double* __restrict__ L,
-                                                              double* __restrict__ g) {
+                                                              const double* __restrict__ S, double* __restrict__ g) {
   constexpr int ROWS = solve_rows<RM>();
   constexpr int W = kSolveThreads / 32;
   // Gram lane blocking: lane owns AI rows x AJ columns of a GI x GJ block of G
@@ -89,12 +93,15 @@ __global__ void __launch_bounds__(kSolveThreads, solve_min_blocks<RM>()) k_solve
   constexpr bool QUAD = RM > 32;
   extern __shared__ double smem[];
   double* sl = smem;                      // R x R (generic R only)
+  __shared__ double ss[64];               // column scaling of M (generic R; ones when S is null)
   // two ROWS x (R + 1) tiles (double-buffered); RR = R as a compile-time
   // constant when R == RM, so row/column splits are shifts
   const int RR = EXACT ? RM : R;
-  const int S = RR + 1;
-  if constexpr (!EXACT)
+  const int SR = RR + 1;  // padded row stride
+  if constexpr (!EXACT) {
     for (int i = threadIdx.x; i < R * R; i += blockDim.x) sl[i] = L[i];
+    for (int i = threadIdx.x; i < R; i += blockDim.x) ss[i] = S ? S[i] : 1.0;  // x * 1.0 is exact
+  }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int qi = QUAD ? (warp >> 1) * 32 : 0, qj = QUAD ? (warp & 1) * 32 : 0;
   const int i0 = qi + (lane >> 2) * AI, j0 = qj + (lane & 3) * AJ;
@@ -115,7 +122,7 @@ __global__ void __launch_bounds__(kSolveThreads, solve_min_blocks<RM>()) k_solve
       for (int j = 0; j < PER; ++j) {
         const int k = threadIdx.x + j * kSolveThreads;
         if (k < n) {
-          const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst + (k / RR) * S + k % RR));
+          const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst + (k / RR) * SR + k % RR));
           asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(m + base * R + k) : "memory");
         }
       }
@@ -139,10 +146,13 @@ __global__ void __launch_bounds__(kSolveThreads, solve_min_blocks<RM>()) k_solve
     __syncthreads();
     if (static_cast<int>(threadIdx.x) < nr) {
       double b[RM];
-      double* row = tile + threadIdx.x * S;
+      double* row = tile + threadIdx.x * SR;
 #pragma unroll
       for (int i = 0; i < RM; ++i)
-        if (i < RR) b[i] = row[i];
+        if (i < RR) {
+          if constexpr (EXACT) b[i] = row[i] * c_S[i];  // ones unless the normalisation is folded
+          else b[i] = row[i] * ss[i];
+        }
 #pragma unroll
       for (int i = 0; i < RM; ++i) {
         if (i < RR) {
@@ -167,9 +177,9 @@ __global__ void __launch_bounds__(kSolveThreads, solve_min_blocks<RM>()) k_solve
         if (i < RR) row[i] = b[i];
     }
     __syncthreads();
-    for (int k = threadIdx.x; k < nr * RR; k += blockDim.x) a[r0 * RR + k] = tile[(k / RR) * S + k % RR];
+    for (int k = threadIdx.x; k < nr * RR; k += blockDim.x) a[r0 * RR + k] = tile[(k / RR) * SR + k % RR];
     for (int r = QUAD ? 0 : warp; r < nr; r += QUAD ? 1 : W) {
-      const double* t = tile + r * S;
+      const double* t = tile + r * SR;
       double xi[AI], yj[AJ];
 #pragma unroll
       for (int x = 0; x < AI; ++x) xi[x] = t[min(i0 + x, R - 1)];
@@ -301,6 +311,16 @@ __global__ void k_small_norm(const double* __restrict__ G, int R, double* __rest
     const int i = p / R, j = p % R;
     const int a = i < j ? i : j, b = i < j ? j : i;  // the upper triangle holds the sums
     gram_out[p] = __ddiv_rn(G[a * R + b], __dmul_rn(l[a], l[b]));
+  }
+}
+
+// s[r] = 1 / prod_{m != n} lambda_m[r] (solve_fold)
+__global__ void k_mscale(const double* __restrict__ lams, int N, int n, int R, double* __restrict__ out) {
+  for (int r = threadIdx.x; r < R; r += blockDim.x) {
+    double p = 1.0;
+    for (int m = 0; m < N; ++m)
+      if (m != n) p = __dmul_rn(p, lams[static_cast<size_t>(m) * R + r]);
+    out[r] = __ddiv_rn(1.0, p);
   }
 }
 
@@ -437,11 +457,16 @@ struct Dense {
   cudaStream_t s = nullptr;  // every launch and copy of the epilogue goes here
   DevBuf<double> L, small;  // small: R x R reduced Gram | R lambda | 1 scalar
   DevBuf<double> parts;     // partial slots (grown on demand)
+  DevBuf<double> ones;      // R ones: c_S when the normalisation is not folded
+  DevBuf<double> mscale;    // solve_fold: 1 / prod_{m != n} lambda_m
 
   // parts is sized up front for the largest reduction of a call (the solve's
   // per-warp Gram slots at full occupancy), so no iteration reallocates --
   // a cudaFree/cudaMalloc inside the loop stalls the queued kernels.
-  explicit Dense(int r) : R(r), L(static_cast<size_t>(r) * r), small(static_cast<size_t>(r) * r + r + 1) {
+  explicit Dense(int r)
+      : R(r), L(static_cast<size_t>(r) * r), small(static_cast<size_t>(r) * r + r + 1), ones(r), mscale(r) {
+    const std::vector<double> h(r, 1.0);
+    B200_CUDA(cudaMemcpy(ones.ptr, h.data(), r * sizeof(double), cudaMemcpyHostToDevice));
     const int nsm = sm_count();
     slots(std::max<uint64_t>(uint64_t(nsm) * 32 * (kSolveThreads / 32) * r * r, uint64_t(nsm) * 16 * 4));
   }
@@ -505,14 +530,19 @@ struct Dense {
   // const_L: R = 16/32 read L from the process-wide __constant__ c_L (only
   // for callers that serialise the whole ALS run, blco_cp_als); otherwise
   // the kernel reads L from this Dense's own device buffer.
+  // mscale (device, R values, or null): columns of M are multiplied by it as
+  // the rows are loaded (cp_als with the normalisation folded, solve_fold).
   void solve(const double* m, double* a, uint64_t rows, const double* dgrams, int N, int n, int* dstatus,
-             bool const_L = false) {
+             bool const_L = false, const double* mscale = nullptr) {
     const int RR = R * R;
     k_small_prep<<<1, 256, 2 * RR * sizeof(double), s>>>(dgrams, N, n, R, L.ptr, dstatus);
     count_launch();
     check_launch("k_small_prep");
-    if (const_L && exact_rank(R))
+    if (const_L && exact_rank(R)) {
       B200_CUDA(cudaMemcpyToSymbolAsync(c_L, L.ptr, RR * sizeof(double), 0, cudaMemcpyDeviceToDevice, s));
+      B200_CUDA(cudaMemcpyToSymbolAsync(c_S, mscale ? mscale : ones.ptr, R * sizeof(double), 0,
+                                        cudaMemcpyDeviceToDevice, s));
+    }
     if (!rows) {
       B200_CUDA(cudaMemsetAsync(small.ptr, 0, RR * sizeof(double), s));
       return;
@@ -529,7 +559,7 @@ struct Dense {
       // R <= 32: every warp writes the whole upper triangle of its slot (the
       // lower one is never read); R = 64: each warp owns one quadrant
       if (rm > 32) B200_CUDA(cudaMemsetAsync(sl, 0, nslots * RR * 8, s));
-      kern<<<grid, kSolveThreads, smem, s>>>(m, a, rows, R, L.ptr, sl);
+      kern<<<grid, kSolveThreads, smem, s>>>(m, a, rows, R, L.ptr, mscale, sl);
       count_launch();
       check_launch("k_solve_gram");
       reduce(nslots, RR);
@@ -569,12 +599,19 @@ struct Dense {
     }
   }
 
-  // One ALS mode's dense steps, enqueued without host round trips: solve,
-  // then normalize with the Gram of this device's rows.  lambda and the Gram
-  // of the normalised A_n stay on the device (dgrams[n], dlam); for the last
-  // mode (m_inner set) also <X, Xhat> into *dinner.
-  void solve_normalize(const double* m, double* a, uint64_t rows, double* dgrams, int N, int n, double* dlam,
-                       int* dstatus, const double* m_inner, double* dinner) {
+  // One ALS mode's dense steps with the column normalisation folded into the
+  // next solves (blco_cp_als): the factors stay UNnormalised on the device,
+  // A_m = A_m' diag(lambda_m) with A_m' the reference's normalised factor
+  // (cpals.cpp:51-61), so an MTTKRP over them is M' diag(prod_{m != n}
+  // lambda_m) column-wise, and the solve multiplies the columns of M by
+  // s = 1 / prod_{m != n} lambda_m as it loads them.  Then lambda_n =
+  // sqrt(diag Gram(A_n)) and Gram(A_n') = Gram(A_n) / (l l^T) as before, with
+  // no pass over A_n (the reference's A_n /= lambda, one read and one write of
+  // I_n x R, is applied once, when the factors are returned).  For the last
+  // mode (dinner set) <X, Xhat> = sum M' lambda A' = sum M s A.
+  // dlams: N x R, every mode's lambda.
+  void solve_fold(const double* m, double* a, uint64_t rows, double* dgrams, int N, int n, double* dlams,
+                  int* dstatus, double* dinner) {
     // BLCO_B200_ALS_PROBE=1: device time of each step of this epilogue (stderr)
     static const bool probe = std::getenv("BLCO_B200_ALS_PROBE") != nullptr;
     cudaEvent_t pe[3] = {};
@@ -584,18 +621,47 @@ struct Dense {
       cudaEventRecord(pe[k], s);
     };
     pmark(0);
-    solve(m, a, rows, dgrams, N, n, dstatus, /*const_L=*/true);  // only blco_cp_als (serialised) gets here
+    k_mscale<<<1, 64, 0, s>>>(dlams, N, n, R, mscale.ptr);
+    count_launch();
+    check_launch("k_mscale");
+    solve(m, a, rows, dgrams, N, n, dstatus, /*const_L=*/true, mscale.ptr);  // only blco_cp_als (serialised)
     pmark(1);
-    normalize(small.ptr, a, rows, dgrams + static_cast<size_t>(n) * R * R, dlam, m_inner, dinner);
+    k_small_norm<<<1, 256, 0, s>>>(small.ptr, R, dgrams + static_cast<size_t>(n) * R * R,
+                                   dlams + static_cast<size_t>(n) * R);
+    count_launch();
+    check_launch("k_small_norm");
+    if (dinner) {
+      B200_CUDA(cudaMemsetAsync(dinner, 0, sizeof(double), s));
+      if (rows) {
+        const unsigned grid = grid_of(rows * R);
+        k_inner<<<grid, kT, 0, s>>>(m, a, rows, R, mscale.ptr, slots(grid));
+        count_launch();
+        check_launch("k_inner");
+        k_reduce_ordered<<<1, 256, 0, s>>>(parts.ptr, grid, 1, dinner);
+        count_launch();
+        check_launch("k_reduce_ordered");
+      }
+    }
     pmark(2);
     if (probe) {
       cudaEventSynchronize(pe[2]);
       float t[2];
       for (int k = 0; k < 2; ++k) cudaEventElapsedTime(&t[k], pe[k], pe[k + 1]);
-      std::fprintf(stderr, "[als probe] mode %d rows %llu: prep+solve+gram %.3f norm+scale %.3f ms\n",
+      std::fprintf(stderr, "[als probe] mode %d rows %llu: prep+solve+gram %.3f norm+inner %.3f ms\n",
                    n, static_cast<unsigned long long>(rows), t[0], t[1]);
       for (int k = 0; k < 3; ++k) cudaEventDestroy(pe[k]);
     }
+  }
+
+  // A /= lambda over `rows` rows (the folded normalisation, applied once)
+  void scale_rows(double* a, uint64_t rows, const double* dlam) {
+    if (!rows) return;
+    const bool v2 = R % 2 == 0 && reinterpret_cast<uintptr_t>(a) % 16 == 0;
+    const unsigned grid = grid_of(v2 ? rows * R / 2 : rows * R);
+    if (v2) k_scale_inner<true><<<grid, kT, 0, s>>>(a, rows, R, dlam, nullptr, nullptr);
+    else k_scale_inner<false><<<grid, kT, 0, s>>>(a, rows, R, dlam, nullptr, nullptr);
+    count_launch();
+    check_launch("k_scale_inner");
   }
 
   double inner(const double* m, const double* a, uint64_t rows, const std::vector<double>& lambda) {
@@ -732,9 +798,20 @@ int blco_cp_als_timed(const blco_tensor* t, uint64_t rank, int max_iters, double
     Dense dense(R);
     const int RR = R * R;
     // Grams, lambda, <X, Xhat>, fit and the singular flag live on the device
-    DevBuf<double> dgrams(static_cast<size_t>(N) * RR), dlam(R), dinner(1), dfit(std::max(1, max_iters));
+    // dlams: every mode's lambda (the factors stay unnormalised, solve_fold)
+    DevBuf<double> dgrams(static_cast<size_t>(N) * RR), dlams(static_cast<size_t>(N) * R), dinner(1),
+        dfit(std::max(1, max_iters));
     DevBuf<int> dstatus(1);
     B200_CUDA(cudaMemset(dstatus.ptr, 0, sizeof(int)));
+    {
+      const std::vector<double> ones(static_cast<size_t>(N) * R, 1.0);
+      B200_CUDA(cudaMemcpy(dlams.ptr, ones.data(), ones.size() * sizeof(double), cudaMemcpyHostToDevice));
+    }
+    const double* dlam_last = dlams.ptr + static_cast<size_t>(N - 1) * R;
+    // the reference's A_n /= lambda_n (cpals.cpp:59-60), applied once on the way out
+    auto normalise_factors = [&] {
+      for (int m = 0; m < N; ++m) dense.scale_rows(A[m].ptr, l.dims[m], dlams.ptr + static_cast<size_t>(m) * R);
+    };
     for (int m = 0; m < N; ++m) {
       const std::vector<double> g = dense.gram(A[m].ptr, l.dims[m]);
       B200_CUDA(cudaMemcpy(dgrams.ptr + static_cast<size_t>(m) * RR, g.data(), RR * sizeof(double),
@@ -769,7 +846,9 @@ int blco_cp_als_timed(const blco_tensor* t, uint64_t rank, int max_iters, double
       acc[slot] += std::chrono::duration<double>(now - t_last).count();
       t_last = now;
     };
-    auto fetch_lambda = [&] { B200_CUDA(cudaMemcpy(lambda.data(), dlam.ptr, R * sizeof(double), cudaMemcpyDeviceToHost)); };
+    auto fetch_lambda = [&] {
+      B200_CUDA(cudaMemcpy(lambda.data(), dlam_last, R * sizeof(double), cudaMemcpyDeviceToHost));
+    };
     for (; it < max_iters; ++it) {
       NvtxRange nv("cp_als iteration");
       if (st) mark(ev_all, true);
@@ -779,12 +858,12 @@ int blco_cp_als_timed(const blco_tensor* t, uint64_t rank, int max_iters, double
         mttkrp_into(*t, ptr, rank, n, strategy, c, mt.ptr);
         if (st) mark(ev_mt, false);
         tick(0);
-        // A_n = normalise(M V^-1) straight into A_n; M of the last mode stays
-        // in mt for the fit's inner product
-        dense.solve_normalize(mt.ptr, A[n].ptr, l.dims[n], dgrams.ptr, N, n, dlam.ptr, dstatus.ptr,
-                              n == N - 1 ? mt.ptr : nullptr, dinner.ptr);
+        // A_n = M V^-1 (unnormalised) straight into A_n; M of the last mode
+        // stays in mt for the fit's inner product
+        dense.solve_fold(mt.ptr, A[n].ptr, l.dims[n], dgrams.ptr, N, n, dlams.ptr, dstatus.ptr,
+                         n == N - 1 ? dinner.ptr : nullptr);
       }
-      k_small_fit<<<1, 32>>>(dgrams.ptr, N, R, dlam.ptr, dinner.ptr, xn, dfit.ptr + it);
+      k_small_fit<<<1, 32>>>(dgrams.ptr, N, R, dlam_last, dinner.ptr, xn, dfit.ptr + it);
       count_launch();
       check_launch("k_small_fit");
       if (st) mark(ev_all, false);
@@ -799,6 +878,7 @@ int blco_cp_als_timed(const blco_tensor* t, uint64_t rank, int max_iters, double
       *iters_out = it + 1;
       if (!std::isfinite(f)) {
         fetch_lambda();
+        normalise_factors();
         emit();
         throw_error("cp_als: non-finite fit at iteration " + std::to_string(it + 1));
       }
@@ -825,6 +905,7 @@ int blco_cp_als_timed(const blco_tensor* t, uint64_t rank, int max_iters, double
     if (trace)
       std::fprintf(stderr, "[blco trace] cp_als %d iters: mttkrp %.3f s, dense epilogue + fit %.3f s\n", it, acc[0],
                    acc[1]);
+    normalise_factors();
     emit();
   });
 }
