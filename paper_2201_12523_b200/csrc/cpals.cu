@@ -535,7 +535,9 @@ struct Dense {
   void solve(const double* m, double* a, uint64_t rows, const double* dgrams, int N, int n, int* dstatus,
              bool const_L = false, const double* mscale = nullptr) {
     const int RR = R * R;
-    k_small_prep<<<1, 256, 2 * RR * sizeof(double), s>>>(dgrams, N, n, R, L.ptr, dstatus);
+    const size_t prep_smem = 2 * static_cast<size_t>(RR) * sizeof(double);  // V and L: 64 KB at R = 64
+    if (prep_smem > 48 * 1024) ensure_dyn_smem(reinterpret_cast<const void*>(k_small_prep), prep_smem);
+    k_small_prep<<<1, 256, prep_smem, s>>>(dgrams, N, n, R, L.ptr, dstatus);
     count_launch();
     check_launch("k_small_prep");
     if (const_L && exact_rank(R)) {
