@@ -542,3 +542,25 @@ def test_tile_relative_stage(gpu, oracle, monkeypatch, dims, rank):
     for mode in range(len(dims)):
         want = oracle.mttkrp_coo(dims, idx, vals, f.factors, mode)
         assert rel_frobenius(gpu.mttkrp(dt, f, mode, strategy=gpu.Strategy.Register), want) <= TOL, mode
+
+
+@pytest.mark.parametrize("rank", [128, 257, 512])
+def test_large_ranks(gpu, oracle, rank):
+    """Ranks beyond one lane-group row (several column chunks per launch):
+    register and hierarchical fp64 within 1e-12, the fp32 variant within
+    1e-5, the deterministic kernel up to its R <= 256 limit."""
+    dims = [70, 50, 90]
+    coo = gpu.synth_uniform_host(dims, 20_000, rank)
+    f = gpu.FactorMatrices.random(dims, rank, 5)
+    t = gpu.build_blco(coo, 12, 3000)
+    for mode in range(3):
+        want = oracle.mttkrp_coo(dims, coo.indices, coo.values, f.factors, mode)
+        for strat in (gpu.Strategy.Register, gpu.Strategy.Hierarchical):
+            assert rel_frobenius(gpu.mttkrp(t, f, mode, strategy=strat), want) <= TOL, (mode, strat)
+        assert rel_frobenius(gpu.mttkrp_f32(t, f, mode).astype(np.float64), want) <= 1e-5, mode
+        if rank <= 256:
+            dt = gpu.DeviceTensor.synthetic(dims, 20_000, rank)
+            idx, vals = oracle.synth_uniform(dims, 20_000, rank)
+            want_d = oracle.mttkrp_coo(dims, idx, vals, f.factors, mode)
+            got = gpu.mttkrp(dt, f, mode, gpu.ExecConfig(deterministic=True))
+            assert rel_frobenius(got, want_d) <= TOL, mode
