@@ -215,14 +215,14 @@ def test_cp_als_deterministic_is_bit_reproducible(gpu, golden):
 
 @pytest.mark.parametrize("dims,rank", [([30, 40, 50], 1), ([30, 40, 50], 7), ([45, 35, 55], 24),
                                        ([50, 60, 70, 40], 33), ([40, 50, 60, 30, 20], 17), ([80, 90, 70], 64),
-                                       ([60, 50, 40], 16)])
+                                       ([60, 50, 40], 16), ([40, 50], 5), ([9, 8, 7, 6, 5, 6, 7, 8], 3)])
 def test_cp_als_random_shapes_match_oracle(gpu, oracle, dims, rank):
     """Device CP-ALS (the normalisation folded into the solves, every solve
     path: constant-bank L for R = 16, shared-memory L for the other ranks)
     against the C restatement of the reference's cp_als (oracle/blco_oracle.c,
-    cpals.cpp:66-111) on random shapes: fit history within 1e-10, factors
-    within 1e-8, lambda within 1e-9 relative."""
-    nnz = 4000
+    cpals.cpp:66-111) on random shapes, orders 2 to 8: fit history within
+    1e-10, factors within 1e-8, lambda within 1e-9 relative."""
+    nnz = min(4000, int(np.prod(dims)) // 2)
     idx, vals = oracle.synth_uniform(dims, nnz, 3 + rank)
     keys, offs, oi, ov = oracle.build(dims, idx, vals)
     fs, lam, fit = oracle.cp_als(dims, keys, offs, oi, ov, rank, 6, -1e300, 11)
