@@ -322,7 +322,7 @@ def traffic_probe_worker(args):
     b.factors_random_device(dims, R, FACTOR_SEED, [a.data_ptr() for a in fac], sptr)
     outs = [torch.zeros((d, R), dtype=torch.float64, device="cuda:0") for d in dims]
     cfg = b.ExecConfig(num_compute_units=torch.cuda.get_device_properties(0).multi_processor_count)
-    for _ in range(2):  # the step's kernels: the fused all-mode kernel where eligible, else one per mode
+    for _ in range(2):  # the step's kernels: one per mode (the fused all-mode kernel only with BLCO_B200_FUSED=1)
         dt.mttkrp_all_device([a.data_ptr() for a in fac], R, [o.data_ptr() for o in outs], b.Strategy.Auto, cfg,
                              accumulate=True, stream=sptr)
     torch.cuda.synchronize()
