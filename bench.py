@@ -523,8 +523,8 @@ def run_ours(args, world, rank_id, local):
         comm.mttkrp_all(dt, fptr, R, [o.data_ptr() for o in outs], [x.data_ptr() for x in shards],
                         reduce=args.reduce, strategy=strategy, config=cfg, stream=sptr)
 
-    # one GPU: the library's all-mode device entry decides between the fused
-    # all-mode kernel (factors in L2: NELL-2) and one kernel per mode (Amazon)
+    # one GPU: the library's all-mode device entry runs one kernel per mode
+    # (the fused all-mode kernel only with BLCO_B200_FUSED=1, factors in L2)
     fused = world == 1 and strategy == b.Strategy.Auto and dt.mttkrp_all_device(
         fptr, R, [o.data_ptr() for o in outs], strategy, cfg, stream=sptr)
 
