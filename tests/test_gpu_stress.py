@@ -81,3 +81,39 @@ def test_random_builds_bit_exact(gpu, oracle, seed):
     assert np.array_equal(t.keys, keys) and np.array_equal(t.offsets, offs)
     assert np.array_equal(t.idx, idx) and np.array_equal(t.vals, vals)
     assert np.array_equal(t.batch_table, oracle.batch_table(np.diff(offs), 512))
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_random_multi_and_stream_paths(gpu, oracle, monkeypatch, seed):
+    """The remaining entry points on random shapes: the per-mode streaming
+    API (stream_mttkrp, 1-3 queues), the library multi-GPU driver at one
+    device and the one-rank communicator with real NCCL communicators
+    (BLCO_B200_NCCL_SINGLE=1, both reductions), against the oracle."""
+    import torch
+    monkeypatch.setenv("BLCO_B200_NCCL_SINGLE", "1")
+    dims, nnz, rank, target, cap = _case(500 + seed)
+    coo = gpu.synth_uniform_host(dims, nnz, seed)
+    f = gpu.FactorMatrices.random(dims, rank, seed + 7)
+    t = gpu.build_blco(coo, target, cap)
+    want = [oracle.mttkrp_coo(dims, coo.indices, coo.values, f.factors, m) for m in range(len(dims))]
+    ctx = (dims, nnz, rank, target, cap)
+    queues = 1 + seed % 3
+    res = min(cap, nnz) * 16
+    for m in range(len(dims)):
+        b = gpu.DeviceBudget(capacity_bytes=1 << 28, num_queues=queues, reservation_bytes=max(res, 16))
+        assert rel_frobenius(gpu.stream_mttkrp(t, f, m, b), want[m]) <= 1e-12, (ctx, m, "stream per mode")
+    reduce = "reducescatter" if seed % 2 else "allreduce"
+    dt = gpu.DeviceTensor.upload(t)
+    got = gpu.MultiDeviceTensor(dt, [0]).mttkrp_all_modes(f, reduce=reduce)
+    for m in range(len(dims)):
+        assert rel_frobenius(got[m], want[m]) <= 1e-12, (ctx, m, "multi")
+    comm = gpu.Communicator(None, 1, 0, 0)
+    fac = [torch.from_numpy(a).cuda() for a in f.factors]
+    outs = [torch.empty((d, rank), dtype=torch.float64, device="cuda") for d in dims]
+    shards = [torch.empty((d, rank), dtype=torch.float64, device="cuda") for d in dims]
+    comm.mttkrp_all(dt, [a.data_ptr() for a in fac], rank, [o.data_ptr() for o in outs],
+                    [x.data_ptr() for x in shards], reduce=reduce)
+    torch.cuda.synchronize()
+    res_t = shards if reduce == "reducescatter" else outs
+    for m in range(len(dims)):
+        assert rel_frobenius(res_t[m].cpu().numpy(), want[m]) <= 1e-12, (ctx, m, "communicator")
