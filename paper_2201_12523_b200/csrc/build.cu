@@ -155,6 +155,66 @@ __global__ void k_encode(EncodeParams p, uint64_t nnz, const uint32_t* __restric
   }
 }
 
+// K1 for orders <= 4: the bit scatter through byte tables in shared memory.
+// tab[(m * 4 + j) * 256 + v] holds, as {lo.x, lo.y, hi.x, hi.y}, the ALTO
+// bits that byte j = v of coordinate m deposits (bit 8j + i of mode m lands
+// at pos[m][8j + i]), so an element costs ceil(b_m / 8) table loads per mode
+// instead of one shift/or chain per bit (ncu on NELL-2: the bit loop issued
+// ~735 instructions per 32 elements and ran at 0.75 TB/s).  Persistent grid:
+// each CTA stages the N x 16 KB tables once.  Same bits as k_encode.
+template <int N>
+__global__ void __launch_bounds__(256) k_encode_lut(EncodeParams p, const uint4* __restrict__ lut, uint64_t nnz,
+                                                    const uint32_t* __restrict__ coords,
+                                                    uint64_t* __restrict__ alto_lo, uint64_t* __restrict__ alto_hi,
+                                                    uint64_t* __restrict__ reenc, uint32_t* __restrict__ perm) {
+  extern __shared__ uint4 tab[];  // [N][4][256]
+  for (int i = threadIdx.x; i < N * 1024; i += blockDim.x) tab[i] = lut[i];
+  __syncthreads();
+  for (uint64_t e = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; e < nnz;
+       e += uint64_t(gridDim.x) * blockDim.x) {
+    uint32_t c[N];
+#pragma unroll
+    for (int m = 0; m < N; ++m) c[m] = __ldcs(coords + m * nnz + e);
+    uint64_t r = 0, lo = 0, hi = 0;
+#pragma unroll
+    for (int m = 0; m < N; ++m) {
+      r |= (static_cast<uint64_t>(c[m]) & p.mask[m]) << p.shift[m];
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (8 * j < p.mode_bits[m]) {
+          const uint4 t = tab[(m * 4 + j) * 256 + ((c[m] >> (8 * j)) & 255u)];
+          lo |= (static_cast<uint64_t>(t.y) << 32) | t.x;
+          hi |= (static_cast<uint64_t>(t.w) << 32) | t.z;
+        }
+    }
+    alto_lo[e] = lo;
+    if (alto_hi) alto_hi[e] = hi;
+    reenc[e] = r;
+    perm[e] = static_cast<uint32_t>(e);
+  }
+}
+
+// The byte tables of k_encode_lut for a layout (host, from pos / mode_bits).
+std::vector<uint4> encode_lut(const EncodeParams& p) {
+  std::vector<uint4> t(static_cast<size_t>(p.order) * 1024, make_uint4(0, 0, 0, 0));
+  for (int m = 0; m < p.order; ++m)
+    for (int j = 0; j < 4; ++j)
+      for (int v = 0; v < 256; ++v) {
+        uint64_t lo = 0, hi = 0;
+        for (int i = 0; i < 8; ++i) {
+          const int k = 8 * j + i;
+          if (k >= p.mode_bits[m] || !((v >> i) & 1)) continue;
+          const int q = p.pos[m][k];
+          if (q < 64) lo |= uint64_t(1) << q;
+          else hi |= uint64_t(1) << (q - 64);
+        }
+        t[(static_cast<size_t>(m) * 4 + j) * 256 + v] =
+            make_uint4(static_cast<uint32_t>(lo), static_cast<uint32_t>(lo >> 32), static_cast<uint32_t>(hi),
+                       static_cast<uint32_t>(hi >> 32));
+      }
+  return t;
+}
+
 using EncodeKernel = void (*)(EncodeParams, uint64_t, const uint32_t*, uint64_t*, uint64_t*, uint64_t*, uint32_t*);
 EncodeKernel encode_kernel(int order) {
   switch (order) {
@@ -167,6 +227,38 @@ EncodeKernel encode_kernel(int order) {
     case 7: return k_encode<7>;
     default: return k_encode<8>;
   }
+}
+
+// K1 launch: byte tables for orders <= 4 (lut: the device copy of
+// encode_lut(ep), or null), the bit loop otherwise.
+void launch_encode(const EncodeParams& ep, const uint4* lut, uint64_t n, const uint32_t* coords, uint64_t* lo,
+                   uint64_t* hi, uint64_t* reenc, uint32_t* perm, cudaStream_t s) {
+  if (lut && ep.order <= 4) {
+    using LutKernel = void (*)(EncodeParams, const uint4*, uint64_t, const uint32_t*, uint64_t*, uint64_t*,
+                               uint64_t*, uint32_t*);
+    const LutKernel k = ep.order == 1   ? k_encode_lut<1>
+                        : ep.order == 2 ? k_encode_lut<2>
+                        : ep.order == 3 ? k_encode_lut<3>
+                                        : k_encode_lut<4>;
+    const size_t smem = static_cast<size_t>(ep.order) * 1024 * sizeof(uint4);
+    ensure_dyn_smem(reinterpret_cast<const void*>(k), smem);
+    const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(
+        1, std::min<uint64_t>(grid_for(n), static_cast<uint64_t>(sm_count()) * 4)));
+    k<<<grid, kThreads, smem, s>>>(ep, lut, n, coords, lo, hi, reenc, perm);
+  } else {
+    encode_kernel(ep.order)<<<grid_for(n, 4), kThreads, 0, s>>>(ep, n, coords, lo, hi, reenc, perm);
+  }
+  count_launch();
+  check_launch("k_encode");
+}
+
+DevBuf<uint4> upload_encode_lut(const EncodeParams& ep) {
+  DevBuf<uint4> d;
+  if (ep.order > 4) return d;
+  const std::vector<uint4> h = encode_lut(ep);
+  d.alloc(h.size());
+  B200_CUDA(cudaMemcpy(d.ptr, h.data(), h.size() * sizeof(uint4), cudaMemcpyHostToDevice));
+  return d;
 }
 
 __global__ void k_iota(uint32_t* __restrict__ out, uint64_t n) {
@@ -338,10 +430,10 @@ void build_from_device_coo(blco_tensor& t, DevBuf<uint32_t>& coords, DevBuf<doub
   DevBuf<uint64_t> lo(nnz), hi(wide ? nnz : 0), reenc(nnz);
   DevBuf<uint32_t> perm(nnz);
   const EncodeParams ep = encode_params(l);
-  encode_kernel(l.order)<<<grid_for(nnz, 4), kThreads, 0, s>>>(ep, nnz, coords.ptr, lo.ptr, hi.ptr, reenc.ptr,
-                                                                 perm.ptr);
-  count_launch();
-  check_launch("k_encode");
+  {
+    const DevBuf<uint4> lut = upload_encode_lut(ep);
+    launch_encode(ep, lut.ptr, nnz, coords.ptr, lo.ptr, hi.ptr, reenc.ptr, perm.ptr, s);
+  }
   coords.reset();
 
   // K2: stable LSD radix sort (low word, then high word), payload = element id
@@ -589,6 +681,7 @@ void build_host_passes(blco_tensor& t, const uint64_t* dims, int order, uint64_t
   DevBuf<uint8_t> flag(chunk);
   DevBuf<unsigned> bad(1);
   B200_CUDA(cudaMemset(bad.ptr, 0, sizeof(unsigned)));
+  const DevBuf<uint4> lut = upload_encode_lut(ep);
   // one chunk of the host COO -> device coordinates, values and ALTO words
   auto load_chunk = [&](uint64_t c0, uint64_t n) {
     for (int m = 0; m < order; ++m) {
@@ -598,9 +691,7 @@ void build_host_passes(blco_tensor& t, const uint64_t* dims, int order, uint64_t
       count_launch();
     }
     B200_CUDA(cudaMemcpy(cv.ptr, vals + c0, n * 8, cudaMemcpyHostToDevice));
-    encode_kernel(order)<<<grid_for(n, 4), kThreads, 0, s>>>(ep, n, cc.ptr, lo.ptr, hi.ptr, reenc.ptr, perm.ptr);
-    count_launch();
-    check_launch("build pass: chunk");
+    launch_encode(ep, lut.ptr, n, cc.ptr, lo.ptr, hi.ptr, reenc.ptr, perm.ptr, s);
   };
   // (1)+(2) passes: histogram a range's ALTO sub-ranges (one stream of the
   // COO), group consecutive sub-ranges into passes of <= cap elements, and
