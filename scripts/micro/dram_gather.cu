@@ -14,6 +14,8 @@
 //   g4     : both rows through gather4.
 // ncu: l1tex__m_l1tex2xbar_req_cycles_active (the Amazon kernel's 88%
 // limiter), l1tex__data_pipe_lsu_wavefronts, dram__bytes.
+//   bulkred: LDG gathers, each product row committed by a 256-byte TMA bulk
+//            reduction (cp.reduce.async.bulk .add.f64) from shared memory.
 // Usage: dram_gather [blocks_per_sm] [variant mask] [row span]
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -68,8 +70,13 @@ __device__ __forceinline__ void gather4(void* dst, const CUtensorMap* map, unsig
 __device__ __forceinline__ void red2(double* p, double a) {
   asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(a) : "memory");
 }
+__device__ __forceinline__ void bulk_red_row(double* dst, const void* src) {
+  asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], 256;" ::"l"(dst),
+               "r"(smem_u32(src))
+               : "memory");
+}
 
-// V = 0 ldg, 1 hybrid, 2 g4
+// V = 0 ldg, 1 hybrid, 2 g4, 3 ldg + TMA bulk-reduce commits
 template <int V>
 __global__ void __launch_bounds__(256) k_mode(const double* __restrict__ A, const double* __restrict__ B,
                                               const __grid_constant__ CUtensorMap mapA,
@@ -83,7 +90,7 @@ __global__ void __launch_bounds__(256) k_mode(const double* __restrict__ A, cons
   const unsigned gg = (blockIdx.x * kWarps + wid) * 2 + grp;  // global group id
   constexpr int kStages = kElemsPerGroup / kE;
   unsigned char* ring = smem + wid * kS * kStageBytes;
-  if constexpr (V > 0) {
+  if constexpr (V == 1 || V == 2) {
     if (lane == 0)
       for (int s = 0; s < kS; ++s) mbar_init(&bars[wid][s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -104,22 +111,22 @@ __global__ void __launch_bounds__(256) k_mode(const double* __restrict__ A, cons
                 rowx(g0 + h, e0 + 2, 1, nB), rowx(g0 + h, e0 + 3, 1, nB), bar);
     }
   };
-  if constexpr (V > 0)
+  if constexpr (V == 1 || V == 2)
     if (lane == 0)
       for (int st = 0; st < kS - 1; ++st) issue(st);
   for (int st = 0; st < kStages; ++st) {
     const int e0 = st * kE;
     double a[kE][2], b[kE][2];
-    if constexpr (V > 0)
+    if constexpr (V == 1 || V == 2)
       if (lane == 0 && st + kS - 1 < kStages) issue(st + kS - 1);
-    if constexpr (V < 2) {
+    if constexpr (V < 2 || V == 3) {
 #pragma unroll
       for (int u = 0; u < kE; ++u) {
         const double* pb = B + rowx(gg, e0 + u, 1, nB) * 32ull;
         b[u][0] = __ldg(pb + q), b[u][1] = __ldg(pb + q + 16);
       }
     }
-    if constexpr (V == 0) {
+    if constexpr (V == 0 || V == 3) {
 #pragma unroll
       for (int u = 0; u < kE; ++u) {
         const double* pa = A + rowx(gg, e0 + u, 0, nA) * 32ull;
@@ -141,13 +148,37 @@ __global__ void __launch_bounds__(256) k_mode(const double* __restrict__ A, cons
       __syncwarp();
       if (lane == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
+    if constexpr (V == 3) {
+      // products staged as rows in a per-warp 2-stage ring, one elected lane
+      // issues a 256-byte bulk reduction per row
+      double* stg = reinterpret_cast<double*>(smem + wid * 2 * (2 * kE * 256)) + (st & 1) * (2 * kE * 32);
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      __syncwarp();
 #pragma unroll
-    for (int u = 0; u < kE; ++u) {
-      double* pm = M + rowx(gg, e0 + u, 2, nM) * 32ull;
-      red2(pm + q, a[u][0] * b[u][0]);
-      red2(pm + q + 16, a[u][1] * b[u][1]);
+      for (int u = 0; u < kE; ++u) {
+        double* r = stg + (grp * kE + u) * 32;
+        r[q] = a[u][0] * b[u][0];
+        r[q + 16] = a[u][1] * b[u][1];
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+        for (int h = 0; h < 2; ++h)
+          for (int u = 0; u < kE; ++u)
+            bulk_red_row(M + rowx(g0 + h, e0 + u, 2, nM) * 32ull, stg + (h * kE + u) * 32);
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < kE; ++u) {
+        double* pm = M + rowx(gg, e0 + u, 2, nM) * 32ull;
+        red2(pm + q, a[u][0] * b[u][0]);
+        red2(pm + q + 16, a[u][1] * b[u][1]);
+      }
     }
   }
+  if constexpr (V == 3)
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 typedef CUresult (*EncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -187,16 +218,18 @@ int main(int argc, char** argv) {
   const size_t sm1 = size_t(kWarps) * kS * 2 * kE * 256, sm2 = 2 * sm1;
   cudaFuncSetAttribute(k_mode<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm1));
   cudaFuncSetAttribute(k_mode<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm2));
+  const size_t sm3 = size_t(kWarps) * 2 * 2 * kE * 256;
   const double elems = double(grid) * kWarps * 2 * kElemsPerGroup;
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  for (int v = 0; v < 3; ++v) {
+  for (int v = 0; v < 4; ++v) {
     if (!(mask & (1 << v))) continue;
     auto launch = [&] {
       if (v == 0) k_mode<0><<<grid, 256>>>(A, B, mapA, mapB, M, nA, nB, nM);
       if (v == 1) k_mode<1><<<grid, 256, sm1>>>(A, B, mapA, mapB, M, nA, nB, nM);
       if (v == 2) k_mode<2><<<grid, 256, sm2>>>(A, B, mapA, mapB, M, nA, nB, nM);
+      if (v == 3) k_mode<3><<<grid, 256, sm3>>>(A, B, mapA, mapB, M, nA, nB, nM);
     };
     cudaMemset(M, 0, size_t(nM) * 256);
     launch();
@@ -213,7 +246,7 @@ int main(int argc, char** argv) {
     for (double x : o) cs += x;
     const cudaError_t err = cudaGetLastError();
     std::printf("span %u %-7s %d/SM: %.3f ms, %.2f G elem/s (%.2f G rows/s gathered), checksum %.6e %s\n",
-                span, v == 0 ? "ldg" : v == 1 ? "hybrid" : "g4", per_sm, ms / 3, elems / (ms / 3 * 1e-3) / 1e9,
+                span, v == 0 ? "ldg" : v == 1 ? "hybrid" : v == 2 ? "g4" : "bulkred", per_sm, ms / 3, elems / (ms / 3 * 1e-3) / 1e9,
                 2 * elems / (ms / 3 * 1e-3) / 1e9, cs, cudaGetErrorString(err));
   }
   return 0;
