@@ -153,11 +153,13 @@ def test_device_pointer_entry(gpu, oracle):
     assert rel_frobenius(out.cpu().numpy(), 2 * want) <= TOL
 
 
-def test_slices_sum_to_whole(gpu, oracle):
-    """Multi-GPU partition unit: span-aligned slices' partial outputs sum to M."""
-    dims = [500, 400, 300]
-    dt = gpu.DeviceTensor.synthetic(dims, 200_000, 4, 20, 30_000)
-    f = gpu.FactorMatrices.random(dims, 16, 2)
+@pytest.mark.parametrize("dims,rank", [([500, 400, 300], 16), ([600_000, 300_000, 300_000], 32)])
+def test_slices_sum_to_whole(gpu, oracle, dims, rank):
+    """Multi-GPU partition unit: span-aligned slices' partial outputs sum to M
+    (the second shape's factors exceed L2, so every slice runs panel-ordered
+    with its own tables)."""
+    dt = gpu.DeviceTensor.synthetic(dims, 200_000, 4, 20 if dims[0] < 1000 else 48, 30_000)
+    f = gpu.FactorMatrices.random(dims, rank, 2)
     idx, vals = oracle.synth_uniform(dims, 200_000, 4)
     for parts in (2, 3, 8):
         ranges = gpu.partition(dt.block_nnz(), 512, parts)
