@@ -267,3 +267,25 @@ def test_oracle_cp_als_matches_reference_r32(oracle):
     for m in range(len(dims)):
         assert rel_frobenius(fs[m], z[f"n32_f{m}"]) <= 1e-9
 
+
+
+@pytest.mark.parametrize("dims,rank", [([30, 40, 50], 1), ([30, 40, 50], 7), ([45, 35, 55], 24),
+                                       ([50, 60, 70, 40], 33), ([40, 50, 60, 30, 20], 17), ([80, 90, 70], 64),
+                                       ([40, 50], 5), ([9, 8, 7, 6, 5, 6, 7, 8], 3)])
+def test_oracle_cp_als_matches_reference_live(oracle, reflib, dims, rank):
+    """The C restatement of cp_als against the live reference (libblco_ref.so
+    cp_als, 1 thread) on the random shapes the GPU CP-ALS is checked on
+    (tests/test_gpu_stream_cpals.py): the oracle those GPU tests trust is
+    itself pinned over ranks 1-64 and orders 2-8."""
+    nnz = min(4000, int(np.prod(dims)) // 2)
+    idx, vals = oracle.synth_uniform(dims, nnz, 3 + rank)
+    keys, offs, oi, ov = oracle.build(dims, idx, vals)
+    fs, lam, fit = oracle.cp_als(dims, keys, offs, oi, ov, rank, 6, -1e300, 11)
+    from pyoracle import cfg_array
+    t = reflib.build(dims, idx, vals, 64)
+    rfs, rlam, rfit = t.cp_als(dims, rank, 6, -1e300, 11, cfg=cfg_array(num_threads=1))
+    assert rfit.size == fit.size == 6
+    assert np.max(np.abs(fit - rfit)) <= 1e-10
+    for m in range(len(dims)):
+        assert rel_frobenius(fs[m], rfs[m]) <= 1e-9, m
+    assert rel_frobenius(lam, rlam) <= 1e-9
