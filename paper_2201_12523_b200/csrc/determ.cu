@@ -48,9 +48,13 @@ struct DetParams {
   const uint32_t* __restrict__ chunk_row;
   const uint32_t* __restrict__ chunk_part;
   uint64_t nchunks;
-  const double* factors[N];  // non-target modes ascending
-  uint32_t shift[N];
-  uint64_t mask[N];
+  // per non-target mode k (ascending): its factor, mode index, field shift
+  // and mask -- indexed by the compile-time k only (a param array indexed by
+  // a runtime value would be copied to local memory)
+  const double* factors[N];
+  int other[N];
+  uint32_t oshift[N];
+  uint64_t omask[N];
   int mode;
   int rank;
   double* out;
@@ -108,11 +112,10 @@ __global__ void __launch_bounds__(32 * kDetWarps) k_mttkrp_det(DetParams<N> p) {
 #pragma unroll
       for (int c = 0; c < CPL; ++c) prod[u][c] = v;
 #pragma unroll
-      for (int m = 0, k = 0; m < N; ++m) {
-        if (m == p.mode) continue;
-        const uint32_t coord = p.block_base[static_cast<uint64_t>(blk) * N + m] |
-                               static_cast<uint32_t>((ix >> p.shift[m]) & p.mask[m]);
-        const double* rp = p.factors[k++] + static_cast<uint64_t>(coord) * R;
+      for (int k = 0; k + 1 < N; ++k) {  // the oracle's order: value, then the modes ascending
+        const uint32_t coord = p.block_base[static_cast<uint64_t>(blk) * N + p.other[k]] |
+                               static_cast<uint32_t>((ix >> p.oshift[k]) & p.omask[k]);
+        const double* rp = p.factors[k] + static_cast<uint64_t>(coord) * R;
 #pragma unroll
         for (int c = 0; c < CPL; ++c) {
           const int col = lane + 32 * c;
@@ -171,9 +174,12 @@ void launch_det(const DetIndex& d, const blco_tensor& t, const MttkrpLaunch& a, 
   p.chunk_part = d.chunk_part.ptr;
   p.nchunks = d.chunk_begin.n;
   for (int m = 0, k = 0; m < N; ++m) {
-    if (m != a.mode) p.factors[k++] = a.factors[m];
-    p.shift[m] = static_cast<uint32_t>(t.layout.field_shift[m]);
-    p.mask[m] = t.layout.field_mask[m];
+    if (m == a.mode) continue;
+    p.factors[k] = a.factors[m];
+    p.other[k] = m;
+    p.oshift[k] = static_cast<uint32_t>(t.layout.field_shift[m]);
+    p.omask[k] = t.layout.field_mask[m];
+    ++k;
   }
   p.mode = a.mode;
   p.rank = static_cast<int>(a.rank);
